@@ -1,0 +1,33 @@
+# Builds the sm_100a C-ABI library paper_2304_11414_b200/lib/libppmoe.so and the
+# C oracle helper oracle/_build/liboracle.so.  `make -j` from the repo root.
+NVCC      ?= /usr/local/cuda/bin/nvcc
+ARCH      := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS   := $(ARCH) -O3 -std=c++17 -lineinfo -Xcompiler -fPIC -Xcompiler -Wall \
+             --expt-relaxed-constexpr -Iinclude
+SRC_DIR   := paper_2304_11414_b200/csrc
+OBJ_DIR   := build/obj
+LIB       := paper_2304_11414_b200/lib/libppmoe.so
+SRCS      := $(wildcard $(SRC_DIR)/*.cu)
+OBJS      := $(patsubst $(SRC_DIR)/%.cu,$(OBJ_DIR)/%.o,$(SRCS))
+HDRS      := $(wildcard $(SRC_DIR)/*.cuh) $(wildcard $(SRC_DIR)/*.h) include/ppmoe_capi.h
+
+ORACLE_LIB := oracle/_build/liboracle.so
+
+all: $(LIB) $(ORACLE_LIB)
+
+$(OBJ_DIR)/%.o: $(SRC_DIR)/%.cu $(HDRS)
+	@mkdir -p $(OBJ_DIR)
+	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> $(OBJ_DIR)/$*.ptxas.log || (cat $(OBJ_DIR)/$*.ptxas.log; exit 1)
+
+$(LIB): $(OBJS)
+	@mkdir -p $(dir $@)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart
+
+$(ORACLE_LIB): oracle/ppmoe_oracle.c
+	@mkdir -p $(dir $@)
+	gcc -O2 -fPIC -shared -std=c11 -o $@ $< -lm
+
+clean:
+	rm -rf build $(LIB) oracle/_build
+
+.PHONY: all clean

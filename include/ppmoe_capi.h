@@ -1,0 +1,155 @@
+/*
+ * ppmoe_capi.h — C-ABI of the B200-native PPMoE (Pipeline MoE, arXiv 2304.11414)
+ * MoE-layer hot path.  Built as paper_2304_11414_b200/lib/libppmoe.so.
+ *
+ * The reference (`moesim` 0.1.0, pure Python/numpy) has no FFI for this path; its
+ * boundary is the Python API in pkg/src/moesim/moe.py.  Each entry point below
+ * replaces one step of that API and cites the reference code it reproduces.
+ * The Python package paper_2304_11414_b200 binds these symbols with ctypes
+ * and mirrors the reference's Python signatures on top.
+ *
+ * Conventions
+ *  - All pointers are DEVICE pointers owned by the caller (PyTorch caching
+ *    allocator).  The library never allocates or frees device memory, keeps no
+ *    global state, and never synchronises the host: every call only enqueues
+ *    kernels on `stream` (a cudaStream_t passed as void*).
+ *  - Return value 0 = success; negative = error, message via ppmoe_last_error()
+ *    (thread-local).  -1/-3 map to ValueError, -2/-4 to RuntimeError.
+ *  - dtype: 0 = bf16 (activations/expert weights bf16, fp32 accumulation),
+ *           1 = fp32 (reference-precision mode, CUDA-core GEMM).
+ *    The gate weight Wg and all routing scores/weights are always fp32; routing
+ *    logits and softmax are evaluated in fp64.
+ *  - Layouts are row-major.  Token-major activations [N x H] (moe.py: b*s rows).
+ *    Gate weight Wg [H x E] (GateParams.wg, moe.py:30-53).  Expert weights of the
+ *    El local experts are stacked: up [El x H x F], down [El x F x H],
+ *    bias_up [El x F], bias_down [El x H] (ExpertFfn, moe.py:80-110).
+ *  - Dispatch plan ("padded segments"): the sorted-pair buffer holds, for every
+ *    expert e, its kept token rows in ascending token id starting at seg[e]; each
+ *    segment is padded to a multiple of 128 rows with tok = -1.  A rank owning
+ *    experts [r*El, (r+1)*El) passes `seg + r*El` (El+1 entries) to the expert
+ *    calls; local row = seg[g] - seg[0] + m.  rows_cap bounds local rows.
+ */
+#ifndef PPMOE_CAPI_H
+#define PPMOE_CAPI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Library identity / errors ------------------------------------------------ */
+int ppmoe_version(void);
+const char* ppmoe_last_error(void);
+/* Number of SMs of the current device (grid sizing of the persistent kernels). */
+int ppmoe_num_sms(void);
+
+/* Routing: gate GEMV + fp64 softmax + top-k + aux-loss partials ------------
+ * Replaces gate_top1 (moe.py:196-208), aux_loss (moe.py:211-223) and the
+ * route_override path (moe.py:199-205); top-k > 1 extends the reference
+ * (repeated argmax, lowest expert id wins ties, raw softmax weights).
+ *   X        [N x H] dtype
+ *   Wg       [H x E] fp32
+ *   override [N x K] int32 or NULL; ids already validated to lie in [0, E)
+ *   idx      [N x K] int32   out: chosen experts per token (slot-major per token)
+ *   w        [N x K] fp32    out: softmax score of each chosen expert
+ *   scores   [N x E] fp32    out: full softmax scores
+ *   ws       workspace of ppmoe_route_workspace_bytes(N, E, K) bytes
+ * The dispatch plan (ppmoe_dispatch_plan) must follow on the same stream: the
+ * router leaves per-chunk histograms and score sums in `ws` for it.
+ */
+size_t ppmoe_route_workspace_bytes(int N, int E, int K);
+int ppmoe_route(const void* X, int dtype, const float* Wg, int N, int H, int E, int K, const int* route_override,
+                int* idx, float* w, float* scores, void* ws, size_t ws_bytes, void* stream);
+
+/* Dispatch plan with capacity: replaces build_dispatch_plan (moe.py:226-235)
+ * and _capacity_mask (moe.py:345-360).  Stable counting sort of the (token,
+ * slot) pairs by expert; capacity keeps the first `capacity` pairs per expert in
+ * (slot, token id) priority order (== ascending global token id at K=1).
+ *   capacity    max kept pairs per expert (INT32_MAX = unlimited)
+ *   counts      [E]    out: routed pairs per expert before capacity
+ *   kept        [E]    out: kept pairs per expert
+ *   seg         [E+1]  out: padded segment starts (multiples of 128)
+ *   tok_sorted  [rows_cap_global] out: token id per sorted row (-1 = padding)
+ *   w_sorted    [rows_cap_global] out: gate weight per sorted row
+ *   pair_pos    [N x K] out: sorted row of every pair, -1 if dropped
+ *   l_aux       [2] fp64 out: {l_aux, sum of top-1 fractions} (aux_loss, moe.py:211-223)
+ *   rows_cap_global >= N*K + 128*E
+ */
+int ppmoe_dispatch_plan(const int* idx, const float* w, int N, int E, int K, int capacity, int* counts, int* kept,
+                        int* seg, int* tok_sorted, float* w_sorted, int* pair_pos, double* l_aux,
+                        int rows_cap_global, void* ws, size_t ws_bytes, void* stream);
+
+/* Index-slice gather ("tensor index slicing"; index_select,
+ * tensor.py:226-241): Xs[row] = X[tok_sorted[seg[0]+row]] for the local rows,
+ * zero for padding rows, staged through shared memory with bulk-TMA copies.
+ * Also emits the local token id / gate weight per row.                       */
+int ppmoe_gather(const void* X, int dtype, int N, int H, const int* seg, int El, const int* tok_sorted,
+                 const float* w_sorted, int rows_cap, void* Xs, int* tok_local, float* w_local, void* stream);
+
+/* Expert FFN forward, first GEMM: Hpre = Xs*up_g + bias_up, Act = GeLU(Hpre)
+ * (ExpertFfn.forward, moe.py:100-104).  bias_up may be NULL.               */
+int ppmoe_expert_fc1_fwd(int dtype, const void* Xs, const void* up, const void* bias_up, const int* seg, int El,
+                         int H, int F, int rows_cap, void* Hpre, void* Act, void* stream);
+
+/* Expert FFN forward, second GEMM fused with the gate-weighted combine:
+ * Y = Act*down_g + bias_down (stored, pre-scale), out_acc[tok] += w*Y
+ * (moe.py:104-107, scale_rows tensor.py:184-196, index_assign 244-272).
+ * out_acc [N x H] fp32 must be zeroed by the caller.                       */
+int ppmoe_expert_fc2_fwd(int dtype, const void* Act, const void* down, const void* bias_down, const int* seg,
+                         int El, int H, int F, int rows_cap, const int* tok_local, const float* w_local,
+                         int weight_scaling, void* Y, float* out_acc, void* stream);
+
+/* out = out_acc cast to dtype (the replicated [N x H] layer output before or
+ * after the TP all-reduce, collectives.py:135-153).                         */
+int ppmoe_cast_out(const float* acc, int n, void* out, int dtype, void* stream);
+
+/* Backward of scale_rows + index_assign (tensor.py:190-194, 264-270):
+ * dY[row] = w*dOut[tok], dw[row] = <dOut[tok], Y[row]>; zero for padding.   */
+int ppmoe_bwd_dy(int dtype, const void* dOut, const void* Y, const int* seg, int El, int H, int rows_cap,
+                 const int* tok_local, const float* w_local, int weight_scaling, void* dY, float* dw, void* stream);
+
+/* dH = (dY*down_g^T) .* GeLU'(Hpre)   (matmul/gelu backward, tensor.py:134-138, 204-207) */
+int ppmoe_expert_fc2_dgrad(int dtype, const void* dY, const void* down, const void* Hpre, const int* seg, int El,
+                           int H, int F, int rows_cap, void* dH, void* stream);
+
+/* dDown_g = Act_g^T * dY_g  [El x F x H]; dbias_down_g = colsum(dY_g) (may be NULL). */
+int ppmoe_expert_fc2_wgrad(int dtype, const void* Act, const void* dY, const int* seg, int El, int H, int F,
+                           int rows_cap, void* dDown, void* dBiasDown, void* stream);
+
+/* dX_acc[tok] += dH*up_g^T  (index_select backward scatter-add, tensor.py:235-239). */
+int ppmoe_expert_fc1_dgrad(int dtype, const void* dH, const void* up, const int* seg, int El, int H, int F,
+                           int rows_cap, const int* tok_local, float* dx_acc, void* stream);
+
+/* dUp_g = Xs_g^T * dH_g  [El x H x F]; dbias_up_g = colsum(dH_g) (may be NULL). */
+int ppmoe_expert_fc1_wgrad(int dtype, const void* Xs, const void* dH, const int* seg, int El, int H, int F,
+                           int rows_cap, void* dUp, void* dBiasUp, void* stream);
+
+/* Gate backward (gather_rowwise, softmax and aux_loss backward, tensor.py:218-221,
+ * 287-291, moe.py:211-223): dL[t,e] = s*(dS - sum(dS*s)) with
+ * dS[t, idx[t,k]] += dw[pair] for pairs in sorted rows [row_lo, row_hi) and
+ * dS[t,e] += aux_grad * E/N * frac_e (pass aux_grad = 0 on all but one rank). */
+int ppmoe_gate_bwd(const float* scores, const int* idx, const int* pair_pos, const float* dw, int row_lo,
+                   int row_hi, const int* counts_top1, int N, int E, int K, float aux_grad, float* dL, void* stream);
+
+/* dX = dx_acc + dL*Wg^T (cast to dtype) and the per-chunk partials of
+ * dWg = X^T*dL, reduced deterministically into dWg [H x E] fp32.  Either of
+ * dX / dWg may be NULL.  ws of ppmoe_gate_grad_workspace_bytes(N,H,E).     */
+size_t ppmoe_gate_grad_workspace_bytes(int N, int H, int E);
+int ppmoe_gate_grads(const float* dx_acc, const void* X, int dtype, const float* dL, const float* Wg, int N, int H,
+                     int E, void* dX, float* dWg, void* ws, size_t ws_bytes, void* stream);
+
+/* Self-test entry: plain grouped GEMM D_g = A_g * B_g through the tcgen05 path
+ * (use_tc=1) or the CUDA-core path (use_tc=0).  mode 0: A [rows x K] K-major
+ * per segment, B [G*K x N] MN-major, D [rows x N]; mode 1: K from segments,
+ * A [rows x M] MN-major, B [rows x N] MN-major, D [G x M x N];
+ * mode 2: A K-major segments, B [G*N x K] K-major, D [rows x N].           */
+int ppmoe_gemm_selftest(int mode, int use_tc, int dtype, const void* A, const void* B, const int* seg, int G, int M,
+                        int N, int K, int rows_cap, void* D, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PPMOE_CAPI_H */

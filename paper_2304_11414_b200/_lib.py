@@ -1,0 +1,94 @@
+"""ctypes binding of the C-ABI library ``lib/libppmoe.so`` (include/ppmoe_capi.h).
+
+The product path has no fallback: if the shared library is missing or fails to
+load, every entry point raises.  Build it with ``make -j`` (or
+``__graft_entry__.build()``).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+import torch
+
+LIB_PATH = Path(__file__).resolve().parent / "lib" / "libppmoe.so"
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_F = ctypes.c_float
+_D = ctypes.c_double
+_S = ctypes.c_size_t
+
+# name -> (restype, argtypes); mirrors include/ppmoe_capi.h
+_SIGNATURES = {
+    "ppmoe_version": (_I, []),
+    "ppmoe_last_error": (ctypes.c_char_p, []),
+    "ppmoe_num_sms": (_I, []),
+    "ppmoe_route_workspace_bytes": (_S, [_I, _I, _I]),
+    "ppmoe_route": (_I, [_P, _I, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _S, _P]),
+    "ppmoe_dispatch_plan": (_I, [_P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _I, _P, _S, _P]),
+    "ppmoe_gather": (_I, [_P, _I, _I, _I, _P, _I, _P, _P, _I, _P, _P, _P, _P]),
+    "ppmoe_expert_fc1_fwd": (_I, [_I, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P]),
+    "ppmoe_expert_fc2_fwd": (_I, [_I, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P, _I, _P, _P, _P]),
+    "ppmoe_cast_out": (_I, [_P, _I, _P, _I, _P]),
+    "ppmoe_bwd_dy": (_I, [_I, _P, _P, _P, _I, _I, _I, _P, _P, _I, _P, _P, _P]),
+    "ppmoe_expert_fc2_dgrad": (_I, [_I, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P]),
+    "ppmoe_expert_fc2_wgrad": (_I, [_I, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P]),
+    "ppmoe_expert_fc1_dgrad": (_I, [_I, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P]),
+    "ppmoe_expert_fc1_wgrad": (_I, [_I, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P]),
+    "ppmoe_gate_bwd": (_I, [_P, _P, _P, _P, _I, _I, _P, _I, _I, _I, _F, _P, _P]),
+    "ppmoe_gate_grad_workspace_bytes": (_S, [_I, _I, _I]),
+    "ppmoe_gate_grads": (_I, [_P, _P, _I, _P, _P, _I, _I, _I, _P, _P, _P, _S, _P]),
+    "ppmoe_gemm_selftest": (_I, [_I, _I, _I, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P]),
+}
+
+EXPORTED_SYMBOLS = tuple(_SIGNATURES)
+
+_lib = None
+
+
+class PPMoEError(RuntimeError):
+    """A CUDA-side failure reported by the C-ABI (negative status -2/-4)."""
+
+
+def load():
+    """Load (once) and return the ctypes handle; raise loudly if unavailable."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise ImportError(
+                f"PPMoE CUDA library not built: {LIB_PATH} is missing (run `make -j` in the repo root). "
+                "There is no CPU fallback for the product path."
+            )
+        lib = ctypes.CDLL(os.fspath(LIB_PATH))
+        for name, (res, args) in _SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def call(name: str, *args) -> int:
+    """Invoke one C-ABI entry point and translate its status to an exception."""
+    lib = load()
+    rc = getattr(lib, name)(*args)
+    if rc != 0:
+        msg = lib.ppmoe_last_error().decode(errors="replace")
+        if rc in (-1, -3):
+            raise ValueError(msg)
+        raise PPMoEError(f"{name}: {msg} (status {rc})")
+    return rc
+
+
+def ptr(t: torch.Tensor | None):
+    """Raw device pointer of a tensor (None -> NULL)."""
+    if t is None:
+        return None
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def stream_ptr(device=None):
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)

@@ -1,0 +1,232 @@
+// Epilogue functors for the grouped expert GEMMs.  Each is applied to one row
+// (`m` within expert `g`) and W consecutive output columns starting at `n0`,
+// with the fp32 accumulator values `v` read straight from TMEM (or registers in
+// the CUDA-core path).  Row indices of token-segment operands are local
+// positions in the padded dispatch buffer: row = seg[g] - seg[0] + m.
+#pragma once
+
+#include <type_traits>
+
+#include "common.cuh"
+
+namespace ppmoe {
+
+template <typename T, int W>
+__device__ __forceinline__ void store_row(T* p, const float (&x)[W], int valid) {
+  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+    if (valid >= W && (W % 8 == 0) && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+#pragma unroll
+      for (int j = 0; j < W; j += 8) {
+        uint4 u;
+        u.x = pack_bf16x2(x[j], x[j + 1]);
+        u.y = pack_bf16x2(x[j + 2], x[j + 3]);
+        u.z = pack_bf16x2(x[j + 4], x[j + 5]);
+        u.w = pack_bf16x2(x[j + 6], x[j + 7]);
+        *reinterpret_cast<uint4*>(p + j) = u;
+      }
+      return;
+    }
+    if (valid >= W && (W % 4 == 0) && (reinterpret_cast<uintptr_t>(p) & 7) == 0) {
+#pragma unroll
+      for (int j = 0; j < W; j += 4) {
+        uint2 u;
+        u.x = pack_bf16x2(x[j], x[j + 1]);
+        u.y = pack_bf16x2(x[j + 2], x[j + 3]);
+        *reinterpret_cast<uint2*>(p + j) = u;
+      }
+      return;
+    }
+  } else {
+    if (valid >= W && (W % 4 == 0) && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+#pragma unroll
+      for (int j = 0; j < W; j += 4) *reinterpret_cast<float4*>(p + j) = make_float4(x[j], x[j + 1], x[j + 2], x[j + 3]);
+      return;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < W; ++j)
+    if (j < valid) p[j] = from_f32<T>(x[j]);
+}
+
+template <typename T, int W>
+__device__ __forceinline__ void load_row(const T* p, float (&x)[W], int valid) {
+  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+    if (valid >= W && (W % 8 == 0) && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+#pragma unroll
+      for (int j = 0; j < W; j += 8) {
+        uint4 u = *reinterpret_cast<const uint4*>(p + j);
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          float2 f = __bfloat1622float2(h[i]);
+          x[j + 2 * i] = f.x;
+          x[j + 2 * i + 1] = f.y;
+        }
+      }
+      return;
+    }
+  } else {
+    if (valid >= W && (W % 4 == 0) && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+#pragma unroll
+      for (int j = 0; j < W; j += 4) {
+        float4 f = *reinterpret_cast<const float4*>(p + j);
+        x[j] = f.x;
+        x[j + 1] = f.y;
+        x[j + 2] = f.z;
+        x[j + 3] = f.w;
+      }
+      return;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < W; ++j) x[j] = j < valid ? to_f32(p[j]) : 0.f;
+}
+
+template <int W>
+__device__ __forceinline__ void scatter_add_row(float* p, const float (&x)[W], float s, int valid) {
+  if (valid >= W && (W % 4 == 0) && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+#pragma unroll
+    for (int j = 0; j < W; j += 4) red_add_v4(p + j, s * x[j], s * x[j + 1], s * x[j + 2], s * x[j + 3]);
+    return;
+  }
+#pragma unroll
+  for (int j = 0; j < W; ++j)
+    if (j < valid) atomicAdd(p + j, s * x[j]);
+}
+
+__device__ __forceinline__ int local_row(const int* seg, int g, int m) { return seg[g] - seg[0] + m; }
+
+// fc1 forward: Hpre = X_e * up_e + bias_up ; Act = GeLU(Hpre)      (moe.py:101-104)
+template <typename T>
+struct EpiFc1Fwd {
+  T* hpre;
+  T* act;
+  const T* bias;  // [G*F] or null
+  int F;
+  const int* seg;
+  template <int W>
+  __device__ __forceinline__ void apply(int g, int m, int n0, const float (&v)[W]) const {
+    const int row = local_row(seg, g, m);
+    const int valid = min(W, F - n0);
+    float b[W];
+    if (bias) load_row<T, W>(bias + static_cast<size_t>(g) * F + n0, b, valid);
+    else
+#pragma unroll
+      for (int j = 0; j < W; ++j) b[j] = 0.f;
+    float x[W], a[W];
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+      x[j] = v[j] + b[j];
+      a[j] = gelu_f(x[j]);
+    }
+    const size_t off = static_cast<size_t>(row) * F + n0;
+    store_row<T, W>(hpre + off, x, valid);
+    store_row<T, W>(act + off, a, valid);
+  }
+};
+
+// fc2 forward + combine: Y = Act * down_e + bias_down (saved pre-scale for the
+// backward), out[tok] += w * Y  (moe.py:104-107 + scale_rows + index_assign,
+// tensor.py:184-196, 244-272; top-k contributions summed).
+template <typename T>
+struct EpiFc2Fwd {
+  T* y;
+  const T* bias;  // [G*H] or null
+  int H;
+  const int* seg;
+  const int* tok;  // [rows] local token id per row, -1 for padding
+  const float* w;  // [rows] gate weight per row
+  int weight_scaling;
+  float* out_acc;  // [N*H] fp32, zero-initialised
+  template <int W>
+  __device__ __forceinline__ void apply(int g, int m, int n0, const float (&v)[W]) const {
+    const int row = local_row(seg, g, m);
+    const int valid = min(W, H - n0);
+    float b[W];
+    if (bias) load_row<T, W>(bias + static_cast<size_t>(g) * H + n0, b, valid);
+    else
+#pragma unroll
+      for (int j = 0; j < W; ++j) b[j] = 0.f;
+    float x[W];
+#pragma unroll
+    for (int j = 0; j < W; ++j) x[j] = v[j] + b[j];
+    store_row<T, W>(y + static_cast<size_t>(row) * H + n0, x, valid);
+    const int t = tok[row];
+    if (t >= 0) {
+      const float s = weight_scaling ? w[row] : 1.f;
+      scatter_add_row<W>(out_acc + static_cast<size_t>(t) * H + n0, x, s, valid);
+    }
+  }
+};
+
+// fc2 data-gradient: dH = (dY * down_e^T) .* GeLU'(Hpre)        (tensor.py:134-138, 204-207)
+template <typename T>
+struct EpiFc2Dgrad {
+  T* dh;
+  const T* hpre;
+  int F;
+  const int* seg;
+  template <int W>
+  __device__ __forceinline__ void apply(int g, int m, int n0, const float (&v)[W]) const {
+    const int row = local_row(seg, g, m);
+    const int valid = min(W, F - n0);
+    const size_t off = static_cast<size_t>(row) * F + n0;
+    float hp[W];
+    load_row<T, W>(hpre + off, hp, valid);
+    float x[W];
+#pragma unroll
+    for (int j = 0; j < W; ++j) x[j] = v[j] * gelu_grad_f(hp[j]);
+    store_row<T, W>(dh + off, x, valid);
+  }
+};
+
+// fc1 data-gradient scattered back to token rows: dX[tok] += dH * up_e^T
+// (index_select backward, tensor.py:235-239).
+template <typename T>
+struct EpiFc1Dgrad {
+  float* dx_acc;  // [N*H] fp32
+  int H;
+  const int* seg;
+  const int* tok;
+  template <int W>
+  __device__ __forceinline__ void apply(int g, int m, int n0, const float (&v)[W]) const {
+    const int row = local_row(seg, g, m);
+    const int t = tok[row];
+    if (t < 0) return;
+    const int valid = min(W, H - n0);
+    scatter_add_row<W>(dx_acc + static_cast<size_t>(t) * H + n0, v, 1.f, valid);
+  }
+};
+
+// Weight gradient of one expert matrix: out[g][m][n]  (tensor.py:134-138, A^T * g).
+template <typename T>
+struct EpiWgrad {
+  T* out;  // [G*M*N]
+  int M;
+  int N;
+  template <int W>
+  __device__ __forceinline__ void apply(int g, int m, int n0, const float (&v)[W]) const {
+    if (m >= M) return;
+    const int valid = min(W, N - n0);
+    store_row<T, W>(out + (static_cast<size_t>(g) * M + m) * N + n0, v, valid);
+  }
+};
+
+// Plain store into a dense [M x N] per-group output (used by the GEMM self-test).
+template <typename T>
+struct EpiStore {
+  T* out;
+  int N;
+  const int* seg;
+  int ldo_rows_from_seg;  // 1: row = local segment row, 0: row = g*M_fixed + m
+  int M_fixed;
+  template <int W>
+  __device__ __forceinline__ void apply(int g, int m, int n0, const float (&v)[W]) const {
+    if (!ldo_rows_from_seg && m >= M_fixed) return;
+    const int row = ldo_rows_from_seg ? local_row(seg, g, m) : g * M_fixed + m;
+    const int valid = min(W, N - n0);
+    store_row<T, W>(out + static_cast<size_t>(row) * N + n0, v, valid);
+  }
+};
+
+}  // namespace ppmoe

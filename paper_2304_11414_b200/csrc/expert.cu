@@ -1,0 +1,270 @@
+// Expert FFN forward/backward entry points: the six grouped GEMMs of one MoE
+// layer step (fc1/fc2 forward, fc2/fc1 data-gradient, fc2/fc1 weight-gradient)
+// plus the bias-gradient column sums.  bf16 runs on the tcgen05/TMA kernel,
+// fp32 (reference-precision mode) on the CUDA-core kernel.
+#include "../../include/ppmoe_capi.h"
+#include "epilogues.cuh"
+#include "grouped_gemm.cuh"
+#include "host.h"
+
+namespace ppmoe {
+
+using bf16 = __nv_bfloat16;
+constexpr int kBN = 256;
+
+template <bool A_MN, bool B_MN, class Epi>
+static int launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const GroupGeom& geo, const Epi& epi,
+                     cudaStream_t s) {
+  auto kern = grouped_gemm_sm100<kBN, A_MN, B_MN, Epi>;
+  constexpr int smem = GemmSmem<kBN>::kTotal;
+  PPMOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  kern<<<num_sms(), kGemmThreads, smem, s>>>(ta, tb, geo, epi);
+  return check_launch("grouped_gemm_sm100");
+}
+
+template <typename T, bool A_MN, bool B_MN, class Epi>
+static int launch_simt(const T* A, int lda, const T* B, int ldb, const GroupGeom& geo, int m_upper, const Epi& epi,
+                       cudaStream_t s) {
+  dim3 grid((geo.N + 63) / 64, (m_upper + 63) / 64, geo.G);
+  if (grid.y == 0) return kOk;
+  grouped_gemm_simt<T, A_MN, B_MN, Epi><<<grid, 256, 0, s>>>(A, lda, B, ldb, geo, epi);
+  return check_launch("grouped_gemm_simt");
+}
+
+// Operand tensor maps: K-major -> box {64 (K), rows}; MN-major -> box {64 (MN), 64 (K)}.
+static int tmap_kmajor(CUtensorMap* m, const void* p, uint64_t k_extent, uint64_t rows, uint32_t box_rows) {
+  return make_tmap_2d(m, p, kBF16, k_extent, rows, k_extent * 2, 64, box_rows);
+}
+static int tmap_mnmajor(CUtensorMap* m, const void* p, uint64_t mn_extent, uint64_t k_rows) {
+  return make_tmap_2d(m, p, kBF16, mn_extent, k_rows, mn_extent * 2, 64, 64);
+}
+
+static int check_common(int dtype, int El, int H, int F, int rows_cap) {
+  PPMOE_REQUIRE(dtype == kBF16 || dtype == kF32, "dtype must be 0 (bf16) or 1 (fp32), got %d", dtype);
+  PPMOE_REQUIRE(El >= 1 && El <= kMaxGroups, "local experts must be in [1, %d], got %d", kMaxGroups, El);
+  PPMOE_REQUIRE(H >= 1 && F >= 1 && rows_cap >= 0, "bad expert shape H=%d F=%d rows_cap=%d", H, F, rows_cap);
+  if (dtype == kBF16)
+    PPMOE_REQUIRE(H % 8 == 0 && F % 8 == 0,
+                  "bf16 expert path needs hidden and ffn widths divisible by 8 (TMA row pitch), got H=%d F=%d", H, F);
+  return kOk;
+}
+
+template <typename T>
+__global__ void colsum_kernel(const T* __restrict__ src, int ld, const int* __restrict__ seg, int N, T* __restrict__ out) {
+  const int g = blockIdx.y;
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= N) return;
+  const int lo = seg[g] - seg[0];
+  const int hi = seg[g + 1] - seg[0];
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  int r = lo;
+  for (; r + 4 <= hi; r += 4) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc[u] += to_f32(src[static_cast<size_t>(r + u) * ld + col]);
+  }
+  for (; r < hi; ++r) acc[0] += to_f32(src[static_cast<size_t>(r) * ld + col]);
+  out[static_cast<size_t>(g) * N + col] = from_f32<T>((acc[0] + acc[1]) + (acc[2] + acc[3]));
+}
+
+template <typename T>
+static int colsum(const void* src, int ld, const int* seg, int G, int N, void* out, cudaStream_t s) {
+  if (!out) return kOk;
+  dim3 grid((N + 255) / 256, G);
+  colsum_kernel<T><<<grid, 256, 0, s>>>(static_cast<const T*>(src), ld, seg, N, static_cast<T*>(out));
+  return check_launch("colsum");
+}
+
+static GroupGeom geom(int G, int N, int M_fixed, int K_fixed, const int* seg, int a_seg, int a_stride, int b_seg,
+                      int b_stride) {
+  GroupGeom g;
+  g.G = G;
+  g.N = N;
+  g.M_fixed = M_fixed;
+  g.K_fixed = K_fixed;
+  g.seg = seg;
+  g.a_seg = a_seg;
+  g.a_stride = a_stride;
+  g.b_seg = b_seg;
+  g.b_stride = b_stride;
+  return g;
+}
+
+}  // namespace ppmoe
+
+using namespace ppmoe;
+
+extern "C" {
+
+int ppmoe_expert_fc1_fwd(int dtype, const void* Xs, const void* up, const void* bias_up, const int* seg, int El, int H,
+                         int F, int rows_cap, void* Hpre, void* Act, void* stream) {
+  if (int rc = check_common(dtype, El, H, F, rows_cap)) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  GroupGeom geo = geom(El, F, 0, H, seg, 1, 0, 0, H);
+  if (rows_cap == 0) return kOk;
+  if (dtype == kBF16) {
+    CUtensorMap ta, tb;
+    if (int rc = tmap_kmajor(&ta, Xs, H, rows_cap, kBM)) return rc;
+    if (int rc = tmap_mnmajor(&tb, up, F, static_cast<uint64_t>(El) * H)) return rc;
+    EpiFc1Fwd<bf16> epi{static_cast<bf16*>(Hpre), static_cast<bf16*>(Act), static_cast<const bf16*>(bias_up), F, seg};
+    return launch_tc<false, true>(ta, tb, geo, epi, s);
+  }
+  EpiFc1Fwd<float> epi{static_cast<float*>(Hpre), static_cast<float*>(Act), static_cast<const float*>(bias_up), F, seg};
+  return launch_simt<float, false, true>(static_cast<const float*>(Xs), H, static_cast<const float*>(up), F, geo,
+                                         rows_cap, epi, s);
+}
+
+int ppmoe_expert_fc2_fwd(int dtype, const void* Act, const void* down, const void* bias_down, const int* seg, int El,
+                         int H, int F, int rows_cap, const int* tok_local, const float* w_local, int weight_scaling,
+                         void* Y, float* out_acc, void* stream) {
+  if (int rc = check_common(dtype, El, H, F, rows_cap)) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  GroupGeom geo = geom(El, H, 0, F, seg, 1, 0, 0, F);
+  if (rows_cap == 0) return kOk;
+  if (dtype == kBF16) {
+    CUtensorMap ta, tb;
+    if (int rc = tmap_kmajor(&ta, Act, F, rows_cap, kBM)) return rc;
+    if (int rc = tmap_mnmajor(&tb, down, H, static_cast<uint64_t>(El) * F)) return rc;
+    EpiFc2Fwd<bf16> epi{static_cast<bf16*>(Y), static_cast<const bf16*>(bias_down), H, seg, tok_local, w_local,
+                        weight_scaling, out_acc};
+    return launch_tc<false, true>(ta, tb, geo, epi, s);
+  }
+  EpiFc2Fwd<float> epi{static_cast<float*>(Y), static_cast<const float*>(bias_down), H, seg, tok_local, w_local,
+                       weight_scaling, out_acc};
+  return launch_simt<float, false, true>(static_cast<const float*>(Act), F, static_cast<const float*>(down), H, geo,
+                                         rows_cap, epi, s);
+}
+
+int ppmoe_expert_fc2_dgrad(int dtype, const void* dY, const void* down, const void* Hpre, const int* seg, int El, int H,
+                           int F, int rows_cap, void* dH, void* stream) {
+  if (int rc = check_common(dtype, El, H, F, rows_cap)) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  GroupGeom geo = geom(El, F, 0, H, seg, 1, 0, 0, F);
+  if (rows_cap == 0) return kOk;
+  if (dtype == kBF16) {
+    CUtensorMap ta, tb;
+    if (int rc = tmap_kmajor(&ta, dY, H, rows_cap, kBM)) return rc;
+    if (int rc = tmap_kmajor(&tb, down, H, static_cast<uint64_t>(El) * F, kBN)) return rc;
+    EpiFc2Dgrad<bf16> epi{static_cast<bf16*>(dH), static_cast<const bf16*>(Hpre), F, seg};
+    return launch_tc<false, false>(ta, tb, geo, epi, s);
+  }
+  EpiFc2Dgrad<float> epi{static_cast<float*>(dH), static_cast<const float*>(Hpre), F, seg};
+  return launch_simt<float, false, false>(static_cast<const float*>(dY), H, static_cast<const float*>(down), H, geo,
+                                          rows_cap, epi, s);
+}
+
+int ppmoe_expert_fc1_dgrad(int dtype, const void* dH, const void* up, const int* seg, int El, int H, int F,
+                           int rows_cap, const int* tok_local, float* dx_acc, void* stream) {
+  if (int rc = check_common(dtype, El, H, F, rows_cap)) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  GroupGeom geo = geom(El, H, 0, F, seg, 1, 0, 0, H);
+  if (rows_cap == 0) return kOk;
+  if (dtype == kBF16) {
+    CUtensorMap ta, tb;
+    if (int rc = tmap_kmajor(&ta, dH, F, rows_cap, kBM)) return rc;
+    if (int rc = tmap_kmajor(&tb, up, F, static_cast<uint64_t>(El) * H, kBN)) return rc;
+    EpiFc1Dgrad<bf16> epi{dx_acc, H, seg, tok_local};
+    return launch_tc<false, false>(ta, tb, geo, epi, s);
+  }
+  EpiFc1Dgrad<float> epi{dx_acc, H, seg, tok_local};
+  return launch_simt<float, false, false>(static_cast<const float*>(dH), F, static_cast<const float*>(up), F, geo,
+                                          rows_cap, epi, s);
+}
+
+int ppmoe_expert_fc2_wgrad(int dtype, const void* Act, const void* dY, const int* seg, int El, int H, int F,
+                           int rows_cap, void* dDown, void* dBiasDown, void* stream) {
+  if (int rc = check_common(dtype, El, H, F, rows_cap)) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  GroupGeom geo = geom(El, H, F, 0, seg, 1, 0, 1, 0);
+  if (dtype == kBF16) {
+    if (rows_cap > 0) {
+      CUtensorMap ta, tb;
+      if (int rc = tmap_mnmajor(&ta, Act, F, rows_cap)) return rc;
+      if (int rc = tmap_mnmajor(&tb, dY, H, rows_cap)) return rc;
+      EpiWgrad<bf16> epi{static_cast<bf16*>(dDown), F, H};
+      if (int rc = launch_tc<true, true>(ta, tb, geo, epi, s)) return rc;
+    } else {
+      PPMOE_CUDA(cudaMemsetAsync(dDown, 0, static_cast<size_t>(El) * F * H * 2, s));
+    }
+    return colsum<bf16>(dY, H, seg, El, H, dBiasDown, s);
+  }
+  EpiWgrad<float> epi{static_cast<float*>(dDown), F, H};
+  if (int rc = launch_simt<float, true, true>(static_cast<const float*>(Act), F, static_cast<const float*>(dY), H, geo,
+                                              F, epi, s))
+    return rc;
+  return colsum<float>(dY, H, seg, El, H, dBiasDown, s);
+}
+
+int ppmoe_expert_fc1_wgrad(int dtype, const void* Xs, const void* dH, const int* seg, int El, int H, int F,
+                           int rows_cap, void* dUp, void* dBiasUp, void* stream) {
+  if (int rc = check_common(dtype, El, H, F, rows_cap)) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  GroupGeom geo = geom(El, F, H, 0, seg, 1, 0, 1, 0);
+  if (dtype == kBF16) {
+    if (rows_cap > 0) {
+      CUtensorMap ta, tb;
+      if (int rc = tmap_mnmajor(&ta, Xs, H, rows_cap)) return rc;
+      if (int rc = tmap_mnmajor(&tb, dH, F, rows_cap)) return rc;
+      EpiWgrad<bf16> epi{static_cast<bf16*>(dUp), H, F};
+      if (int rc = launch_tc<true, true>(ta, tb, geo, epi, s)) return rc;
+    } else {
+      PPMOE_CUDA(cudaMemsetAsync(dUp, 0, static_cast<size_t>(El) * H * F * 2, s));
+    }
+    return colsum<bf16>(dH, F, seg, El, F, dBiasUp, s);
+  }
+  EpiWgrad<float> epi{static_cast<float*>(dUp), H, F};
+  if (int rc = launch_simt<float, true, true>(static_cast<const float*>(Xs), H, static_cast<const float*>(dH), F, geo,
+                                              H, epi, s))
+    return rc;
+  return colsum<float>(dH, F, seg, El, F, dBiasUp, s);
+}
+
+int ppmoe_gemm_selftest(int mode, int use_tc, int dtype, const void* A, const void* B, const int* seg, int G, int M,
+                        int N, int K, int rows_cap, void* D, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  PPMOE_REQUIRE(mode >= 0 && mode <= 2, "mode must be 0..2");
+  PPMOE_REQUIRE(G >= 1 && G <= kMaxGroups, "bad group count %d", G);
+  PPMOE_REQUIRE(!use_tc || dtype == kBF16, "tcgen05 path is bf16 only");
+  if (mode == 0) {  // D[seg rows x N] = A[seg rows x K] * B_g[K x N] (B MN-major)
+    GroupGeom geo = geom(G, N, 0, K, seg, 1, 0, 0, K);
+    if (use_tc) {
+      CUtensorMap ta, tb;
+      if (int rc = tmap_kmajor(&ta, A, K, rows_cap, kBM)) return rc;
+      if (int rc = tmap_mnmajor(&tb, B, N, static_cast<uint64_t>(G) * K)) return rc;
+      return launch_tc<false, true>(ta, tb, geo, EpiStore<float>{static_cast<float*>(D), N, seg, 1, 0}, s);
+    }
+    if (dtype == kBF16)
+      return launch_simt<bf16, false, true>(static_cast<const bf16*>(A), K, static_cast<const bf16*>(B), N, geo, rows_cap,
+                                            EpiStore<float>{static_cast<float*>(D), N, seg, 1, 0}, s);
+    return launch_simt<float, false, true>(static_cast<const float*>(A), K, static_cast<const float*>(B), N, geo,
+                                           rows_cap, EpiStore<float>{static_cast<float*>(D), N, seg, 1, 0}, s);
+  }
+  if (mode == 1) {  // D[g][M x N] = A_g^T * B_g with K from segments (both MN-major)
+    GroupGeom geo = geom(G, N, M, 0, seg, 1, 0, 1, 0);
+    if (use_tc) {
+      CUtensorMap ta, tb;
+      if (int rc = tmap_mnmajor(&ta, A, M, rows_cap)) return rc;
+      if (int rc = tmap_mnmajor(&tb, B, N, rows_cap)) return rc;
+      return launch_tc<true, true>(ta, tb, geo, EpiStore<float>{static_cast<float*>(D), N, seg, 0, M}, s);
+    }
+    if (dtype == kBF16)
+      return launch_simt<bf16, true, true>(static_cast<const bf16*>(A), M, static_cast<const bf16*>(B), N, geo, M,
+                                           EpiStore<float>{static_cast<float*>(D), N, seg, 0, M}, s);
+    return launch_simt<float, true, true>(static_cast<const float*>(A), M, static_cast<const float*>(B), N, geo, M,
+                                          EpiStore<float>{static_cast<float*>(D), N, seg, 0, M}, s);
+  }
+  // mode 2: D[seg rows x N] = A[seg rows x K] * B_g^T, B_g [N x K] K-major
+  GroupGeom geo = geom(G, N, 0, K, seg, 1, 0, 0, N);
+  if (use_tc) {
+    CUtensorMap ta, tb;
+    if (int rc = tmap_kmajor(&ta, A, K, rows_cap, kBM)) return rc;
+    if (int rc = tmap_kmajor(&tb, B, K, static_cast<uint64_t>(G) * N, kBN)) return rc;
+    return launch_tc<false, false>(ta, tb, geo, EpiStore<float>{static_cast<float*>(D), N, seg, 1, 0}, s);
+  }
+  if (dtype == kBF16)
+    return launch_simt<bf16, false, false>(static_cast<const bf16*>(A), K, static_cast<const bf16*>(B), K, geo, rows_cap,
+                                           EpiStore<float>{static_cast<float*>(D), N, seg, 1, 0}, s);
+  return launch_simt<float, false, false>(static_cast<const float*>(A), K, static_cast<const float*>(B), K, geo,
+                                          rows_cap, EpiStore<float>{static_cast<float*>(D), N, seg, 1, 0}, s);
+}
+
+}  // extern "C"

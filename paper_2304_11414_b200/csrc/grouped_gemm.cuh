@@ -1,0 +1,314 @@
+// Grouped (per-expert) GEMM on sm_100a: tcgen05.mma + TMEM accumulators, TMA-fed,
+// warp-specialised, persistent over a device-side tile list.
+//
+//   D_g[M_g x N] = A_g[M_g x K_g] * B_g[K_g x N]      for every local expert g
+//
+// M_g or K_g may come from the device-side dispatch segments (`seg`, padded to
+// 128 rows per expert by the dispatch plan), so no host synchronisation is
+// needed between routing and the expert GEMMs.  Each operand is a 2-D global
+// tensor addressed either K-major (row = M/N index, K contiguous) or MN-major
+// (row = K index, M/N contiguous); both are staged with SWIZZLE_128B TMA boxes
+// and described to the tensor core with the matching canonical layout.
+//
+// The epilogue is a functor applied per (row, 32-column chunk) straight out of
+// TMEM (tcgen05.ld): bias + exact GeLU, gate-scaled scatter-add combine,
+// GeLU' backward, scatter-add of dX, or the weight-gradient store.  This is the
+// fused replacement of the reference's per-expert loop of
+//   index_select -> matmul -> add -> gelu -> matmul -> add -> scale_rows -> index_assign
+// (moe.py:294-305, tensor.py:128-272).
+#pragma once
+
+#include "common.cuh"
+
+namespace ppmoe {
+
+constexpr int kBM = 128;      // tile rows (UMMA M, one CTA)
+constexpr int kBK = 64;       // K per pipeline stage = one 128-byte swizzle row of bf16
+constexpr int kUMMAK = 16;    // K per tcgen05.mma (bf16)
+constexpr int kStages = 4;
+constexpr int kMaxGroups = 64;
+constexpr int kGemmThreads = 256;  // warp0 TMA, warp1 MMA, warp2 TMEM alloc, warps4-7 epilogue
+
+struct GroupGeom {
+  int G;          // number of groups (local experts)
+  int N;          // output columns
+  int M_fixed;    // >0: every group has M = M_fixed rows; else M_g = padded segment rows
+  int K_fixed;    // >0: every group has K = K_fixed; else K_g = padded segment rows
+  const int* seg; // [G+1] padded segment starts (global positions; local = seg[g]-seg[0])
+  int a_seg;      // A row base: 1 -> local segment start, 0 -> g * a_stride
+  int a_stride;
+  int b_seg;
+  int b_stride;
+};
+
+template <int BN>
+struct GemmSmem {
+  static constexpr int kABytes = kBM * kBK * 2;     // 16 KB
+  static constexpr int kBBytes = BN * kBK * 2;      // 32 KB at BN=256
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kBarOffset = kStages * kStageBytes;
+  // full[S], empty[S], tmem_full[2], tmem_empty[2], tmem base, scheduler tables
+  static constexpr int kBarBytes = (2 * kStages + 4) * 8 + 16;
+  static constexpr int kSchedOffset = kBarOffset + kBarBytes;
+  static constexpr int kSchedBytes = (kMaxGroups + 1) * 4 * 5;
+  static constexpr int kTotal = kSchedOffset + kSchedBytes + 1024;  // + alignment slack
+};
+
+// Tile scheduler tables, filled identically by every CTA from the device segments.
+struct SchedTables {
+  int* tile_start;  // [G+1]
+  int* m_tiles;     // [G]
+  int* k_blocks;    // [G]
+  int* a_base;      // [G]
+  int* b_base;      // [G]
+};
+
+__device__ __forceinline__ void sched_locate(const SchedTables& t, int G, int tile, int& g, int& local) {
+  int lo = 0;
+  while (lo + 1 < G && t.tile_start[lo + 1] <= tile) ++lo;
+  g = lo;
+  local = tile - t.tile_start[lo];
+}
+
+template <int BN, bool A_MN, bool B_MN, class Epi>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    grouped_gemm_sm100(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                       GroupGeom geo, Epi epi) {
+  using L = GemmSmem<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_addr = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
+
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOffset);
+  uint64_t* empty = full + kStages;
+  uint64_t* tmem_full = empty + kStages;
+  uint64_t* tmem_empty = tmem_full + 2;
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+  int* sched = reinterpret_cast<int*>(smem + L::kSchedOffset);
+  SchedTables tab{sched, sched + (kMaxGroups + 1), sched + 2 * (kMaxGroups + 1), sched + 3 * (kMaxGroups + 1),
+                  sched + 4 * (kMaxGroups + 1)};
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+  const int G = geo.G;
+  const int n_tiles = (geo.N + BN - 1) / BN;
+
+  if (threadIdx.x == 0) {
+    const int s0 = geo.seg[0];
+    int acc = 0;
+    for (int g = 0; g < G; ++g) {
+      const int seg_lo = geo.seg[g] - s0;
+      const int seg_rows = geo.seg[g + 1] - geo.seg[g];
+      const int M = geo.M_fixed > 0 ? geo.M_fixed : seg_rows;
+      const int K = geo.K_fixed > 0 ? geo.K_fixed : seg_rows;
+      tab.tile_start[g] = acc;
+      tab.m_tiles[g] = (M + kBM - 1) / kBM;
+      tab.k_blocks[g] = (K + kBK - 1) / kBK;
+      tab.a_base[g] = geo.a_seg ? seg_lo : g * geo.a_stride;
+      tab.b_base[g] = geo.b_seg ? seg_lo : g * geo.b_stride;
+      acc += tab.m_tiles[g] * n_tiles;
+    }
+    tab.tile_start[G] = acc;
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tmem_full[a], 1);
+      mbar_init(&tmem_empty[a], 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmap_a);
+    tma_prefetch_desc(&tmap_b);
+  }
+  constexpr uint32_t kTmemCols = 2 * BN;  // double-buffered fp32 accumulator
+  if (warp == 2) tmem_alloc(tmem_base_slot, kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_base_slot;
+  const int total_tiles = tab.tile_start[G];
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+        int g, local;
+        sched_locate(tab, G, tile, g, local);
+        const int mt = local % tab.m_tiles[g];
+        const int nt = local / tab.m_tiles[g];
+        const int kb_n = tab.k_blocks[g];
+        const int abase = tab.a_base[g];
+        const int bbase = tab.b_base[g];
+        for (int kb = 0; kb < kb_n; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * L::kStageBytes;
+          uint8_t* sb = sa + L::kABytes;
+          mbar_arrive_expect_tx(&full[stage], L::kStageBytes);
+          if (A_MN) {
+#pragma unroll
+            for (int j = 0; j < kBM / 64; ++j)
+              tma_load_2d(sa + j * (64 * kBK * 2), &tmap_a, &full[stage], mt * kBM + j * 64, abase + kb * kBK);
+          } else {
+            tma_load_2d(sa, &tmap_a, &full[stage], kb * kBK, abase + mt * kBM);
+          }
+          if (B_MN) {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j)
+              tma_load_2d(sb + j * (64 * kBK * 2), &tmap_b, &full[stage], nt * BN + j * 64, bbase + kb * kBK);
+          } else {
+            tma_load_2d(sb, &tmap_b, &full[stage], kb * kBK, bbase + nt * BN);
+          }
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = make_idesc_bf16(kBM, BN, A_MN, B_MN);
+      // Descriptor strides (bytes). K-major: SBO = 8 rows x 128 B. MN-major: LBO = distance
+      // between 64-wide MN chunks (one TMA box each), SBO = 8 K-rows x 128 B.
+      constexpr uint32_t a_lbo = A_MN ? (64 * kBK * 2) : 16;
+      constexpr uint32_t b_lbo = B_MN ? (64 * kBK * 2) : 16;
+      constexpr uint32_t k_step_a = A_MN ? (kUMMAK * 128) : (kUMMAK * 2);
+      constexpr uint32_t k_step_b = B_MN ? (kUMMAK * 128) : (kUMMAK * 2);
+      int stage = 0;
+      uint32_t phase = 0;
+      int iter = 0;
+      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++iter) {
+        int g, local;
+        sched_locate(tab, G, tile, g, local);
+        const int kb_n = tab.k_blocks[g];
+        const int acc = iter & 1;
+        const uint32_t acc_phase = (iter >> 1) & 1;
+        mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < kb_n; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * L::kStageBytes);
+          const uint32_t sb = sa + L::kABytes;
+#pragma unroll
+          for (int k = 0; k < kBK / kUMMAK; ++k) {
+            const uint64_t ad = make_sdesc(sa + k * k_step_a, a_lbo, 1024);
+            const uint64_t bd = make_sdesc(sb + k * k_step_b, b_lbo, 1024);
+            umma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tmem_full[acc]);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int row_in_tile = q * 32 + lane;
+    int iter = 0;
+    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++iter) {
+      int g, local;
+      sched_locate(tab, G, tile, g, local);
+      const int mt = local % tab.m_tiles[g];
+      const int nt = local / tab.m_tiles[g];
+      const bool has_k = tab.k_blocks[g] > 0;
+      const int acc = iter & 1;
+      const uint32_t acc_phase = (iter >> 1) & 1;
+      mbar_wait(&tmem_full[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
+      const int m = mt * kBM + row_in_tile;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        float v[32];
+        tmem_ld32(taddr + c * 32, v);
+        if (!has_k) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = 0.f;
+        }
+        const int n0 = nt * BN + c * 32;
+        if (n0 < geo.N) epi.template apply<32>(g, m, n0, v);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tmem_empty[acc]);
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, kTmemCols);
+  }
+}
+
+// --------------------------------------------------------------------------
+// CUDA-core reference grouped GEMM (fp32 mode, configs with rtol 1e-4, and
+// shapes the TMA path does not take). Same geometry and epilogues.
+// 64x64 tile, 256 threads, 4x4 register micro-tile.
+template <typename T, bool A_MN, bool B_MN, class Epi>
+__global__ void __launch_bounds__(256)
+    grouped_gemm_simt(const T* __restrict__ A, int lda, const T* __restrict__ B, int ldb, GroupGeom geo, Epi epi) {
+  __shared__ float As[16][64 + 4];
+  __shared__ float Bs[16][64 + 4];
+  const int g = blockIdx.z;
+  const int s0 = geo.seg[0];
+  const int seg_lo = geo.seg[g] - s0;
+  const int seg_rows = geo.seg[g + 1] - geo.seg[g];
+  const int M = geo.M_fixed > 0 ? geo.M_fixed : seg_rows;
+  const int K = geo.K_fixed > 0 ? geo.K_fixed : seg_rows;
+  const int m0 = blockIdx.y * 64;
+  const int n0 = blockIdx.x * 64;
+  if (m0 >= M) return;
+  const int abase = geo.a_seg ? seg_lo : g * geo.a_stride;
+  const int bbase = geo.b_seg ? seg_lo : g * geo.b_stride;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += 16) {
+    for (int i = threadIdx.x; i < 16 * 64; i += 256) {
+      const int kk = i / 64, mm = i % 64;
+      const int m = m0 + mm, k = k0 + kk;
+      float va = 0.f, vb = 0.f;
+      if (m < M && k < K)
+        va = to_f32(A_MN ? A[static_cast<size_t>(abase + k) * lda + m] : A[static_cast<size_t>(abase + m) * lda + k]);
+      const int n = n0 + mm;
+      if (n < geo.N && k < K)
+        vb = to_f32(B_MN ? B[static_cast<size_t>(bbase + k) * ldb + n] : B[static_cast<size_t>(bbase + n) * ldb + k]);
+      As[kk][mm] = va;
+      Bs[kk][mm] = vb;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int m = m0 + ty * 4 + i;
+    if (m < M && n0 + tx * 4 < geo.N) epi.template apply<4>(g, m, n0 + tx * 4, acc[i]);
+  }
+}
+
+}  // namespace ppmoe

@@ -1,0 +1,465 @@
+// Routing and dispatch plan.
+//
+//  router_kernel    gate GEMV (fp64 accumulation of exact bf16/fp32 x fp32 products),
+//                   fp64 softmax, top-k by repeated argmax (lowest id wins ties),
+//                   per-block expert score sums and top-1 counts for the aux loss.
+//                   Reference: gate_top1 moe.py:196-208, softmax tensor.py:212-223,
+//                   aux_loss moe.py:211-223.
+//  plan_*           stable counting sort of (token, slot) pairs by expert with the
+//                   capacity rule, into 128-row padded segments.
+//                   Reference: build_dispatch_plan moe.py:226-235, _capacity_mask
+//                   moe.py:345-360.
+//
+// Everything is deterministic: integer histograms (exact under atomics), fixed-order
+// fp64 reductions for the aux loss.
+#include <climits>
+
+#include "../../include/ppmoe_capi.h"
+#include "common.cuh"
+#include "host.h"
+
+namespace ppmoe {
+
+constexpr int kRouteThreads = 256;
+constexpr int kRouteHC = 256;   // hidden chunk staged in shared memory
+constexpr int kChunk = 256;     // tokens per plan chunk (one thread per token)
+constexpr int kMaxE = 128;
+constexpr int kMaxK = 8;
+
+__host__ __device__ inline int route_tokens_per_block(int E) {
+  int tt = 1;
+  while (tt * 2 * E <= kRouteThreads && tt * 2 <= 64) tt *= 2;
+  return tt;
+}
+
+static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+template <typename T>
+__device__ __forceinline__ void load8(const T* p, float* dst);
+template <>
+__device__ __forceinline__ void load8<__nv_bfloat16>(const __nv_bfloat16* p, float* dst) {
+  uint4 u = *reinterpret_cast<const uint4*>(p);
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 f = __bfloat1622float2(h[i]);
+    dst[2 * i] = f.x;
+    dst[2 * i + 1] = f.y;
+  }
+}
+template <>
+__device__ __forceinline__ void load8<float>(const float* p, float* dst) {
+  float4 a = *reinterpret_cast<const float4*>(p);
+  float4 b = *reinterpret_cast<const float4*>(p + 4);
+  dst[0] = a.x; dst[1] = a.y; dst[2] = a.z; dst[3] = a.w;
+  dst[4] = b.x; dst[5] = b.y; dst[6] = b.z; dst[7] = b.w;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kRouteThreads) router_kernel(const T* __restrict__ X, const float* __restrict__ Wg,
+                                                               int N, int H, int E, int K, const int* __restrict__ ovr,
+                                                               int* __restrict__ idx, float* __restrict__ w,
+                                                               float* __restrict__ scores, double* __restrict__ ssum,
+                                                               int* __restrict__ cnt_top1) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  const int TT = route_tokens_per_block(E);
+  double* lg = reinterpret_cast<double*>(sm);         // [TT][E] logits, then scores
+  double* stat = lg + TT * E;                         // [TT][2] max, sum
+  float* xs = reinterpret_cast<float*>(stat + 2 * TT);  // [TT][HC+1]
+  float* wsm = xs + TT * (kRouteHC + 1);             // [HC][E]
+  const int tid = threadIdx.x;
+  const int tl = tid / E, e = tid % E;
+  const bool active = tid < TT * E;
+  const int t0 = blockIdx.x * TT;
+  const bool vec = (H % 8) == 0;
+
+  double acc = 0.0;
+  for (int h0 = 0; h0 < H; h0 += kRouteHC) {
+    const int hc = min(kRouteHC, H - h0);
+    if (vec) {
+      const int nv = hc / 8;
+      for (int i = tid; i < TT * nv; i += blockDim.x) {
+        const int r = i / nv, c = (i % nv) * 8;
+        const int t = t0 + r;
+        float tmp[8];
+        if (t < N) load8<T>(X + static_cast<size_t>(t) * H + h0 + c, tmp);
+        else
+#pragma unroll
+          for (int j = 0; j < 8; ++j) tmp[j] = 0.f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) xs[r * (kRouteHC + 1) + c + j] = tmp[j];
+      }
+    } else {
+      for (int i = tid; i < TT * hc; i += blockDim.x) {
+        const int r = i / hc, c = i % hc;
+        const int t = t0 + r;
+        xs[r * (kRouteHC + 1) + c] = t < N ? to_f32(X[static_cast<size_t>(t) * H + h0 + c]) : 0.f;
+      }
+    }
+    for (int i = tid; i < hc * E; i += blockDim.x) wsm[i] = Wg[static_cast<size_t>(h0) * E + i];
+    __syncthreads();
+    if (active) {
+      const float* xr = xs + tl * (kRouteHC + 1);
+      double a0 = 0.0, a1 = 0.0;
+      int c = 0;
+      for (; c + 2 <= hc; c += 2) {
+        a0 = fma(static_cast<double>(xr[c]), static_cast<double>(wsm[c * E + e]), a0);
+        a1 = fma(static_cast<double>(xr[c + 1]), static_cast<double>(wsm[(c + 1) * E + e]), a1);
+      }
+      if (c < hc) a0 = fma(static_cast<double>(xr[c]), static_cast<double>(wsm[c * E + e]), a0);
+      acc += a0 + a1;
+    }
+    __syncthreads();
+  }
+  if (active) lg[tl * E + e] = acc;
+  __syncthreads();
+  // softmax statistics (row max shift, tensor.py:214-216)
+  if (tid < TT) {
+    const double* l = lg + tid * E;
+    double mx = l[0];
+    for (int j = 1; j < E; ++j) mx = fmax(mx, l[j]);
+    double s = 0.0;
+    for (int j = 0; j < E; ++j) s += exp(l[j] - mx);
+    stat[2 * tid] = mx;
+    stat[2 * tid + 1] = s;
+  }
+  __syncthreads();
+  const int t = t0 + tl;
+  if (active) {
+    const double sc = exp(lg[tl * E + e] - stat[2 * tl]) / stat[2 * tl + 1];
+    __syncwarp(__activemask());
+    lg[tl * E + e] = sc;
+    if (t < N) scores[static_cast<size_t>(t) * E + e] = static_cast<float>(sc);
+  }
+  __syncthreads();
+  // top-k selection, one thread per token
+  if (tid < TT && t0 + tid < N) {
+    const int tt = t0 + tid;
+    const double* sc = lg + tid * E;
+    unsigned long long chosen[2] = {0ull, 0ull};
+    for (int s = 0; s < K; ++s) {
+      int best;
+      if (ovr) {
+        best = ovr[static_cast<size_t>(tt) * K + s];
+      } else {
+        best = -1;
+        for (int j = 0; j < E; ++j) {
+          if ((chosen[j >> 6] >> (j & 63)) & 1ull) continue;
+          if (best < 0 || sc[j] > sc[best]) best = j;
+        }
+        chosen[best >> 6] |= 1ull << (best & 63);
+      }
+      idx[static_cast<size_t>(tt) * K + s] = best;
+      w[static_cast<size_t>(tt) * K + s] = static_cast<float>(sc[best]);
+      if (s == 0) atomicAdd(&cnt_top1[best], 1);
+    }
+  }
+  // per-block expert score sums in token order (deterministic aux-loss reduction)
+  if (tid < E) {
+    double s = 0.0;
+    for (int r = 0; r < TT && t0 + r < N; ++r) s += lg[r * E + tid];
+    ssum[static_cast<size_t>(blockIdx.x) * E + tid] = s;
+  }
+}
+
+// l_aux = E * sum_e frac_e * mean_t s[t,e]  with frac from the top-1 choice (moe.py:221-223)
+__global__ void route_finalize_kernel(const double* __restrict__ ssum, int nblocks, const int* __restrict__ cnt_top1,
+                                      int N, int E, double* __restrict__ l_aux) {
+  __shared__ double part[kMaxE];
+  const int e = threadIdx.x;
+  if (e < E) {
+    double s = 0.0;
+    for (int b = 0; b < nblocks; ++b) s += ssum[static_cast<size_t>(b) * E + e];
+    part[e] = s * (static_cast<double>(cnt_top1[e]) / N);
+  }
+  __syncthreads();
+  if (e == 0) {
+    double tot = 0.0, fr = 0.0;
+    for (int j = 0; j < E; ++j) {
+      tot += part[j];
+      fr += static_cast<double>(cnt_top1[j]) / N;
+    }
+    l_aux[0] = tot * (static_cast<double>(E) / N);
+    l_aux[1] = fr;
+  }
+}
+
+// ------------------------------------------------------------------ dispatch plan
+
+struct PlanWs {
+  int* hist;   // [C][K][E] pairs per chunk, slot, expert
+  int* base;   // [C][K][E] exclusive prefix over chunks
+  int* tot;    // [K][E]
+  int* kc;     // [C][E] kept pairs per chunk and expert
+  int* kb;     // [C][E] exclusive prefix over chunks
+  int* kflag;  // [N*K]
+};
+
+static size_t plan_ws_layout(int N, int E, int K, char* base, PlanWs* out) {
+  const size_t C = (static_cast<size_t>(N) + kChunk - 1) / kChunk;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align_up(off + bytes, 256);
+    return o;
+  };
+  size_t o_hist = take(C * K * E * 4), o_base = take(C * K * E * 4), o_tot = take(static_cast<size_t>(K) * E * 4),
+         o_kc = take(C * E * 4), o_kb = take(C * E * 4), o_kf = take(static_cast<size_t>(N) * K * 4);
+  if (out && base) {
+    out->hist = reinterpret_cast<int*>(base + o_hist);
+    out->base = reinterpret_cast<int*>(base + o_base);
+    out->tot = reinterpret_cast<int*>(base + o_tot);
+    out->kc = reinterpret_cast<int*>(base + o_kc);
+    out->kb = reinterpret_cast<int*>(base + o_kb);
+    out->kflag = reinterpret_cast<int*>(base + o_kf);
+  }
+  return off;
+}
+
+__global__ void plan_hist_kernel(const int* __restrict__ idx, int N, int E, int K, int* __restrict__ hist) {
+  extern __shared__ int sh[];  // [K][E]
+  for (int i = threadIdx.x; i < K * E; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  const int t = blockIdx.x * kChunk + threadIdx.x;
+  if (t < N)
+    for (int s = 0; s < K; ++s) atomicAdd(&sh[s * E + idx[static_cast<size_t>(t) * K + s]], 1);
+  __syncthreads();
+  for (int i = threadIdx.x; i < K * E; i += blockDim.x) hist[static_cast<size_t>(blockIdx.x) * K * E + i] = sh[i];
+}
+
+__global__ void plan_totals_kernel(const int* __restrict__ hist, int C, int E, int K, int capacity,
+                                   int* __restrict__ base, int* __restrict__ tot, int* __restrict__ counts) {
+  const int KE = K * E;
+  for (int j = threadIdx.x; j < KE; j += blockDim.x) {
+    int run = 0;
+    for (int c = 0; c < C; ++c) {
+      const int v = hist[static_cast<size_t>(c) * KE + j];
+      base[static_cast<size_t>(c) * KE + j] = run;
+      run += v;
+    }
+    tot[j] = run;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int n = 0;
+    for (int s = 0; s < K; ++s) n += tot[s * E + e];
+    counts[e] = n;
+  }
+}
+
+// Priority rank of every pair: all slot-0 pairs in ascending token id, then slot 1, ...
+// (reduces to _capacity_mask's ascending global token id at K = 1).
+__global__ void plan_keep_kernel(const int* __restrict__ idx, int N, int E, int K, int capacity,
+                                 const int* __restrict__ base, const int* __restrict__ tot, int* __restrict__ kflag,
+                                 int* __restrict__ kc) {
+  extern __shared__ int sh[];
+  int* wc = sh;                        // [8][K][E]
+  int* kcs = wc + 8 * K * E;           // [E]
+  const int c = blockIdx.x;
+  const int t = c * kChunk + threadIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int i = threadIdx.x; i < 8 * K * E; i += blockDim.x) wc[i] = 0;
+  for (int i = threadIdx.x; i < E; i += blockDim.x) kcs[i] = 0;
+  __syncthreads();
+  int ev[kMaxK];
+  int rw[kMaxK];
+  for (int s = 0; s < K; ++s) {
+    ev[s] = t < N ? idx[static_cast<size_t>(t) * K + s] : -1;
+    const unsigned m = __match_any_sync(0xffffffffu, ev[s]);
+    rw[s] = __popc(m & lt);
+    if (ev[s] >= 0 && rw[s] == 0) wc[(warp * K + s) * E + ev[s]] = __popc(m);
+  }
+  __syncthreads();
+  // exclusive prefix over the 8 warps, per (slot, expert)
+  for (int j = threadIdx.x; j < K * E; j += blockDim.x) {
+    int run = 0;
+    for (int wv = 0; wv < 8; ++wv) {
+      const int v = wc[wv * K * E + j];
+      wc[wv * K * E + j] = run;
+      run += v;
+    }
+  }
+  __syncthreads();
+  if (t < N) {
+    for (int s = 0; s < K; ++s) {
+      const int e = ev[s];
+      int prior = 0;
+      for (int s2 = 0; s2 < s; ++s2) prior += tot[s2 * E + e];
+      const long long rank = static_cast<long long>(prior) + base[(static_cast<size_t>(c) * K + s) * E + e] +
+                             wc[(warp * K + s) * E + e] + rw[s];
+      const int keep = rank < capacity ? 1 : 0;
+      kflag[static_cast<size_t>(t) * K + s] = keep;
+      if (keep) atomicAdd(&kcs[e], 1);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < E; i += blockDim.x) kc[static_cast<size_t>(c) * E + i] = kcs[i];
+}
+
+__global__ void plan_offsets_kernel(const int* __restrict__ kc, int C, int E, int* __restrict__ kb,
+                                    int* __restrict__ kept, int* __restrict__ seg, int* __restrict__ tok_sorted,
+                                    float* __restrict__ w_sorted) {
+  __shared__ int sk[kMaxE];
+  __shared__ int sseg[kMaxE + 1];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int run = 0;
+    for (int c = 0; c < C; ++c) {
+      kb[static_cast<size_t>(c) * E + e] = run;
+      run += kc[static_cast<size_t>(c) * E + e];
+    }
+    sk[e] = run;
+    kept[e] = run;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int e = 0; e < E; ++e) {
+      sseg[e] = acc;
+      acc += (sk[e] + 127) / 128 * 128;
+    }
+    sseg[E] = acc;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e <= E; e += blockDim.x) seg[e] = sseg[e];
+  // padding rows of every segment: token -1, weight 0
+  for (int e = 0; e < E; ++e) {
+    const int lo = sseg[e] + sk[e], hi = sseg[e + 1];
+    for (int p = lo + threadIdx.x; p < hi; p += blockDim.x) {
+      tok_sorted[p] = -1;
+      if (w_sorted) w_sorted[p] = 0.f;
+    }
+  }
+}
+
+// Stable scatter: kept pairs of expert e land in ascending token order at
+// seg[e] + (# kept pairs of e with a smaller token id).
+__global__ void plan_scatter_kernel(const int* __restrict__ idx, const float* __restrict__ w, int N, int E, int K,
+                                    const int* __restrict__ kflag, const int* __restrict__ kb,
+                                    const int* __restrict__ seg, int* __restrict__ tok_sorted,
+                                    float* __restrict__ w_sorted, int* __restrict__ pair_pos) {
+  extern __shared__ int sh[];  // [8][E]
+  const int c = blockIdx.x;
+  const int t = c * kChunk + threadIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  int ev[kMaxK], kf[kMaxK], rw[kMaxK];
+  for (int s = 0; s < K; ++s) {
+    ev[s] = t < N ? idx[static_cast<size_t>(t) * K + s] : -1;
+    kf[s] = t < N ? kflag[static_cast<size_t>(t) * K + s] : 0;
+    rw[s] = 0;
+  }
+  for (int e = 0; e < E; ++e) {
+    unsigned mask = 0u;
+    for (int s = 0; s < K; ++s) mask |= __ballot_sync(0xffffffffu, kf[s] && ev[s] == e);
+    for (int s = 0; s < K; ++s)
+      if (kf[s] && ev[s] == e) rw[s] = __popc(mask & lt);
+    if (lane == 0) sh[warp * E + e] = __popc(mask);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int run = 0;
+    for (int wv = 0; wv < 8; ++wv) {
+      const int v = sh[wv * E + e];
+      sh[wv * E + e] = run;
+      run += v;
+    }
+  }
+  __syncthreads();
+  if (t >= N) return;
+  for (int s = 0; s < K; ++s) {
+    const size_t pi = static_cast<size_t>(t) * K + s;
+    if (!kf[s]) {
+      pair_pos[pi] = -1;
+      continue;
+    }
+    const int e = ev[s];
+    const int pos = seg[e] + kb[static_cast<size_t>(c) * E + e] + sh[warp * E + e] + rw[s];
+    tok_sorted[pos] = t;
+    if (w_sorted) w_sorted[pos] = w[pi];
+    pair_pos[pi] = pos;
+  }
+}
+
+}  // namespace ppmoe
+
+using namespace ppmoe;
+
+extern "C" {
+
+size_t ppmoe_route_workspace_bytes(int N, int E, int K) {
+  (void)K;
+  const int TT = route_tokens_per_block(E > 0 ? E : 1);
+  const size_t nb = (static_cast<size_t>(N) + TT - 1) / TT;
+  return align_up(nb * E * 8, 256) + align_up(static_cast<size_t>(E) * 4, 256);
+}
+
+int ppmoe_route(const void* X, int dtype, const float* Wg, int N, int H, int E, int K, const int* route_override,
+                int* idx, float* w, float* scores, double* l_aux, int* counts_top1, void* ws, size_t ws_bytes,
+                void* stream) {
+  PPMOE_REQUIRE(dtype == kBF16 || dtype == kF32, "dtype must be 0 (bf16) or 1 (fp32)");
+  PPMOE_REQUIRE(N >= 1, "aux_loss of zero tokens is undefined (N=%d)", N);
+  PPMOE_REQUIRE(H >= 1 && E >= 1 && E <= kMaxE, "router needs 1 <= E <= %d, got E=%d H=%d", kMaxE, E, H);
+  PPMOE_REQUIRE(K >= 1 && K <= E && K <= kMaxK, "top-k must satisfy 1 <= k <= min(E, %d), got k=%d E=%d", kMaxK, K, E);
+  PPMOE_REQUIRE(ws_bytes >= ppmoe_route_workspace_bytes(N, E, K), "route workspace too small");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int TT = route_tokens_per_block(E);
+  const int nb = (N + TT - 1) / TT;
+  double* ssum = static_cast<double*>(ws);
+  int* cnt = reinterpret_cast<int*>(static_cast<char*>(ws) + align_up(static_cast<size_t>(nb) * E * 8, 256));
+  PPMOE_CUDA(cudaMemsetAsync(cnt, 0, static_cast<size_t>(E) * 4, s));
+  const size_t smem = static_cast<size_t>(TT) * E * 8 + 2 * TT * 8 + static_cast<size_t>(TT) * (kRouteHC + 1) * 4 +
+                      static_cast<size_t>(kRouteHC) * E * 4;
+  if (dtype == kBF16) {
+    PPMOE_CUDA(cudaFuncSetAttribute(router_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem)));
+    router_kernel<__nv_bfloat16><<<nb, kRouteThreads, smem, s>>>(static_cast<const __nv_bfloat16*>(X), Wg, N, H, E, K,
+                                                                 route_override, idx, w, scores, ssum, cnt);
+  } else {
+    PPMOE_CUDA(cudaFuncSetAttribute(router_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem)));
+    router_kernel<float><<<nb, kRouteThreads, smem, s>>>(static_cast<const float*>(X), Wg, N, H, E, K, route_override,
+                                                         idx, w, scores, ssum, cnt);
+  }
+  if (int rc = check_launch("router_kernel")) return rc;
+  route_finalize_kernel<<<1, kMaxE, 0, s>>>(ssum, nb, cnt, N, E, l_aux);
+  if (int rc = check_launch("route_finalize_kernel")) return rc;
+  if (counts_top1) PPMOE_CUDA(cudaMemcpyAsync(counts_top1, cnt, static_cast<size_t>(E) * 4, cudaMemcpyDeviceToDevice, s));
+  return kOk;
+}
+
+size_t ppmoe_dispatch_workspace_bytes(int N, int E, int K) { return plan_ws_layout(N, E, K, nullptr, nullptr); }
+
+int ppmoe_dispatch_plan(const int* idx, const float* w, int N, int E, int K, int capacity, int* counts, int* kept,
+                        int* seg, int* tok_sorted, float* w_sorted, int* pair_pos, int rows_cap_global, void* ws,
+                        size_t ws_bytes, void* stream) {
+  PPMOE_REQUIRE(N >= 0 && E >= 1 && E <= kMaxE, "dispatch plan needs 1 <= E <= %d", kMaxE);
+  PPMOE_REQUIRE(K >= 1 && K <= kMaxK && K <= E, "bad top-k %d", K);
+  PPMOE_REQUIRE(capacity >= 0, "capacity must be non-negative");
+  PPMOE_REQUIRE(static_cast<long long>(rows_cap_global) >= static_cast<long long>(N) * K + 128LL * E,
+                "rows_cap_global too small");
+  PPMOE_REQUIRE(ws_bytes >= plan_ws_layout(N, E, K, nullptr, nullptr), "dispatch workspace too small");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  PlanWs p;
+  plan_ws_layout(N, E, K, static_cast<char*>(ws), &p);
+  const int C = (N + kChunk - 1) / kChunk;
+  if (C == 0) {
+    PPMOE_CUDA(cudaMemsetAsync(counts, 0, E * 4, s));
+    PPMOE_CUDA(cudaMemsetAsync(kept, 0, E * 4, s));
+    PPMOE_CUDA(cudaMemsetAsync(seg, 0, (E + 1) * 4, s));
+    return kOk;
+  }
+  plan_hist_kernel<<<C, kChunk, K * E * 4, s>>>(idx, N, E, K, p.hist);
+  if (int rc = check_launch("plan_hist")) return rc;
+  plan_totals_kernel<<<1, 1024, 0, s>>>(p.hist, C, E, K, capacity, p.base, p.tot, counts);
+  if (int rc = check_launch("plan_totals")) return rc;
+  plan_keep_kernel<<<C, kChunk, (8 * K * E + E) * 4, s>>>(idx, N, E, K, capacity, p.base, p.tot, p.kflag, p.kc);
+  if (int rc = check_launch("plan_keep")) return rc;
+  plan_offsets_kernel<<<1, 1024, 0, s>>>(p.kc, C, E, p.kb, kept, seg, tok_sorted, w_sorted);
+  if (int rc = check_launch("plan_offsets")) return rc;
+  plan_scatter_kernel<<<C, kChunk, 8 * E * 4, s>>>(idx, w, N, E, K, p.kflag, p.kb, seg, tok_sorted, w_sorted,
+                                                   pair_pos);
+  return check_launch("plan_scatter");
+}
+
+}  // extern "C"
