@@ -11,9 +11,8 @@ SRCS      := $(wildcard $(SRC_DIR)/*.cu)
 OBJS      := $(patsubst $(SRC_DIR)/%.cu,$(OBJ_DIR)/%.o,$(SRCS))
 HDRS      := $(wildcard $(SRC_DIR)/*.cuh) $(wildcard $(SRC_DIR)/*.h) include/ppmoe_capi.h
 
-ORACLE_LIB := oracle/_build/liboracle.so
 
-all: $(LIB) $(ORACLE_LIB)
+all: $(LIB)
 
 $(OBJ_DIR)/%.o: $(SRC_DIR)/%.cu $(HDRS)
 	@mkdir -p $(OBJ_DIR)
@@ -22,10 +21,6 @@ $(OBJ_DIR)/%.o: $(SRC_DIR)/%.cu $(HDRS)
 $(LIB): $(OBJS)
 	@mkdir -p $(dir $@)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart
-
-$(ORACLE_LIB): oracle/ppmoe_oracle.c
-	@mkdir -p $(dir $@)
-	gcc -O2 -fPIC -shared -std=c11 -o $@ $< -lm
 
 clean:
 	rm -rf build $(LIB) oracle/_build

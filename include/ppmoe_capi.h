@@ -45,28 +45,32 @@ const char* ppmoe_last_error(void);
 /* Number of SMs of the current device (grid sizing of the persistent kernels). */
 int ppmoe_num_sms(void);
 
-/* Routing: gate GEMV + fp64 softmax + top-k + aux-loss partials ------------
+/* Routing: gate GEMV + fp64 softmax + top-k + aux loss ---------------------
  * Replaces gate_top1 (moe.py:196-208), aux_loss (moe.py:211-223) and the
  * route_override path (moe.py:199-205); top-k > 1 extends the reference
- * (repeated argmax, lowest expert id wins ties, raw softmax weights).
+ * (repeated argmax, lowest expert id wins ties, raw softmax weights, aux-loss
+ * fractions from the top-1 choice).
  *   X        [N x H] dtype
  *   Wg       [H x E] fp32
  *   override [N x K] int32 or NULL; ids already validated to lie in [0, E)
  *   idx      [N x K] int32   out: chosen experts per token (slot-major per token)
  *   w        [N x K] fp32    out: softmax score of each chosen expert
  *   scores   [N x E] fp32    out: full softmax scores
+ *   l_aux    [2] fp64        out: {l_aux, sum_e frac_e (== 1)}
+ *   counts_top1 [E] int32    out: tokens whose slot-0 expert is e (or NULL)
  *   ws       workspace of ppmoe_route_workspace_bytes(N, E, K) bytes
- * The dispatch plan (ppmoe_dispatch_plan) must follow on the same stream: the
- * router leaves per-chunk histograms and score sums in `ws` for it.
  */
 size_t ppmoe_route_workspace_bytes(int N, int E, int K);
 int ppmoe_route(const void* X, int dtype, const float* Wg, int N, int H, int E, int K, const int* route_override,
-                int* idx, float* w, float* scores, void* ws, size_t ws_bytes, void* stream);
+                int* idx, float* w, float* scores, double* l_aux, int* counts_top1, void* ws, size_t ws_bytes,
+                void* stream);
 
 /* Dispatch plan with capacity: replaces build_dispatch_plan (moe.py:226-235)
  * and _capacity_mask (moe.py:345-360).  Stable counting sort of the (token,
  * slot) pairs by expert; capacity keeps the first `capacity` pairs per expert in
  * (slot, token id) priority order (== ascending global token id at K=1).
+ *   idx         [N x K] expert ids in [0, E) (validated by the caller)
+ *   w           [N x K] gate weights or NULL (then w_sorted may be NULL)
  *   capacity    max kept pairs per expert (INT32_MAX = unlimited)
  *   counts      [E]    out: routed pairs per expert before capacity
  *   kept        [E]    out: kept pairs per expert
@@ -74,12 +78,12 @@ int ppmoe_route(const void* X, int dtype, const float* Wg, int N, int H, int E, 
  *   tok_sorted  [rows_cap_global] out: token id per sorted row (-1 = padding)
  *   w_sorted    [rows_cap_global] out: gate weight per sorted row
  *   pair_pos    [N x K] out: sorted row of every pair, -1 if dropped
- *   l_aux       [2] fp64 out: {l_aux, sum of top-1 fractions} (aux_loss, moe.py:211-223)
  *   rows_cap_global >= N*K + 128*E
  */
+size_t ppmoe_dispatch_workspace_bytes(int N, int E, int K);
 int ppmoe_dispatch_plan(const int* idx, const float* w, int N, int E, int K, int capacity, int* counts, int* kept,
-                        int* seg, int* tok_sorted, float* w_sorted, int* pair_pos, double* l_aux,
-                        int rows_cap_global, void* ws, size_t ws_bytes, void* stream);
+                        int* seg, int* tok_sorted, float* w_sorted, int* pair_pos, int rows_cap_global, void* ws,
+                        size_t ws_bytes, void* stream);
 
 /* Index-slice gather ("tensor index slicing"; index_select,
  * tensor.py:226-241): Xs[row] = X[tok_sorted[seg[0]+row]] for the local rows,

@@ -27,8 +27,9 @@ _SIGNATURES = {
     "ppmoe_last_error": (ctypes.c_char_p, []),
     "ppmoe_num_sms": (_I, []),
     "ppmoe_route_workspace_bytes": (_S, [_I, _I, _I]),
-    "ppmoe_route": (_I, [_P, _I, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _S, _P]),
-    "ppmoe_dispatch_plan": (_I, [_P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _I, _P, _S, _P]),
+    "ppmoe_route": (_I, [_P, _I, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _S, _P]),
+    "ppmoe_dispatch_workspace_bytes": (_S, [_I, _I, _I]),
+    "ppmoe_dispatch_plan": (_I, [_P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _I, _P, _S, _P]),
     "ppmoe_gather": (_I, [_P, _I, _I, _I, _P, _I, _P, _P, _I, _P, _P, _P, _P]),
     "ppmoe_expert_fc1_fwd": (_I, [_I, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P]),
     "ppmoe_expert_fc2_fwd": (_I, [_I, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P, _I, _P, _P, _P]),

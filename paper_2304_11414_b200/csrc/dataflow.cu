@@ -1,0 +1,391 @@
+// Token data movement and the small backward kernels of the PPMoE layer:
+//   gather_bulk_kernel   index-slice of replicated hidden rows into the padded
+//                        expert-major buffer, bulk-TMA (cp.async.bulk) staged
+//                        through a shared-memory ring (index_select, tensor.py:226-241;
+//                        the paper's replacement for the all-to-all dispatch).
+//   cast_kernel          fp32 combine accumulator -> output dtype.
+//   bwd_dy_kernel        dY = w * dOut[tok], dw = <dOut[tok], Y>  (scale_rows and
+//                        index_assign backward, tensor.py:190-194, 264-270).
+//   gate_bwd_kernel      dL = s .* (dS - <dS, s>) with dS from dw and the aux loss
+//                        (gather_rowwise / softmax / aux_loss backward,
+//                        tensor.py:218-221, 287-291, moe.py:211-223).
+//   gate_grads_kernel    dX = dx_acc + dL Wg^T and per-chunk X^T dL partials
+//                        (matmul backward of the gate projection, tensor.py:134-138).
+#include "../../include/ppmoe_capi.h"
+#include "common.cuh"
+#include "host.h"
+
+namespace ppmoe {
+
+__host__ __device__ inline size_t align_to(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// ------------------------------------------------------------------ gather
+
+constexpr int kGatherThreads = 128;
+constexpr int kGatherLag = 2;  // store groups allowed in flight before a slot is recycled
+
+template <typename T>
+__global__ void __launch_bounds__(kGatherThreads)
+    gather_bulk_kernel(const T* __restrict__ X, int H, const int* __restrict__ seg, int El,
+                       const int* __restrict__ tok_sorted, const float* __restrict__ w_sorted, T* __restrict__ Xs,
+                       int* __restrict__ tok_local, float* __restrict__ w_local, int R) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  const uint32_t row_bytes = static_cast<uint32_t>(H) * sizeof(T);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm);
+  unsigned char* zero = sm + align_to(static_cast<size_t>(R) * 8, 128);
+  unsigned char* slots = zero + align_to(row_bytes, 128);
+  const int s0 = seg[0];
+  const int rows = seg[El] - s0;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
+    tok_local[r] = tok_sorted[s0 + r];
+    w_local[r] = w_sorted ? w_sorted[s0 + r] : 1.f;
+  }
+  for (uint32_t i = threadIdx.x; i < row_bytes / 16; i += blockDim.x) reinterpret_cast<uint4*>(zero)[i] = make_uint4(0, 0, 0, 0);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < R; ++i) mbar_init(&bars[i], 1);
+    fence_mbar_init();
+  }
+  fence_proxy_async_smem();
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  const int n = rows > static_cast<int>(blockIdx.x) ? (rows - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  auto row_of = [&](int i) { return static_cast<int>(blockIdx.x) + i * static_cast<int>(gridDim.x); };
+  auto issue = [&](int i) {
+    const int slot = i % R;
+    const int tok = tok_sorted[s0 + row_of(i)];
+    if (tok >= 0) {
+      mbar_arrive_expect_tx(&bars[slot], row_bytes);
+      bulk_load(slots + static_cast<size_t>(slot) * row_bytes, X + static_cast<size_t>(tok) * H, row_bytes, &bars[slot]);
+    } else {
+      mbar_arrive(&bars[slot]);
+    }
+  };
+  int issued = 0;
+  for (; issued < n && issued <= R - kGatherLag; ++issued) issue(issued);
+  for (int i = 0; i < n; ++i) {
+    const int slot = i % R;
+    const int tok = tok_sorted[s0 + row_of(i)];
+    mbar_wait(&bars[slot], (i / R) & 1);
+    bulk_store(Xs + static_cast<size_t>(row_of(i)) * H, tok >= 0 ? slots + static_cast<size_t>(slot) * row_bytes : zero,
+               row_bytes);
+    bulk_commit();
+    if (issued < n) {
+      bulk_wait_read<kGatherLag - 1>();  // store of the row that last used this slot has left smem
+      issue(issued++);
+    }
+  }
+  bulk_wait<0>();
+}
+
+// Fallback for rows whose byte size is not a multiple of 16 or too large for the ring.
+template <typename T>
+__global__ void gather_warp_kernel(const T* __restrict__ X, int H, const int* __restrict__ seg, int El,
+                                   const int* __restrict__ tok_sorted, const float* __restrict__ w_sorted,
+                                   T* __restrict__ Xs, int* __restrict__ tok_local, float* __restrict__ w_local) {
+  const int s0 = seg[0];
+  const int rows = seg[El] - s0;
+  const int lane = threadIdx.x & 31;
+  const int wpb = blockDim.x / 32;
+  for (int r = blockIdx.x * wpb + (threadIdx.x >> 5); r < rows; r += gridDim.x * wpb) {
+    const int tok = tok_sorted[s0 + r];
+    if (lane == 0) {
+      tok_local[r] = tok;
+      w_local[r] = w_sorted ? w_sorted[s0 + r] : 1.f;
+    }
+    T* dst = Xs + static_cast<size_t>(r) * H;
+    if (tok >= 0) {
+      const T* src = X + static_cast<size_t>(tok) * H;
+      for (int j = lane; j < H; j += 32) dst[j] = src[j];
+    } else {
+      for (int j = lane; j < H; j += 32) dst[j] = from_f32<T>(0.f);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ casts
+
+template <typename T>
+__global__ void cast_kernel(const float* __restrict__ src, size_t n, T* __restrict__ dst) {
+  const size_t i0 = (static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x * 4;
+  for (size_t i = i0; i < n; i += stride) {
+    if (i + 4 <= n) {
+      float4 v = *reinterpret_cast<const float4*>(src + i);
+      if constexpr (sizeof(T) == 2) {
+        uint2 u;
+        u.x = pack_bf16x2(v.x, v.y);
+        u.y = pack_bf16x2(v.z, v.w);
+        *reinterpret_cast<uint2*>(dst + i) = u;
+      } else {
+        *reinterpret_cast<float4*>(dst + i) = v;
+      }
+    } else {
+      for (size_t j = i; j < n; ++j) dst[j] = from_f32<T>(src[j]);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ dY / dw
+
+template <typename T>
+__global__ void bwd_dy_kernel(const T* __restrict__ dOut, const T* __restrict__ Y, const int* __restrict__ seg, int El,
+                              int H, const int* __restrict__ tok_local, const float* __restrict__ w_local,
+                              int weight_scaling, T* __restrict__ dY, float* __restrict__ dw) {
+  const int rows = seg[El] - seg[0];
+  const int lane = threadIdx.x & 31;
+  const int wpb = blockDim.x / 32;
+  const bool vec = (H % 8 == 0);
+  for (int r = blockIdx.x * wpb + (threadIdx.x >> 5); r < rows; r += gridDim.x * wpb) {
+    const int tok = tok_local[r];
+    T* dy = dY + static_cast<size_t>(r) * H;
+    if (tok < 0) {
+      for (int j = lane; j < H; j += 32) dy[j] = from_f32<T>(0.f);
+      if (lane == 0) dw[r] = 0.f;
+      continue;
+    }
+    const float s = weight_scaling ? w_local[r] : 1.f;
+    const T* g = dOut + static_cast<size_t>(tok) * H;
+    const T* y = Y + static_cast<size_t>(r) * H;
+    float acc = 0.f;
+    if (vec && sizeof(T) == 2) {
+      for (int j = lane * 8; j < H; j += 256) {
+        uint4 gu = *reinterpret_cast<const uint4*>(g + j);
+        uint4 yu = *reinterpret_cast<const uint4*>(y + j);
+        const __nv_bfloat162* gh = reinterpret_cast<const __nv_bfloat162*>(&gu);
+        const __nv_bfloat162* yh = reinterpret_cast<const __nv_bfloat162*>(&yu);
+        uint4 out;
+        uint32_t* o = reinterpret_cast<uint32_t*>(&out);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          float2 gf = __bfloat1622float2(gh[i]);
+          float2 yf = __bfloat1622float2(yh[i]);
+          acc = fmaf(gf.x, yf.x, acc);
+          acc = fmaf(gf.y, yf.y, acc);
+          o[i] = pack_bf16x2(s * gf.x, s * gf.y);
+        }
+        *reinterpret_cast<uint4*>(dy + j) = out;
+      }
+    } else {
+      for (int j = lane; j < H; j += 32) {
+        const float gv = to_f32(g[j]);
+        acc = fmaf(gv, to_f32(y[j]), acc);
+        dy[j] = from_f32<T>(s * gv);
+      }
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) dw[r] = weight_scaling ? acc : 0.f;
+  }
+}
+
+// ------------------------------------------------------------------ gate backward
+
+__global__ void gate_bwd_kernel(const float* __restrict__ scores, const int* __restrict__ idx,
+                                const int* __restrict__ pair_pos, const float* __restrict__ dw, int row_lo,
+                                int row_hi, const int* __restrict__ cnt_top1, int N, int E, int K, float aux_grad,
+                                float* __restrict__ dL) {
+  extern __shared__ float prod[];  // [TT][E] dS*s, then [TT] row sums
+  const int TT = blockDim.x / E;
+  float* red = prod + TT * E;
+  const int tl = threadIdx.x / E, e = threadIdx.x % E;
+  const int t = blockIdx.x * TT + tl;
+  const bool active = tl < TT && t < N;
+  float ds = 0.f, s = 0.f;
+  if (active) {
+    s = scores[static_cast<size_t>(t) * E + e];
+    ds = aux_grad * (static_cast<float>(E) / N) * (static_cast<float>(cnt_top1[e]) / N);
+    for (int k = 0; k < K; ++k) {
+      const size_t pi = static_cast<size_t>(t) * K + k;
+      if (idx[pi] != e) continue;
+      const int pos = pair_pos[pi];
+      if (pos >= row_lo && pos < row_hi) ds += dw[pos - row_lo];
+    }
+  }
+  if (tl < TT) prod[tl * E + e] = ds * s;
+  __syncthreads();
+  if (threadIdx.x < TT) {
+    float acc = 0.f;  // fixed order: deterministic
+    for (int j = 0; j < E; ++j) acc += prod[threadIdx.x * E + j];
+    red[threadIdx.x] = acc;
+  }
+  __syncthreads();
+  if (active) dL[static_cast<size_t>(t) * E + e] = s * (ds - red[tl]);
+}
+
+constexpr int kGradTC = 128;  // tokens per chunk of the dWg partials
+
+template <typename T, int EB>
+__global__ void __launch_bounds__(256)
+    gate_grads_kernel(const float* __restrict__ dx_acc, const T* __restrict__ X, const float* __restrict__ dL,
+                      const float* __restrict__ Wg, int N, int H, int E, T* __restrict__ dX, float* __restrict__ part) {
+  __shared__ float sdl[kGradTC][EB];
+  const int j = blockIdx.x * 256 + threadIdx.x;
+  const int c = blockIdx.y;
+  const int t0 = c * kGradTC;
+  for (int i = threadIdx.x; i < kGradTC * EB; i += 256) {
+    const int tt = i / EB, e = i % EB;
+    const int t = t0 + tt;
+    sdl[tt][e] = (t < N && e < E) ? dL[static_cast<size_t>(t) * E + e] : 0.f;
+  }
+  __syncthreads();
+  if (j >= H) return;
+  float wg[EB], acc[EB];
+#pragma unroll
+  for (int e = 0; e < EB; ++e) {
+    wg[e] = e < E ? Wg[static_cast<size_t>(j) * E + e] : 0.f;
+    acc[e] = 0.f;
+  }
+  const int tn = min(kGradTC, N - t0);
+  for (int tt = 0; tt < tn; ++tt) {
+    const size_t o = static_cast<size_t>(t0 + tt) * H + j;
+    if (dX) {
+      float v = dx_acc ? dx_acc[o] : 0.f;
+#pragma unroll
+      for (int e = 0; e < EB; ++e) v = fmaf(sdl[tt][e], wg[e], v);
+      dX[o] = from_f32<T>(v);
+    }
+    if (part) {
+      const float x = to_f32(X[o]);
+#pragma unroll
+      for (int e = 0; e < EB; ++e) acc[e] = fmaf(x, sdl[tt][e], acc[e]);
+    }
+  }
+  if (part) {
+    float* p = part + (static_cast<size_t>(c) * H + j) * E;
+#pragma unroll
+    for (int e = 0; e < EB; ++e)
+      if (e < E) p[e] = acc[e];
+  }
+}
+
+__global__ void dwg_reduce_kernel(const float* __restrict__ part, int C, int HE, float* __restrict__ dWg) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= HE) return;
+  float s = 0.f;
+  for (int c = 0; c < C; ++c) s += part[static_cast<size_t>(c) * HE + i];
+  dWg[i] = s;
+}
+
+}  // namespace ppmoe
+
+using namespace ppmoe;
+
+extern "C" {
+
+int ppmoe_gather(const void* X, int dtype, int N, int H, const int* seg, int El, const int* tok_sorted,
+                 const float* w_sorted, int rows_cap, void* Xs, int* tok_local, float* w_local, void* stream) {
+  PPMOE_REQUIRE(dtype == kBF16 || dtype == kF32, "bad dtype");
+  PPMOE_REQUIRE(N >= 0 && H >= 1 && El >= 1, "bad gather shape");
+  (void)N;
+  if (rows_cap == 0) return kOk;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t esz = dtype == kBF16 ? 2 : 4;
+  const size_t row_bytes = static_cast<size_t>(H) * esz;
+  const size_t budget = 200 * 1024;
+  int R = static_cast<int>((budget - align_to(row_bytes, 128) - 512) / row_bytes);
+  if (R > 32) R = 32;
+  const int grid = num_sms();
+  if (row_bytes % 16 == 0 && R >= kGatherLag + 2) {
+    const size_t smem = align_to(static_cast<size_t>(R) * 8, 128) + align_to(row_bytes, 128) + R * row_bytes;
+    if (dtype == kBF16) {
+      auto k = gather_bulk_kernel<__nv_bfloat16>;
+      PPMOE_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      k<<<grid, kGatherThreads, smem, s>>>(static_cast<const __nv_bfloat16*>(X), H, seg, El, tok_sorted, w_sorted,
+                                           static_cast<__nv_bfloat16*>(Xs), tok_local, w_local, R);
+    } else {
+      auto k = gather_bulk_kernel<float>;
+      PPMOE_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      k<<<grid, kGatherThreads, smem, s>>>(static_cast<const float*>(X), H, seg, El, tok_sorted, w_sorted,
+                                           static_cast<float*>(Xs), tok_local, w_local, R);
+    }
+    return check_launch("gather_bulk_kernel");
+  }
+  if (dtype == kBF16)
+    gather_warp_kernel<__nv_bfloat16><<<grid * 4, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(X), H, seg, El,
+                                                               tok_sorted, w_sorted, static_cast<__nv_bfloat16*>(Xs),
+                                                               tok_local, w_local);
+  else
+    gather_warp_kernel<float><<<grid * 4, 256, 0, s>>>(static_cast<const float*>(X), H, seg, El, tok_sorted, w_sorted,
+                                                       static_cast<float*>(Xs), tok_local, w_local);
+  return check_launch("gather_warp_kernel");
+}
+
+int ppmoe_cast_out(const float* acc, int n, void* out, int dtype, void* stream) {
+  PPMOE_REQUIRE(dtype == kBF16 || dtype == kF32, "bad dtype");
+  if (n <= 0) return kOk;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int grid = num_sms() * 4;
+  if (dtype == kBF16) cast_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(acc, n, static_cast<__nv_bfloat16*>(out));
+  else cast_kernel<float><<<grid, 256, 0, s>>>(acc, n, static_cast<float*>(out));
+  return check_launch("cast_kernel");
+}
+
+int ppmoe_bwd_dy(int dtype, const void* dOut, const void* Y, const int* seg, int El, int H, int rows_cap,
+                 const int* tok_local, const float* w_local, int weight_scaling, void* dY, float* dw, void* stream) {
+  PPMOE_REQUIRE(dtype == kBF16 || dtype == kF32, "bad dtype");
+  if (rows_cap == 0) return kOk;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int grid = num_sms() * 8;
+  if (dtype == kBF16)
+    bwd_dy_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(dOut),
+                                                      static_cast<const __nv_bfloat16*>(Y), seg, El, H, tok_local,
+                                                      w_local, weight_scaling, static_cast<__nv_bfloat16*>(dY), dw);
+  else
+    bwd_dy_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(dOut), static_cast<const float*>(Y), seg, El, H,
+                                              tok_local, w_local, weight_scaling, static_cast<float*>(dY), dw);
+  return check_launch("bwd_dy_kernel");
+}
+
+int ppmoe_gate_bwd(const float* scores, const int* idx, const int* pair_pos, const float* dw, int row_lo, int row_hi,
+                   const int* counts_top1, int N, int E, int K, float aux_grad, float* dL, void* stream) {
+  PPMOE_REQUIRE(N >= 1 && E >= 1 && E <= 256 && K >= 1 && K <= E, "bad gate backward shape N=%d E=%d K=%d", N, E, K);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int TT = 256 / E;
+  if (TT < 1) TT = 1;
+  const int threads = TT * E;
+  const int grid = (N + TT - 1) / TT;
+  gate_bwd_kernel<<<grid, threads, (TT * E + TT) * 4, s>>>(scores, idx, pair_pos, dw, row_lo, row_hi, counts_top1, N, E, K,
+                                               aux_grad, dL);
+  return check_launch("gate_bwd_kernel");
+}
+
+size_t ppmoe_gate_grad_workspace_bytes(int N, int H, int E) {
+  const size_t C = (static_cast<size_t>(N) + kGradTC - 1) / kGradTC;
+  return C * H * E * 4;
+}
+
+int ppmoe_gate_grads(const float* dx_acc, const void* X, int dtype, const float* dL, const float* Wg, int N, int H,
+                     int E, void* dX, float* dWg, void* ws, size_t ws_bytes, void* stream) {
+  PPMOE_REQUIRE(dtype == kBF16 || dtype == kF32, "bad dtype");
+  PPMOE_REQUIRE(N >= 1 && H >= 1 && E >= 1 && E <= 64, "gate gradients support 1 <= E <= 64, got E=%d", E);
+  PPMOE_REQUIRE(!dWg || ws_bytes >= ppmoe_gate_grad_workspace_bytes(N, H, E), "gate-grad workspace too small");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int C = (N + kGradTC - 1) / kGradTC;
+  dim3 grid((H + 255) / 256, C);
+  float* part = dWg ? static_cast<float*>(ws) : nullptr;
+#define PPMOE_GG(T, EB)                                                                                            \
+  gate_grads_kernel<T, EB><<<grid, 256, 0, s>>>(dx_acc, static_cast<const T*>(X), dL, Wg, N, H, E, static_cast<T*>(dX), \
+                                                part)
+  if (dtype == kBF16) {
+    using T = __nv_bfloat16;
+    if (E <= 8) PPMOE_GG(T, 8);
+    else if (E <= 16) PPMOE_GG(T, 16);
+    else if (E <= 32) PPMOE_GG(T, 32);
+    else PPMOE_GG(T, 64);
+  } else {
+    using T = float;
+    if (E <= 8) PPMOE_GG(T, 8);
+    else if (E <= 16) PPMOE_GG(T, 16);
+    else if (E <= 32) PPMOE_GG(T, 32);
+    else PPMOE_GG(T, 64);
+  }
+#undef PPMOE_GG
+  if (int rc = check_launch("gate_grads_kernel")) return rc;
+  if (dWg) {
+    const int HE = H * E;
+    dwg_reduce_kernel<<<(HE + 255) / 256, 256, 0, s>>>(part, C, HE, dWg);
+    return check_launch("dwg_reduce_kernel");
+  }
+  return kOk;
+}
+
+}  // extern "C"

@@ -127,7 +127,6 @@ __global__ void __launch_bounds__(kRouteThreads) router_kernel(const T* __restri
   const int t = t0 + tl;
   if (active) {
     const double sc = exp(lg[tl * E + e] - stat[2 * tl]) / stat[2 * tl + 1];
-    __syncwarp(__activemask());
     lg[tl * E + e] = sc;
     if (t < N) scores[static_cast<size_t>(t) * E + e] = static_cast<float>(sc);
   }
