@@ -1,0 +1,368 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 PPMoE MoE layer: tokens/s of one layer forward + backward.
+
+Workload (BASELINE.json configs[1], "C2"): hidden 4096, ffn 16384, 8 experts, top-2,
+16384 tokens, bf16 activations/expert weights, fp32 gate.  With --gpus N (under
+torchrun, one process per GPU) the N GPUs form one tensor-parallel group (TP=N):
+every rank routes the replicated tokens, runs its E/N experts and the group
+all-reduces the output (forward) and the input gradient (backward) over NCCL;
+the gate-weight gradient is all-reduced once per step (= one global batch).
+Total work is fixed as N grows ("scaling": "strong").
+
+One step = route + dispatch plan + gather + expert fc1/fc2 (+combine) + all-reduce,
+then the full backward (all parameter and input gradients) + the dX all-reduce +
+the gate-gradient all-reduce.
+
+    python bench.py [--gpus N --steps K --warmup W]             # our CUDA path
+    python bench.py --impl reference [--steps K --warmup W]     # CPU reference path (oracle port)
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "MoE-layer tokens/sec (fwd+bwd) at 1/2/4/8 B200; % of HBM/tensor roofline"
+UNIT = "tokens/s"
+C2 = {"hidden": 4096, "ffn": 16384, "experts": 8, "top_k": 2, "tokens": 16384}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--tokens", type=int, default=C2["tokens"])
+    ap.add_argument("--hidden", type=int, default=C2["hidden"])
+    ap.add_argument("--experts", type=int, default=C2["experts"])
+    ap.add_argument("--top-k", type=int, default=C2["top_k"])
+    ap.add_argument("--capacity-factor", type=float, default=math.inf)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU time of the cpu_baseline sample")
+    return ap.parse_args()
+
+
+def config_of(a, n_gpus):
+    return {
+        "workload": f"C2 PPMoE layer h={a.hidden} ffn={4 * a.hidden} E={a.experts} top-{a.top_k} "
+                    f"N={a.tokens} bf16, TP={n_gpus}",
+        "hidden": a.hidden, "ffn": 4 * a.hidden, "experts": a.experts, "top_k": a.top_k, "tokens": a.tokens,
+        "capacity_factor": "inf" if math.isinf(a.capacity_factor) else a.capacity_factor,
+        "tp": n_gpus, "parallelism": f"tp{n_gpus} (experts {a.experts // n_gpus}/GPU)",
+        "l2": "per-step working set (weights 2.1 GB + activations) >> 126 MB L2; no flush needed",
+    }
+
+
+# ----------------------------------------------------------------------------- clocks
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        return False
+
+    def summary(self):
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- CPU baseline
+
+
+def cpu_baseline(hidden, experts, top_k, ffn, weights_np=None, target_s=12.0, max_tokens=4096):
+    """Time the CPU oracle port (numpy fp64, all host BLAS threads) on a bounded token
+    sample of the same layer shape.  Test infrastructure; never on the product path."""
+    import numpy as np
+
+    from oracle import ppmoe_oracle as O
+
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max((i.get("num_threads", 1) for i in threadpool_info()), default=os.cpu_count())
+    except Exception:  # pragma: no cover
+        threads = os.cpu_count()
+    if weights_np is None:
+        import torch
+        g = torch.Generator().manual_seed(0)
+        sc = hidden ** -0.5
+
+        def rnd(*s):
+            return (torch.randn(*s, generator=g) * sc).to(torch.bfloat16).double().numpy()
+
+        weights_np = O.OracleLayer(rnd(hidden, experts), [rnd(hidden, ffn) for _ in range(experts)],
+                                   [rnd(ffn, hidden) for _ in range(experts)], [rnd(ffn) for _ in range(experts)],
+                                   [rnd(hidden) for _ in range(experts)])
+    rng = np.random.default_rng(1)
+
+    def run(n):
+        x = rng.standard_normal((n, hidden))
+        t0 = time.perf_counter()
+        O.ppmoe_layer(x, weights_np, k=top_k)
+        return time.perf_counter() - t0
+
+    n = 128
+    t = run(n)
+    n2 = int(min(max_tokens, max(n, n * target_s / max(t, 1e-3))))
+    n2 = max(64, n2 // 64 * 64)
+    t2 = run(n2)
+    return {"value": n2 / t2, "unit": UNIT, "cores": int(threads), "kind": "port",
+            "sample": f"{n2} tokens of the same layer (h={hidden}, ffn={ffn}, E={experts}, top-{top_k}), "
+                      f"one fwd+bwd of oracle/ppmoe_oracle.py (numpy fp64 closed form of moesim ppmoe_forward + "
+                      f"tensor.backward), {t2:.1f} s; host os.cpu_count()={os.cpu_count()}"}, weights_np
+
+
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    hidden, experts, top_k = a.hidden, a.experts, a.top_k
+    ffn = 4 * hidden
+    steps, warmup = a.steps, a.warmup
+    cb, weights = cpu_baseline(hidden, experts, top_k, ffn, target_s=min(a.cpu_seconds, 8.0), max_tokens=2048)
+    n = int(cb["sample"].split()[0])
+    import numpy as np
+
+    from oracle import ppmoe_oracle as O
+    rng = np.random.default_rng(2)
+    times = []
+    for i in range(warmup + steps):
+        x = rng.standard_normal((n, hidden))
+        t0 = time.perf_counter()
+        O.ppmoe_layer(x, weights, k=top_k)
+        dt = time.perf_counter() - t0
+        if i >= warmup:
+            times.append(dt)
+    t = sum(times)
+    value = n * steps / t
+    cb = dict(cb)
+    cb["value"] = value
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus, "steps": steps, "warmup": warmup,
+            "ms_per_step": 1e3 * t / steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic", "impl": "reference", "config": config_of(a, a.gpus),
+            "cpu_baseline": cb, "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- GPU path
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        return run_reference(a)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2304_11414_b200 as P
+    from paper_2304_11414_b200 import _lib, _ops
+
+    world_size = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world_size != a.gpus:
+        if world_size == 1 and a.gpus > 1:
+            print(f"--gpus {a.gpus} needs torchrun with {a.gpus} processes", file=sys.stderr)
+            return 2
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    distributed = world_size > 1
+    if distributed:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=dev)
+    tp = world_size
+    h, E, k, n = a.hidden, a.experts, a.top_k, a.tokens
+    f = 4 * h
+    if E % tp:
+        raise SystemExit(f"experts {E} must divide over {tp} GPUs")
+    world = P.World(1, tp, distributed=distributed)
+    group = P.ProcessGroup(P.EP, tuple(range(tp)))
+    el = E // tp
+    block = range(rank * el, (rank + 1) * el)
+    w = P.MoeLayerWeights.random(h, E, seed=0, dtype=torch.bfloat16, device=dev, experts=block)
+    experts_by_rank = [w.bank if r == rank else None for r in range(tp)] if distributed else [w.bank]
+    if not distributed:
+        group = P.ProcessGroup(P.EP, (0,))
+    gen = torch.Generator(device=dev).manual_seed(1234)  # same hidden on every rank (replicated activation)
+    x = torch.randn(n, h, device=dev, generator=gen).to(torch.bfloat16).requires_grad_()
+    g_out = torch.ones(n, h, device=dev, dtype=torch.bfloat16)
+    g_aux = torch.ones((), device=dev, dtype=torch.float32)
+    params = w.leaf_parameters()
+
+    def step(xin):
+        for p in params:
+            p.grad = None
+        xin.grad = None
+        out, l_aux = P.ppmoe_forward(world, group, xin, w.gate, experts_by_rank, top_k=k,
+                                     capacity_factor=a.capacity_factor)
+        torch.autograd.backward([out, l_aux], [g_out, g_aux])
+        P.sync_gate_gradients(world, group, w.gate)
+        return out, l_aux
+
+    def barrier():
+        if distributed:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(a.warmup):
+        step(x)
+    barrier()
+
+    lib = _lib.load()
+    launches0 = lib.ppmoe_kernel_launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk, _ops.KernelProfile() as prof:
+        barrier()
+        ev0.record()
+        for _ in range(a.steps):
+            step(x)
+        ev1.record()
+        barrier()
+    launches = lib.ppmoe_kernel_launches() - launches0
+    ms = ev0.elapsed_time(ev1) / a.steps
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if distributed:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t)
+    value = n / (ms / 1e3)
+    ksum = prof.summary()
+
+    # ---- roofline of the dominant kernel: the grouped expert GEMM (six launches per step)
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    peak = peaks.get("bf16_tflops_sustained", 1400.0)
+    peak_src = "MEASURED_PEAKS.json bf16_tflops_sustained" if "bf16_tflops_sustained" in peaks else "fallback 1.4 PF/s"
+    gemm_names = ["ppmoe_expert_fc1_fwd", "ppmoe_expert_fc2_fwd", "ppmoe_expert_fc2_dgrad", "ppmoe_expert_fc2_wgrad",
+                  "ppmoe_expert_fc1_dgrad", "ppmoe_expert_fc1_wgrad"]
+    pairs = n * k  # kept pairs (no capacity drops at cf=inf); per rank P/tp under balance
+    flop_per_gemm = 2.0 * pairs * h * f / tp
+    gemm_ms = sum(ksum.get(nm, {}).get("ms", 0.0) for nm in gemm_names) / a.steps
+    gemm_launches = sum(ksum.get(nm, {}).get("launches", 0) for nm in gemm_names) / a.steps
+    achieved = 6 * flop_per_gemm / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
+    traffic = None
+    tfile = ROOT / "profiles" / "ncu_traffic.json"
+    if tfile.exists():
+        try:
+            traffic = json.loads(tfile.read_text()).get("grouped_gemm_sm100_bytes_per_launch")
+        except Exception:
+            traffic = None
+    per_kernel = {nm: {"ms_per_step": round(v["ms"] / a.steps, 4), "launches_per_step": v["launches"] / a.steps}
+                  for nm, v in sorted(ksum.items())}
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                "kernel": "grouped_gemm_sm100 (6 launches/step: fc1/fc2 fwd, dgrad, wgrad)",
+                "algorithmic": f"12*P*h*f/TP flop per step, P={pairs} pairs; {gemm_ms:.3f} ms of GEMM per step",
+                "peak_source": peak_src, "gemm_share_of_step": gemm_ms / ms if ms else None}
+
+    # ---- end to end: host (pinned) input -> device -> fwd+bwd -> loss back to host
+    e2e = None
+    if not a.no_e2e:
+        x_host = torch.randn(n, h, generator=torch.Generator().manual_seed(1234)).to(torch.bfloat16).pin_memory()
+        x_dev = torch.empty(n, h, device=dev, dtype=torch.bfloat16)
+        loss_host = torch.empty(1, dtype=torch.float32).pin_memory()
+
+        def e2e_step():
+            x_dev.copy_(x_host, non_blocking=True)
+            xin = x_dev.detach().requires_grad_()
+            out, l_aux = step(xin)
+            loss = out.float().sum() + l_aux
+            loss_host.copy_(loss.reshape(1), non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            return float(loss_host[0])
+
+        for _ in range(2):
+            e2e_step()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(a.steps):
+            e2e_step()
+        e1.record()
+        barrier()
+        ems = e0.elapsed_time(e1) / a.steps
+        te = torch.tensor([ems], device=dev, dtype=torch.float64)
+        if distributed:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": n / (float(te) / 1e3), "unit": UNIT, "h2d_bytes_per_step": n * h * 2, "d2h_bytes_per_step": 4,
+               "ms_per_step": float(te), "path": "paper_2304_11414_b200.ppmoe_forward + backward (C-ABI) from pinned host"}
+
+    cb = None
+    if rank == 0 and world_size == 1 and not a.no_cpu_baseline:
+        cb, _ = cpu_baseline(h, E, k, f, target_s=a.cpu_seconds)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world_size, "steps": a.steps,
+                "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights of the C2 layer, N(0,1) tokens)",
+                "config": config_of(a, world_size), "roofline": roofline, "cpu_baseline": cb, "e2e": e2e,
+                "gpu_launches": int(launches), "clocks": clk.summary(), "kernels": per_kernel,
+                "gemm_launches_per_step": gemm_launches}
+        print(json.dumps(line), flush=True)
+    if distributed:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

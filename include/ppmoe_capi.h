@@ -44,6 +44,8 @@ int ppmoe_version(void);
 const char* ppmoe_last_error(void);
 /* Number of SMs of the current device (grid sizing of the persistent kernels). */
 int ppmoe_num_sms(void);
+/* Diagnostic counter: kernels this library has launched in this process (all threads). */
+unsigned long long ppmoe_kernel_launches(void);
 
 /* Routing: gate GEMV + fp64 softmax + top-k + aux loss ---------------------
  * Replaces gate_top1 (moe.py:196-208), aux_loss (moe.py:211-223) and the
@@ -132,10 +134,11 @@ int ppmoe_expert_fc1_wgrad(int dtype, const void* Xs, const void* dH, const int*
 
 /* Gate backward (gather_rowwise, softmax and aux_loss backward, tensor.py:218-221,
  * 287-291, moe.py:211-223): dL[t,e] = s*(dS - sum(dS*s)) with
- * dS[t, idx[t,k]] += dw[pair] for pairs in sorted rows [row_lo, row_hi) and
- * dS[t,e] += aux_grad * E/N * frac_e (pass aux_grad = 0 on all but one rank). */
-int ppmoe_gate_bwd(const float* scores, const int* idx, const int* pair_pos, const float* dw, int row_lo,
-                   int row_hi, const int* counts_top1, int N, int E, int K, float aux_grad, float* dL, void* stream);
+ * dS[t, idx[t,k]] += dw[pair] for pairs in sorted rows [seg[0], seg[El]) and
+ * dS[t,e] += aux_grad[0] * E/N * frac_e; aux_grad is a device scalar (the upstream
+ * gradient of l_aux) or NULL — pass it on exactly one rank of the TP group.   */
+int ppmoe_gate_bwd(const float* scores, const int* idx, const int* pair_pos, const float* dw, const int* seg, int El,
+                   const int* counts_top1, int N, int E, int K, const float* aux_grad, float* dL, void* stream);
 
 /* dX = dx_acc + dL*Wg^T (cast to dtype) and the per-chunk partials of
  * dWg = X^T*dL, reduced deterministically into dWg [H x E] fp32.  Either of

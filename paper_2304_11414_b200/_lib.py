@@ -26,6 +26,7 @@ _SIGNATURES = {
     "ppmoe_version": (_I, []),
     "ppmoe_last_error": (ctypes.c_char_p, []),
     "ppmoe_num_sms": (_I, []),
+    "ppmoe_kernel_launches": (ctypes.c_ulonglong, []),
     "ppmoe_route_workspace_bytes": (_S, [_I, _I, _I]),
     "ppmoe_route": (_I, [_P, _I, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _S, _P]),
     "ppmoe_dispatch_workspace_bytes": (_S, [_I, _I, _I]),
@@ -39,7 +40,7 @@ _SIGNATURES = {
     "ppmoe_expert_fc2_wgrad": (_I, [_I, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P]),
     "ppmoe_expert_fc1_dgrad": (_I, [_I, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P]),
     "ppmoe_expert_fc1_wgrad": (_I, [_I, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P]),
-    "ppmoe_gate_bwd": (_I, [_P, _P, _P, _P, _I, _I, _P, _I, _I, _I, _F, _P, _P]),
+    "ppmoe_gate_bwd": (_I, [_P, _P, _P, _P, _P, _I, _P, _I, _I, _I, _P, _P, _P]),
     "ppmoe_gate_grad_workspace_bytes": (_S, [_I, _I, _I]),
     "ppmoe_gate_grads": (_I, [_P, _P, _I, _P, _P, _I, _I, _I, _P, _P, _P, _S, _P]),
     "ppmoe_gemm_selftest": (_I, [_I, _I, _I, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P]),

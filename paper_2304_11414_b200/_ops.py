@@ -1,0 +1,251 @@
+"""Orchestration of the sm_100a kernels for one PPMoE layer step (forward + backward).
+
+Every device computation below goes through the C-ABI library (``_lib``); torch
+only allocates buffers, provides the stream and runs NCCL collectives.  There is
+no host synchronisation between routing and the expert GEMMs: the dispatch plan
+stays on the device (padded segments) and the GEMM tile schedulers read it.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from ._lib import ptr
+
+INT32_MAX = 2**31 - 1
+_DTYPE_CODE = {torch.bfloat16: 0, torch.float32: 1}
+
+
+def dtype_code(dt: torch.dtype) -> int:
+    try:
+        return _DTYPE_CODE[dt]
+    except KeyError:
+        raise ValueError(f"PPMoE kernels support bf16 and fp32 activations, got {dt}") from None
+
+
+def _ws(nbytes: int, device) -> torch.Tensor:
+    return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
+
+
+def _stream():
+    return _lib.stream_ptr()
+
+
+class KernelProfile:
+    """Per-entry-point CUDA-event timing of the C-ABI calls made inside the block
+    (events on the launching stream; used by bench.py for the roofline numbers)."""
+
+    def __init__(self):
+        self.records = []
+
+    def __enter__(self):
+        global _PROFILE
+        _PROFILE = self
+        return self
+
+    def __exit__(self, *exc):
+        global _PROFILE
+        _PROFILE = None
+        return False
+
+    def summary(self) -> dict:
+        torch.cuda.synchronize()
+        out: dict = {}
+        for name, a, b in self.records:
+            cell = out.setdefault(name, {"launches": 0, "ms": 0.0})
+            cell["launches"] += 1
+            cell["ms"] += a.elapsed_time(b)
+        return out
+
+
+_PROFILE: KernelProfile | None = None
+
+
+def call(name: str, *args):
+    """C-ABI call; timed with CUDA events when a KernelProfile is active."""
+    prof = _PROFILE
+    if prof is None:
+        return _lib.call(name, *args)
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    rc = _lib.call(name, *args)
+    b.record()
+    prof.records.append((name, a, b))
+    return rc
+
+
+# --------------------------------------------------------------------- routing
+
+
+@dataclass
+class Route:
+    idx: torch.Tensor  # [N, k] int32
+    w: torch.Tensor  # [N, k] fp32
+    scores: torch.Tensor  # [N, E] fp32
+    l_aux: torch.Tensor  # [2] fp64 (value, sum of fractions)
+    top1_counts: torch.Tensor  # [E] int32
+
+
+@dataclass
+class Plan:
+    counts: torch.Tensor  # [E] routed pairs per expert (pre-capacity)
+    kept: torch.Tensor  # [E]
+    seg: torch.Tensor  # [E+1] padded segment starts
+    tok_sorted: torch.Tensor  # [rows_cap_global]
+    w_sorted: torch.Tensor
+    pair_pos: torch.Tensor  # [N, k]
+    capacity: int
+
+
+def route(hidden: torch.Tensor, wg: torch.Tensor, k: int, override: torch.Tensor | None = None) -> Route:
+    """Gate GEMV + softmax + top-k + aux loss (moe.py:196-223) on the device."""
+    n, h = hidden.shape
+    e = wg.shape[1]
+    dev = hidden.device
+    idx = torch.empty((n, k), dtype=torch.int32, device=dev)
+    w = torch.empty((n, k), dtype=torch.float32, device=dev)
+    scores = torch.empty((n, e), dtype=torch.float32, device=dev)
+    l_aux = torch.empty(2, dtype=torch.float64, device=dev)
+    cnt1 = torch.empty(e, dtype=torch.int32, device=dev)
+    lib = _lib.load()
+    ws = _ws(lib.ppmoe_route_workspace_bytes(n, e, k), dev)
+    call("ppmoe_route", ptr(hidden), dtype_code(hidden.dtype), ptr(wg), n, h, e, k, ptr(override), ptr(idx), ptr(w),
+         ptr(scores), ptr(l_aux), ptr(cnt1), ptr(ws), ws.numel(), _stream())
+    return Route(idx, w, scores, l_aux, cnt1)
+
+
+def capacity_for(capacity_factor: float, tokens: int, k: int, num_experts: int) -> int:
+    """C = ceil(cf * k * tokens / E), the k-slot generalisation of moe.py:352."""
+    if math.isinf(capacity_factor):
+        return INT32_MAX
+    return min(INT32_MAX, math.ceil(capacity_factor * k * tokens / num_experts))
+
+
+def plan(idx: torch.Tensor, w: torch.Tensor | None, num_experts: int, capacity: int = INT32_MAX) -> Plan:
+    """Stable per-expert dispatch plan with capacity (moe.py:226-235, 345-360)."""
+    n, k = idx.shape
+    dev = idx.device
+    e = num_experts
+    rows_cap = n * k + 128 * e
+    counts = torch.empty(e, dtype=torch.int32, device=dev)
+    kept = torch.empty(e, dtype=torch.int32, device=dev)
+    seg = torch.empty(e + 1, dtype=torch.int32, device=dev)
+    tok_sorted = torch.empty(rows_cap, dtype=torch.int32, device=dev)
+    w_sorted = torch.empty(rows_cap, dtype=torch.float32, device=dev)
+    pair_pos = torch.empty((n, k), dtype=torch.int32, device=dev)
+    lib = _lib.load()
+    ws = _ws(lib.ppmoe_dispatch_workspace_bytes(n, e, k), dev)
+    call("ppmoe_dispatch_plan", ptr(idx), ptr(w), n, e, k, int(capacity), ptr(counts), ptr(kept), ptr(seg),
+         ptr(tok_sorted), ptr(w_sorted), ptr(pair_pos), rows_cap, ptr(ws), ws.numel(), _stream())
+    return Plan(counts, kept, seg, tok_sorted, w_sorted, pair_pos, capacity)
+
+
+def local_rows_cap(n: int, k: int, el: int, capacity: int) -> int:
+    """Upper bound of the padded rows of `el` experts (no host sync on the true count)."""
+    pairs = min(n * k, n * el)
+    if capacity < INT32_MAX:
+        pairs = min(pairs, capacity * el)
+    return pairs + 128 * el
+
+
+# --------------------------------------------------------------------- experts
+
+
+@dataclass
+class ExpertFwdState:
+    e0: int
+    el: int
+    rows_cap: int
+    seg: torch.Tensor  # view of plan.seg starting at e0 (el+1 entries)
+    xs: torch.Tensor
+    tok_l: torch.Tensor
+    w_l: torch.Tensor
+    hpre: torch.Tensor
+    act: torch.Tensor
+    y: torch.Tensor
+
+
+def experts_forward(hidden, pl: Plan, e0: int, el: int, up, down, bias_up, bias_down, k: int, weight_scaling: bool,
+                    out_acc: torch.Tensor) -> ExpertFwdState:
+    """index-slice gather -> fc1 (+bias, GeLU) -> fc2 (+bias, gate-scaled scatter-add combine)
+    for experts [e0, e0+el) (moe.py:294-305)."""
+    n, h = hidden.shape
+    f = up.shape[2]
+    dt = dtype_code(hidden.dtype)
+    dev = hidden.device
+    rows_cap = local_rows_cap(n, k, el, pl.capacity)
+    seg = pl.seg[e0:e0 + el + 1]
+    xs = torch.empty((rows_cap, h), dtype=hidden.dtype, device=dev)
+    tok_l = torch.empty(rows_cap, dtype=torch.int32, device=dev)
+    w_l = torch.empty(rows_cap, dtype=torch.float32, device=dev)
+    s = _stream()
+    call("ppmoe_gather", ptr(hidden), dt, n, h, ptr(seg), el, ptr(pl.tok_sorted), ptr(pl.w_sorted), rows_cap, ptr(xs),
+         ptr(tok_l), ptr(w_l), s)
+    hpre = torch.empty((rows_cap, f), dtype=hidden.dtype, device=dev)
+    act = torch.empty((rows_cap, f), dtype=hidden.dtype, device=dev)
+    call("ppmoe_expert_fc1_fwd", dt, ptr(xs), ptr(up), ptr(bias_up), ptr(seg), el, h, f, rows_cap, ptr(hpre), ptr(act), s)
+    y = torch.empty((rows_cap, h), dtype=hidden.dtype, device=dev)
+    call("ppmoe_expert_fc2_fwd", dt, ptr(act), ptr(down), ptr(bias_down), ptr(seg), el, h, f, rows_cap, ptr(tok_l),
+         ptr(w_l), int(bool(weight_scaling)), ptr(y), ptr(out_acc), s)
+    return ExpertFwdState(e0, el, rows_cap, seg, xs, tok_l, w_l, hpre, act, y)
+
+
+def experts_backward(grad_out, st: ExpertFwdState, up, down, has_bias: bool, weight_scaling: bool,
+                     dx_acc: torch.Tensor):
+    """Backward of experts [e0, e0+el): returns (dw per local row, dUp, dDown, dBiasUp, dBiasDown)
+    and accumulates the data gradient of the gathered rows into dx_acc."""
+    h = grad_out.shape[1]
+    f = up.shape[2]
+    el, rows_cap = st.el, st.rows_cap
+    dt = dtype_code(grad_out.dtype)
+    dev = grad_out.device
+    s = _stream()
+    dy = torch.empty((rows_cap, h), dtype=grad_out.dtype, device=dev)
+    dw = torch.empty(rows_cap, dtype=torch.float32, device=dev)
+    call("ppmoe_bwd_dy", dt, ptr(grad_out), ptr(st.y), ptr(st.seg), el, h, rows_cap, ptr(st.tok_l), ptr(st.w_l),
+         int(bool(weight_scaling)), ptr(dy), ptr(dw), s)
+    dh = torch.empty((rows_cap, f), dtype=grad_out.dtype, device=dev)
+    call("ppmoe_expert_fc2_dgrad", dt, ptr(dy), ptr(down), ptr(st.hpre), ptr(st.seg), el, h, f, rows_cap, ptr(dh), s)
+    d_down = torch.empty_like(down)
+    d_bd = torch.empty((el, h), dtype=grad_out.dtype, device=dev) if has_bias else None
+    call("ppmoe_expert_fc2_wgrad", dt, ptr(st.act), ptr(dy), ptr(st.seg), el, h, f, rows_cap, ptr(d_down), ptr(d_bd), s)
+    call("ppmoe_expert_fc1_dgrad", dt, ptr(dh), ptr(up), ptr(st.seg), el, h, f, rows_cap, ptr(st.tok_l), ptr(dx_acc), s)
+    d_up = torch.empty_like(up)
+    d_bu = torch.empty((el, f), dtype=grad_out.dtype, device=dev) if has_bias else None
+    call("ppmoe_expert_fc1_wgrad", dt, ptr(st.xs), ptr(dh), ptr(st.seg), el, h, f, rows_cap, ptr(d_up), ptr(d_bu), s)
+    return dw, d_up, d_down, d_bu, d_bd
+
+
+def gate_backward(rt: Route, pl: Plan, st: ExpertFwdState, dw: torch.Tensor, aux_grad: torch.Tensor | None) -> torch.Tensor:
+    """dL = d(loss)/d(logits) from the local pairs' dw and (on one rank) the aux loss."""
+    n, e = rt.scores.shape
+    k = rt.idx.shape[1]
+    dl = torch.empty((n, e), dtype=torch.float32, device=rt.scores.device)
+    call("ppmoe_gate_bwd", ptr(rt.scores), ptr(rt.idx), ptr(pl.pair_pos), ptr(dw), ptr(st.seg), st.el,
+         ptr(rt.top1_counts), n, e, k, ptr(aux_grad), ptr(dl), _stream())
+    return dl
+
+
+def gate_grads(dx_acc, hidden, dl, wg, want_dx: bool, want_dwg: bool):
+    """dX = dx_acc + dL Wg^T (activation dtype) and dWg = X^T dL (fp32)."""
+    n, h = hidden.shape
+    e = wg.shape[1]
+    dev = hidden.device
+    dx = torch.empty_like(hidden) if want_dx else None
+    dwg = torch.empty((h, e), dtype=torch.float32, device=dev) if want_dwg else None
+    lib = _lib.load()
+    ws = _ws(lib.ppmoe_gate_grad_workspace_bytes(n, h, e) if want_dwg else 0, dev)
+    call("ppmoe_gate_grads", ptr(dx_acc), ptr(hidden), dtype_code(hidden.dtype), ptr(dl), ptr(wg), n, h, e, ptr(dx),
+         ptr(dwg), ptr(ws), ws.numel(), _stream())
+    return dx, dwg
+
+
+def cast_out(acc: torch.Tensor, dtype: torch.dtype) -> torch.Tensor:
+    out = torch.empty(acc.shape, dtype=dtype, device=acc.device)
+    call("ppmoe_cast_out", ptr(acc), acc.numel(), ptr(out), dtype_code(dtype), _stream())
+    return out

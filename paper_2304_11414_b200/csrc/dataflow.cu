@@ -180,9 +180,11 @@ __global__ void bwd_dy_kernel(const T* __restrict__ dOut, const T* __restrict__ 
 // ------------------------------------------------------------------ gate backward
 
 __global__ void gate_bwd_kernel(const float* __restrict__ scores, const int* __restrict__ idx,
-                                const int* __restrict__ pair_pos, const float* __restrict__ dw, int row_lo,
-                                int row_hi, const int* __restrict__ cnt_top1, int N, int E, int K, float aux_grad,
-                                float* __restrict__ dL) {
+                                const int* __restrict__ pair_pos, const float* __restrict__ dw,
+                                const int* __restrict__ seg, int El, const int* __restrict__ cnt_top1, int N, int E,
+                                int K, const float* __restrict__ aux_grad_p, float* __restrict__ dL) {
+  const float aux_grad = aux_grad_p ? aux_grad_p[0] : 0.f;
+  const int row_lo = seg[0], row_hi = seg[El];
   extern __shared__ float prod[];  // [TT][E] dS*s, then [TT] row sums
   const int TT = blockDim.x / E;
   float* red = prod + TT * E;
@@ -335,15 +337,15 @@ int ppmoe_bwd_dy(int dtype, const void* dOut, const void* Y, const int* seg, int
   return check_launch("bwd_dy_kernel");
 }
 
-int ppmoe_gate_bwd(const float* scores, const int* idx, const int* pair_pos, const float* dw, int row_lo, int row_hi,
-                   const int* counts_top1, int N, int E, int K, float aux_grad, float* dL, void* stream) {
+int ppmoe_gate_bwd(const float* scores, const int* idx, const int* pair_pos, const float* dw, const int* seg, int El,
+                   const int* counts_top1, int N, int E, int K, const float* aux_grad, float* dL, void* stream) {
   PPMOE_REQUIRE(N >= 1 && E >= 1 && E <= 256 && K >= 1 && K <= E, "bad gate backward shape N=%d E=%d K=%d", N, E, K);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int TT = 256 / E;
   if (TT < 1) TT = 1;
   const int threads = TT * E;
   const int grid = (N + TT - 1) / TT;
-  gate_bwd_kernel<<<grid, threads, (TT * E + TT) * 4, s>>>(scores, idx, pair_pos, dw, row_lo, row_hi, counts_top1, N, E, K,
+  gate_bwd_kernel<<<grid, threads, (TT * E + TT) * 4, s>>>(scores, idx, pair_pos, dw, seg, El, counts_top1, N, E, K,
                                                aux_grad, dL);
   return check_launch("gate_bwd_kernel");
 }

@@ -2,11 +2,14 @@
 // TMA tensor-map encoding through the driver entry point.
 #include "host.h"
 
+#include <atomic>
+
 #include "../../include/ppmoe_capi.h"
 
 namespace ppmoe {
 
 static thread_local std::string g_last_error;
+static std::atomic<unsigned long long> g_launches{0};  // diagnostic: kernels launched by this library
 
 int set_error(int code, const char* fmt, ...) {
   char buf[1024];
@@ -21,6 +24,7 @@ int set_error(int code, const char* fmt, ...) {
 const char* last_error() { return g_last_error.c_str(); }
 
 int check_launch(const char* what) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(kErrCuda, "%s: launch failed: %s", what, cudaGetErrorString(e));
   return kOk;
@@ -89,5 +93,6 @@ extern "C" {
 int ppmoe_version(void) { return 1; }
 const char* ppmoe_last_error(void) { return ppmoe::last_error(); }
 int ppmoe_num_sms(void) { return ppmoe::num_sms(); }
+unsigned long long ppmoe_kernel_launches(void) { return ppmoe::g_launches.load(std::memory_order_relaxed); }
 
 }  // extern "C"

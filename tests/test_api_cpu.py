@@ -1,0 +1,174 @@
+"""Host-side checks that need no GPU: the C-ABI library loads and exports the header's
+symbols, the reference-mirroring API (config, groups, ledger, Rng), and the
+multi-process collective plumbing over gloo."""
+
+import math
+import os
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import paper_2304_11414_b200 as P
+from paper_2304_11414_b200 import _lib
+from oracle import ppmoe_oracle as O
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def header_symbols():
+    text = (ROOT / "include" / "ppmoe_capi.h").read_text()
+    return sorted(set(re.findall(r"^(?:int|size_t|const char\*|unsigned long long)\s+(ppmoe_\w+)\(", text, flags=re.M)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = _lib.load()
+    syms = header_symbols()
+    assert len(syms) >= 18
+    for name in syms:
+        assert hasattr(lib, name), name
+        assert name in _lib.EXPORTED_SYMBOLS, f"{name} has no ctypes signature"
+    assert lib.ppmoe_version() == 1
+
+
+def test_workspace_queries_are_host_only():
+    lib = _lib.load()
+    assert lib.ppmoe_route_workspace_bytes(16384, 8, 2) > 0
+    assert lib.ppmoe_dispatch_workspace_bytes(16384, 8, 2) > 0
+    assert lib.ppmoe_gate_grad_workspace_bytes(16384, 4096, 8) == 128 * 4096 * 8 * 4
+
+
+def test_invalid_arguments_raise_value_error_without_gpu():
+    # argument validation happens before any CUDA call
+    with pytest.raises(ValueError, match="top-k"):
+        _lib.call("ppmoe_route", None, 0, None, 8, 16, 4, 5, None, None, None, None, None, None, None, 0, None)
+    with pytest.raises(ValueError, match="zero tokens"):
+        _lib.call("ppmoe_route", None, 0, None, 0, 16, 4, 1, None, None, None, None, None, None, None, 0, None)
+    with pytest.raises(ValueError, match="divisible by 8"):
+        _lib.call("ppmoe_expert_fc1_fwd", 0, None, None, None, None, 2, 12, 48, 128, None, None, None)
+
+
+def test_layer_config_round_trip():
+    cfg = P.LayerConfig.from_dict({"hidden": 16, "experts": 4, "tp": 2, "capacity_factor": 1.25,
+                                   "weight_scaling": False, "dropout_p": 0.1, "seed": 3})
+    assert cfg.to_dict()["capacity_factor"] == 1.25
+    assert cfg.top_k == 1
+    inf_cfg = P.LayerConfig.from_dict({"hidden": 16, "experts": 4, "tp": 2})
+    assert math.isinf(inf_cfg.capacity_factor)
+    assert inf_cfg.to_dict()["capacity_factor"] == "inf"
+    k2 = P.LayerConfig.from_dict({"hidden": 4096, "experts": 8, "tp": 8, "top_k": 2})
+    assert k2.to_dict()["top_k"] == 2
+
+
+def test_layer_config_rejects_unknown_and_bad_fields():
+    with pytest.raises(ValueError, match="unknown layer config"):
+        P.LayerConfig.from_dict({"hidden": 16, "experts": 4, "tp": 2, "oops": 1})
+    with pytest.raises(ValueError, match="divide over tp"):
+        P.LayerConfig.from_dict({"hidden": 16, "experts": 5, "tp": 2})
+    with pytest.raises(ValueError, match="capacity_factor"):
+        P.LayerConfig.from_dict({"hidden": 16, "experts": 4, "tp": 2, "capacity_factor": 0})
+    with pytest.raises(ValueError, match="top_k"):
+        P.LayerConfig.from_dict({"hidden": 16, "experts": 4, "tp": 2, "top_k": 5})
+
+
+def test_rng_streams_identical_to_reference_philox():
+    r = P.Rng(7, 3)
+    a = r.normal((5, 4), 0.5)
+    b = O.philox(7, 3).normal(0.0, 0.5, size=(5, 4))
+    assert np.array_equal(a, b)
+    assert np.array_equal(P.Rng(1).spawn(10).normal((3,)), O.philox(1, 10).normal(0.0, 1.0, size=(3,)))
+    with pytest.raises(ValueError):
+        P.Rng(-1)
+
+
+def test_process_group_and_world_errors():
+    with pytest.raises(P.ConfigurationError):
+        P.ProcessGroup(P.TP, (1, 0))
+    with pytest.raises(P.ConfigurationError):
+        P.ProcessGroup(P.TP, (0, 0))
+    with pytest.raises(P.ConfigurationError):
+        P.World(0, 8)
+    w = P.World(1, 8)
+    assert not w.distributed
+    with pytest.raises(P.ConfigurationError):
+        P.tp_groups(w, 3, 8)
+    with pytest.raises(P.ConfigurationError):
+        P.tp_groups(w, 4, 6)
+    gs = P.tp_groups(w, 4, 8)
+    assert gs.tp[1].members == (4, 5, 6, 7)
+    assert gs.group_of("EP", 5).members == (4, 5, 6, 7)
+
+
+def test_ledger_ring_bytes_and_gate_sync_ratio():
+    # combine bytes == dense TP FFN bytes == 2(T-1) * N*h*2 (test_moe.py:372-388)
+    tp, n, h, e, micros = 4, 12, 8, 16, 3
+    w = P.World(1, tp)
+    g = P.ProcessGroup(P.EP, tuple(range(tp)))
+    w.charge_all_reduce(g, n * h)
+    assert w.ledger.bytes_for("EP", "all_reduce") == 2 * (tp - 1) * (n * h * 2.0)
+    # gate-sync ratio E / (2 N m) (test_moe.py:391-407) with the forward+backward charges per step
+    w2 = P.World(1, tp)
+    tokens = 500
+    for _ in range(micros):
+        w2.charge_all_reduce(g, tokens * h)
+        w2.charge_all_reduce(g, tokens * h)
+    w2.account_gradient_sync(g, h * e)
+    ratio = w2.ledger.bytes_for("EP", "gradient_sync") / w2.ledger.bytes_for("EP", "all_reduce")
+    assert abs(ratio - e / (2 * tokens * micros)) < 1e-12
+    assert w2.ledger.count_for("EP", "all_reduce") == 2 * micros
+    assert '"EP"' in w2.ledger.to_json()
+
+
+def test_all_reduce_sum_simulated_semantics():
+    w = P.World(1, 2)
+    g = P.ProcessGroup(P.EP, (0, 1))
+    a, b = torch.ones(3), torch.full((3,), 2.0)
+    out = w.all_reduce_sum(g, [a, b])
+    assert len(out) == 2 and torch.equal(out[0], torch.full((3,), 3.0))
+    with pytest.raises(ValueError, match="rank"):
+        w.all_reduce_sum(g, [a, torch.ones(4)])
+
+
+def _gloo_worker(rank, world_size, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world_size)
+    try:
+        world = P.World(1, world_size)
+        assert world.distributed
+        g = P.ProcessGroup(P.EP, tuple(range(world_size)))
+        assert world.rank_in(g) == rank
+        # forward combine: disjoint per-rank partials sum to the dense output
+        part = torch.zeros(4, 3)
+        part[rank::world_size] = rank + 1.0
+        world.all_reduce_(g, part)
+        # gate gradient sync once per global batch (moe.py:311-313)
+        wg = torch.zeros(3, 2, requires_grad=True)
+        wg.grad = torch.full((3, 2), float(rank + 1))
+        P.sync_gate_gradients(world, g, P.GateParams(wg))
+        q.put((rank, part.tolist(), wg.grad.tolist(), world.ledger.count_for("EP", "gradient_sync")))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_distributed_world_gloo_two_ranks():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29500 + os.getpid() % 1000
+    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = dict((r, (part, grad, cnt)) for r, part, grad, cnt in (q.get(timeout=120) for _ in procs))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    expect = [[1.0] * 3, [2.0] * 3, [1.0] * 3, [2.0] * 3]
+    for r in range(2):
+        part, grad, cnt = results[r]
+        assert part == expect
+        assert grad == [[3.0, 3.0]] * 3
+        assert cnt == 1

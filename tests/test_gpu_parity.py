@@ -1,0 +1,257 @@
+"""Parity of the sm_100a CUDA path with the reference (golden vectors) and the CPU oracle.
+
+Every call here goes through the package API -> ctypes -> lib/libppmoe.so.
+Routing indices, counts and per-expert lists must be bit-exact; activations and
+gradients within rtol 2e-2 (bf16) / 1e-4 (fp32) scaled by max|ref|.
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2304_11414_b200 as P
+from golden_util import golden_inputs, load, unpack_lists
+from oracle import ppmoe_oracle as O
+from ppmoe_testlib import TOL, device_weights, oracle_rounded, run_cuda_layer, scaled_err
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN_LAYERS = ["ppmoe_h64_e4_tp2", "ppmoe_h128_e8_tp4", "ppmoe_nobias_noscale", "ppmoe_override", "ppmoe_c1"]
+
+
+@pytest.fixture(autouse=True)
+def _seed():
+    torch.manual_seed(0)
+
+
+# ------------------------------------------------------------------ grouped GEMM self-test
+
+
+def _segments(counts):
+    seg = [0]
+    for c in counts:
+        seg.append(seg[-1] + (c + 127) // 128 * 128)
+    return seg
+
+
+@pytest.mark.parametrize("use_tc", [1, 0])
+@pytest.mark.parametrize("mode,counts,M,N,K", [
+    (0, [128], 0, 256, 64), (0, [100, 300, 0, 5], 0, 512, 256), (0, [700, 64], 0, 768, 448),
+    (2, [128], 0, 256, 64), (2, [200, 33], 0, 512, 320),
+    (1, [128], 128, 256, 0), (1, [250, 0, 77], 256, 512, 0), (1, [513], 384, 320, 0),
+])
+def test_grouped_gemm_selftest(use_tc, mode, counts, M, N, K):
+    from paper_2304_11414_b200 import _lib
+
+    seg = _segments(counts)
+    G, rows = len(counts), seg[-1]
+    segt = torch.tensor(seg, dtype=torch.int32, device="cuda")
+    if mode == 0:
+        A = torch.randn(rows, K, device="cuda").bfloat16()
+        B = torch.randn(G * K, N, device="cuda").bfloat16()
+        D = torch.full((rows, N), float("nan"), device="cuda")
+        ref = torch.cat([A[seg[g]:seg[g + 1]].float() @ B[g * K:(g + 1) * K].float() for g in range(G)])
+    elif mode == 1:
+        A = torch.randn(rows, M, device="cuda").bfloat16()
+        B = torch.randn(rows, N, device="cuda").bfloat16()
+        D = torch.full((G, M, N), float("nan"), device="cuda")
+        ref = torch.stack([A[seg[g]:seg[g + 1]].float().T @ B[seg[g]:seg[g + 1]].float() for g in range(G)])
+    else:
+        A = torch.randn(rows, K, device="cuda").bfloat16()
+        B = torch.randn(G * N, K, device="cuda").bfloat16()
+        D = torch.full((rows, N), float("nan"), device="cuda")
+        ref = torch.cat([A[seg[g]:seg[g + 1]].float() @ B[g * N:(g + 1) * N].float().T for g in range(G)])
+    _lib.call("ppmoe_gemm_selftest", mode, use_tc, 0, _lib.ptr(A), _lib.ptr(B), _lib.ptr(segt), G, M, N, K, rows,
+              _lib.ptr(D), _lib.stream_ptr())
+    torch.cuda.synchronize()
+    assert not torch.isnan(D).any()
+    assert (D - ref).abs().max().item() / ref.abs().max().item() < 1e-5
+
+
+# ------------------------------------------------------------------ routing
+
+
+def test_gate_small_golden_fp32():
+    _, a = load("gate_small")
+    x = torch.tensor(a["hidden"], dtype=torch.float32, device="cuda")
+    gate = P.GateParams(torch.tensor(a["wg"], dtype=torch.float32, device="cuda"))
+    out = P.gate_top1(x, gate)
+    assert out.indices.cpu().numpy().tolist() == a["indices"].tolist()
+    assert np.abs(out.weights.cpu().numpy() - a["weights"]).max() < 1e-6
+    assert np.abs(out.scores.cpu().numpy() - a["scores"]).max() < 1e-6
+    assert abs(float(out.l_aux) - float(a["l_aux"])) < 1e-6
+
+
+def test_gate_tie_breaks_to_lowest_id_and_argmax():
+    gate = P.GateParams(torch.eye(2, device="cuda"))
+    out = P.gate_top1(torch.tensor(np.log([[0.5, 0.5]]), dtype=torch.float32, device="cuda"), gate)
+    assert out.indices.tolist() == [0]
+    gate = P.GateParams(torch.eye(3, device="cuda"))
+    out = P.gate_top1(torch.tensor(np.log([[0.1, 0.7, 0.2]]), dtype=torch.float32, device="cuda"), gate)
+    assert out.indices.tolist() == [1]
+    assert abs(float(out.weights[0]) - 0.7) < 1e-6
+
+
+@pytest.mark.parametrize("n,h,e,k", [(4096, 1024, 8, 1), (4096, 1024, 8, 2), (2048, 512, 16, 2),
+                                     (1000, 256, 5, 3), (16384, 4096, 8, 2)])
+def test_routing_bit_exact_vs_oracle(n, h, e, k):
+    g = torch.Generator(device="cuda").manual_seed(n + e + k)
+    x = torch.randn(n, h, device="cuda", generator=g).bfloat16()
+    wg = (torch.randn(h, e, device="cuda", generator=g) * h ** -0.5).float()
+    out = P.gate_topk(x, P.GateParams(wg), k)
+    ref = O.gate_topk(x.double().cpu().numpy(), wg.double().cpu().numpy(), k)
+    idx = out.indices.cpu().numpy().reshape(n, k)
+    assert np.array_equal(idx, ref.indices), f"{(idx != ref.indices).sum()} routing mismatches"
+    assert np.abs(out.weights.cpu().numpy().reshape(n, k) - ref.weights).max() < 1e-6
+    assert abs(float(out.l_aux) - ref.l_aux) < 1e-5
+
+
+@pytest.mark.parametrize("n,e,k,cap", [(40, 6, 1, None), (1000, 8, 1, 100), (1000, 8, 2, 260), (5000, 5, 2, None),
+                                       (777, 16, 3, 150), (9, 4, 2, 2)])
+def test_dispatch_plan_bit_exact_vs_oracle(n, e, k, cap):
+    rng = np.random.default_rng(n + e)
+    rows = []
+    for t in range(n):  # a third of the tokens pick expert 0 first, so capacity bites
+        if t % 3 == 0:
+            rows.append([0] + (1 + rng.permutation(e - 1))[: k - 1].tolist())
+        else:
+            rows.append(rng.permutation(e)[:k].tolist())
+    idx = np.array(rows)
+    lists, kept, counts = O.dispatch_plan(idx, e, cap)
+    plan = P.build_dispatch_plan(torch.tensor(idx, device="cuda"), e, capacity=cap)
+    assert plan.per_expert == lists
+    assert np.array_equal(plan.kept_mask.cpu().numpy(), kept)
+    assert plan.device_plan.counts.cpu().numpy().tolist() == counts.tolist()
+    seg = plan.device_plan.seg.cpu().numpy()
+    assert (seg % 128 == 0).all() and (np.diff(seg) >= np.array([len(x) for x in lists])).all()
+
+
+def test_dispatch_worked_example_on_device():
+    plan = P.build_dispatch_plan([2, 3, 1, 2, 0, 3, 2, 0], 4)
+    assert plan.per_expert == [[4, 7], [2], [0, 3, 6], [1, 5]]
+
+
+def test_dispatch_out_of_range():
+    with pytest.raises(ValueError, match="expert id 4"):
+        P.build_dispatch_plan([0, 4], 4)
+
+
+# ------------------------------------------------------------------ full layer vs reference goldens
+
+
+def _compare(res, ref_out, ref_dx, ref_grads, dtype, rows=None, name=""):
+    tol = TOL[dtype]
+    out, dx = res["out"], res["grad_hidden"]
+    if rows is not None:
+        out, dx = out[rows], dx[rows]
+    errs = {"out": scaled_err(out, ref_out), "grad_hidden": scaled_err(dx, ref_dx)}
+    for k, g in ref_grads.items():
+        got = res["grads"][k]
+        if got is None:
+            got = np.zeros_like(g)
+        errs[k] = scaled_err(got, g)
+    bad = {k: v for k, v in errs.items() if not v < tol}
+    assert not bad, f"{name}: errors above {tol}: {bad}"
+    return errs
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("name", GOLDEN_LAYERS)
+def test_layer_vs_reference_golden(name, dtype):
+    meta, a = load(name)
+    case = meta["case"]
+    hidden, layer = golden_inputs(case)
+    w = device_weights(layer, dtype)
+    ov = case.get("override")
+    res = run_cuda_layer(hidden, w, tp=case["tp"], weight_scaling=case.get("weight_scaling", True),
+                         route_override=ov, dtype=dtype)
+    grads = {"gate.wg": a["grad_gate.wg"]}
+    grads.update({k[5:]: v for k, v in a.items() if k.startswith("grad_expert")})
+    _compare(res, a["out"], a["grad_hidden"], grads, dtype, rows=a["rows"], name=name)
+    assert abs(res["l_aux"] - float(a["l_aux"])) < 1e-5
+    # per-expert gradient checksums (all cases, incl. the ones without stored grads)
+    for k, (s, sa, sq) in meta["grad_checksums"].items():
+        g = res["grads"][k]
+        assert abs(float(np.abs(g).sum()) - sa) <= TOL[dtype] * sa * 2, k
+    # ledger: forward combine + backward input-gradient all-reduce (test_moe.py:405)
+    assert res["world"].ledger.count_for("EP", "all_reduce") == 2
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("name", ["capacity_cf050", "capacity_cf100_skew"])
+def test_capacity_vs_reference_dpmoe_golden(name, dtype):
+    meta, a = load(name)
+    case = meta["case"]
+    hidden, layer = golden_inputs(case)
+    w = device_weights(layer, dtype)
+    res = run_cuda_layer(hidden, w, capacity_factor=case["capacity_factor"], route_override=case.get("override"),
+                         dtype=dtype)
+    grads = {k[5:]: v for k, v in a.items() if k.startswith("grad_") and k != "grad_hidden"}
+    _compare(res, a["out"], a["grad_hidden"], grads, dtype, name=name)
+    # dropped tokens have exactly zero output rows
+    dropped = np.all(a["out"] == 0, axis=1)
+    assert dropped.any() and np.all(res["out"][dropped] == 0)
+
+
+# ------------------------------------------------------------------ layer vs oracle (extensions, bigger shapes)
+
+
+@pytest.mark.parametrize("dtype,h,e,n,k,tp,cf", [
+    (torch.bfloat16, 256, 8, 1024, 2, 1, math.inf),
+    (torch.bfloat16, 256, 8, 1024, 2, 4, 1.0),
+    (torch.bfloat16, 512, 16, 2048, 2, 8, 1.25),
+    (torch.float32, 128, 4, 512, 2, 2, 0.8),
+    (torch.bfloat16, 1024, 8, 4096, 1, 1, math.inf),
+])
+def test_layer_vs_oracle(dtype, h, e, n, k, tp, cf):
+    layer = O.init_layer(h, e, seed=h + e + n)
+    layer = oracle_rounded(layer, dtype)
+    hidden = torch.randn(n, h, generator=torch.Generator().manual_seed(7)).to(dtype).double().numpy()
+    gout = torch.randn(n, h, generator=torch.Generator().manual_seed(8)).to(dtype).double().numpy()
+    ref = O.ppmoe_layer(hidden, layer, k=k, capacity_factor=cf, grad_out=gout)
+    res = run_cuda_layer(hidden, device_weights(layer, dtype), tp=tp, k=k, capacity_factor=cf, dtype=dtype,
+                         grad_out=gout)
+    _compare(res, ref.out, ref.grad_hidden, ref.grads, dtype, name=f"h{h}e{e}k{k}")
+    assert abs(res["l_aux"] - ref.l_aux) < 1e-5
+
+
+def test_single_expert_reduces_to_dense_ffn():
+    layer = oracle_rounded(O.init_layer(128, 1, seed=53), torch.float32)
+    hidden = np.asarray(torch.randn(96, 128).double())
+    w = device_weights(layer, torch.float32)
+    ex = w.experts[0]
+    got = ex.forward(torch.tensor(hidden, dtype=torch.float32, device="cuda")).double().cpu().numpy()
+    ref = O.gelu(hidden @ layer.up[0] + layer.bias_up[0]) @ layer.down[0] + layer.bias_down[0]
+    assert scaled_err(got, ref) < 1e-5
+
+
+def test_replica_divergence_detected():
+    layer = oracle_rounded(O.init_layer(64, 2, seed=61), torch.bfloat16)
+    w = device_weights(layer, torch.bfloat16)
+    a = torch.randn(4, 64, device="cuda").bfloat16()
+    b = a.clone()
+    b[0, 0] += 1.0
+    with pytest.raises(ValueError, match="TP replica divergence"):
+        P.ppmoe_forward(P.World(1, 2), P.ProcessGroup(P.EP, (0, 1)), [a, b], w.gate, w.shard(2))
+
+
+def test_expert_shard_mismatch_error():
+    layer = oracle_rounded(O.init_layer(64, 4, seed=65), torch.bfloat16)
+    w = device_weights(layer, torch.bfloat16)
+    ex = w.experts
+    with pytest.raises(ValueError, match="spread evenly"):
+        P.ppmoe_forward(P.World(1, 2), P.ProcessGroup(P.EP, (0, 1)), torch.zeros(4, 64, device="cuda").bfloat16(),
+                        w.gate, [ex[:3], ex[3:]])
+
+
+def test_deterministic_bit_identical_runs():
+    layer = oracle_rounded(O.init_layer(256, 8, seed=5), torch.bfloat16)
+    hidden = torch.randn(2048, 256).bfloat16().double().numpy()
+    r1 = run_cuda_layer(hidden, device_weights(layer, torch.bfloat16), k=2)
+    r2 = run_cuda_layer(hidden, device_weights(layer, torch.bfloat16), k=2)
+    assert np.array_equal(r1["out"], r2["out"])
+    assert np.array_equal(r1["grad_hidden"], r2["grad_hidden"])
+    for k in r1["grads"]:
+        assert np.array_equal(r1["grads"][k], r2["grads"][k]), k
