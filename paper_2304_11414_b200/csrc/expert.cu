@@ -49,27 +49,45 @@ static int check_common(int dtype, int El, int H, int F, int rows_cap) {
   return kOk;
 }
 
+// Bias gradients: column sums of a per-expert row segment.  Block = 64 columns x 8 row
+// groups; each warp reads one 128-byte row slice per step; the 8 partial sums are
+// combined in a fixed order (deterministic, no atomics).
 template <typename T>
-__global__ void colsum_kernel(const T* __restrict__ src, int ld, const int* __restrict__ seg, int N, T* __restrict__ out) {
+__global__ void __launch_bounds__(256) colsum_kernel(const T* __restrict__ src, int ld, const int* __restrict__ seg,
+                                                     int N, T* __restrict__ out) {
+  __shared__ float red[8][64];
   const int g = blockIdx.y;
-  const int col = blockIdx.x * blockDim.x + threadIdx.x;
-  if (col >= N) return;
+  const int lane = threadIdx.x & 31, rg = threadIdx.x >> 5;
+  const int col = blockIdx.x * 64 + 2 * lane;
   const int lo = seg[g] - seg[0];
   const int hi = seg[g + 1] - seg[0];
-  float acc[4] = {0.f, 0.f, 0.f, 0.f};
-  int r = lo;
-  for (; r + 4 <= hi; r += 4) {
-#pragma unroll
-    for (int u = 0; u < 4; ++u) acc[u] += to_f32(src[static_cast<size_t>(r + u) * ld + col]);
+  float s0 = 0.f, s1 = 0.f;
+  if (col < N) {
+    const bool pair = col + 1 < N;
+    int r = lo + rg;
+#pragma unroll 4
+    for (; r < hi; r += 8) {
+      const T* p = src + static_cast<size_t>(r) * ld + col;
+      s0 += to_f32(p[0]);
+      if (pair) s1 += to_f32(p[1]);
+    }
   }
-  for (; r < hi; ++r) acc[0] += to_f32(src[static_cast<size_t>(r) * ld + col]);
-  out[static_cast<size_t>(g) * N + col] = from_f32<T>((acc[0] + acc[1]) + (acc[2] + acc[3]));
+  red[rg][2 * lane] = s0;
+  red[rg][2 * lane + 1] = s1;
+  __syncthreads();
+  if (threadIdx.x < 64) {
+    const int c = blockIdx.x * 64 + threadIdx.x;
+    float t = 0.f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) t += red[q][threadIdx.x];
+    if (c < N) out[static_cast<size_t>(g) * N + c] = from_f32<T>(t);
+  }
 }
 
 template <typename T>
 static int colsum(const void* src, int ld, const int* seg, int G, int N, void* out, cudaStream_t s) {
   if (!out) return kOk;
-  dim3 grid((N + 255) / 256, G);
+  dim3 grid((N + 63) / 64, G);
   colsum_kernel<T><<<grid, 256, 0, s>>>(static_cast<const T*>(src), ld, seg, N, static_cast<T*>(out));
   return check_launch("colsum");
 }

@@ -21,100 +21,148 @@
 namespace ppmoe {
 
 constexpr int kRouteThreads = 256;
-constexpr int kRouteHC = 256;   // hidden chunk staged in shared memory
+constexpr int kRouteTB = 64;    // tokens per block
+constexpr int kRouteTPT = 2;    // tokens per thread (each staged Wg value feeds 2 tokens)
+constexpr int kRouteKS = 8;     // hidden-dimension splits per token (threads per token pair)
+constexpr int kRouteHC = 512;   // hidden chunk of Wg staged as fp64 in shared memory
 constexpr int kChunk = 256;     // tokens per plan chunk (one thread per token)
 constexpr int kMaxE = 128;
 constexpr int kMaxK = 8;
 
-__host__ __device__ inline int route_tokens_per_block(int E) {
-  int tt = 1;
-  while (tt * 2 * E <= kRouteThreads && tt * 2 <= 64) tt *= 2;
-  return tt;
-}
-
 static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
+// Exact fp32 -> fp64 widening with integer ops (keeps the conversions off the FP64
+// pipe, which the logit FMAs saturate).  Zero/subnormal/inf/nan take the F2F path.
+__device__ __forceinline__ double f32bits_to_f64(uint32_t b) {
+  const uint32_t ex = (b >> 23) & 0xFFu;
+  if (ex == 0u || ex == 0xFFu) return static_cast<double>(__uint_as_float(b));
+  const unsigned long long bits = (static_cast<unsigned long long>(b >> 31) << 63) |
+                                  (static_cast<unsigned long long>(ex + 896u) << 52) |
+                                  (static_cast<unsigned long long>(b & 0x7FFFFFu) << 29);
+  return __longlong_as_double(static_cast<long long>(bits));
+}
+
 template <typename T>
-__device__ __forceinline__ void load8(const T* p, float* dst);
+__device__ __forceinline__ void load8_f64(const T* p, double* dst);
 template <>
-__device__ __forceinline__ void load8<__nv_bfloat16>(const __nv_bfloat16* p, float* dst) {
-  uint4 u = *reinterpret_cast<const uint4*>(p);
-  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+__device__ __forceinline__ void load8_f64<__nv_bfloat16>(const __nv_bfloat16* p, double* dst) {
+  const uint4 u = *reinterpret_cast<const uint4*>(p);
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    float2 f = __bfloat1622float2(h[i]);
-    dst[2 * i] = f.x;
-    dst[2 * i + 1] = f.y;
+    dst[2 * i] = f32bits_to_f64(w[i] << 16);
+    dst[2 * i + 1] = f32bits_to_f64(w[i] & 0xFFFF0000u);
   }
 }
 template <>
-__device__ __forceinline__ void load8<float>(const float* p, float* dst) {
-  float4 a = *reinterpret_cast<const float4*>(p);
-  float4 b = *reinterpret_cast<const float4*>(p + 4);
-  dst[0] = a.x; dst[1] = a.y; dst[2] = a.z; dst[3] = a.w;
-  dst[4] = b.x; dst[5] = b.y; dst[6] = b.z; dst[7] = b.w;
+__device__ __forceinline__ void load8_f64<float>(const float* p, double* dst) {
+  const uint4 a = *reinterpret_cast<const uint4*>(p);
+  const uint4 b = *reinterpret_cast<const uint4*>(p + 4);
+  dst[0] = f32bits_to_f64(a.x); dst[1] = f32bits_to_f64(a.y); dst[2] = f32bits_to_f64(a.z); dst[3] = f32bits_to_f64(a.w);
+  dst[4] = f32bits_to_f64(b.x); dst[5] = f32bits_to_f64(b.y); dst[6] = f32bits_to_f64(b.z); dst[7] = f32bits_to_f64(b.w);
 }
 
-template <typename T>
+__host__ __device__ inline int route_eb(int E) { return E <= 8 ? 8 : 16; }
+
+__host__ inline size_t route_smem_bytes(int E) {
+  const int EB = route_eb(E);
+  return static_cast<size_t>(kRouteHC) * EB * 8                       // staged Wg chunk (fp64)
+         + static_cast<size_t>(kRouteKS) * kRouteTB * EB * 8         // split-K partials
+         + static_cast<size_t>(kRouteTB) * E * 8 + 2 * kRouteTB * 8;  // logits/scores + softmax stats
+}
+
+// Gate logits X*Wg in fp64 (bf16/fp32 x fp32 products are exact in fp64), softmax,
+// top-k and aux-loss partials.  Block: 64 tokens; thread = (2 tokens, 1 of 8 hidden
+// splits); experts in register passes of EB.  Every lane of a warp reads the same
+// staged Wg value (shared-memory broadcast).
+template <typename T, int EB>
 __global__ void __launch_bounds__(kRouteThreads) router_kernel(const T* __restrict__ X, const float* __restrict__ Wg,
                                                                int N, int H, int E, int K, const int* __restrict__ ovr,
                                                                int* __restrict__ idx, float* __restrict__ w,
                                                                float* __restrict__ scores, double* __restrict__ ssum,
                                                                int* __restrict__ cnt_top1) {
   extern __shared__ __align__(16) unsigned char sm[];
-  const int TT = route_tokens_per_block(E);
-  double* lg = reinterpret_cast<double*>(sm);         // [TT][E] logits, then scores
-  double* stat = lg + TT * E;                         // [TT][2] max, sum
-  float* xs = reinterpret_cast<float*>(stat + 2 * TT);  // [TT][HC+1]
-  float* wsm = xs + TT * (kRouteHC + 1);             // [HC][E]
+  double* wsm = reinterpret_cast<double*>(sm);                 // [HC][EB]
+  double* part = wsm + kRouteHC * EB;                          // [KS][TB][EB]
+  double* lg = part + kRouteKS * kRouteTB * EB;                // [TB][E]
+  double* stat = lg + kRouteTB * E;                            // [TB][2]
   const int tid = threadIdx.x;
-  const int tl = tid / E, e = tid % E;
-  const bool active = tid < TT * E;
-  const int t0 = blockIdx.x * TT;
-  const bool vec = (H % 8) == 0;
+  const int ks = tid >> 5;                  // warp = one hidden split
+  const int tl0 = tid & 31, tl1 = tl0 + 32;  // the thread's two tokens (block-local)
+  const int t0 = blockIdx.x * kRouteTB;
+  const bool ok0 = t0 + tl0 < N, ok1 = t0 + tl1 < N;
+  const bool vec = (H % (8 * kRouteKS)) == 0;
+  const T* x0 = X + static_cast<size_t>(ok0 ? t0 + tl0 : 0) * H;
+  const T* x1 = X + static_cast<size_t>(ok1 ? t0 + tl1 : 0) * H;
 
-  double acc = 0.0;
-  for (int h0 = 0; h0 < H; h0 += kRouteHC) {
-    const int hc = min(kRouteHC, H - h0);
-    if (vec) {
-      const int nv = hc / 8;
-      for (int i = tid; i < TT * nv; i += blockDim.x) {
-        const int r = i / nv, c = (i % nv) * 8;
-        const int t = t0 + r;
-        float tmp[8];
-        if (t < N) load8<T>(X + static_cast<size_t>(t) * H + h0 + c, tmp);
-        else
+  for (int e0 = 0; e0 < E; e0 += EB) {
+    double a0[EB], a1[EB];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) tmp[j] = 0.f;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) xs[r * (kRouteHC + 1) + c + j] = tmp[j];
+    for (int j = 0; j < EB; ++j) a0[j] = a1[j] = 0.0;
+    for (int h0 = 0; h0 < H; h0 += kRouteHC) {
+      const int hc = min(kRouteHC, H - h0);
+      __syncthreads();
+      for (int i = tid; i < hc * EB; i += kRouteThreads) {
+        const int c = i / EB, j = i % EB;
+        wsm[i] = e0 + j < E ? static_cast<double>(Wg[static_cast<size_t>(h0 + c) * E + e0 + j]) : 0.0;
       }
-    } else {
-      for (int i = tid; i < TT * hc; i += blockDim.x) {
-        const int r = i / hc, c = i % hc;
-        const int t = t0 + r;
-        xs[r * (kRouteHC + 1) + c] = t < N ? to_f32(X[static_cast<size_t>(t) * H + h0 + c]) : 0.f;
+      __syncthreads();
+      if (vec) {
+        const int span = hc / kRouteKS;
+        const int c_lo = ks * span;
+        for (int c = c_lo; c < c_lo + span; c += 8) {
+          double xa[8], xb[8];
+          if (ok0) load8_f64<T>(x0 + h0 + c, xa);
+          else
+#pragma unroll
+            for (int i = 0; i < 8; ++i) xa[i] = 0.0;
+          if (ok1) load8_f64<T>(x1 + h0 + c, xb);
+          else
+#pragma unroll
+            for (int i = 0; i < 8; ++i) xb[i] = 0.0;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const double* wr = wsm + (c + i) * EB;
+#pragma unroll
+            for (int j = 0; j < EB; j += 2) {
+              const double2 wv = *reinterpret_cast<const double2*>(wr + j);
+              a0[j] = fma(xa[i], wv.x, a0[j]);
+              a0[j + 1] = fma(xa[i], wv.y, a0[j + 1]);
+              a1[j] = fma(xb[i], wv.x, a1[j]);
+              a1[j + 1] = fma(xb[i], wv.y, a1[j + 1]);
+            }
+          }
+        }
+      } else {
+        for (int c = ks; c < hc; c += kRouteKS) {
+          const double xa = ok0 ? static_cast<double>(to_f32(x0[h0 + c])) : 0.0;
+          const double xb = ok1 ? static_cast<double>(to_f32(x1[h0 + c])) : 0.0;
+#pragma unroll
+          for (int j = 0; j < EB; ++j) {
+            a0[j] = fma(xa, wsm[c * EB + j], a0[j]);
+            a1[j] = fma(xb, wsm[c * EB + j], a1[j]);
+          }
+        }
       }
     }
-    for (int i = tid; i < hc * E; i += blockDim.x) wsm[i] = Wg[static_cast<size_t>(h0) * E + i];
-    __syncthreads();
-    if (active) {
-      const float* xr = xs + tl * (kRouteHC + 1);
-      double a0 = 0.0, a1 = 0.0;
-      int c = 0;
-      for (; c + 2 <= hc; c += 2) {
-        a0 = fma(static_cast<double>(xr[c]), static_cast<double>(wsm[c * E + e]), a0);
-        a1 = fma(static_cast<double>(xr[c + 1]), static_cast<double>(wsm[(c + 1) * E + e]), a1);
-      }
-      if (c < hc) a0 = fma(static_cast<double>(xr[c]), static_cast<double>(wsm[c * E + e]), a0);
-      acc += a0 + a1;
+    // deterministic split-K reduction: ks = 0..KS-1 in order
+#pragma unroll
+    for (int j = 0; j < EB; ++j) {
+      part[(ks * kRouteTB + tl0) * EB + j] = a0[j];
+      part[(ks * kRouteTB + tl1) * EB + j] = a1[j];
     }
     __syncthreads();
+    for (int i = tid; i < kRouteTB * EB; i += kRouteThreads) {
+      const int tl = i / EB, j = i % EB;
+      if (e0 + j >= E) continue;
+      double s = 0.0;
+      for (int q = 0; q < kRouteKS; ++q) s += part[(q * kRouteTB + tl) * EB + j];
+      lg[tl * E + e0 + j] = s;
+    }
   }
-  if (active) lg[tl * E + e] = acc;
   __syncthreads();
   // softmax statistics (row max shift, tensor.py:214-216)
-  if (tid < TT) {
+  if (tid < kRouteTB) {
     const double* l = lg + tid * E;
     double mx = l[0];
     for (int j = 1; j < E; ++j) mx = fmax(mx, l[j]);
@@ -124,15 +172,15 @@ __global__ void __launch_bounds__(kRouteThreads) router_kernel(const T* __restri
     stat[2 * tid + 1] = s;
   }
   __syncthreads();
-  const int t = t0 + tl;
-  if (active) {
-    const double sc = exp(lg[tl * E + e] - stat[2 * tl]) / stat[2 * tl + 1];
-    lg[tl * E + e] = sc;
-    if (t < N) scores[static_cast<size_t>(t) * E + e] = static_cast<float>(sc);
+  for (int i = tid; i < kRouteTB * E; i += kRouteThreads) {
+    const int tl = i / E, e = i % E;
+    const double sc = exp(lg[i] - stat[2 * tl]) / stat[2 * tl + 1];
+    lg[i] = sc;
+    if (t0 + tl < N) scores[static_cast<size_t>(t0 + tl) * E + e] = static_cast<float>(sc);
   }
   __syncthreads();
   // top-k selection, one thread per token
-  if (tid < TT && t0 + tid < N) {
+  if (tid < kRouteTB && t0 + tid < N) {
     const int tt = t0 + tid;
     const double* sc = lg + tid * E;
     unsigned long long chosen[2] = {0ull, 0ull};
@@ -154,10 +202,10 @@ __global__ void __launch_bounds__(kRouteThreads) router_kernel(const T* __restri
     }
   }
   // per-block expert score sums in token order (deterministic aux-loss reduction)
-  if (tid < E) {
+  for (int e = tid; e < E; e += kRouteThreads) {
     double s = 0.0;
-    for (int r = 0; r < TT && t0 + r < N; ++r) s += lg[r * E + tid];
-    ssum[static_cast<size_t>(blockIdx.x) * E + tid] = s;
+    for (int r = 0; r < kRouteTB && t0 + r < N; ++r) s += lg[r * E + e];
+    ssum[static_cast<size_t>(blockIdx.x) * E + e] = s;
   }
 }
 
@@ -375,9 +423,20 @@ __global__ void plan_scatter_kernel(const int* __restrict__ idx, const float* __
     const int e = ev[s];
     const int pos = seg[e] + kb[static_cast<size_t>(c) * E + e] + sh[warp * E + e] + rw[s];
     tok_sorted[pos] = t;
-    if (w_sorted) w_sorted[pos] = w[pi];
+    if (w_sorted) w_sorted[pos] = w ? w[pi] : 1.f;
     pair_pos[pi] = pos;
   }
+}
+
+template <typename T, int EB>
+static int launch_router(const void* X, const float* Wg, int N, int H, int E, int K, const int* ovr, int* idx, float* w,
+                         float* scores, double* ssum, int* cnt, cudaStream_t s) {
+  const size_t smem = route_smem_bytes(E);
+  auto k = router_kernel<T, EB>;
+  PPMOE_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  const int nb = (N + kRouteTB - 1) / kRouteTB;
+  k<<<nb, kRouteThreads, smem, s>>>(static_cast<const T*>(X), Wg, N, H, E, K, ovr, idx, w, scores, ssum, cnt);
+  return check_launch("router_kernel");
 }
 
 }  // namespace ppmoe
@@ -388,9 +447,8 @@ extern "C" {
 
 size_t ppmoe_route_workspace_bytes(int N, int E, int K) {
   (void)K;
-  const int TT = route_tokens_per_block(E > 0 ? E : 1);
-  const size_t nb = (static_cast<size_t>(N) + TT - 1) / TT;
-  return align_up(nb * E * 8, 256) + align_up(static_cast<size_t>(E) * 4, 256);
+  const size_t nb = (static_cast<size_t>(N) + kRouteTB - 1) / kRouteTB;
+  return align_up(nb * (E > 0 ? E : 1) * 8, 256) + align_up(static_cast<size_t>(E) * 4, 256);
 }
 
 int ppmoe_route(const void* X, int dtype, const float* Wg, int N, int H, int E, int K, const int* route_override,
@@ -402,27 +460,20 @@ int ppmoe_route(const void* X, int dtype, const float* Wg, int N, int H, int E, 
   PPMOE_REQUIRE(K >= 1 && K <= E && K <= kMaxK, "top-k must satisfy 1 <= k <= min(E, %d), got k=%d E=%d", kMaxK, K, E);
   PPMOE_REQUIRE(ws_bytes >= ppmoe_route_workspace_bytes(N, E, K), "route workspace too small");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int TT = route_tokens_per_block(E);
-  const int nb = (N + TT - 1) / TT;
+  const int nb = (N + kRouteTB - 1) / kRouteTB;
   double* ssum = static_cast<double*>(ws);
   int* cnt = reinterpret_cast<int*>(static_cast<char*>(ws) + align_up(static_cast<size_t>(nb) * E * 8, 256));
   PPMOE_CUDA(cudaMemsetAsync(cnt, 0, static_cast<size_t>(E) * 4, s));
-  const size_t smem = static_cast<size_t>(TT) * E * 8 + 2 * TT * 8 + static_cast<size_t>(TT) * (kRouteHC + 1) * 4 +
-                      static_cast<size_t>(kRouteHC) * E * 4;
-  if (dtype == kBF16) {
-    PPMOE_CUDA(cudaFuncSetAttribute(router_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(smem)));
-    router_kernel<__nv_bfloat16><<<nb, kRouteThreads, smem, s>>>(static_cast<const __nv_bfloat16*>(X), Wg, N, H, E, K,
-                                                                 route_override, idx, w, scores, ssum, cnt);
-  } else {
-    PPMOE_CUDA(cudaFuncSetAttribute(router_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(smem)));
-    router_kernel<float><<<nb, kRouteThreads, smem, s>>>(static_cast<const float*>(X), Wg, N, H, E, K, route_override,
-                                                         idx, w, scores, ssum, cnt);
-  }
-  if (int rc = check_launch("router_kernel")) return rc;
+  int rc;
+  if (dtype == kBF16)
+    rc = E <= 8 ? launch_router<__nv_bfloat16, 8>(X, Wg, N, H, E, K, route_override, idx, w, scores, ssum, cnt, s)
+                : launch_router<__nv_bfloat16, 16>(X, Wg, N, H, E, K, route_override, idx, w, scores, ssum, cnt, s);
+  else
+    rc = E <= 8 ? launch_router<float, 8>(X, Wg, N, H, E, K, route_override, idx, w, scores, ssum, cnt, s)
+                : launch_router<float, 16>(X, Wg, N, H, E, K, route_override, idx, w, scores, ssum, cnt, s);
+  if (rc) return rc;
   route_finalize_kernel<<<1, kMaxE, 0, s>>>(ssum, nb, cnt, N, E, l_aux);
-  if (int rc = check_launch("route_finalize_kernel")) return rc;
+  if (int rc2 = check_launch("route_finalize_kernel")) return rc2;
   if (counts_top1) PPMOE_CUDA(cudaMemcpyAsync(counts_top1, cnt, static_cast<size_t>(E) * 4, cudaMemcpyDeviceToDevice, s));
   return kOk;
 }

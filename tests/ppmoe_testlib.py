@@ -49,7 +49,7 @@ def run_cuda_layer(hidden: np.ndarray, w: P.MoeLayerWeights, *, tp=1, k=1, capac
     grads = {k2: (None if v is None else v.detach().double().cpu().numpy()) for k2, v in w.named_grads().items()}
     return {
         "out": out.detach().double().cpu().numpy(),
-        "l_aux": float(l_aux),
+        "l_aux": float(l_aux.detach()),
         "grad_hidden": x.grad.detach().double().cpu().numpy(),
         "grads": grads,
         "world": world,

@@ -222,7 +222,7 @@ def test_single_expert_reduces_to_dense_ffn():
     hidden = np.asarray(torch.randn(96, 128).double())
     w = device_weights(layer, torch.float32)
     ex = w.experts[0]
-    got = ex.forward(torch.tensor(hidden, dtype=torch.float32, device="cuda")).double().cpu().numpy()
+    got = ex.forward(torch.tensor(hidden, dtype=torch.float32, device="cuda")).detach().double().cpu().numpy()
     ref = O.gelu(hidden @ layer.up[0] + layer.bias_up[0]) @ layer.down[0] + layer.bias_down[0]
     assert scaled_err(got, ref) < 1e-5
 
