@@ -50,7 +50,7 @@ struct GemmSmem {
   // full[S], empty[S], tmem_full[2], tmem_empty[2], tmem base, scheduler tables
   static constexpr int kBarBytes = (2 * kStages + 4) * 8 + 16;
   static constexpr int kSchedOffset = kBarOffset + kBarBytes;
-  static constexpr int kSchedBytes = (kMaxGroups + 1) * 4 * 5;
+  static constexpr int kSchedBytes = (kMaxGroups + 1) * 4 * 6;
   static constexpr int kTotal = kSchedOffset + kSchedBytes + 1024;  // + alignment slack
 };
 
@@ -61,7 +61,20 @@ struct SchedTables {
   int* k_blocks;    // [G]
   int* a_base;      // [G]
   int* b_base;      // [G]
+  int* n_fast;      // [G] 1: walk n-tiles fastest (A panel larger than B panel), else m-tiles fastest
 };
+
+// Tile (m, n) of the local index inside group g.  The operand whose whole panel is
+// smaller stays L2-resident while the other streams through once.
+__device__ __forceinline__ void tile_coords(const SchedTables& t, int g, int local, int n_tiles, int& mt, int& nt) {
+  if (t.n_fast[g]) {
+    mt = local / n_tiles;
+    nt = local % n_tiles;
+  } else {
+    mt = local % t.m_tiles[g];
+    nt = local / t.m_tiles[g];
+  }
+}
 
 __device__ __forceinline__ void sched_locate(const SchedTables& t, int G, int tile, int& g, int& local) {
   int lo = 0;
@@ -86,7 +99,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
   int* sched = reinterpret_cast<int*>(smem + L::kSchedOffset);
   SchedTables tab{sched, sched + (kMaxGroups + 1), sched + 2 * (kMaxGroups + 1), sched + 3 * (kMaxGroups + 1),
-                  sched + 4 * (kMaxGroups + 1)};
+                  sched + 4 * (kMaxGroups + 1), sched + 5 * (kMaxGroups + 1)};
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -106,6 +119,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       tab.k_blocks[g] = (K + kBK - 1) / kBK;
       tab.a_base[g] = geo.a_seg ? seg_lo : g * geo.a_stride;
       tab.b_base[g] = geo.b_seg ? seg_lo : g * geo.b_stride;
+      tab.n_fast[g] = M > geo.N ? 1 : 0;
       acc += tab.m_tiles[g] * n_tiles;
     }
     tab.tile_start[G] = acc;
@@ -139,8 +153,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
         int g, local;
         sched_locate(tab, G, tile, g, local);
-        const int mt = local % tab.m_tiles[g];
-        const int nt = local / tab.m_tiles[g];
+        int mt, nt;
+        tile_coords(tab, g, local, n_tiles, mt, nt);
         const int kb_n = tab.k_blocks[g];
         const int abase = tab.a_base[g];
         const int bbase = tab.b_base[g];
@@ -222,8 +236,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++iter) {
       int g, local;
       sched_locate(tab, G, tile, g, local);
-      const int mt = local % tab.m_tiles[g];
-      const int nt = local / tab.m_tiles[g];
+      int mt, nt;
+      tile_coords(tab, g, local, n_tiles, mt, nt);
       const bool has_k = tab.k_blocks[g] > 0;
       const int acc = iter & 1;
       const uint32_t acc_phase = (iter >> 1) & 1;

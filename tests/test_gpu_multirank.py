@@ -1,0 +1,91 @@
+"""Tensor-parallel PPMoE over real NCCL (one process per GPU) vs the single-process
+simulated world: same outputs and gradients (the reference's T-rank semantics,
+moe.py:254-313).  Needs >= 2 GPUs; skipped otherwise."""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _worker(rank, world, port, q, k, cf):
+    import torch.distributed as dist
+
+    import paper_2304_11414_b200 as P
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    try:
+        h, e, n = 512, 8, 1024
+        el = e // world
+        full = P.MoeLayerWeights.random(h, e, seed=11, device="cuda")  # identical on every rank
+        local = P.MoeLayerWeights(P.GateParams(full.gate.wg.detach().clone().requires_grad_()),
+                                  full.bank.slice(rank * el, (rank + 1) * el))
+        local.bank = P.ExpertBank(*(None if t is None else t.detach().clone().requires_grad_()
+                                    for t in (local.bank.up, local.bank.down, local.bank.bias_up, local.bank.bias_down)),
+                                  first=rank * el)
+        x = torch.randn(n, h, device="cuda", generator=torch.Generator(device="cuda").manual_seed(5)).bfloat16()
+        x.requires_grad_()
+        wd = P.World(1, world)
+        g = P.ProcessGroup(P.EP, tuple(range(world)))
+        ebr = [local.bank if r == rank else None for r in range(world)]
+        out, l_aux = P.ppmoe_forward(wd, g, x, local.gate, ebr, top_k=k, capacity_factor=cf, check_replicas=True)
+        (out.float().sum() + l_aux).backward()
+        P.sync_gate_gradients(wd, g, local.gate)
+        torch.cuda.synchronize()
+        res = {"out": out.detach().float().cpu().numpy(), "dx": x.grad.float().cpu().numpy(),
+               "dwg": local.gate.wg.grad.cpu().numpy(), "dup": local.bank.up.grad.float().cpu().numpy(),
+               "dbd": local.bank.bias_down.grad.float().cpu().numpy(), "l_aux": float(l_aux.detach()),
+               "ar": wd.ledger.count_for("EP", "all_reduce"), "gs": wd.ledger.count_for("EP", "gradient_sync")}
+        q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,k,cf", [(2, 2, float("inf")), (2, 1, 1.0)])
+def test_tp_nccl_matches_simulated(world, k, cf):
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    import paper_2304_11414_b200 as P
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29600 + os.getpid() % 500
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, k, cf)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    # single-process reference: simulated TP world on GPU 0
+    h, e, n = 512, 8, 1024
+    full = P.MoeLayerWeights.random(h, e, seed=11, device="cuda")
+    x = torch.randn(n, h, device="cuda", generator=torch.Generator(device="cuda").manual_seed(5)).bfloat16()
+    x.requires_grad_()
+    out, l_aux = P.ppmoe_forward(P.World(1, world), P.ProcessGroup(P.EP, tuple(range(world))), x, full.gate,
+                                 full.shard(world), top_k=k, capacity_factor=cf)
+    (out.float().sum() + l_aux).backward()
+    ref_out = out.detach().float().cpu().numpy()
+
+    def err(a, b):
+        return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-30))
+
+    el = e // world
+    for r in range(world):
+        res = got[r]
+        assert err(res["out"], ref_out) < 2e-2
+        assert err(res["dx"], x.grad.float().cpu().numpy()) < 2e-2
+        assert err(res["dwg"], full.gate.wg.grad.cpu().numpy()) < 2e-2
+        assert err(res["dup"], full.bank.up.grad[r * el:(r + 1) * el].float().cpu().numpy()) < 2e-2
+        assert err(res["dbd"], full.bank.bias_down.grad[r * el:(r + 1) * el].float().cpu().numpy()) < 2e-2
+        assert abs(res["l_aux"] - float(l_aux.detach())) < 1e-5
+        assert res["ar"] == 2 and res["gs"] == 1
+    # every rank holds the identical replicated output
+    assert np.array_equal(got[0]["out"], got[1]["out"])

@@ -1,0 +1,24 @@
+"""Dev tool: two C2 PPMoE steps (fwd+bwd) for ncu captures; kernel order per step:
+router, finalize, plan x5, gather, fc1_fwd, fc2_fwd, cast, bwd_dy, fc2_dgrad, fc2_wgrad,
+colsum, fc1_dgrad, fc1_wgrad, colsum, gate_bwd, gate_grads, dwg_reduce."""
+import sys
+sys.path.insert(0, ".")
+import torch
+import paper_2304_11414_b200 as P
+
+h, E, k, n = 4096, 8, 2, 16384
+if len(sys.argv) > 1:
+    n = int(sys.argv[1])
+dev = torch.device("cuda", 0)
+w = P.MoeLayerWeights.random(h, E, seed=0, device=dev)
+x = torch.randn(n, h, device=dev).bfloat16().requires_grad_()
+g_out = torch.ones(n, h, device=dev, dtype=torch.bfloat16)
+g_aux = torch.ones((), device=dev)
+world, group = P.World(1, 1), P.ProcessGroup(P.EP, (0,))
+for _ in range(2):
+    for p in w.leaf_parameters():
+        p.grad = None
+    out, l_aux = P.ppmoe_forward(world, group, x, w.gate, [w.bank], top_k=k)
+    torch.autograd.backward([out, l_aux], [g_out, g_aux])
+torch.cuda.synchronize()
+print("ok")
