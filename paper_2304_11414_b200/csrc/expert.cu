@@ -7,14 +7,39 @@
 #include "grouped_gemm.cuh"
 #include "host.h"
 
+#include <cstdlib>
+#include <cstring>
+
 namespace ppmoe {
 
 using bf16 = __nv_bfloat16;
 constexpr int kBN = 256;
 
+// Which tcgen05 kernel runs the grouped GEMMs: the CTA-pair (cta_group::2, 256x256)
+// kernel by default; PPMOE_GEMM=single selects the 1-CTA 128x256 kernel.
+static thread_local int g_force_mode = 0;  // 0: env/default, 1: single, 2: pair
+static bool use_pair() {
+  if (g_force_mode) return g_force_mode == 2;
+  static const int env_mode = [] {
+    const char* e = getenv("PPMOE_GEMM");
+    return (e && strcmp(e, "single") == 0) ? 1 : 2;
+  }();
+  return env_mode == 2;
+}
+
+// Rows of a K-major B box: the pair kernel stages half of the 256-wide N tile per CTA.
+static uint32_t b_box_rows() { return use_pair() ? kBN / 2 : kBN; }
+
 template <bool A_MN, bool B_MN, class Epi>
 static int launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const GroupGeom& geo, const Epi& epi,
                      cudaStream_t s) {
+  if (use_pair()) {
+    auto kern = grouped_gemm_sm100_pair<kBN, A_MN, B_MN, Epi>;
+    constexpr int smem = PairSmem<kBN>::kTotal;
+    PPMOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    kern<<<num_sms() / 2 * 2, kGemmThreads, smem, s>>>(ta, tb, geo, epi);
+    return check_launch("grouped_gemm_sm100_pair");
+  }
   auto kern = grouped_gemm_sm100<kBN, A_MN, B_MN, Epi>;
   constexpr int smem = GemmSmem<kBN>::kTotal;
   PPMOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -161,7 +186,7 @@ int ppmoe_expert_fc2_dgrad(int dtype, const void* dY, const void* down, const vo
   if (dtype == kBF16) {
     CUtensorMap ta, tb;
     if (int rc = tmap_kmajor(&ta, dY, H, rows_cap, kBM)) return rc;
-    if (int rc = tmap_kmajor(&tb, down, H, static_cast<uint64_t>(El) * F, kBN)) return rc;
+    if (int rc = tmap_kmajor(&tb, down, H, static_cast<uint64_t>(El) * F, b_box_rows())) return rc;
     EpiFc2Dgrad<bf16> epi{static_cast<bf16*>(dH), static_cast<const bf16*>(Hpre), F, seg};
     return launch_tc<false, false>(ta, tb, geo, epi, s);
   }
@@ -179,7 +204,7 @@ int ppmoe_expert_fc1_dgrad(int dtype, const void* dH, const void* up, const int*
   if (dtype == kBF16) {
     CUtensorMap ta, tb;
     if (int rc = tmap_kmajor(&ta, dH, F, rows_cap, kBM)) return rc;
-    if (int rc = tmap_kmajor(&tb, up, F, static_cast<uint64_t>(El) * H, kBN)) return rc;
+    if (int rc = tmap_kmajor(&tb, up, F, static_cast<uint64_t>(El) * H, b_box_rows())) return rc;
     EpiFc1Dgrad<bf16> epi{dx_acc, H, seg, tok_local};
     return launch_tc<false, false>(ta, tb, geo, epi, s);
   }
@@ -240,6 +265,11 @@ int ppmoe_gemm_selftest(int mode, int use_tc, int dtype, const void* A, const vo
                         int N, int K, int rows_cap, void* D, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   PPMOE_REQUIRE(mode >= 0 && mode <= 2, "mode must be 0..2");
+  PPMOE_REQUIRE(use_tc >= 0 && use_tc <= 3, "use_tc: 0 CUDA cores, 1 default tcgen05, 2 1-CTA, 3 CTA pair");
+  struct ForceGuard {
+    explicit ForceGuard(int m) { g_force_mode = m; }
+    ~ForceGuard() { g_force_mode = 0; }
+  } guard(use_tc >= 2 ? use_tc - 1 : 0);
   PPMOE_REQUIRE(G >= 1 && G <= kMaxGroups, "bad group count %d", G);
   PPMOE_REQUIRE(!use_tc || dtype == kBF16, "tcgen05 path is bf16 only");
   if (mode == 0) {  // D[seg rows x N] = A[seg rows x K] * B_g[K x N] (B MN-major)
@@ -275,7 +305,7 @@ int ppmoe_gemm_selftest(int mode, int use_tc, int dtype, const void* A, const vo
   if (use_tc) {
     CUtensorMap ta, tb;
     if (int rc = tmap_kmajor(&ta, A, K, rows_cap, kBM)) return rc;
-    if (int rc = tmap_kmajor(&tb, B, K, static_cast<uint64_t>(G) * N, kBN)) return rc;
+    if (int rc = tmap_kmajor(&tb, B, K, static_cast<uint64_t>(G) * N, b_box_rows())) return rc;
     return launch_tc<false, false>(ta, tb, geo, EpiStore<float>{static_cast<float*>(D), N, seg, 1, 0}, s);
   }
   if (dtype == kBF16)

@@ -50,7 +50,7 @@ struct GemmSmem {
   // full[S], empty[S], tmem_full[2], tmem_empty[2], tmem base, scheduler tables
   static constexpr int kBarBytes = (2 * kStages + 4) * 8 + 16;
   static constexpr int kSchedOffset = kBarOffset + kBarBytes;
-  static constexpr int kSchedBytes = (kMaxGroups + 1) * 4 * 6;
+  static constexpr int kSchedBytes = (kMaxGroups + 1) * 4 * 7;
   static constexpr int kTotal = kSchedOffset + kSchedBytes + 1024;  // + alignment slack
 };
 
@@ -62,6 +62,7 @@ struct SchedTables {
   int* a_base;      // [G]
   int* b_base;      // [G]
   int* n_fast;      // [G] 1: walk n-tiles fastest (A panel larger than B panel), else m-tiles fastest
+  int* m_rows;      // [G] valid rows of the group (epilogue row mask)
 };
 
 // Tile (m, n) of the local index inside group g.  The operand whose whole panel is
@@ -99,7 +100,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
   int* sched = reinterpret_cast<int*>(smem + L::kSchedOffset);
   SchedTables tab{sched, sched + (kMaxGroups + 1), sched + 2 * (kMaxGroups + 1), sched + 3 * (kMaxGroups + 1),
-                  sched + 4 * (kMaxGroups + 1), sched + 5 * (kMaxGroups + 1)};
+                  sched + 4 * (kMaxGroups + 1), sched + 5 * (kMaxGroups + 1), sched + 6 * (kMaxGroups + 1)};
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -120,6 +121,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       tab.a_base[g] = geo.a_seg ? seg_lo : g * geo.a_stride;
       tab.b_base[g] = geo.b_seg ? seg_lo : g * geo.b_stride;
       tab.n_fast[g] = M > geo.N ? 1 : 0;
+      tab.m_rows[g] = M;
       acc += tab.m_tiles[g] * n_tiles;
     }
     tab.tile_start[G] = acc;
@@ -254,7 +256,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           for (int j = 0; j < 32; ++j) v[j] = 0.f;
         }
         const int n0 = nt * BN + c * 32;
-        if (n0 < geo.N) epi.template apply<32>(g, m, n0, v);
+        if (n0 < geo.N && m < tab.m_rows[g]) epi.template apply<32>(g, m, n0, v);
       }
       tc_fence_before();
       __syncwarp();
@@ -265,6 +267,224 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem_base, kTmemCols);
+  }
+}
+
+// --------------------------------------------------------------------------
+// CTA-pair variant (cta_group::2): one 256 x 256 tile per CTA pair (cluster of 2).
+// CTA r of the pair stages A rows [256*mt + 128 r, +128) and B columns
+// [256*nt + 128 r, +128) (32 KB per stage per CTA, 6 stages); the leader issues
+// tcgen05.mma.cta_group::2 M=256 N=256, each CTA's TMEM receives its 128 rows.
+// Per-SM operand traffic is 2/3 of the 1-CTA 128x256 tile.
+//   full[s]      (leader) 2 arrivals (one per CTA, with its tx bytes)
+//   empty[s]     (both)   multicast commit from the leader's MMA
+//   tmem_full[a] (both)   multicast commit
+//   tmem_empty[a](leader) 8 arrivals: 4 epilogue warps x 2 CTAs
+constexpr int kPairBM = 256;
+constexpr int kPairStages = 6;
+
+template <int BN>
+struct PairSmem {
+  static constexpr int kABytes = 128 * kBK * 2;          // 16 KB: this CTA's half of A
+  static constexpr int kBBytes = (BN / 2) * kBK * 2;     // 16 KB: this CTA's half of B
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kBarOffset = kPairStages * kStageBytes;
+  static constexpr int kBarBytes = (2 * kPairStages + 4) * 8 + 16;
+  static constexpr int kSchedOffset = kBarOffset + kBarBytes;
+  static constexpr int kSchedBytes = (kMaxGroups + 1) * 4 * 7;
+  static constexpr int kTotal = kSchedOffset + kSchedBytes + 1024;
+};
+
+template <int BN, bool A_MN, bool B_MN, class Epi>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
+    grouped_gemm_sm100_pair(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                            GroupGeom geo, Epi epi) {
+  using L = PairSmem<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_addr = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
+
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOffset);
+  uint64_t* empty = full + kPairStages;
+  uint64_t* tmem_full = empty + kPairStages;
+  uint64_t* tmem_empty = tmem_full + 2;
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+  int* sched = reinterpret_cast<int*>(smem + L::kSchedOffset);
+  SchedTables tab{sched, sched + (kMaxGroups + 1), sched + 2 * (kMaxGroups + 1), sched + 3 * (kMaxGroups + 1),
+                  sched + 4 * (kMaxGroups + 1), sched + 5 * (kMaxGroups + 1), sched + 6 * (kMaxGroups + 1)};
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1;
+  const int num_pairs = gridDim.x >> 1;
+  const int G = geo.G;
+  const int n_tiles = (geo.N + BN - 1) / BN;
+
+  if (threadIdx.x == 0) {
+    const int s0 = geo.seg[0];
+    int acc = 0;
+    for (int g = 0; g < G; ++g) {
+      const int seg_lo = geo.seg[g] - s0;
+      const int seg_rows = geo.seg[g + 1] - geo.seg[g];
+      const int M = geo.M_fixed > 0 ? geo.M_fixed : seg_rows;
+      const int K = geo.K_fixed > 0 ? geo.K_fixed : seg_rows;
+      tab.tile_start[g] = acc;
+      tab.m_tiles[g] = (M + kPairBM - 1) / kPairBM;
+      tab.k_blocks[g] = (K + kBK - 1) / kBK;
+      tab.a_base[g] = geo.a_seg ? seg_lo : g * geo.a_stride;
+      tab.b_base[g] = geo.b_seg ? seg_lo : g * geo.b_stride;
+      tab.n_fast[g] = M > geo.N ? 1 : 0;
+      tab.m_rows[g] = M;
+      acc += tab.m_tiles[g] * n_tiles;
+    }
+    tab.tile_start[G] = acc;
+    for (int s = 0; s < kPairStages; ++s) {
+      mbar_init(&full[s], 2);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tmem_full[a], 1);
+      mbar_init(&tmem_empty[a], 8);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmap_a);
+    tma_prefetch_desc(&tmap_b);
+  }
+  constexpr uint32_t kTmemCols = 2 * BN;
+  if (warp == 2) tmem_alloc_pair(tmem_base_slot, kTmemCols);
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_base_slot;
+  const int total_tiles = tab.tile_start[G];
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer (both CTAs)
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = pair; tile < total_tiles; tile += num_pairs) {
+        int g, local;
+        sched_locate(tab, G, tile, g, local);
+        int mt, nt;
+        tile_coords(tab, g, local, n_tiles, mt, nt);
+        const int kb_n = tab.k_blocks[g];
+        const int arow = mt * kPairBM + static_cast<int>(rank) * 128;
+        const int bcol = nt * BN + static_cast<int>(rank) * (BN / 2);
+        const int abase = tab.a_base[g];
+        const int bbase = tab.b_base[g];
+        for (int kb = 0; kb < kb_n; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * L::kStageBytes;
+          uint8_t* sb = sa + L::kABytes;
+          const uint32_t fbar = mapa_shared(&full[stage], 0);
+          mbar_arrive_expect_tx_cluster(fbar, L::kStageBytes);
+          if (A_MN) {
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+              tma_load_2d_pair(sa + j * (64 * kBK * 2), &tmap_a, fbar, arow + j * 64, abase + kb * kBK);
+          } else {
+            tma_load_2d_pair(sa, &tmap_a, fbar, kb * kBK, abase + arow);
+          }
+          if (B_MN) {
+#pragma unroll
+            for (int j = 0; j < BN / 128; ++j)
+              tma_load_2d_pair(sb + j * (64 * kBK * 2), &tmap_b, fbar, bcol + j * 64, bbase + kb * kBK);
+          } else {
+            tma_load_2d_pair(sb, &tmap_b, fbar, kb * kBK, bbase + bcol);
+          }
+          if (++stage == kPairStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (leader only)
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = make_idesc_bf16(kPairBM, BN, A_MN, B_MN);
+      constexpr uint32_t a_lbo = A_MN ? (64 * kBK * 2) : 16;
+      constexpr uint32_t b_lbo = B_MN ? (64 * kBK * 2) : 16;
+      constexpr uint32_t k_step_a = A_MN ? (kUMMAK * 128) : (kUMMAK * 2);
+      constexpr uint32_t k_step_b = B_MN ? (kUMMAK * 128) : (kUMMAK * 2);
+      int stage = 0;
+      uint32_t phase = 0;
+      int iter = 0;
+      for (int tile = pair; tile < total_tiles; tile += num_pairs, ++iter) {
+        int g, local;
+        sched_locate(tab, G, tile, g, local);
+        const int kb_n = tab.k_blocks[g];
+        const int acc = iter & 1;
+        const uint32_t acc_phase = (iter >> 1) & 1;
+        mbar_wait_cluster(&tmem_empty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < kb_n; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * L::kStageBytes);
+          const uint32_t sb = sa + L::kABytes;
+#pragma unroll
+          for (int k = 0; k < kBK / kUMMAK; ++k) {
+            const uint64_t ad = make_sdesc(sa + k * k_step_a, a_lbo, 1024);
+            const uint64_t bd = make_sdesc(sb + k * k_step_b, b_lbo, 1024);
+            umma_bf16_pair(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+          }
+          umma_commit_pair_mc(&empty[stage], 0x3);
+          if (++stage == kPairStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit_pair_mc(&tmem_full[acc], 0x3);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue (both CTAs)
+    const int q = warp & 3;
+    const int row_in_tile = static_cast<int>(rank) * 128 + q * 32 + lane;
+    const uint32_t empty_leader = mapa_shared(&tmem_empty[0], 0);
+    int iter = 0;
+    for (int tile = pair; tile < total_tiles; tile += num_pairs, ++iter) {
+      int g, local;
+      sched_locate(tab, G, tile, g, local);
+      int mt, nt;
+      tile_coords(tab, g, local, n_tiles, mt, nt);
+      const bool has_k = tab.k_blocks[g] > 0;
+      const int acc = iter & 1;
+      const uint32_t acc_phase = (iter >> 1) & 1;
+      mbar_wait(&tmem_full[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
+      const int m = mt * kPairBM + row_in_tile;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        float v[32];
+        tmem_ld32(taddr + c * 32, v);
+        if (!has_k) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = 0.f;
+        }
+        const int n0 = nt * BN + c * 32;
+        if (n0 < geo.N && m < tab.m_rows[g]) epi.template apply<32>(g, m, n0, v);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(empty_leader + acc * 8);
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem_base, kTmemCols);
   }
 }
 

@@ -44,15 +44,47 @@ __device__ __forceinline__ double f32bits_to_f64(uint32_t b) {
 
 template <typename T>
 __device__ __forceinline__ void load8_f64(const T* p, double* dst);
+// bf16 bits -> fp64: sign | (exponent+896, mantissa) moved into the high word.  Zero,
+// subnormal, inf and nan (exponent field 0 or 255) take the exact F2F path.
+__device__ __forceinline__ double bf16bits_to_f64(uint32_t b) {
+  const uint32_t m = b & 0x7FFFu;
+  if (m - 0x80u >= 0x7F00u) return static_cast<double>(__uint_as_float(b << 16));
+  const uint32_t hi = ((b & 0x8000u) << 16) | ((m << 13) + 0x38000000u);
+  return __hiloint2double(static_cast<int>(hi), 0);
+}
+
 template <>
 __device__ __forceinline__ void load8_f64<__nv_bfloat16>(const __nv_bfloat16* p, double* dst) {
   const uint4 u = *reinterpret_cast<const uint4*>(p);
   const uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    dst[2 * i] = f32bits_to_f64(w[i] << 16);
-    dst[2 * i + 1] = f32bits_to_f64(w[i] & 0xFFFF0000u);
+    dst[2 * i] = bf16bits_to_f64(w[i] & 0xFFFFu);
+    dst[2 * i + 1] = bf16bits_to_f64(w[i] >> 16);
   }
+}
+
+template <typename T>
+__device__ __forceinline__ uint4 ldg16(const T* p) {
+  return __ldg(reinterpret_cast<const uint4*>(p));
+}
+
+template <typename T>
+__device__ __forceinline__ void widen8(const uint4* u, double* dst);
+template <>
+__device__ __forceinline__ void widen8<__nv_bfloat16>(const uint4* u, double* dst) {
+  const uint32_t w[4] = {u->x, u->y, u->z, u->w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    dst[2 * i] = bf16bits_to_f64(w[i] & 0xFFFFu);
+    dst[2 * i + 1] = bf16bits_to_f64(w[i] >> 16);
+  }
+}
+template <>
+__device__ __forceinline__ void widen8<float>(const uint4* u, double* dst) {
+  dst[0] = f32bits_to_f64(u[0].x); dst[1] = f32bits_to_f64(u[0].y); dst[2] = f32bits_to_f64(u[0].z);
+  dst[3] = f32bits_to_f64(u[0].w); dst[4] = f32bits_to_f64(u[1].x); dst[5] = f32bits_to_f64(u[1].y);
+  dst[6] = f32bits_to_f64(u[1].z); dst[7] = f32bits_to_f64(u[1].w);
 }
 template <>
 __device__ __forceinline__ void load8_f64<float>(const float* p, double* dst) {
@@ -66,9 +98,8 @@ __host__ __device__ inline int route_eb(int E) { return E <= 8 ? 8 : 16; }
 
 __host__ inline size_t route_smem_bytes(int E) {
   const int EB = route_eb(E);
-  return static_cast<size_t>(kRouteHC) * EB * 8                       // staged Wg chunk (fp64)
-         + static_cast<size_t>(kRouteKS) * kRouteTB * EB * 8         // split-K partials
-         + static_cast<size_t>(kRouteTB) * E * 8 + 2 * kRouteTB * 8;  // logits/scores + softmax stats
+  // staged Wg chunk (fp64), reused for the split-K partials (KS*TB == HC)
+  return static_cast<size_t>(kRouteHC) * EB * 8 + static_cast<size_t>(kRouteTB) * E * 8 + 2 * kRouteTB * 8;
 }
 
 // Gate logits X*Wg in fp64 (bf16/fp32 x fp32 products are exact in fp64), softmax,
@@ -76,15 +107,16 @@ __host__ inline size_t route_smem_bytes(int E) {
 // splits); experts in register passes of EB.  Every lane of a warp reads the same
 // staged Wg value (shared-memory broadcast).
 template <typename T, int EB>
-__global__ void __launch_bounds__(kRouteThreads) router_kernel(const T* __restrict__ X, const float* __restrict__ Wg,
+__global__ void __launch_bounds__(kRouteThreads, 2) router_kernel(const T* __restrict__ X, const float* __restrict__ Wg,
                                                                int N, int H, int E, int K, const int* __restrict__ ovr,
                                                                int* __restrict__ idx, float* __restrict__ w,
                                                                float* __restrict__ scores, double* __restrict__ ssum,
                                                                int* __restrict__ cnt_top1) {
   extern __shared__ __align__(16) unsigned char sm[];
+  static_assert(kRouteKS * kRouteTB == kRouteHC, "split-K partials alias the Wg staging buffer");
   double* wsm = reinterpret_cast<double*>(sm);                 // [HC][EB]
-  double* part = wsm + kRouteHC * EB;                          // [KS][TB][EB]
-  double* lg = part + kRouteKS * kRouteTB * EB;                // [TB][E]
+  double* part = wsm;                                          // [KS][TB][EB] (after the last chunk)
+  double* lg = wsm + kRouteHC * EB;                            // [TB][E]
   double* stat = lg + kRouteTB * E;                            // [TB][2]
   const int tid = threadIdx.x;
   const int ks = tid >> 5;                  // warp = one hidden split
@@ -108,28 +140,39 @@ __global__ void __launch_bounds__(kRouteThreads) router_kernel(const T* __restri
       }
       __syncthreads();
       if (vec) {
-        const int span = hc / kRouteKS;
+        const int span = hc / kRouteKS;  // multiple of 8
         const int c_lo = ks * span;
-        for (int c = c_lo; c < c_lo + span; c += 8) {
-          double xa[8], xb[8];
-          if (ok0) load8_f64<T>(x0 + h0 + c, xa);
-          else
+        constexpr int kU = sizeof(T) == 2 ? 1 : 2;  // uint4 per 8 values
+        for (int c0 = c_lo; c0 < c_lo + span; c0 += 32) {
+          const int nsub = min(4, (c_lo + span - c0) / 8);
+          uint4 ua[4][kU], ub[4][kU];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) xa[i] = 0.0;
-          if (ok1) load8_f64<T>(x1 + h0 + c, xb);
-          else
+          for (int u = 0; u < 4; ++u) {
+            if (u < nsub) {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) xb[i] = 0.0;
+              for (int q = 0; q < kU; ++q) {
+                ua[u][q] = ok0 ? ldg16(x0 + h0 + c0 + 8 * u + 4 * q) : make_uint4(0, 0, 0, 0);
+                ub[u][q] = ok1 ? ldg16(x1 + h0 + c0 + 8 * u + 4 * q) : make_uint4(0, 0, 0, 0);
+              }
+            }
+          }
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const double* wr = wsm + (c + i) * EB;
+          for (int u = 0; u < 4; ++u) {
+            if (u >= nsub) break;
+            double xa[8], xb[8];
+            widen8<T>(ua[u], xa);
+            widen8<T>(ub[u], xb);
 #pragma unroll
-            for (int j = 0; j < EB; j += 2) {
-              const double2 wv = *reinterpret_cast<const double2*>(wr + j);
-              a0[j] = fma(xa[i], wv.x, a0[j]);
-              a0[j + 1] = fma(xa[i], wv.y, a0[j + 1]);
-              a1[j] = fma(xb[i], wv.x, a1[j]);
-              a1[j + 1] = fma(xb[i], wv.y, a1[j + 1]);
+            for (int i = 0; i < 8; ++i) {
+              const double* wr = wsm + (c0 + 8 * u + i) * EB;
+#pragma unroll
+              for (int j = 0; j < EB; j += 2) {
+                const double2 wv = *reinterpret_cast<const double2*>(wr + j);
+                a0[j] = fma(xa[i], wv.x, a0[j]);
+                a0[j + 1] = fma(xa[i], wv.y, a0[j + 1]);
+                a1[j] = fma(xb[i], wv.x, a1[j]);
+                a1[j + 1] = fma(xb[i], wv.y, a1[j + 1]);
+              }
             }
           }
         }
@@ -146,6 +189,7 @@ __global__ void __launch_bounds__(kRouteThreads) router_kernel(const T* __restri
       }
     }
     // deterministic split-K reduction: ks = 0..KS-1 in order
+    __syncthreads();  // partials alias the Wg staging buffer
 #pragma unroll
     for (int j = 0; j < EB; ++j) {
       part[(ks * kRouteTB + tl0) * EB + j] = a0[j];
@@ -159,6 +203,7 @@ __global__ void __launch_bounds__(kRouteThreads) router_kernel(const T* __restri
       for (int q = 0; q < kRouteKS; ++q) s += part[(q * kRouteTB + tl) * EB + j];
       lg[tl * E + e0 + j] = s;
     }
+    __syncthreads();  // the next expert pass restages Wg over the partials
   }
   __syncthreads();
   // softmax statistics (row max shift, tensor.py:214-216)
