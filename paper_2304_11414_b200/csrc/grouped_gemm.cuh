@@ -276,7 +276,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 // [256*nt + 128 r, +128) (32 KB per stage per CTA, 6 stages); the leader issues
 // tcgen05.mma.cta_group::2 M=256 N=256, each CTA's TMEM receives its 128 rows.
 // Per-SM operand traffic is 2/3 of the 1-CTA 128x256 tile.
-//   full[s]      (leader) 2 arrivals (one per CTA, with its tx bytes)
+//   full[s]      (leader) 1 arrival: the leader expects both CTAs' bytes; the peer's TMA
+//                         completes its transactions on the leader's barrier
 //   empty[s]     (both)   multicast commit from the leader's MMA
 //   tmem_full[a] (both)   multicast commit
 //   tmem_empty[a](leader) 8 arrivals: 4 epilogue warps x 2 CTAs
@@ -341,7 +342,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     }
     tab.tile_start[G] = acc;
     for (int s = 0; s < kPairStages; ++s) {
-      mbar_init(&full[s], 2);
+      mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -382,7 +383,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           uint8_t* sa = smem + stage * L::kStageBytes;
           uint8_t* sb = sa + L::kABytes;
           const uint32_t fbar = mapa_shared(&full[stage], 0);
-          mbar_arrive_expect_tx_cluster(fbar, L::kStageBytes);
+          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * L::kStageBytes);
           if (A_MN) {
 #pragma unroll
             for (int j = 0; j < 2; ++j)
