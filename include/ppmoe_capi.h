@@ -94,10 +94,11 @@ int ppmoe_dispatch_plan(const int* idx, const float* w, int N, int E, int K, int
 int ppmoe_gather(const void* X, int dtype, int N, int H, const int* seg, int El, const int* tok_sorted,
                  const float* w_sorted, int rows_cap, void* Xs, int* tok_local, float* w_local, void* stream);
 
-/* Expert FFN forward, first GEMM: Hpre = Xs*up_g + bias_up, Act = GeLU(Hpre)
- * (ExpertFfn.forward, moe.py:100-104).  bias_up may be NULL.               */
+/* Expert FFN forward, first GEMM: a = Xs*up_g + bias_up, Act = GeLU(a), and
+ * GeluGrad = GeLU'(a) saved for the backward (ExpertFfn.forward, moe.py:100-104;
+ * gelu backward tensor.py:204-207).  bias_up may be NULL.                  */
 int ppmoe_expert_fc1_fwd(int dtype, const void* Xs, const void* up, const void* bias_up, const int* seg, int El,
-                         int H, int F, int rows_cap, void* Hpre, void* Act, void* stream);
+                         int H, int F, int rows_cap, void* GeluGrad, void* Act, void* stream);
 
 /* Expert FFN forward, second GEMM fused with the gate-weighted combine:
  * Y = Act*down_g + bias_down (stored, pre-scale), out_acc[tok] += w*Y
@@ -116,8 +117,8 @@ int ppmoe_cast_out(const float* acc, int n, void* out, int dtype, void* stream);
 int ppmoe_bwd_dy(int dtype, const void* dOut, const void* Y, const int* seg, int El, int H, int rows_cap,
                  const int* tok_local, const float* w_local, int weight_scaling, void* dY, float* dw, void* stream);
 
-/* dH = (dY*down_g^T) .* GeLU'(Hpre)   (matmul/gelu backward, tensor.py:134-138, 204-207) */
-int ppmoe_expert_fc2_dgrad(int dtype, const void* dY, const void* down, const void* Hpre, const int* seg, int El,
+/* dH = (dY*down_g^T) .* GeluGrad   (matmul/gelu backward, tensor.py:134-138, 204-207) */
+int ppmoe_expert_fc2_dgrad(int dtype, const void* dY, const void* down, const void* GeluGrad, const int* seg, int El,
                            int H, int F, int rows_cap, void* dH, void* stream);
 
 /* dDown_g = Act_g^T * dY_g  [El x F x H]; dbias_down_g = colsum(dY_g) (may be NULL). */

@@ -165,7 +165,7 @@ class ExpertFwdState:
     xs: torch.Tensor
     tok_l: torch.Tensor
     w_l: torch.Tensor
-    hpre: torch.Tensor
+    gelu_grad: torch.Tensor
     act: torch.Tensor
     y: torch.Tensor
 
@@ -186,13 +186,13 @@ def experts_forward(hidden, pl: Plan, e0: int, el: int, up, down, bias_up, bias_
     s = _stream()
     call("ppmoe_gather", ptr(hidden), dt, n, h, ptr(seg), el, ptr(pl.tok_sorted), ptr(pl.w_sorted), rows_cap, ptr(xs),
          ptr(tok_l), ptr(w_l), s)
-    hpre = torch.empty((rows_cap, f), dtype=hidden.dtype, device=dev)
+    gelu_grad = torch.empty((rows_cap, f), dtype=hidden.dtype, device=dev)
     act = torch.empty((rows_cap, f), dtype=hidden.dtype, device=dev)
-    call("ppmoe_expert_fc1_fwd", dt, ptr(xs), ptr(up), ptr(bias_up), ptr(seg), el, h, f, rows_cap, ptr(hpre), ptr(act), s)
+    call("ppmoe_expert_fc1_fwd", dt, ptr(xs), ptr(up), ptr(bias_up), ptr(seg), el, h, f, rows_cap, ptr(gelu_grad), ptr(act), s)
     y = torch.empty((rows_cap, h), dtype=hidden.dtype, device=dev)
     call("ppmoe_expert_fc2_fwd", dt, ptr(act), ptr(down), ptr(bias_down), ptr(seg), el, h, f, rows_cap, ptr(tok_l),
          ptr(w_l), int(bool(weight_scaling)), ptr(y), ptr(out_acc), s)
-    return ExpertFwdState(e0, el, rows_cap, seg, xs, tok_l, w_l, hpre, act, y)
+    return ExpertFwdState(e0, el, rows_cap, seg, xs, tok_l, w_l, gelu_grad, act, y)
 
 
 def experts_backward(grad_out, st: ExpertFwdState, up, down, has_bias: bool, weight_scaling: bool,
@@ -210,7 +210,7 @@ def experts_backward(grad_out, st: ExpertFwdState, up, down, has_bias: bool, wei
     call("ppmoe_bwd_dy", dt, ptr(grad_out), ptr(st.y), ptr(st.seg), el, h, rows_cap, ptr(st.tok_l), ptr(st.w_l),
          int(bool(weight_scaling)), ptr(dy), ptr(dw), s)
     dh = torch.empty((rows_cap, f), dtype=grad_out.dtype, device=dev)
-    call("ppmoe_expert_fc2_dgrad", dt, ptr(dy), ptr(down), ptr(st.hpre), ptr(st.seg), el, h, f, rows_cap, ptr(dh), s)
+    call("ppmoe_expert_fc2_dgrad", dt, ptr(dy), ptr(down), ptr(st.gelu_grad), ptr(st.seg), el, h, f, rows_cap, ptr(dh), s)
     d_down = torch.empty_like(down)
     d_bd = torch.empty((el, h), dtype=grad_out.dtype, device=dev) if has_bias else None
     call("ppmoe_expert_fc2_wgrad", dt, ptr(st.act), ptr(dy), ptr(st.seg), el, h, f, rows_cap, ptr(d_down), ptr(d_bd), s)

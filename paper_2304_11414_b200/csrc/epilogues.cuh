@@ -96,10 +96,12 @@ __device__ __forceinline__ void scatter_add_row(float* p, const float (&x)[W], f
 
 __device__ __forceinline__ int local_row(const int* seg, int g, int m) { return seg[g] - seg[0] + m; }
 
-// fc1 forward: Hpre = X_e * up_e + bias_up ; Act = GeLU(Hpre)      (moe.py:101-104)
+// fc1 forward: a = X_e * up_e + bias_up ; Act = GeLU(a), and GeLU'(a) saved for the
+// backward so the fc2 data-gradient epilogue is a plain multiply (moe.py:101-104,
+// tensor.py:199-207).
 template <typename T>
 struct EpiFc1Fwd {
-  T* hpre;
+  T* gelu_grad;
   T* act;
   const T* bias;  // [G*F] or null
   int F;
@@ -113,14 +115,16 @@ struct EpiFc1Fwd {
     else
 #pragma unroll
       for (int j = 0; j < W; ++j) b[j] = 0.f;
-    float x[W], a[W];
+    float d[W], a[W];
 #pragma unroll
     for (int j = 0; j < W; ++j) {
-      x[j] = v[j] + b[j];
-      a[j] = gelu_f(x[j]);
+      const float x = v[j] + b[j];
+      const float cdf = 0.5f * (1.0f + erff(x * 0.70710678118654752f));
+      a[j] = x * cdf;
+      d[j] = cdf + x * (__expf(-0.5f * x * x) * 0.39894228040143268f);
     }
     const size_t off = static_cast<size_t>(row) * F + n0;
-    store_row<T, W>(hpre + off, x, valid);
+    store_row<T, W>(gelu_grad + off, d, valid);
     store_row<T, W>(act + off, a, valid);
   }
 };
@@ -159,11 +163,11 @@ struct EpiFc2Fwd {
   }
 };
 
-// fc2 data-gradient: dH = (dY * down_e^T) .* GeLU'(Hpre)        (tensor.py:134-138, 204-207)
+// fc2 data-gradient: dH = (dY * down_e^T) .* GeLU'(a)        (tensor.py:134-138, 204-207)
 template <typename T>
 struct EpiFc2Dgrad {
   T* dh;
-  const T* hpre;
+  const T* gelu_grad;
   int F;
   const int* seg;
   template <int W>
@@ -171,11 +175,11 @@ struct EpiFc2Dgrad {
     const int row = local_row(seg, g, m);
     const int valid = min(W, F - n0);
     const size_t off = static_cast<size_t>(row) * F + n0;
-    float hp[W];
-    load_row<T, W>(hpre + off, hp, valid);
+    float gd[W];
+    load_row<T, W>(gelu_grad + off, gd, valid);
     float x[W];
 #pragma unroll
-    for (int j = 0; j < W; ++j) x[j] = v[j] * gelu_grad_f(hp[j]);
+    for (int j = 0; j < W; ++j) x[j] = v[j] * gd[j];
     store_row<T, W>(dh + off, x, valid);
   }
 };

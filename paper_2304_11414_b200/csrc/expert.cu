@@ -139,7 +139,7 @@ using namespace ppmoe;
 extern "C" {
 
 int ppmoe_expert_fc1_fwd(int dtype, const void* Xs, const void* up, const void* bias_up, const int* seg, int El, int H,
-                         int F, int rows_cap, void* Hpre, void* Act, void* stream) {
+                         int F, int rows_cap, void* GeluGrad, void* Act, void* stream) {
   if (int rc = check_common(dtype, El, H, F, rows_cap)) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   GroupGeom geo = geom(El, F, 0, H, seg, 1, 0, 0, H);
@@ -148,10 +148,10 @@ int ppmoe_expert_fc1_fwd(int dtype, const void* Xs, const void* up, const void* 
     CUtensorMap ta, tb;
     if (int rc = tmap_kmajor(&ta, Xs, H, rows_cap, kBM)) return rc;
     if (int rc = tmap_mnmajor(&tb, up, F, static_cast<uint64_t>(El) * H)) return rc;
-    EpiFc1Fwd<bf16> epi{static_cast<bf16*>(Hpre), static_cast<bf16*>(Act), static_cast<const bf16*>(bias_up), F, seg};
+    EpiFc1Fwd<bf16> epi{static_cast<bf16*>(GeluGrad), static_cast<bf16*>(Act), static_cast<const bf16*>(bias_up), F, seg};
     return launch_tc<false, true>(ta, tb, geo, epi, s);
   }
-  EpiFc1Fwd<float> epi{static_cast<float*>(Hpre), static_cast<float*>(Act), static_cast<const float*>(bias_up), F, seg};
+  EpiFc1Fwd<float> epi{static_cast<float*>(GeluGrad), static_cast<float*>(Act), static_cast<const float*>(bias_up), F, seg};
   return launch_simt<float, false, true>(static_cast<const float*>(Xs), H, static_cast<const float*>(up), F, geo,
                                          rows_cap, epi, s);
 }
@@ -177,7 +177,7 @@ int ppmoe_expert_fc2_fwd(int dtype, const void* Act, const void* down, const voi
                                          rows_cap, epi, s);
 }
 
-int ppmoe_expert_fc2_dgrad(int dtype, const void* dY, const void* down, const void* Hpre, const int* seg, int El, int H,
+int ppmoe_expert_fc2_dgrad(int dtype, const void* dY, const void* down, const void* GeluGrad, const int* seg, int El, int H,
                            int F, int rows_cap, void* dH, void* stream) {
   if (int rc = check_common(dtype, El, H, F, rows_cap)) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -187,10 +187,10 @@ int ppmoe_expert_fc2_dgrad(int dtype, const void* dY, const void* down, const vo
     CUtensorMap ta, tb;
     if (int rc = tmap_kmajor(&ta, dY, H, rows_cap, kBM)) return rc;
     if (int rc = tmap_kmajor(&tb, down, H, static_cast<uint64_t>(El) * F, b_box_rows())) return rc;
-    EpiFc2Dgrad<bf16> epi{static_cast<bf16*>(dH), static_cast<const bf16*>(Hpre), F, seg};
+    EpiFc2Dgrad<bf16> epi{static_cast<bf16*>(dH), static_cast<const bf16*>(GeluGrad), F, seg};
     return launch_tc<false, false>(ta, tb, geo, epi, s);
   }
-  EpiFc2Dgrad<float> epi{static_cast<float*>(dH), static_cast<const float*>(Hpre), F, seg};
+  EpiFc2Dgrad<float> epi{static_cast<float*>(dH), static_cast<const float*>(GeluGrad), F, seg};
   return launch_simt<float, false, false>(static_cast<const float*>(dY), H, static_cast<const float*>(down), H, geo,
                                           rows_cap, epi, s);
 }

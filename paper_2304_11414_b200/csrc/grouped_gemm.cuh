@@ -65,15 +65,26 @@ struct SchedTables {
   int* m_rows;      // [G] valid rows of the group (epilogue row mask)
 };
 
-// Tile (m, n) of the local index inside group g.  The operand whose whole panel is
-// smaller stays L2-resident while the other streams through once.
+// Tile (m, n) of the local index inside group g.  Tiles are walked in bands of
+// kBand tiles along the slow dimension with the fast dimension inside the band, so a
+// wave of concurrent tiles covers a roughly square block of the output: both operand
+// panels of that block are shared through L2 while the K loop streams.  The fast
+// dimension is N when the A panel is the larger one.
+constexpr int kBand = 8;
 __device__ __forceinline__ void tile_coords(const SchedTables& t, int g, int local, int n_tiles, int& mt, int& nt) {
-  if (t.n_fast[g]) {
-    mt = local / n_tiles;
-    nt = local % n_tiles;
-  } else {
-    mt = local % t.m_tiles[g];
-    nt = local / t.m_tiles[g];
+  const int m_tiles = t.m_tiles[g];
+  if (t.n_fast[g]) {  // bands of kBand m-tiles, n advances slowest inside a band
+    const int per_band = kBand * n_tiles;
+    const int b = local / per_band, r = local % per_band;
+    const int bw = min(kBand, m_tiles - b * kBand);
+    mt = b * kBand + r % bw;
+    nt = r / bw;
+  } else {  // bands of kBand n-tiles, m advances slowest inside a band
+    const int per_band = kBand * m_tiles;
+    const int b = local / per_band, r = local % per_band;
+    const int bw = min(kBand, n_tiles - b * kBand);
+    nt = b * kBand + r % bw;
+    mt = r / bw;
   }
 }
 
