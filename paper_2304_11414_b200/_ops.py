@@ -195,10 +195,9 @@ def experts_forward(hidden, pl: Plan, e0: int, el: int, up, down, bias_up, bias_
     return ExpertFwdState(e0, el, rows_cap, seg, xs, tok_l, w_l, gelu_grad, act, y)
 
 
-def experts_backward(grad_out, st: ExpertFwdState, up, down, has_bias: bool, weight_scaling: bool,
-                     dx_acc: torch.Tensor):
-    """Backward of experts [e0, e0+el): returns (dw per local row, dUp, dDown, dBiasUp, dBiasDown)
-    and accumulates the data gradient of the gathered rows into dx_acc."""
+def experts_backward_data(grad_out, st: ExpertFwdState, up, down, weight_scaling: bool, dx_acc: torch.Tensor):
+    """Data-gradient half of the experts' backward: dY/dw (scale_rows + index_assign backward),
+    dH = dY·downᵀ ⊙ GeLU', and dX_acc[tok] += dH·upᵀ.  Returns (dy, dh, dw)."""
     h = grad_out.shape[1]
     f = up.shape[2]
     el, rows_cap = st.el, st.rows_cap
@@ -211,14 +210,26 @@ def experts_backward(grad_out, st: ExpertFwdState, up, down, has_bias: bool, wei
          int(bool(weight_scaling)), ptr(dy), ptr(dw), s)
     dh = torch.empty((rows_cap, f), dtype=grad_out.dtype, device=dev)
     call("ppmoe_expert_fc2_dgrad", dt, ptr(dy), ptr(down), ptr(st.gelu_grad), ptr(st.seg), el, h, f, rows_cap, ptr(dh), s)
-    d_down = torch.empty_like(down)
-    d_bd = torch.empty((el, h), dtype=grad_out.dtype, device=dev) if has_bias else None
-    call("ppmoe_expert_fc2_wgrad", dt, ptr(st.act), ptr(dy), ptr(st.seg), el, h, f, rows_cap, ptr(d_down), ptr(d_bd), s)
     call("ppmoe_expert_fc1_dgrad", dt, ptr(dh), ptr(up), ptr(st.seg), el, h, f, rows_cap, ptr(st.tok_l), ptr(dx_acc), s)
+    return dy, dh, dw
+
+
+def experts_backward_weights(st: ExpertFwdState, dy, dh, up, down, has_bias: bool):
+    """Weight-gradient half: d down = Actᵀ·dY, d up = Xsᵀ·dH (variable-K grouped GEMMs) and
+    the bias column sums.  Independent of dX, so it overlaps the dX all-reduce."""
+    h = dy.shape[1]
+    f = up.shape[2]
+    el, rows_cap = st.el, st.rows_cap
+    dt = dtype_code(dy.dtype)
+    dev = dy.device
+    s = _stream()
+    d_down = torch.empty_like(down)
+    d_bd = torch.empty((el, h), dtype=dy.dtype, device=dev) if has_bias else None
+    call("ppmoe_expert_fc2_wgrad", dt, ptr(st.act), ptr(dy), ptr(st.seg), el, h, f, rows_cap, ptr(d_down), ptr(d_bd), s)
     d_up = torch.empty_like(up)
-    d_bu = torch.empty((el, f), dtype=grad_out.dtype, device=dev) if has_bias else None
+    d_bu = torch.empty((el, f), dtype=dy.dtype, device=dev) if has_bias else None
     call("ppmoe_expert_fc1_wgrad", dt, ptr(st.xs), ptr(dh), ptr(st.seg), el, h, f, rows_cap, ptr(d_up), ptr(d_bu), s)
-    return dw, d_up, d_down, d_bu, d_bd
+    return d_up, d_down, d_bu, d_bd
 
 
 def gate_backward(rt: Route, pl: Plan, st: ExpertFwdState, dw: torch.Tensor, aux_grad: torch.Tensor | None) -> torch.Tensor:

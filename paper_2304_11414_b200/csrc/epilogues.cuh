@@ -11,8 +11,9 @@
 
 namespace ppmoe {
 
+// `cs`: store with the streaming (evict-first) cache policy.
 template <typename T, int W>
-__device__ __forceinline__ void store_row(T* p, const float (&x)[W], int valid) {
+__device__ __forceinline__ void store_row(T* p, const float (&x)[W], int valid, bool cs = false) {
   if constexpr (std::is_same<T, __nv_bfloat16>::value) {
     if (valid >= W && (W % 8 == 0) && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
 #pragma unroll
@@ -22,7 +23,8 @@ __device__ __forceinline__ void store_row(T* p, const float (&x)[W], int valid) 
         u.y = pack_bf16x2(x[j + 2], x[j + 3]);
         u.z = pack_bf16x2(x[j + 4], x[j + 5]);
         u.w = pack_bf16x2(x[j + 6], x[j + 7]);
-        *reinterpret_cast<uint4*>(p + j) = u;
+        if (cs) st_cs_v4(p + j, u);
+        else *reinterpret_cast<uint4*>(p + j) = u;
       }
       return;
     }
@@ -106,6 +108,7 @@ struct EpiFc1Fwd {
   const T* bias;  // [G*F] or null
   int F;
   const int* seg;
+  int cs;
   template <int W>
   __device__ __forceinline__ void apply(int g, int m, int n0, const float (&v)[W]) const {
     const int row = local_row(seg, g, m);
@@ -124,8 +127,8 @@ struct EpiFc1Fwd {
       d[j] = cdf + x * (__expf(-0.5f * x * x) * 0.39894228040143268f);
     }
     const size_t off = static_cast<size_t>(row) * F + n0;
-    store_row<T, W>(gelu_grad + off, d, valid);
-    store_row<T, W>(act + off, a, valid);
+    store_row<T, W>(gelu_grad + off, d, valid, cs);
+    store_row<T, W>(act + off, a, valid, cs);
   }
 };
 
@@ -142,6 +145,7 @@ struct EpiFc2Fwd {
   const float* w;  // [rows] gate weight per row
   int weight_scaling;
   float* out_acc;  // [N*H] fp32, zero-initialised
+  int cs;
   template <int W>
   __device__ __forceinline__ void apply(int g, int m, int n0, const float (&v)[W]) const {
     const int row = local_row(seg, g, m);
@@ -154,7 +158,7 @@ struct EpiFc2Fwd {
     float x[W];
 #pragma unroll
     for (int j = 0; j < W; ++j) x[j] = v[j] + b[j];
-    store_row<T, W>(y + static_cast<size_t>(row) * H + n0, x, valid);
+    store_row<T, W>(y + static_cast<size_t>(row) * H + n0, x, valid, cs);
     const int t = tok[row];
     if (t >= 0) {
       const float s = weight_scaling ? w[row] : 1.f;
@@ -170,6 +174,7 @@ struct EpiFc2Dgrad {
   const T* gelu_grad;
   int F;
   const int* seg;
+  int cs;
   template <int W>
   __device__ __forceinline__ void apply(int g, int m, int n0, const float (&v)[W]) const {
     const int row = local_row(seg, g, m);
@@ -180,7 +185,7 @@ struct EpiFc2Dgrad {
     float x[W];
 #pragma unroll
     for (int j = 0; j < W; ++j) x[j] = v[j] * gd[j];
-    store_row<T, W>(dh + off, x, valid);
+    store_row<T, W>(dh + off, x, valid, cs);
   }
 };
 
@@ -208,11 +213,12 @@ struct EpiWgrad {
   T* out;  // [G*M*N]
   int M;
   int N;
+  int cs;
   template <int W>
   __device__ __forceinline__ void apply(int g, int m, int n0, const float (&v)[W]) const {
     if (m >= M) return;
     const int valid = min(W, N - n0);
-    store_row<T, W>(out + (static_cast<size_t>(g) * M + m) * N + n0, v, valid);
+    store_row<T, W>(out + (static_cast<size_t>(g) * M + m) * N + n0, v, valid, cs);
   }
 };
 

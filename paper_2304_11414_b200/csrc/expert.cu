@@ -117,9 +117,36 @@ static int colsum(const void* src, int ld, const int* seg, int G, int N, void* o
   return check_launch("colsum");
 }
 
+// Tile order of the tcgen05 kernels (panel by default; PPMOE_ORDER=band selects the
+// banded order) and the epilogue store cache policy (streaming by default;
+// PPMOE_STORE=normal disables it).
+static int banded_order() {
+  static const int v = [] {
+    const char* e = getenv("PPMOE_ORDER");
+    return (e && strcmp(e, "band") == 0) ? 1 : 0;
+  }();
+  return v;
+}
+static int load_hint() {
+  static const int v = [] {
+    const char* e = getenv("PPMOE_HINT");
+    return (e && strcmp(e, "1") == 0) ? 1 : 0;
+  }();
+  return v;
+}
+static int stream_stores() {
+  static const int v = [] {
+    const char* e = getenv("PPMOE_STORE");
+    return (e && strcmp(e, "cs") == 0) ? 1 : 0;
+  }();
+  return v;
+}
+
 static GroupGeom geom(int G, int N, int M_fixed, int K_fixed, const int* seg, int a_seg, int a_stride, int b_seg,
                       int b_stride) {
   GroupGeom g;
+  g.banded = banded_order();
+  g.hint = load_hint();
   g.G = G;
   g.N = N;
   g.M_fixed = M_fixed;
@@ -148,10 +175,10 @@ int ppmoe_expert_fc1_fwd(int dtype, const void* Xs, const void* up, const void* 
     CUtensorMap ta, tb;
     if (int rc = tmap_kmajor(&ta, Xs, H, rows_cap, kBM)) return rc;
     if (int rc = tmap_mnmajor(&tb, up, F, static_cast<uint64_t>(El) * H)) return rc;
-    EpiFc1Fwd<bf16> epi{static_cast<bf16*>(GeluGrad), static_cast<bf16*>(Act), static_cast<const bf16*>(bias_up), F, seg};
+    EpiFc1Fwd<bf16> epi{static_cast<bf16*>(GeluGrad), static_cast<bf16*>(Act), static_cast<const bf16*>(bias_up), F, seg, stream_stores()};
     return launch_tc<false, true>(ta, tb, geo, epi, s);
   }
-  EpiFc1Fwd<float> epi{static_cast<float*>(GeluGrad), static_cast<float*>(Act), static_cast<const float*>(bias_up), F, seg};
+  EpiFc1Fwd<float> epi{static_cast<float*>(GeluGrad), static_cast<float*>(Act), static_cast<const float*>(bias_up), F, seg, 0};
   return launch_simt<float, false, true>(static_cast<const float*>(Xs), H, static_cast<const float*>(up), F, geo,
                                          rows_cap, epi, s);
 }
@@ -168,11 +195,11 @@ int ppmoe_expert_fc2_fwd(int dtype, const void* Act, const void* down, const voi
     if (int rc = tmap_kmajor(&ta, Act, F, rows_cap, kBM)) return rc;
     if (int rc = tmap_mnmajor(&tb, down, H, static_cast<uint64_t>(El) * F)) return rc;
     EpiFc2Fwd<bf16> epi{static_cast<bf16*>(Y), static_cast<const bf16*>(bias_down), H, seg, tok_local, w_local,
-                        weight_scaling, out_acc};
+                        weight_scaling, out_acc, stream_stores()};
     return launch_tc<false, true>(ta, tb, geo, epi, s);
   }
   EpiFc2Fwd<float> epi{static_cast<float*>(Y), static_cast<const float*>(bias_down), H, seg, tok_local, w_local,
-                       weight_scaling, out_acc};
+                       weight_scaling, out_acc, 0};
   return launch_simt<float, false, true>(static_cast<const float*>(Act), F, static_cast<const float*>(down), H, geo,
                                          rows_cap, epi, s);
 }
@@ -187,10 +214,10 @@ int ppmoe_expert_fc2_dgrad(int dtype, const void* dY, const void* down, const vo
     CUtensorMap ta, tb;
     if (int rc = tmap_kmajor(&ta, dY, H, rows_cap, kBM)) return rc;
     if (int rc = tmap_kmajor(&tb, down, H, static_cast<uint64_t>(El) * F, b_box_rows())) return rc;
-    EpiFc2Dgrad<bf16> epi{static_cast<bf16*>(dH), static_cast<const bf16*>(GeluGrad), F, seg};
+    EpiFc2Dgrad<bf16> epi{static_cast<bf16*>(dH), static_cast<const bf16*>(GeluGrad), F, seg, stream_stores()};
     return launch_tc<false, false>(ta, tb, geo, epi, s);
   }
-  EpiFc2Dgrad<float> epi{static_cast<float*>(dH), static_cast<const float*>(GeluGrad), F, seg};
+  EpiFc2Dgrad<float> epi{static_cast<float*>(dH), static_cast<const float*>(GeluGrad), F, seg, 0};
   return launch_simt<float, false, false>(static_cast<const float*>(dY), H, static_cast<const float*>(down), H, geo,
                                           rows_cap, epi, s);
 }
@@ -223,14 +250,14 @@ int ppmoe_expert_fc2_wgrad(int dtype, const void* Act, const void* dY, const int
       CUtensorMap ta, tb;
       if (int rc = tmap_mnmajor(&ta, Act, F, rows_cap)) return rc;
       if (int rc = tmap_mnmajor(&tb, dY, H, rows_cap)) return rc;
-      EpiWgrad<bf16> epi{static_cast<bf16*>(dDown), F, H};
+      EpiWgrad<bf16> epi{static_cast<bf16*>(dDown), F, H, stream_stores()};
       if (int rc = launch_tc<true, true>(ta, tb, geo, epi, s)) return rc;
     } else {
       PPMOE_CUDA(cudaMemsetAsync(dDown, 0, static_cast<size_t>(El) * F * H * 2, s));
     }
     return colsum<bf16>(dY, H, seg, El, H, dBiasDown, s);
   }
-  EpiWgrad<float> epi{static_cast<float*>(dDown), F, H};
+  EpiWgrad<float> epi{static_cast<float*>(dDown), F, H, 0};
   if (int rc = launch_simt<float, true, true>(static_cast<const float*>(Act), F, static_cast<const float*>(dY), H, geo,
                                               F, epi, s))
     return rc;
@@ -247,14 +274,14 @@ int ppmoe_expert_fc1_wgrad(int dtype, const void* Xs, const void* dH, const int*
       CUtensorMap ta, tb;
       if (int rc = tmap_mnmajor(&ta, Xs, H, rows_cap)) return rc;
       if (int rc = tmap_mnmajor(&tb, dH, F, rows_cap)) return rc;
-      EpiWgrad<bf16> epi{static_cast<bf16*>(dUp), H, F};
+      EpiWgrad<bf16> epi{static_cast<bf16*>(dUp), H, F, stream_stores()};
       if (int rc = launch_tc<true, true>(ta, tb, geo, epi, s)) return rc;
     } else {
       PPMOE_CUDA(cudaMemsetAsync(dUp, 0, static_cast<size_t>(El) * H * F * 2, s));
     }
     return colsum<bf16>(dH, F, seg, El, F, dBiasUp, s);
   }
-  EpiWgrad<float> epi{static_cast<float*>(dUp), H, F};
+  EpiWgrad<float> epi{static_cast<float*>(dUp), H, F, 0};
   if (int rc = launch_simt<float, true, true>(static_cast<const float*>(Xs), H, static_cast<const float*>(dH), F, geo,
                                               H, epi, s))
     return rc;

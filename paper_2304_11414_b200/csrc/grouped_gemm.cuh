@@ -39,6 +39,8 @@ struct GroupGeom {
   int a_stride;
   int b_seg;
   int b_stride;
+  int banded;     // 1: banded 2-D tile order with L2 residency hints, 0: panel order
+  int hint;       // panel order: load the streaming operand with evict-first priority
 };
 
 template <int BN>
@@ -71,15 +73,26 @@ struct SchedTables {
 // panels of that block are shared through L2 while the K loop streams.  The fast
 // dimension is N when the A panel is the larger one.
 constexpr int kBand = 8;
-__device__ __forceinline__ void tile_coords(const SchedTables& t, int g, int local, int n_tiles, int& mt, int& nt) {
+__device__ __forceinline__ void tile_coords(const SchedTables& t, int g, int local, int n_tiles, int& mt, int& nt,
+                                            int banded) {
   const int m_tiles = t.m_tiles[g];
-  if (t.n_fast[g]) {  // bands of kBand m-tiles, n advances slowest inside a band
+  if (!banded) {  // panel order: the fast dimension's whole panel shared by the wave
+    if (t.n_fast[g]) {
+      mt = local / n_tiles;
+      nt = local % n_tiles;
+    } else {
+      mt = local % m_tiles;
+      nt = local / m_tiles;
+    }
+    return;
+  }
+  if (t.n_fast[g]) {  // bands of kBand m-tiles (A band L2-resident), n advances slowest inside a band
     const int per_band = kBand * n_tiles;
     const int b = local / per_band, r = local % per_band;
     const int bw = min(kBand, m_tiles - b * kBand);
     mt = b * kBand + r % bw;
     nt = r / bw;
-  } else {  // bands of kBand n-tiles, m advances slowest inside a band
+  } else {  // bands of kBand n-tiles (B band L2-resident), m advances slowest inside a band
     const int per_band = kBand * m_tiles;
     const int b = local / per_band, r = local % per_band;
     const int bw = min(kBand, n_tiles - b * kBand);
@@ -167,7 +180,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         int g, local;
         sched_locate(tab, G, tile, g, local);
         int mt, nt;
-        tile_coords(tab, g, local, n_tiles, mt, nt);
+        tile_coords(tab, g, local, n_tiles, mt, nt, geo.banded);
         const int kb_n = tab.k_blocks[g];
         const int abase = tab.a_base[g];
         const int bbase = tab.b_base[g];
@@ -250,7 +263,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       int g, local;
       sched_locate(tab, G, tile, g, local);
       int mt, nt;
-      tile_coords(tab, g, local, n_tiles, mt, nt);
+      tile_coords(tab, g, local, n_tiles, mt, nt, geo.banded);
       const bool has_k = tab.k_blocks[g] > 0;
       const int acc = iter & 1;
       const uint32_t acc_phase = (iter >> 1) & 1;
@@ -383,12 +396,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         int g, local;
         sched_locate(tab, G, tile, g, local);
         int mt, nt;
-        tile_coords(tab, g, local, n_tiles, mt, nt);
+        tile_coords(tab, g, local, n_tiles, mt, nt, geo.banded);
         const int kb_n = tab.k_blocks[g];
         const int arow = mt * kPairBM + static_cast<int>(rank) * 128;
         const int bcol = nt * BN + static_cast<int>(rank) * (BN / 2);
         const int abase = tab.a_base[g];
         const int bbase = tab.b_base[g];
+        // the band-resident operand is kept in L2, the streaming one is evicted first
+        const bool a_res = tab.n_fast[g] != 0;
+        constexpr uint64_t kNormal = 0x1000000000000000ull;
+        uint64_t pol_a, pol_b;
+        if (geo.banded) {
+          pol_a = a_res ? kL2EvictLast : kL2EvictFirst;
+          pol_b = a_res ? kL2EvictFirst : kL2EvictLast;
+        } else {  // panel order: the fast dimension's operand is shared by the wave, the other streams
+          pol_a = (geo.hint && a_res) ? kL2EvictFirst : kNormal;
+          pol_b = (geo.hint && !a_res) ? kL2EvictFirst : kNormal;
+        }
         for (int kb = 0; kb < kb_n; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * L::kStageBytes;
@@ -398,16 +422,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           if (A_MN) {
 #pragma unroll
             for (int j = 0; j < 2; ++j)
-              tma_load_2d_pair(sa + j * (64 * kBK * 2), &tmap_a, fbar, arow + j * 64, abase + kb * kBK);
+              tma_load_2d_pair_hint(sa + j * (64 * kBK * 2), &tmap_a, fbar, arow + j * 64, abase + kb * kBK, pol_a);
           } else {
-            tma_load_2d_pair(sa, &tmap_a, fbar, kb * kBK, abase + arow);
+            tma_load_2d_pair_hint(sa, &tmap_a, fbar, kb * kBK, abase + arow, pol_a);
           }
           if (B_MN) {
 #pragma unroll
             for (int j = 0; j < BN / 128; ++j)
-              tma_load_2d_pair(sb + j * (64 * kBK * 2), &tmap_b, fbar, bcol + j * 64, bbase + kb * kBK);
+              tma_load_2d_pair_hint(sb + j * (64 * kBK * 2), &tmap_b, fbar, bcol + j * 64, bbase + kb * kBK, pol_b);
           } else {
-            tma_load_2d_pair(sb, &tmap_b, fbar, kb * kBK, bbase + bcol);
+            tma_load_2d_pair_hint(sb, &tmap_b, fbar, kb * kBK, bbase + bcol, pol_b);
           }
           if (++stage == kPairStages) {
             stage = 0;
@@ -468,7 +492,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       int g, local;
       sched_locate(tab, G, tile, g, local);
       int mt, nt;
-      tile_coords(tab, g, local, n_tiles, mt, nt);
+      tile_coords(tab, g, local, n_tiles, mt, nt, geo.banded);
       const bool has_k = tab.k_blocks[g] > 0;
       const int acc = iter & 1;
       const uint32_t acc_phase = (iter >> 1) & 1;

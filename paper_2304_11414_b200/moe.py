@@ -455,14 +455,19 @@ class _PPMoEFunction(torch.autograd.Function):
         if spec.aux_here and g_aux is not None:
             aux = g_aux.detach().to(torch.float32).reshape(1).contiguous()
         dx_acc = torch.zeros((n, h), dtype=torch.float32, device=hidden.device)
-        dw, d_up, d_down, d_bu, d_bd = _ops.experts_backward(g_out, st, up, down, has_bias, spec.weight_scaling,
-                                                             dx_acc)
+        # data gradients first: dX can go on the wire while the weight gradients compute
+        dy, dh, dw = _ops.experts_backward_data(g_out, st, up, down, spec.weight_scaling, dx_acc)
         dl = _ops.gate_backward(rt, pl, st, dw, aux)
         need_dx = ctx.needs_input_grad[0]
         need_dwg = ctx.needs_input_grad[1]
         dx, dwg = _ops.gate_grads(dx_acc, hidden, dl, wg, need_dx, need_dwg)
-        if need_dx:
-            spec.world.all_reduce_(spec.group, dx)  # copy_to_tensor_parallel_region backward
+        del dx_acc
+        work = None
+        if need_dx:  # copy_to_tensor_parallel_region backward (collectives.py:215-221)
+            work = spec.world.all_reduce_async(spec.group, dx)
+        d_up, d_down, d_bu, d_bd = _ops.experts_backward_weights(st, dy, dh, up, down, has_bias)
+        if work is not None:
+            work.wait()  # stream-ordered: the compute stream waits for the NCCL stream
         ctx.state = None
         return dx, dwg, d_up, d_down, d_bu, d_bd, None
 
