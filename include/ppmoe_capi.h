@@ -94,19 +94,29 @@ int ppmoe_dispatch_plan(const int* idx, const float* w, int N, int E, int K, int
 int ppmoe_gather(const void* X, int dtype, int N, int H, const int* seg, int El, const int* tok_sorted,
                  const float* w_sorted, int rows_cap, void* Xs, int* tok_local, float* w_local, void* stream);
 
+/* Token-chunk row ranges: for chunk c of C (tokens [c*N/C, (c+1)*N/C)) and local
+ * expert g, row_lo/row_hi[c*El+g] = local rows of that expert's segment holding the
+ * chunk's tokens (segments are ascending in token id).  kept = plan kept counts of the
+ * El local experts.  Used to pipeline the forward combine all-reduce by token chunk. */
+int ppmoe_chunk_rows(const int* tok_local, const int* seg, const int* kept, int El, int N, int C, int* row_lo,
+                     int* row_hi, void* stream);
+
 /* Expert FFN forward, first GEMM: a = Xs*up_g + bias_up, Act = GeLU(a), and
  * GeluGrad = GeLU'(a) saved for the backward (ExpertFfn.forward, moe.py:100-104;
- * gelu backward tensor.py:204-207).  bias_up may be NULL.                  */
+ * gelu backward tensor.py:204-207).  bias_up may be NULL.  row_lo/row_hi [El]
+ * (both NULL = whole segments) restrict each expert to a row range.           */
 int ppmoe_expert_fc1_fwd(int dtype, const void* Xs, const void* up, const void* bias_up, const int* seg, int El,
-                         int H, int F, int rows_cap, void* GeluGrad, void* Act, void* stream);
+                         int H, int F, int rows_cap, const int* row_lo, const int* row_hi, void* GeluGrad, void* Act,
+                         void* stream);
 
 /* Expert FFN forward, second GEMM fused with the gate-weighted combine:
  * Y = Act*down_g + bias_down (stored, pre-scale), out_acc[tok] += w*Y
  * (moe.py:104-107, scale_rows tensor.py:184-196, index_assign 244-272).
  * out_acc [N x H] fp32 must be zeroed by the caller.                       */
 int ppmoe_expert_fc2_fwd(int dtype, const void* Act, const void* down, const void* bias_down, const int* seg,
-                         int El, int H, int F, int rows_cap, const int* tok_local, const float* w_local,
-                         int weight_scaling, void* Y, float* out_acc, void* stream);
+                         int El, int H, int F, int rows_cap, const int* row_lo, const int* row_hi,
+                         const int* tok_local, const float* w_local, int weight_scaling, void* Y, float* out_acc,
+                         void* stream);
 
 /* out = out_acc cast to dtype (the replicated [N x H] layer output before or
  * after the TP all-reduce, collectives.py:135-153).                         */

@@ -171,9 +171,11 @@ class ExpertFwdState:
 
 
 def experts_forward(hidden, pl: Plan, e0: int, el: int, up, down, bias_up, bias_down, k: int, weight_scaling: bool,
-                    out_acc: torch.Tensor) -> ExpertFwdState:
+                    out_acc: torch.Tensor, chunks: int = 1, on_chunk=None) -> ExpertFwdState:
     """index-slice gather -> fc1 (+bias, GeLU) -> fc2 (+bias, gate-scaled scatter-add combine)
-    for experts [e0, e0+el) (moe.py:294-305)."""
+    for experts [e0, e0+el) (moe.py:294-305).  With chunks > 1 the two GEMMs run per token
+    chunk (each expert segment is ascending in token id, so a chunk is a row range) and
+    ``on_chunk(c)`` is called once chunk c's rows of out_acc are final on this rank."""
     n, h = hidden.shape
     f = up.shape[2]
     dt = dtype_code(hidden.dtype)
@@ -188,10 +190,24 @@ def experts_forward(hidden, pl: Plan, e0: int, el: int, up, down, bias_up, bias_
          ptr(tok_l), ptr(w_l), s)
     gelu_grad = torch.empty((rows_cap, f), dtype=hidden.dtype, device=dev)
     act = torch.empty((rows_cap, f), dtype=hidden.dtype, device=dev)
-    call("ppmoe_expert_fc1_fwd", dt, ptr(xs), ptr(up), ptr(bias_up), ptr(seg), el, h, f, rows_cap, ptr(gelu_grad), ptr(act), s)
     y = torch.empty((rows_cap, h), dtype=hidden.dtype, device=dev)
-    call("ppmoe_expert_fc2_fwd", dt, ptr(act), ptr(down), ptr(bias_down), ptr(seg), el, h, f, rows_cap, ptr(tok_l),
-         ptr(w_l), int(bool(weight_scaling)), ptr(y), ptr(out_acc), s)
+
+    def gemms(rlo, rhi):
+        call("ppmoe_expert_fc1_fwd", dt, ptr(xs), ptr(up), ptr(bias_up), ptr(seg), el, h, f, rows_cap, ptr(rlo),
+             ptr(rhi), ptr(gelu_grad), ptr(act), s)
+        call("ppmoe_expert_fc2_fwd", dt, ptr(act), ptr(down), ptr(bias_down), ptr(seg), el, h, f, rows_cap, ptr(rlo),
+             ptr(rhi), ptr(tok_l), ptr(w_l), int(bool(weight_scaling)), ptr(y), ptr(out_acc), s)
+
+    if chunks <= 1:
+        gemms(None, None)
+    else:
+        rlo = torch.empty(chunks * el, dtype=torch.int32, device=dev)
+        rhi = torch.empty(chunks * el, dtype=torch.int32, device=dev)
+        call("ppmoe_chunk_rows", ptr(tok_l), ptr(seg), ptr(pl.kept[e0:e0 + el]), el, n, chunks, ptr(rlo), ptr(rhi), s)
+        for c in range(chunks):
+            gemms(rlo[c * el:(c + 1) * el], rhi[c * el:(c + 1) * el])
+            if on_chunk is not None:
+                on_chunk(c)
     return ExpertFwdState(e0, el, rows_cap, seg, xs, tok_l, w_l, gelu_grad, act, y)
 
 
@@ -256,7 +272,8 @@ def gate_grads(dx_acc, hidden, dl, wg, want_dx: bool, want_dwg: bool):
     return dx, dwg
 
 
-def cast_out(acc: torch.Tensor, dtype: torch.dtype) -> torch.Tensor:
-    out = torch.empty(acc.shape, dtype=dtype, device=acc.device)
+def cast_out(acc: torch.Tensor, dtype: torch.dtype, out: torch.Tensor | None = None) -> torch.Tensor:
+    if out is None:
+        out = torch.empty(acc.shape, dtype=dtype, device=acc.device)
     call("ppmoe_cast_out", ptr(acc), acc.numel(), ptr(out), dtype_code(dtype), _stream())
     return out

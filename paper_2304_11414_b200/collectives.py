@@ -165,11 +165,13 @@ class World:
             dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.torch_group(group))
         return t
 
-    def all_reduce_async(self, group: ProcessGroup, t: torch.Tensor, op_kind: str = "all_reduce"):
+    def all_reduce_async(self, group: ProcessGroup, t: torch.Tensor, op_kind: str = "all_reduce",
+                         charge: bool = True):
         """Start an in-place NCCL sum on the process group's stream (after the work already
         queued on the current stream); returns a handle whose ``wait()`` makes the current
         stream wait for it, or None when there is nothing to communicate."""
-        self.charge_all_reduce(group, t.numel(), op_kind)
+        if charge:
+            self.charge_all_reduce(group, t.numel(), op_kind)
         if self.distributed and group.size > 1:
             return dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.torch_group(group), async_op=True)
         return None

@@ -213,6 +213,32 @@ __global__ void gate_bwd_kernel(const float* __restrict__ scores, const int* __r
   if (active) dL[static_cast<size_t>(t) * E + e] = s * (ds - red[tl]);
 }
 
+// Token-chunk row ranges of every local expert segment: rows are in ascending token
+// order inside a segment, so chunk c (tokens [c*N/C, (c+1)*N/C)) is a contiguous row
+// range found by binary search over the segment's kept rows.
+__global__ void chunk_rows_kernel(const int* __restrict__ tok_local, const int* __restrict__ seg,
+                                  const int* __restrict__ kept, int El, int N, int C, int* __restrict__ row_lo,
+                                  int* __restrict__ row_hi) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= C * El) return;
+  const int c = i / El, g = i % El;
+  const int base = seg[g] - seg[0];
+  const int cnt = kept[g];
+  auto lower = [&](int t) {
+    int lo = 0, hi = cnt;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (tok_local[base + mid] < t) lo = mid + 1;
+      else hi = mid;
+    }
+    return base + lo;
+  };
+  const long long t_lo = static_cast<long long>(c) * N / C;
+  const long long t_hi = static_cast<long long>(c + 1) * N / C;
+  row_lo[i] = lower(static_cast<int>(t_lo));
+  row_hi[i] = lower(static_cast<int>(t_hi));
+}
+
 constexpr int kGradTC = 128;  // tokens per chunk of the dWg partials
 
 template <typename T, int EB>
@@ -309,6 +335,15 @@ int ppmoe_gather(const void* X, int dtype, int N, int H, const int* seg, int El,
     gather_warp_kernel<float><<<grid * 4, 256, 0, s>>>(static_cast<const float*>(X), H, seg, El, tok_sorted, w_sorted,
                                                        static_cast<float*>(Xs), tok_local, w_local);
   return check_launch("gather_warp_kernel");
+}
+
+int ppmoe_chunk_rows(const int* tok_local, const int* seg, const int* kept, int El, int N, int C, int* row_lo,
+                     int* row_hi, void* stream) {
+  PPMOE_REQUIRE(El >= 1 && N >= 0 && C >= 1, "bad chunk_rows arguments El=%d N=%d C=%d", El, N, C);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int n = C * El;
+  chunk_rows_kernel<<<(n + 127) / 128, 128, 0, s>>>(tok_local, seg, kept, El, N, C, row_lo, row_hi);
+  return check_launch("chunk_rows_kernel");
 }
 
 int ppmoe_cast_out(const float* acc, int n, void* out, int dtype, void* stream) {

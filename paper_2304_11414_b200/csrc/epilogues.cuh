@@ -1,8 +1,8 @@
 // Epilogue functors for the grouped expert GEMMs.  Each is applied to one row
-// (`m` within expert `g`) and W consecutive output columns starting at `n0`,
+// (`m` within expert `g`; `row` = its local position in the padded dispatch buffer
+// for token-segment outputs) and W consecutive output columns starting at `n0`,
 // with the fp32 accumulator values `v` read straight from TMEM (or registers in
-// the CUDA-core path).  Row indices of token-segment operands are local
-// positions in the padded dispatch buffer: row = seg[g] - seg[0] + m.
+// the CUDA-core path).
 #pragma once
 
 #include <type_traits>
@@ -96,8 +96,6 @@ __device__ __forceinline__ void scatter_add_row(float* p, const float (&x)[W], f
     if (j < valid) atomicAdd(p + j, s * x[j]);
 }
 
-__device__ __forceinline__ int local_row(const int* seg, int g, int m) { return seg[g] - seg[0] + m; }
-
 // fc1 forward: a = X_e * up_e + bias_up ; Act = GeLU(a), and GeLU'(a) saved for the
 // backward so the fc2 data-gradient epilogue is a plain multiply (moe.py:101-104,
 // tensor.py:199-207).
@@ -110,8 +108,7 @@ struct EpiFc1Fwd {
   const int* seg;
   int cs;
   template <int W>
-  __device__ __forceinline__ void apply(int g, int m, int n0, const float (&v)[W]) const {
-    const int row = local_row(seg, g, m);
+  __device__ __forceinline__ void apply(int g, int m, int row, int n0, const float (&v)[W]) const {
     const int valid = min(W, F - n0);
     float b[W];
     if (bias) load_row<T, W>(bias + static_cast<size_t>(g) * F + n0, b, valid);
@@ -147,8 +144,7 @@ struct EpiFc2Fwd {
   float* out_acc;  // [N*H] fp32, zero-initialised
   int cs;
   template <int W>
-  __device__ __forceinline__ void apply(int g, int m, int n0, const float (&v)[W]) const {
-    const int row = local_row(seg, g, m);
+  __device__ __forceinline__ void apply(int g, int m, int row, int n0, const float (&v)[W]) const {
     const int valid = min(W, H - n0);
     float b[W];
     if (bias) load_row<T, W>(bias + static_cast<size_t>(g) * H + n0, b, valid);
@@ -176,8 +172,7 @@ struct EpiFc2Dgrad {
   const int* seg;
   int cs;
   template <int W>
-  __device__ __forceinline__ void apply(int g, int m, int n0, const float (&v)[W]) const {
-    const int row = local_row(seg, g, m);
+  __device__ __forceinline__ void apply(int g, int m, int row, int n0, const float (&v)[W]) const {
     const int valid = min(W, F - n0);
     const size_t off = static_cast<size_t>(row) * F + n0;
     float gd[W];
@@ -198,8 +193,7 @@ struct EpiFc1Dgrad {
   const int* seg;
   const int* tok;
   template <int W>
-  __device__ __forceinline__ void apply(int g, int m, int n0, const float (&v)[W]) const {
-    const int row = local_row(seg, g, m);
+  __device__ __forceinline__ void apply(int g, int m, int row, int n0, const float (&v)[W]) const {
     const int t = tok[row];
     if (t < 0) return;
     const int valid = min(W, H - n0);
@@ -215,7 +209,7 @@ struct EpiWgrad {
   int N;
   int cs;
   template <int W>
-  __device__ __forceinline__ void apply(int g, int m, int n0, const float (&v)[W]) const {
+  __device__ __forceinline__ void apply(int g, int m, int row, int n0, const float (&v)[W]) const {
     if (m >= M) return;
     const int valid = min(W, N - n0);
     store_row<T, W>(out + (static_cast<size_t>(g) * M + m) * N + n0, v, valid, cs);
@@ -231,11 +225,11 @@ struct EpiStore {
   int ldo_rows_from_seg;  // 1: row = local segment row, 0: row = g*M_fixed + m
   int M_fixed;
   template <int W>
-  __device__ __forceinline__ void apply(int g, int m, int n0, const float (&v)[W]) const {
+  __device__ __forceinline__ void apply(int g, int m, int row, int n0, const float (&v)[W]) const {
     if (!ldo_rows_from_seg && m >= M_fixed) return;
-    const int row = ldo_rows_from_seg ? local_row(seg, g, m) : g * M_fixed + m;
+    const int orow = ldo_rows_from_seg ? row : g * M_fixed + m;
     const int valid = min(W, N - n0);
-    store_row<T, W>(out + static_cast<size_t>(row) * N + n0, v, valid);
+    store_row<T, W>(out + static_cast<size_t>(orow) * N + n0, v, valid);
   }
 };
 

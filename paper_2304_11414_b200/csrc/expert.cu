@@ -145,6 +145,8 @@ static int stream_stores() {
 static GroupGeom geom(int G, int N, int M_fixed, int K_fixed, const int* seg, int a_seg, int a_stride, int b_seg,
                       int b_stride) {
   GroupGeom g;
+  g.rlo = nullptr;
+  g.rhi = nullptr;
   g.banded = banded_order();
   g.hint = load_hint();
   g.G = G;
@@ -166,10 +168,14 @@ using namespace ppmoe;
 extern "C" {
 
 int ppmoe_expert_fc1_fwd(int dtype, const void* Xs, const void* up, const void* bias_up, const int* seg, int El, int H,
-                         int F, int rows_cap, void* GeluGrad, void* Act, void* stream) {
+                         int F, int rows_cap, const int* row_lo, const int* row_hi, void* GeluGrad, void* Act,
+                         void* stream) {
   if (int rc = check_common(dtype, El, H, F, rows_cap)) return rc;
+  PPMOE_REQUIRE((row_lo == nullptr) == (row_hi == nullptr), "row_lo and row_hi must both be given or both be NULL");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   GroupGeom geo = geom(El, F, 0, H, seg, 1, 0, 0, H);
+  geo.rlo = row_lo;
+  geo.rhi = row_hi;
   if (rows_cap == 0) return kOk;
   if (dtype == kBF16) {
     CUtensorMap ta, tb;
@@ -184,11 +190,14 @@ int ppmoe_expert_fc1_fwd(int dtype, const void* Xs, const void* up, const void* 
 }
 
 int ppmoe_expert_fc2_fwd(int dtype, const void* Act, const void* down, const void* bias_down, const int* seg, int El,
-                         int H, int F, int rows_cap, const int* tok_local, const float* w_local, int weight_scaling,
-                         void* Y, float* out_acc, void* stream) {
+                         int H, int F, int rows_cap, const int* row_lo, const int* row_hi, const int* tok_local,
+                         const float* w_local, int weight_scaling, void* Y, float* out_acc, void* stream) {
   if (int rc = check_common(dtype, El, H, F, rows_cap)) return rc;
+  PPMOE_REQUIRE((row_lo == nullptr) == (row_hi == nullptr), "row_lo and row_hi must both be given or both be NULL");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   GroupGeom geo = geom(El, H, 0, F, seg, 1, 0, 0, F);
+  geo.rlo = row_lo;
+  geo.rhi = row_hi;
   if (rows_cap == 0) return kOk;
   if (dtype == kBF16) {
     CUtensorMap ta, tb;

@@ -39,6 +39,8 @@ struct GroupGeom {
   int a_stride;
   int b_seg;
   int b_stride;
+  const int* rlo; // optional [G] local first row of each group (token chunk of a segment)
+  const int* rhi; // optional [G] local end row; when set, M_g = rhi - rlo (seg ignored for rows)
   int banded;     // 1: banded 2-D tile order with L2 residency hints, 0: panel order
   int hint;       // panel order: load the streaming operand with evict-first priority
 };
@@ -52,7 +54,7 @@ struct GemmSmem {
   // full[S], empty[S], tmem_full[2], tmem_empty[2], tmem base, scheduler tables
   static constexpr int kBarBytes = (2 * kStages + 4) * 8 + 16;
   static constexpr int kSchedOffset = kBarOffset + kBarBytes;
-  static constexpr int kSchedBytes = (kMaxGroups + 1) * 4 * 7;
+  static constexpr int kSchedBytes = (kMaxGroups + 1) * 4 * 8;
   static constexpr int kTotal = kSchedOffset + kSchedBytes + 1024;  // + alignment slack
 };
 
@@ -65,6 +67,7 @@ struct SchedTables {
   int* b_base;      // [G]
   int* n_fast;      // [G] 1: walk n-tiles fastest (A panel larger than B panel), else m-tiles fastest
   int* m_rows;      // [G] valid rows of the group (epilogue row mask)
+  int* row_base;    // [G] local buffer row of the group's first row
 };
 
 // Tile (m, n) of the local index inside group g.  Tiles are walked in bands of
@@ -124,7 +127,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
   int* sched = reinterpret_cast<int*>(smem + L::kSchedOffset);
   SchedTables tab{sched, sched + (kMaxGroups + 1), sched + 2 * (kMaxGroups + 1), sched + 3 * (kMaxGroups + 1),
-                  sched + 4 * (kMaxGroups + 1), sched + 5 * (kMaxGroups + 1), sched + 6 * (kMaxGroups + 1)};
+                  sched + 4 * (kMaxGroups + 1), sched + 5 * (kMaxGroups + 1), sched + 6 * (kMaxGroups + 1),
+                  sched + 7 * (kMaxGroups + 1)};
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -135,8 +139,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int s0 = geo.seg[0];
     int acc = 0;
     for (int g = 0; g < G; ++g) {
-      const int seg_lo = geo.seg[g] - s0;
-      const int seg_rows = geo.seg[g + 1] - geo.seg[g];
+      const int seg_lo = geo.rlo ? geo.rlo[g] : geo.seg[g] - s0;
+      const int seg_rows = geo.rlo ? geo.rhi[g] - geo.rlo[g] : geo.seg[g + 1] - geo.seg[g];
       const int M = geo.M_fixed > 0 ? geo.M_fixed : seg_rows;
       const int K = geo.K_fixed > 0 ? geo.K_fixed : seg_rows;
       tab.tile_start[g] = acc;
@@ -146,6 +150,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       tab.b_base[g] = geo.b_seg ? seg_lo : g * geo.b_stride;
       tab.n_fast[g] = M > geo.N ? 1 : 0;
       tab.m_rows[g] = M;
+      tab.row_base[g] = seg_lo;
       acc += tab.m_tiles[g] * n_tiles;
     }
     tab.tile_start[G] = acc;
@@ -280,7 +285,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           for (int j = 0; j < 32; ++j) v[j] = 0.f;
         }
         const int n0 = nt * BN + c * 32;
-        if (n0 < geo.N && m < tab.m_rows[g]) epi.template apply<32>(g, m, n0, v);
+        if (n0 < geo.N && m < tab.m_rows[g]) epi.template apply<32>(g, m, tab.row_base[g] + m, n0, v);
       }
       tc_fence_before();
       __syncwarp();
@@ -316,7 +321,7 @@ struct PairSmem {
   static constexpr int kBarOffset = kPairStages * kStageBytes;
   static constexpr int kBarBytes = (2 * kPairStages + 4) * 8 + 16;
   static constexpr int kSchedOffset = kBarOffset + kBarBytes;
-  static constexpr int kSchedBytes = (kMaxGroups + 1) * 4 * 7;
+  static constexpr int kSchedBytes = (kMaxGroups + 1) * 4 * 8;
   static constexpr int kTotal = kSchedOffset + kSchedBytes + 1024;
 };
 
@@ -336,7 +341,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
   int* sched = reinterpret_cast<int*>(smem + L::kSchedOffset);
   SchedTables tab{sched, sched + (kMaxGroups + 1), sched + 2 * (kMaxGroups + 1), sched + 3 * (kMaxGroups + 1),
-                  sched + 4 * (kMaxGroups + 1), sched + 5 * (kMaxGroups + 1), sched + 6 * (kMaxGroups + 1)};
+                  sched + 4 * (kMaxGroups + 1), sched + 5 * (kMaxGroups + 1), sched + 6 * (kMaxGroups + 1),
+                  sched + 7 * (kMaxGroups + 1)};
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -351,8 +357,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     const int s0 = geo.seg[0];
     int acc = 0;
     for (int g = 0; g < G; ++g) {
-      const int seg_lo = geo.seg[g] - s0;
-      const int seg_rows = geo.seg[g + 1] - geo.seg[g];
+      const int seg_lo = geo.rlo ? geo.rlo[g] : geo.seg[g] - s0;
+      const int seg_rows = geo.rlo ? geo.rhi[g] - geo.rlo[g] : geo.seg[g + 1] - geo.seg[g];
       const int M = geo.M_fixed > 0 ? geo.M_fixed : seg_rows;
       const int K = geo.K_fixed > 0 ? geo.K_fixed : seg_rows;
       tab.tile_start[g] = acc;
@@ -362,6 +368,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       tab.b_base[g] = geo.b_seg ? seg_lo : g * geo.b_stride;
       tab.n_fast[g] = M > geo.N ? 1 : 0;
       tab.m_rows[g] = M;
+      tab.row_base[g] = seg_lo;
       acc += tab.m_tiles[g] * n_tiles;
     }
     tab.tile_start[G] = acc;
@@ -509,7 +516,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           for (int j = 0; j < 32; ++j) v[j] = 0.f;
         }
         const int n0 = nt * BN + c * 32;
-        if (n0 < geo.N && m < tab.m_rows[g]) epi.template apply<32>(g, m, n0, v);
+        if (n0 < geo.N && m < tab.m_rows[g]) epi.template apply<32>(g, m, tab.row_base[g] + m, n0, v);
       }
       tc_fence_before();
       __syncwarp();
@@ -535,8 +542,8 @@ __global__ void __launch_bounds__(256)
   __shared__ float Bs[16][64 + 4];
   const int g = blockIdx.z;
   const int s0 = geo.seg[0];
-  const int seg_lo = geo.seg[g] - s0;
-  const int seg_rows = geo.seg[g + 1] - geo.seg[g];
+  const int seg_lo = geo.rlo ? geo.rlo[g] : geo.seg[g] - s0;
+  const int seg_rows = geo.rlo ? geo.rhi[g] - geo.rlo[g] : geo.seg[g + 1] - geo.seg[g];
   const int M = geo.M_fixed > 0 ? geo.M_fixed : seg_rows;
   const int K = geo.K_fixed > 0 ? geo.K_fixed : seg_rows;
   const int m0 = blockIdx.y * 64;
@@ -577,7 +584,7 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int m = m0 + ty * 4 + i;
-    if (m < M && n0 + tx * 4 < geo.N) epi.template apply<4>(g, m, n0 + tx * 4, acc[i]);
+    if (m < M && n0 + tx * 4 < geo.N) epi.template apply<4>(g, m, seg_lo + m, n0 + tx * 4, acc[i]);
   }
 }
 

@@ -16,6 +16,7 @@ grouped GEMM serves all of them; ``ExpertFfn`` objects are views into a bank.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -418,6 +419,7 @@ class _Spec:
     e0: int
     el: int
     aux_here: bool
+    fwd_chunks: int = 1
 
 
 class _PPMoEFunction(torch.autograd.Function):
@@ -433,11 +435,31 @@ class _PPMoEFunction(torch.autograd.Function):
         cap = _ops.capacity_for(spec.capacity_factor, n, spec.k, e)
         pl = _ops.plan(rt.idx, rt.w, e, cap)
         out_acc = torch.zeros((n, h), dtype=torch.float32, device=hidden.device)
-        st = _ops.experts_forward(hidden, pl, spec.e0, spec.el, up, down, bias_up, bias_down, spec.k,
-                                  spec.weight_scaling, out_acc)
-        out = _ops.cast_out(out_acc, hidden.dtype)
+        if spec.fwd_chunks > 1:
+            # combine all-reduce pipelined by token chunk: chunk c goes on the wire while the
+            # expert GEMMs of chunk c+1 run (reduce_from_tensor_parallel_region, moe.py:307)
+            out = torch.empty((n, h), dtype=hidden.dtype, device=hidden.device)
+            works = []
+            bounds = [c * n // spec.fwd_chunks for c in range(spec.fwd_chunks + 1)]
+
+            def on_chunk(c):
+                lo, hi = bounds[c], bounds[c + 1]
+                if hi > lo:
+                    _ops.cast_out(out_acc[lo:hi], hidden.dtype, out[lo:hi])
+                    works.append(spec.world.all_reduce_async(spec.group, out[lo:hi], charge=False))
+
+            st = _ops.experts_forward(hidden, pl, spec.e0, spec.el, up, down, bias_up, bias_down, spec.k,
+                                      spec.weight_scaling, out_acc, spec.fwd_chunks, on_chunk)
+            spec.world.charge_all_reduce(spec.group, out.numel())
+            for wk in works:
+                if wk is not None:
+                    wk.wait()
+        else:
+            st = _ops.experts_forward(hidden, pl, spec.e0, spec.el, up, down, bias_up, bias_down, spec.k,
+                                      spec.weight_scaling, out_acc)
+            out = _ops.cast_out(out_acc, hidden.dtype)
+            spec.world.all_reduce_(spec.group, out)  # reduce_from_tensor_parallel_region (moe.py:307)
         del out_acc
-        spec.world.all_reduce_(spec.group, out)  # reduce_from_tensor_parallel_region (moe.py:307)
         ctx.save_for_backward(hidden, wg, up, down)
         ctx.state = (rt, pl, st, bias_up is not None, spec)
         l_aux = rt.l_aux[0].to(torch.float32)
@@ -537,7 +559,12 @@ def ppmoe_forward(world: World, group: ProcessGroup, hidden, gate, experts_by_ra
     for p in (local.up, local.down, local.bias_up, local.bias_down):
         if p is not None and p.dtype != wdt:
             raise ValueError(f"expert weights must match the hidden dtype {wdt}, got {p.dtype}")
-    spec = _Spec(world, group, top_k, float(capacity_factor), bool(weight_scaling), ov, e0, el, aux_here)
+    env_chunks = os.environ.get("PPMOE_FWD_CHUNKS")
+    if env_chunks is not None:
+        chunks = max(1, int(env_chunks))
+    else:
+        chunks = 4 if (world.distributed and tp > 1) else 1
+    spec = _Spec(world, group, top_k, float(capacity_factor), bool(weight_scaling), ov, e0, el, aux_here, chunks)
     wg = gate.wg if gate.wg.dtype == torch.float32 else gate.wg.float()
     out, l_aux = _PPMoEFunction.apply(hidden.contiguous(), wg, local.up.contiguous(), local.down.contiguous(),
                                       None if local.bias_up is None else local.bias_up.contiguous(),

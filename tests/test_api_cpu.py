@@ -49,7 +49,7 @@ def test_invalid_arguments_raise_value_error_without_gpu():
     with pytest.raises(ValueError, match="zero tokens"):
         _lib.call("ppmoe_route", None, 0, None, 0, 16, 4, 1, None, None, None, None, None, None, None, 0, None)
     with pytest.raises(ValueError, match="divisible by 8"):
-        _lib.call("ppmoe_expert_fc1_fwd", 0, None, None, None, None, 2, 12, 48, 128, None, None, None)
+        _lib.call("ppmoe_expert_fc1_fwd", 0, None, None, None, None, 2, 12, 48, 128, None, None, None, None, None)
 
 
 def test_layer_config_round_trip():

@@ -255,3 +255,17 @@ def test_deterministic_bit_identical_runs():
     assert np.array_equal(r1["grad_hidden"], r2["grad_hidden"])
     for k in r1["grads"]:
         assert np.array_equal(r1["grads"][k], r2["grads"][k]), k
+
+
+@pytest.mark.parametrize("chunks", [2, 3, 5])
+def test_token_chunked_forward_bit_identical(chunks, monkeypatch):
+    """The all-reduce pipelining path (fc1/fc2 per token chunk) gives bit-identical results."""
+    layer = oracle_rounded(O.init_layer(256, 8, seed=9), torch.bfloat16)
+    hidden = torch.randn(1500, 256).bfloat16().double().numpy()
+    base = run_cuda_layer(hidden, device_weights(layer, torch.bfloat16), k=2, capacity_factor=1.1)
+    monkeypatch.setenv("PPMOE_FWD_CHUNKS", str(chunks))
+    got = run_cuda_layer(hidden, device_weights(layer, torch.bfloat16), k=2, capacity_factor=1.1)
+    assert np.array_equal(base["out"], got["out"])
+    assert np.array_equal(base["grad_hidden"], got["grad_hidden"])
+    for k in base["grads"]:
+        assert np.array_equal(base["grads"][k], got["grads"][k]), k
