@@ -44,6 +44,9 @@ int ppmoe_version(void);
 const char* ppmoe_last_error(void);
 /* Number of SMs of the current device (grid sizing of the persistent kernels). */
 int ppmoe_num_sms(void);
+/* Persistent-GEMM grid budget for the calling host thread: 0 = one CTA per SM (default);
+ * n > 0 = at most n CTAs, leaving SMs free for a collective that runs concurrently. */
+int ppmoe_set_gemm_sm_budget(int sms);
 /* Diagnostic counter: kernels this library has launched in this process (all threads). */
 unsigned long long ppmoe_kernel_launches(void);
 
@@ -97,7 +100,8 @@ int ppmoe_gather(const void* X, int dtype, int N, int H, const int* seg, int El,
 /* Token-chunk row ranges: for chunk c of C (tokens [c*N/C, (c+1)*N/C)) and local
  * expert g, row_lo/row_hi[c*El+g] = local rows of that expert's segment holding the
  * chunk's tokens (segments are ascending in token id).  kept = plan kept counts of the
- * El local experts.  Used to pipeline the forward combine all-reduce by token chunk. */
+ * El local experts; row_lo/row_hi hold (C+1)*El entries, the last El being each segment's
+ * padding rows.  Used to pipeline the forward combine all-reduce by token chunk.        */
 int ppmoe_chunk_rows(const int* tok_local, const int* seg, const int* kept, int El, int N, int C, int* row_lo,
                      int* row_hi, void* stream);
 

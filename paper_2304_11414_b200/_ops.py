@@ -9,6 +9,7 @@ stays on the device (padded segments) and the GEMM tile schedulers read it.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import torch
@@ -27,12 +28,47 @@ def dtype_code(dt: torch.dtype) -> int:
         raise ValueError(f"PPMoE kernels support bf16 and fp32 activations, got {dt}") from None
 
 
+def _act(shape, dtype, device) -> torch.Tensor:
+    """Activation/scratch buffer.  PPMOE_POISON=1 fills it with NaN (ints: -7) so that any
+    read of a row a kernel should have written shows up in the parity tests."""
+    if os.environ.get("PPMOE_POISON") == "1":
+        return torch.full(shape, float("nan") if dtype.is_floating_point else -7, dtype=dtype, device=device)
+    return torch.empty(shape, dtype=dtype, device=device)
+
+
 def _ws(nbytes: int, device) -> torch.Tensor:
     return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
 
 
 def _stream():
     return _lib.stream_ptr()
+
+
+class sm_budget:
+    """Context manager: persistent GEMMs use at most `sms` SMs (0 = all) so that an NCCL
+    collective running concurrently on its own stream gets SMs (overlap instead of queueing)."""
+
+    def __init__(self, sms: int):
+        self.sms = int(sms)
+
+    def __enter__(self):
+        if self.sms:
+            _lib.call("ppmoe_set_gemm_sm_budget", self.sms)
+        return self
+
+    def __exit__(self, *exc):
+        if self.sms:
+            _lib.call("ppmoe_set_gemm_sm_budget", 0)
+        return False
+
+
+def overlap_sm_budget() -> int:
+    """GEMM SM budget while a collective is in flight: PPMOE_OVERLAP_SMS (default: all but 16)."""
+    v = os.environ.get("PPMOE_OVERLAP_SMS")
+    if v is not None:
+        return int(v)
+    n = _lib.load().ppmoe_num_sms()
+    return max(2, n - 16)
 
 
 class KernelProfile:
@@ -182,15 +218,15 @@ def experts_forward(hidden, pl: Plan, e0: int, el: int, up, down, bias_up, bias_
     dev = hidden.device
     rows_cap = local_rows_cap(n, k, el, pl.capacity)
     seg = pl.seg[e0:e0 + el + 1]
-    xs = torch.empty((rows_cap, h), dtype=hidden.dtype, device=dev)
-    tok_l = torch.empty(rows_cap, dtype=torch.int32, device=dev)
-    w_l = torch.empty(rows_cap, dtype=torch.float32, device=dev)
+    xs = _act((rows_cap, h), hidden.dtype, dev)
+    tok_l = _act(rows_cap, torch.int32, dev)
+    w_l = _act(rows_cap, torch.float32, dev)
     s = _stream()
     call("ppmoe_gather", ptr(hidden), dt, n, h, ptr(seg), el, ptr(pl.tok_sorted), ptr(pl.w_sorted), rows_cap, ptr(xs),
          ptr(tok_l), ptr(w_l), s)
-    gelu_grad = torch.empty((rows_cap, f), dtype=hidden.dtype, device=dev)
-    act = torch.empty((rows_cap, f), dtype=hidden.dtype, device=dev)
-    y = torch.empty((rows_cap, h), dtype=hidden.dtype, device=dev)
+    gelu_grad = _act((rows_cap, f), hidden.dtype, dev)
+    act = _act((rows_cap, f), hidden.dtype, dev)
+    y = _act((rows_cap, h), hidden.dtype, dev)
 
     def gemms(rlo, rhi):
         call("ppmoe_expert_fc1_fwd", dt, ptr(xs), ptr(up), ptr(bias_up), ptr(seg), el, h, f, rows_cap, ptr(rlo),
@@ -201,13 +237,20 @@ def experts_forward(hidden, pl: Plan, e0: int, el: int, up, down, bias_up, bias_
     if chunks <= 1:
         gemms(None, None)
     else:
-        rlo = torch.empty(chunks * el, dtype=torch.int32, device=dev)
-        rhi = torch.empty(chunks * el, dtype=torch.int32, device=dev)
+        rlo = torch.empty((chunks + 1) * el, dtype=torch.int32, device=dev)
+        rhi = torch.empty((chunks + 1) * el, dtype=torch.int32, device=dev)
         call("ppmoe_chunk_rows", ptr(tok_l), ptr(seg), ptr(pl.kept[e0:e0 + el]), el, n, chunks, ptr(rlo), ptr(rhi), s)
+        budget = overlap_sm_budget()
         for c in range(chunks):
-            gemms(rlo[c * el:(c + 1) * el], rhi[c * el:(c + 1) * el])
+            # from chunk 1 on, the previous chunk's all-reduce runs concurrently
+            with sm_budget(budget if c > 0 else 0):
+                gemms(rlo[c * el:(c + 1) * el], rhi[c * el:(c + 1) * el])
             if on_chunk is not None:
                 on_chunk(c)
+        # padding rows still need fc1 (their GeLU'/Act rows meet zero dY in the backward)
+        pad_lo, pad_hi = rlo[chunks * el:], rhi[chunks * el:]
+        call("ppmoe_expert_fc1_fwd", dt, ptr(xs), ptr(up), ptr(bias_up), ptr(seg), el, h, f, rows_cap, ptr(pad_lo),
+             ptr(pad_hi), ptr(gelu_grad), ptr(act), s)
     return ExpertFwdState(e0, el, rows_cap, seg, xs, tok_l, w_l, gelu_grad, act, y)
 
 
@@ -220,11 +263,11 @@ def experts_backward_data(grad_out, st: ExpertFwdState, up, down, weight_scaling
     dt = dtype_code(grad_out.dtype)
     dev = grad_out.device
     s = _stream()
-    dy = torch.empty((rows_cap, h), dtype=grad_out.dtype, device=dev)
-    dw = torch.empty(rows_cap, dtype=torch.float32, device=dev)
+    dy = _act((rows_cap, h), grad_out.dtype, dev)
+    dw = _act(rows_cap, torch.float32, dev)
     call("ppmoe_bwd_dy", dt, ptr(grad_out), ptr(st.y), ptr(st.seg), el, h, rows_cap, ptr(st.tok_l), ptr(st.w_l),
          int(bool(weight_scaling)), ptr(dy), ptr(dw), s)
-    dh = torch.empty((rows_cap, f), dtype=grad_out.dtype, device=dev)
+    dh = _act((rows_cap, f), grad_out.dtype, dev)
     call("ppmoe_expert_fc2_dgrad", dt, ptr(dy), ptr(down), ptr(st.gelu_grad), ptr(st.seg), el, h, f, rows_cap, ptr(dh), s)
     call("ppmoe_expert_fc1_dgrad", dt, ptr(dh), ptr(up), ptr(st.seg), el, h, f, rows_cap, ptr(st.tok_l), ptr(dx_acc), s)
     return dy, dh, dw

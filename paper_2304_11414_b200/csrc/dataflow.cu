@@ -220,10 +220,15 @@ __global__ void chunk_rows_kernel(const int* __restrict__ tok_local, const int* 
                                   const int* __restrict__ kept, int El, int N, int C, int* __restrict__ row_lo,
                                   int* __restrict__ row_hi) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= C * El) return;
+  if (i >= (C + 1) * El) return;
   const int c = i / El, g = i % El;
   const int base = seg[g] - seg[0];
   const int cnt = kept[g];
+  if (c == C) {  // padding rows of the segment (token -1)
+    row_lo[i] = base + cnt;
+    row_hi[i] = seg[g + 1] - seg[0];
+    return;
+  }
   auto lower = [&](int t) {
     int lo = 0, hi = cnt;
     while (lo < hi) {
@@ -341,7 +346,7 @@ int ppmoe_chunk_rows(const int* tok_local, const int* seg, const int* kept, int 
                      int* row_hi, void* stream) {
   PPMOE_REQUIRE(El >= 1 && N >= 0 && C >= 1, "bad chunk_rows arguments El=%d N=%d C=%d", El, N, C);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int n = C * El;
+  const int n = (C + 1) * El;
   chunk_rows_kernel<<<(n + 127) / 128, 128, 0, s>>>(tok_local, seg, kept, El, N, C, row_lo, row_hi);
   return check_launch("chunk_rows_kernel");
 }

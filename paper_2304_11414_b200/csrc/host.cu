@@ -41,6 +41,12 @@ int num_sms() {
   return cached;
 }
 
+static thread_local int g_gemm_sm_budget = 0;
+int gemm_ctas() {
+  const int n = num_sms();
+  return (g_gemm_sm_budget > 0 && g_gemm_sm_budget < n) ? g_gemm_sm_budget : n;
+}
+
 int max_smem_optin() {
   int dev = 0, v = 0;
   cudaGetDevice(&dev);
@@ -93,6 +99,11 @@ extern "C" {
 int ppmoe_version(void) { return 1; }
 const char* ppmoe_last_error(void) { return ppmoe::last_error(); }
 int ppmoe_num_sms(void) { return ppmoe::num_sms(); }
+int ppmoe_set_gemm_sm_budget(int sms) {
+  if (sms < 0) return ppmoe::set_error(ppmoe::kErrInvalidArg, "sm budget must be >= 0 (0 = all SMs)");
+  ppmoe::g_gemm_sm_budget = sms;
+  return 0;
+}
 unsigned long long ppmoe_kernel_launches(void) { return ppmoe::g_launches.load(std::memory_order_relaxed); }
 
 }  // extern "C"

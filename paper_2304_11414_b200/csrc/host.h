@@ -25,6 +25,9 @@ int set_error(int code, const char* fmt, ...);
 const char* last_error();
 int check_launch(const char* what);
 int num_sms();
+// CTAs for the persistent GEMM grids: all SMs unless a budget was set (to leave SMs to
+// a concurrently running collective).
+int gemm_ctas();
 int max_smem_optin();
 
 // Encodes a 2-D bf16/fp32 tensor map with SWIZZLE_128B boxes of box_inner x box_outer

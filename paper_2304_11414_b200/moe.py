@@ -487,7 +487,8 @@ class _PPMoEFunction(torch.autograd.Function):
         work = None
         if need_dx:  # copy_to_tensor_parallel_region backward (collectives.py:215-221)
             work = spec.world.all_reduce_async(spec.group, dx)
-        d_up, d_down, d_bu, d_bd = _ops.experts_backward_weights(st, dy, dh, up, down, has_bias)
+        with _ops.sm_budget(_ops.overlap_sm_budget() if work is not None else 0):
+            d_up, d_down, d_bu, d_bd = _ops.experts_backward_weights(st, dy, dh, up, down, has_bias)
         if work is not None:
             work.wait()  # stream-ordered: the compute stream waits for the NCCL stream
         ctx.state = None

@@ -246,7 +246,8 @@ def test_expert_shard_mismatch_error():
                         w.gate, [ex[:3], ex[3:]])
 
 
-def test_deterministic_bit_identical_runs():
+def test_deterministic_bit_identical_runs(monkeypatch):
+    monkeypatch.setenv("PPMOE_POISON", "1")  # unwritten rows would surface as NaN
     layer = oracle_rounded(O.init_layer(256, 8, seed=5), torch.bfloat16)
     hidden = torch.randn(2048, 256).bfloat16().double().numpy()
     r1 = run_cuda_layer(hidden, device_weights(layer, torch.bfloat16), k=2)
@@ -262,6 +263,7 @@ def test_token_chunked_forward_bit_identical(chunks, monkeypatch):
     """The all-reduce pipelining path (fc1/fc2 per token chunk) gives bit-identical results."""
     layer = oracle_rounded(O.init_layer(256, 8, seed=9), torch.bfloat16)
     hidden = torch.randn(1500, 256).bfloat16().double().numpy()
+    monkeypatch.setenv("PPMOE_POISON", "1")
     base = run_cuda_layer(hidden, device_weights(layer, torch.bfloat16), k=2, capacity_factor=1.1)
     monkeypatch.setenv("PPMOE_FWD_CHUNKS", str(chunks))
     got = run_cuda_layer(hidden, device_weights(layer, torch.bfloat16), k=2, capacity_factor=1.1)
