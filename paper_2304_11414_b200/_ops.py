@@ -32,6 +32,7 @@ def _act(shape, dtype, device) -> torch.Tensor:
     """Activation/scratch buffer.  PPMOE_POISON=1 fills it with NaN (ints: -7) so that any
     read of a row a kernel should have written shows up in the parity tests."""
     if os.environ.get("PPMOE_POISON") == "1":
+        shape = tuple(shape) if isinstance(shape, (tuple, list)) else (int(shape),)
         return torch.full(shape, float("nan") if dtype.is_floating_point else -7, dtype=dtype, device=device)
     return torch.empty(shape, dtype=dtype, device=device)
 

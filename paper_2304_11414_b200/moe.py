@@ -564,7 +564,7 @@ def ppmoe_forward(world: World, group: ProcessGroup, hidden, gate, experts_by_ra
     if env_chunks is not None:
         chunks = max(1, int(env_chunks))
     else:
-        chunks = 4 if (world.distributed and tp > 1) else 1
+        chunks = 1  # token-chunked combine measured slower than one all-reduce
     spec = _Spec(world, group, top_k, float(capacity_factor), bool(weight_scaling), ov, e0, el, aux_here, chunks)
     wg = gate.wg if gate.wg.dtype == torch.float32 else gate.wg.float()
     out, l_aux = _PPMoEFunction.apply(hidden.contiguous(), wg, local.up.contiguous(), local.down.contiguous(),
