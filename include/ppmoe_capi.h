@@ -47,6 +47,9 @@ int ppmoe_num_sms(void);
 /* Persistent-GEMM grid budget for the calling host thread: 0 = one CTA per SM (default);
  * n > 0 = at most n CTAs, leaving SMs free for a collective that runs concurrently. */
 int ppmoe_set_gemm_sm_budget(int sms);
+/* Grouped-GEMM kernel selection for the calling host thread: 0 = automatic (CTA pair,
+ * 1-CTA for long-K token GEMMs; PPMOE_GEMM env overrides), 1 = 1-CTA, 2 = CTA pair. */
+int ppmoe_set_gemm_mode(int mode);
 /* Diagnostic counter: kernels this library has launched in this process (all threads). */
 unsigned long long ppmoe_kernel_launches(void);
 

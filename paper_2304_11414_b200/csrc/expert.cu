@@ -15,11 +15,11 @@ namespace ppmoe {
 using bf16 = __nv_bfloat16;
 constexpr int kBN = 256;
 
-// Which tcgen05 kernel runs a grouped GEMM.  Default ("auto"): the CTA-pair
-// (cta_group::2, 256x256) kernel, except for token-segment GEMMs with a long K
-// (fc2 forward and fc1 data-gradient, K = ffn), where the 1-CTA 128x256 kernel keeps
-// more of the operand panels in L2 (measured ~40 % less DRAM traffic and a higher
-// clock under the power cap).  PPMOE_GEMM=single|pair forces one kernel.
+// Which tcgen05 kernel runs a grouped GEMM.  Default: the CTA-pair (cta_group::2,
+// 256x256) kernel (fastest in interleaved A/B runs of the whole C2 step, tools/ab.py).
+// PPMOE_GEMM=single forces the 1-CTA 128x256 kernel; PPMOE_GEMM=auto uses the 1-CTA
+// kernel for token-segment GEMMs with a long K (fc2 forward, fc1 data-gradient), which
+// in isolation (ncu) move ~40 % less DRAM.
 static thread_local int g_force_mode = 0;  // 0: env/default, 1: single, 2: pair
 static thread_local int g_long_k = 0;      // the GEMM being launched has K >= kLongK
 constexpr int kLongK = 8192;
@@ -28,8 +28,8 @@ static bool use_pair() {
   static const int env_mode = [] {
     const char* e = getenv("PPMOE_GEMM");
     if (e && strcmp(e, "single") == 0) return 1;
-    if (e && strcmp(e, "pair") == 0) return 2;
-    return 0;
+    if (e && strcmp(e, "auto") == 0) return 0;
+    return 2;
   }();
   if (env_mode) return env_mode == 2;
   return !g_long_k;
@@ -178,6 +178,12 @@ static GroupGeom geom(int G, int N, int M_fixed, int K_fixed, const int* seg, in
 using namespace ppmoe;
 
 extern "C" {
+
+int ppmoe_set_gemm_mode(int mode) {
+  PPMOE_REQUIRE(mode >= 0 && mode <= 2, "gemm mode: 0 auto/env, 1 single-CTA, 2 CTA pair");
+  g_force_mode = mode;
+  return kOk;
+}
 
 int ppmoe_expert_fc1_fwd(int dtype, const void* Xs, const void* up, const void* bias_up, const int* seg, int El, int H,
                          int F, int rows_cap, const int* row_lo, const int* row_hi, void* GeluGrad, void* Act,
