@@ -80,6 +80,8 @@ int ppmoe_route(const void* X, int dtype, const float* Wg, int N, int H, int E, 
  *   idx         [N x K] expert ids in [0, E) (validated by the caller)
  *   w           [N x K] gate weights or NULL (then w_sorted may be NULL)
  *   capacity    max kept pairs per expert (INT32_MAX = unlimited)
+ *   rank_offset [K x E] or NULL: pairs of higher priority held by other ranks (the
+ *               all-to-all comparator's global token order, moe.py:352-359)
  *   counts      [E]    out: routed pairs per expert before capacity
  *   kept        [E]    out: kept pairs per expert
  *   seg         [E+1]  out: padded segment starts (multiples of 128)
@@ -89,9 +91,9 @@ int ppmoe_route(const void* X, int dtype, const float* Wg, int N, int H, int E, 
  *   rows_cap_global >= N*K + 128*E
  */
 size_t ppmoe_dispatch_workspace_bytes(int N, int E, int K);
-int ppmoe_dispatch_plan(const int* idx, const float* w, int N, int E, int K, int capacity, int* counts, int* kept,
-                        int* seg, int* tok_sorted, float* w_sorted, int* pair_pos, int rows_cap_global, void* ws,
-                        size_t ws_bytes, void* stream);
+int ppmoe_dispatch_plan(const int* idx, const float* w, int N, int E, int K, int capacity, const int* rank_offset,
+                        int* counts, int* kept, int* seg, int* tok_sorted, float* w_sorted, int* pair_pos,
+                        int rows_cap_global, void* ws, size_t ws_bytes, void* stream);
 
 /* Index-slice gather ("tensor index slicing"; index_select,
  * tensor.py:226-241): Xs[row] = X[tok_sorted[seg[0]+row]] for the local rows,
@@ -164,6 +166,23 @@ int ppmoe_gate_bwd(const float* scores, const int* idx, const int* pair_pos, con
 size_t ppmoe_gate_grad_workspace_bytes(int N, int H, int E);
 int ppmoe_gate_grads(const float* dx_acc, const void* X, int dtype, const float* dL, const float* Wg, int N, int H,
                      int E, void* dX, float* dWg, void* ws, size_t ws_bytes, void* stream);
+
+/* All-to-all expert-parallel comparator (dpmoe_forward, moe.py:363-469) ------------ */
+/* Compact expert-major layout of this rank's kept pairs (the dispatch send buffer order,
+ * moe.py:405-414): cstart [E+1], tok_c/w_c per compact row, pair_pos_c [N*K] = compact
+ * row of every pair (-1 dropped).  w_sorted/w_c may be NULL.                          */
+int ppmoe_a2a_compact(const int* tok_sorted, const float* w_sorted, const int* seg, const int* kept, int E,
+                      const int* idx, const int* pair_pos, int NK, int* cstart, int* tok_c, float* w_c,
+                      int* pair_pos_c, void* stream);
+/* Owner-side regrouping of received rows (source-major) into expert-major padded
+ * segments with sources in rank order: seg_out [El+1], map[owner row] = receive row
+ * (-1 padding).  recv_counts [T x El] rows per (source, local expert).             */
+int ppmoe_a2a_owner_layout(const int* recv_counts, int T, int El, int rows_cap, int* seg_out, int* map,
+                           void* stream);
+/* dst[tok[r]] += w[r]*src[r] (fp32 dst, src in dtype) for r < nrows[0] (device scalar),
+ * tok < 0 skipped, w NULL = 1 (index_assign back to token order, moe.py:461-467).   */
+int ppmoe_scatter_rows(const void* src, int dtype, int H, const int* nrows, const int* tok, const float* w, float* dst,
+                       void* stream);
 
 /* Self-test entry: plain grouped GEMM D_g = A_g * B_g through the tcgen05 path
  * (use_tc=1) or the CUDA-core path (use_tc=0).  mode 0: A [rows x K] K-major

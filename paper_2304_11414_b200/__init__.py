@@ -21,6 +21,7 @@ from .moe import (
     ppmoe_forward,
     sync_gate_gradients,
 )
+from .dpmoe import dpmoe_forward, dpmoe_sync_gradients
 from .rng import Rng
 
 __version__ = "0.1.0"
@@ -29,5 +30,5 @@ __all__ = [
     "DP", "EP", "PP", "TP", "ConfigurationError", "GroupSet", "ProcessGroup", "TrafficLedger", "World", "tp_groups",
     "DispatchPlan", "ExpertBank", "ExpertFfn", "GateOutput", "GateParams", "LayerConfig", "MoeLayerWeights",
     "PPMoELayer", "aux_loss", "build_dispatch_plan", "gate_top1", "gate_topk", "ppmoe_forward",
-    "sync_gate_gradients", "Rng",
+    "sync_gate_gradients", "Rng", "dpmoe_forward", "dpmoe_sync_gradients",
 ]

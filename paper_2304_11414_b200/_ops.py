@@ -163,7 +163,8 @@ def capacity_for(capacity_factor: float, tokens: int, k: int, num_experts: int) 
     return min(INT32_MAX, math.ceil(capacity_factor * k * tokens / num_experts))
 
 
-def plan(idx: torch.Tensor, w: torch.Tensor | None, num_experts: int, capacity: int = INT32_MAX) -> Plan:
+def plan(idx: torch.Tensor, w: torch.Tensor | None, num_experts: int, capacity: int = INT32_MAX,
+         rank_offset: torch.Tensor | None = None) -> Plan:
     """Stable per-expert dispatch plan with capacity (moe.py:226-235, 345-360)."""
     n, k = idx.shape
     dev = idx.device
@@ -177,7 +178,8 @@ def plan(idx: torch.Tensor, w: torch.Tensor | None, num_experts: int, capacity: 
     pair_pos = torch.empty((n, k), dtype=torch.int32, device=dev)
     lib = _lib.load()
     ws = _ws(lib.ppmoe_dispatch_workspace_bytes(n, e, k), dev)
-    call("ppmoe_dispatch_plan", ptr(idx), ptr(w), n, e, k, int(capacity), ptr(counts), ptr(kept), ptr(seg),
+    call("ppmoe_dispatch_plan", ptr(idx), ptr(w), n, e, k, int(capacity), ptr(rank_offset), ptr(counts), ptr(kept),
+         ptr(seg),
          ptr(tok_sorted), ptr(w_sorted), ptr(pair_pos), rows_cap, ptr(ws), ws.numel(), _stream())
     return Plan(counts, kept, seg, tok_sorted, w_sorted, pair_pos, capacity)
 
@@ -253,6 +255,60 @@ def experts_forward(hidden, pl: Plan, e0: int, el: int, up, down, bias_up, bias_
         call("ppmoe_expert_fc1_fwd", dt, ptr(xs), ptr(up), ptr(bias_up), ptr(seg), el, h, f, rows_cap, ptr(pad_lo),
              ptr(pad_hi), ptr(gelu_grad), ptr(act), s)
     return ExpertFwdState(e0, el, rows_cap, seg, xs, tok_l, w_l, gelu_grad, act, y)
+
+
+def expert_pipeline(xsrc: torch.Tensor, seg: torch.Tensor, el: int, tok_sorted: torch.Tensor,
+                    w_sorted: torch.Tensor | None, rows_cap: int, up, down, bias_up, bias_down, weight_scaling: bool,
+                    out_acc: torch.Tensor) -> ExpertFwdState:
+    """gather(xsrc rows by tok_sorted) -> fc1 -> fc2 with the scatter-add into out_acc[tok],
+    for an arbitrary padded-segment layout (used by the all-to-all comparator's owner side,
+    where tok_sorted maps owner rows to receive-buffer rows)."""
+    n, h = xsrc.shape
+    f = up.shape[2]
+    dt = dtype_code(xsrc.dtype)
+    dev = xsrc.device
+    xs = _act((rows_cap, h), xsrc.dtype, dev)
+    tok_l = _act(rows_cap, torch.int32, dev)
+    w_l = _act(rows_cap, torch.float32, dev)
+    s = _stream()
+    call("ppmoe_gather", ptr(xsrc), dt, n, h, ptr(seg), el, ptr(tok_sorted), ptr(w_sorted), rows_cap, ptr(xs),
+         ptr(tok_l), ptr(w_l), s)
+    gelu_grad = _act((rows_cap, f), xsrc.dtype, dev)
+    act = _act((rows_cap, f), xsrc.dtype, dev)
+    y = _act((rows_cap, h), xsrc.dtype, dev)
+    call("ppmoe_expert_fc1_fwd", dt, ptr(xs), ptr(up), ptr(bias_up), ptr(seg), el, h, f, rows_cap, None, None,
+         ptr(gelu_grad), ptr(act), s)
+    call("ppmoe_expert_fc2_fwd", dt, ptr(act), ptr(down), ptr(bias_down), ptr(seg), el, h, f, rows_cap, None, None,
+         ptr(tok_l), ptr(w_l), int(bool(weight_scaling)), ptr(y), ptr(out_acc), s)
+    return ExpertFwdState(0, el, rows_cap, seg, xs, tok_l, w_l, gelu_grad, act, y)
+
+
+def a2a_compact(pl: Plan, idx: torch.Tensor, num_experts: int):
+    """Compact expert-major layout of the kept pairs: (cstart [E+1], tok_c, w_c, pair_pos_c)."""
+    dev = idx.device
+    n, k = idx.shape
+    rows = n * k
+    cstart = torch.empty(num_experts + 1, dtype=torch.int32, device=dev)
+    tok_c = _act(max(rows, 1), torch.int32, dev)
+    w_c = _act(max(rows, 1), torch.float32, dev)
+    pos_c = torch.empty((n, k), dtype=torch.int32, device=dev)
+    call("ppmoe_a2a_compact", ptr(pl.tok_sorted), ptr(pl.w_sorted), ptr(pl.seg), ptr(pl.kept), num_experts, ptr(idx),
+         ptr(pl.pair_pos), n * k, ptr(cstart), ptr(tok_c), ptr(w_c), ptr(pos_c), _stream())
+    return cstart, tok_c, w_c, pos_c
+
+
+def owner_layout(recv_counts: torch.Tensor, t: int, el: int, rows_cap: int):
+    dev = recv_counts.device
+    seg = torch.empty(el + 1, dtype=torch.int32, device=dev)
+    rmap = torch.empty(max(rows_cap, 1), dtype=torch.int32, device=dev)
+    call("ppmoe_a2a_owner_layout", ptr(recv_counts), t, el, rows_cap, ptr(seg), ptr(rmap), _stream())
+    return seg, rmap
+
+
+def scatter_rows(src: torch.Tensor, nrows: torch.Tensor, tok: torch.Tensor, w: torch.Tensor | None,
+                 dst: torch.Tensor) -> None:
+    call("ppmoe_scatter_rows", ptr(src), dtype_code(src.dtype), src.shape[1], ptr(nrows), ptr(tok), ptr(w), ptr(dst),
+         _stream())
 
 
 def experts_backward_data(grad_out, st: ExpertFwdState, up, down, weight_scaling: bool, dx_acc: torch.Tensor):

@@ -342,7 +342,8 @@ __global__ void plan_totals_kernel(const int* __restrict__ hist, int C, int E, i
 // Priority rank of every pair: all slot-0 pairs in ascending token id, then slot 1, ...
 // (reduces to _capacity_mask's ascending global token id at K = 1).
 __global__ void plan_keep_kernel(const int* __restrict__ idx, int N, int E, int K, int capacity,
-                                 const int* __restrict__ base, const int* __restrict__ tot, int* __restrict__ kflag,
+                                 const int* __restrict__ base, const int* __restrict__ tot,
+                                 const int* __restrict__ rank_offset, int* __restrict__ kflag,
                                  int* __restrict__ kc) {
   extern __shared__ int sh[];
   int* wc = sh;                        // [8][K][E]
@@ -379,7 +380,7 @@ __global__ void plan_keep_kernel(const int* __restrict__ idx, int N, int E, int 
       int prior = 0;
       for (int s2 = 0; s2 < s; ++s2) prior += tot[s2 * E + e];
       const long long rank = static_cast<long long>(prior) + base[(static_cast<size_t>(c) * K + s) * E + e] +
-                             wc[(warp * K + s) * E + e] + rw[s];
+                             wc[(warp * K + s) * E + e] + rw[s] + (rank_offset ? rank_offset[s * E + e] : 0);
       const int keep = rank < capacity ? 1 : 0;
       kflag[static_cast<size_t>(t) * K + s] = keep;
       if (keep) atomicAdd(&kcs[e], 1);
@@ -525,9 +526,9 @@ int ppmoe_route(const void* X, int dtype, const float* Wg, int N, int H, int E, 
 
 size_t ppmoe_dispatch_workspace_bytes(int N, int E, int K) { return plan_ws_layout(N, E, K, nullptr, nullptr); }
 
-int ppmoe_dispatch_plan(const int* idx, const float* w, int N, int E, int K, int capacity, int* counts, int* kept,
-                        int* seg, int* tok_sorted, float* w_sorted, int* pair_pos, int rows_cap_global, void* ws,
-                        size_t ws_bytes, void* stream) {
+int ppmoe_dispatch_plan(const int* idx, const float* w, int N, int E, int K, int capacity, const int* rank_offset,
+                        int* counts, int* kept, int* seg, int* tok_sorted, float* w_sorted, int* pair_pos,
+                        int rows_cap_global, void* ws, size_t ws_bytes, void* stream) {
   PPMOE_REQUIRE(N >= 0 && E >= 1 && E <= kMaxE, "dispatch plan needs 1 <= E <= %d", kMaxE);
   PPMOE_REQUIRE(K >= 1 && K <= kMaxK && K <= E, "bad top-k %d", K);
   PPMOE_REQUIRE(capacity >= 0, "capacity must be non-negative");
@@ -548,7 +549,8 @@ int ppmoe_dispatch_plan(const int* idx, const float* w, int N, int E, int K, int
   if (int rc = check_launch("plan_hist")) return rc;
   plan_totals_kernel<<<1, 1024, 0, s>>>(p.hist, C, E, K, capacity, p.base, p.tot, counts);
   if (int rc = check_launch("plan_totals")) return rc;
-  plan_keep_kernel<<<C, kChunk, (8 * K * E + E) * 4, s>>>(idx, N, E, K, capacity, p.base, p.tot, p.kflag, p.kc);
+  plan_keep_kernel<<<C, kChunk, (8 * K * E + E) * 4, s>>>(idx, N, E, K, capacity, p.base, p.tot, rank_offset,
+                                                         p.kflag, p.kc);
   if (int rc = check_launch("plan_keep")) return rc;
   plan_offsets_kernel<<<1, 1024, 0, s>>>(p.kc, C, E, p.kb, kept, seg, tok_sorted, w_sorted);
   if (int rc = check_launch("plan_offsets")) return rc;

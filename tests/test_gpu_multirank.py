@@ -89,3 +89,76 @@ def test_tp_nccl_matches_simulated(world, k, cf):
         assert res["ar"] == 2 and res["gs"] == 1
     # every rank holds the identical replicated output
     assert np.array_equal(got[0]["out"], got[1]["out"])
+
+
+def _dp_worker(rank, world, port, q, k, cf):
+    import torch.distributed as dist
+
+    import paper_2304_11414_b200 as P
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    try:
+        h, e, n = 512, 8, 1024
+        el = e // world
+        full = P.MoeLayerWeights.random(h, e, seed=11, device="cuda")
+        gate = P.GateParams(full.gate.wg.detach().clone().requires_grad_())
+        bank = P.ExpertBank(*(None if t is None else t.detach().clone()[rank * el:(rank + 1) * el].contiguous().requires_grad_()
+                              for t in (full.bank.up, full.bank.down, full.bank.bias_up, full.bank.bias_down)),
+                            first=rank * el)
+        xall = torch.randn(n, h, device="cuda", generator=torch.Generator(device="cuda").manual_seed(5)).bfloat16()
+        nr = n // world
+        x = xall[rank * nr:(rank + 1) * nr].clone().requires_grad_()
+        wd = P.World(1, world)
+        g = P.ProcessGroup(P.EP, tuple(range(world)))
+        ebr = [bank if r == rank else None for r in range(world)]
+        out, l_aux = P.dpmoe_forward(wd, g, x, gate, experts_by_rank=ebr, top_k=k, capacity_factor=cf)
+        out.float().sum().backward()  # weight path only: aux terms differ between spans
+        P.dpmoe_sync_gradients(wd, g, gate)
+        torch.cuda.synchronize()
+        q.put((rank, {"out": out.detach().float().cpu().numpy(), "dx": x.grad.float().cpu().numpy(),
+                      "dwg": gate.wg.grad.cpu().numpy(), "dup": bank.up.grad.float().cpu().numpy(),
+                      "a2a": wd.ledger.count_for("EP", "all_to_all")}))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,k,cf", [(2, 2, float("inf")), (2, 1, 0.9)])
+def test_a2a_comparator_matches_ppmoe_on_global_batch(world, k, cf):
+    """DPMoE over the ranks' micro-batches == PPMoE over their concatenation (same global
+    capacity order), for outputs, dX and all weight gradients (moe.py:363-469 vs 254-308)."""
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    import paper_2304_11414_b200 as P
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29700 + os.getpid() % 500
+    procs = [ctx.Process(target=_dp_worker, args=(r, world, port, q, k, cf)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    h, e, n = 512, 8, 1024
+    full = P.MoeLayerWeights.random(h, e, seed=11, device="cuda")
+    x = torch.randn(n, h, device="cuda", generator=torch.Generator(device="cuda").manual_seed(5)).bfloat16()
+    x.requires_grad_()
+    out, _ = P.ppmoe_forward(P.World(1, 1), P.ProcessGroup(P.EP, (0,)), x, full.gate, [full.bank], top_k=k,
+                             capacity_factor=cf)
+    out.float().sum().backward()
+
+    def err(a, b):
+        return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-30))
+
+    nr, el = n // world, e // world
+    for r in range(world):
+        res = got[r]
+        assert err(res["out"], out.detach().float().cpu().numpy()[r * nr:(r + 1) * nr]) < 2e-2
+        assert err(res["dx"], x.grad.float().cpu().numpy()[r * nr:(r + 1) * nr]) < 2e-2
+        assert err(res["dwg"], full.gate.wg.grad.cpu().numpy()) < 2e-2
+        assert err(res["dup"], full.bank.up.grad[r * el:(r + 1) * el].float().cpu().numpy()) < 2e-2
+        assert res["a2a"] == 5

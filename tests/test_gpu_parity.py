@@ -271,3 +271,43 @@ def test_token_chunked_forward_bit_identical(chunks, monkeypatch):
     assert np.array_equal(base["grad_hidden"], got["grad_hidden"])
     for k in base["grads"]:
         assert np.array_equal(base["grads"][k], got["grads"][k]), k
+
+
+# ------------------------------------------------------------------ all-to-all comparator (DPMoE)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("name", ["capacity_cf050", "capacity_cf100_skew"])
+def test_dpmoe_single_rank_vs_reference_golden(name, dtype):
+    """dpmoe_forward on one rank == the reference's single-rank dpmoe_forward (capacity)."""
+    meta, a = load(name)
+    case = meta["case"]
+    hidden, layer = golden_inputs(case)
+    w = device_weights(layer, dtype)
+    x = torch.as_tensor(hidden, dtype=torch.float64).to("cuda", dtype).requires_grad_()
+    world = P.World(1, 1)
+    ov = case.get("override")
+    out, l_aux = P.dpmoe_forward(world, P.ProcessGroup(P.EP, (0,)), [x], w.gate, experts_by_rank=w.shard(1),
+                                 capacity_factor=case["capacity_factor"], route_overrides=None if ov is None else [ov])
+    (out.float().sum() + l_aux).backward()
+    res = {"out": out.detach().double().cpu().numpy(), "grad_hidden": x.grad.double().cpu().numpy(),
+           "grads": {k: (None if v is None else v.detach().double().cpu().numpy()) for k, v in w.named_grads().items()}}
+    grads = {k[5:]: v for k, v in a.items() if k.startswith("grad_") and k != "grad_hidden"}
+    _compare(res, a["out"], a["grad_hidden"], grads, dtype, name=name)
+    assert abs(float(l_aux.detach()) - float(a["l_aux"])) < 1e-5
+    assert world.ledger.count_for("EP", "all_to_all") == 5  # counts + dispatch + return (+2 backward)
+
+
+def test_dpmoe_single_rank_matches_ppmoe():
+    layer = oracle_rounded(O.init_layer(256, 8, seed=66), torch.bfloat16)
+    hidden = torch.randn(1000, 256).bfloat16().double().numpy()
+    pp = run_cuda_layer(hidden, device_weights(layer, torch.bfloat16), k=2)
+    w = device_weights(layer, torch.bfloat16)
+    x = torch.as_tensor(hidden).to("cuda", torch.bfloat16).requires_grad_()
+    out, l_aux = P.dpmoe_forward(P.World(1, 1), P.ProcessGroup(P.EP, (0,)), x, w.gate, experts_by_rank=w.shard(1),
+                                 top_k=2)
+    (out.float().sum() + l_aux).backward()
+    assert scaled_err(out.detach().double().cpu().numpy(), pp["out"]) < 1e-2
+    assert scaled_err(x.grad.double().cpu().numpy(), pp["grad_hidden"]) < 1e-2
+    for k, g in w.named_grads().items():
+        assert scaled_err(g.double().cpu().numpy(), pp["grads"][k]) < 2e-2, k
