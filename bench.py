@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--capacity-factor", type=float, default=math.inf)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-a2a", action="store_true", help="skip the all-to-all (DPMoE) comparator")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU time of the cpu_baseline sample")
     return ap.parse_args()
 
@@ -346,6 +347,39 @@ def main():
         e2e = {"value": n / (float(te) / 1e3), "unit": UNIT, "h2d_bytes_per_step": n * h * 2, "d2h_bytes_per_step": 4,
                "ms_per_step": float(te), "path": "paper_2304_11414_b200.ppmoe_forward + backward (C-ABI) from pinned host"}
 
+    # ---- conventional all-to-all expert-parallel layer (DPMoE) at the same global N:
+    # each rank routes its own N/T tokens and exchanges rows with two all-to-alls per pass
+    a2a = None
+    if not a.no_a2a:
+        nr = n // tp
+        x_dp = x.detach()[rank * nr:(rank + 1) * nr].clone().requires_grad_()
+        g_dp = torch.ones(nr, h, device=dev, dtype=torch.bfloat16)
+
+        def dp_step():
+            for p in params:
+                p.grad = None
+            x_dp.grad = None
+            out, l_aux = P.dpmoe_forward(world, group, x_dp, w.gate, experts_by_rank=experts_by_rank, top_k=k,
+                                         capacity_factor=a.capacity_factor)
+            torch.autograd.backward([out, l_aux], [g_dp, g_aux])
+            P.dpmoe_sync_gradients(world, group, w.gate)
+
+        for _ in range(a.warmup):
+            dp_step()
+        barrier()
+        d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        d0.record()
+        for _ in range(a.steps):
+            dp_step()
+        d1.record()
+        barrier()
+        dms = torch.tensor([d0.elapsed_time(d1) / a.steps], device=dev, dtype=torch.float64)
+        if distributed:
+            dist.all_reduce(dms, op=dist.ReduceOp.MAX)
+        a2a_value = n / (float(dms) / 1e3)
+        a2a = {"value": a2a_value, "unit": UNIT, "ms_per_step": float(dms), "ppmoe_over_a2a": value / a2a_value,
+               "layer": "dpmoe_forward (all-to-all dispatch/return, same grouped GEMM kernels), N/T tokens per rank"}
+
     cb = None
     if rank == 0 and world_size == 1 and not a.no_cpu_baseline:
         cb, _ = cpu_baseline(h, E, k, f, target_s=a.cpu_seconds)
@@ -355,7 +389,7 @@ def main():
                 "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights of the C2 layer, N(0,1) tokens)",
                 "config": config_of(a, world_size), "roofline": roofline, "cpu_baseline": cb, "e2e": e2e,
-                "gpu_launches": int(launches), "clocks": clk.summary(), "kernels": per_kernel,
+                "gpu_launches": int(launches), "clocks": clk.summary(), "a2a_comparator": a2a, "kernels": per_kernel,
                 "gemm_launches_per_step": gemm_launches}
         print(json.dumps(line), flush=True)
     if distributed:
