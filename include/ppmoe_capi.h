@@ -119,22 +119,25 @@ int ppmoe_expert_fc1_fwd(int dtype, const void* Xs, const void* up, const void* 
                          void* stream);
 
 /* Expert FFN forward, second GEMM fused with the gate-weighted combine:
- * Y = Act*down_g + bias_down (stored, pre-scale), out_acc[tok] += w*Y
- * (moe.py:104-107, scale_rows tensor.py:184-196, index_assign 244-272).
+ * Y = Dropout(Act*down_g + bias_down) (stored, pre-scale), out_acc[tok] += w*Y
+ * (moe.py:104-107, scale_rows tensor.py:184-196, index_assign 244-272, dropout
+ * tensor.py:315-330 with a counter-based mask hash(seed, local row, column)).
  * out_acc [N x H] fp32 must be zeroed by the caller.                       */
 int ppmoe_expert_fc2_fwd(int dtype, const void* Act, const void* down, const void* bias_down, const int* seg,
                          int El, int H, int F, int rows_cap, const int* row_lo, const int* row_hi,
-                         const int* tok_local, const float* w_local, int weight_scaling, void* Y, float* out_acc,
-                         void* stream);
+                         const int* tok_local, const float* w_local, int weight_scaling, float dropout_p,
+                         unsigned long long seed, void* Y, float* out_acc, void* stream);
 
 /* out = out_acc cast to dtype (the replicated [N x H] layer output before or
  * after the TP all-reduce, collectives.py:135-153).                         */
 int ppmoe_cast_out(const float* acc, int n, void* out, int dtype, void* stream);
 
-/* Backward of scale_rows + index_assign (tensor.py:190-194, 264-270):
- * dY[row] = w*dOut[tok], dw[row] = <dOut[tok], Y[row]>; zero for padding.   */
+/* Backward of scale_rows + index_assign + dropout (tensor.py:190-194, 264-270, 326-328):
+ * dY[row] = w*dOut[tok] (times the forward's dropout mask / (1-p)),
+ * dw[row] = <dOut[tok], Y[row]>; zero for padding.                          */
 int ppmoe_bwd_dy(int dtype, const void* dOut, const void* Y, const int* seg, int El, int H, int rows_cap,
-                 const int* tok_local, const float* w_local, int weight_scaling, void* dY, float* dw, void* stream);
+                 const int* tok_local, const float* w_local, int weight_scaling, float dropout_p,
+                 unsigned long long seed, void* dY, float* dw, void* stream);
 
 /* dH = (dY*down_g^T) .* GeluGrad   (matmul/gelu backward, tensor.py:134-138, 204-207) */
 int ppmoe_expert_fc2_dgrad(int dtype, const void* dY, const void* down, const void* GeluGrad, const int* seg, int El,

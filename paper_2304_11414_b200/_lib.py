@@ -20,6 +20,7 @@ _I = ctypes.c_int
 _F = ctypes.c_float
 _D = ctypes.c_double
 _S = ctypes.c_size_t
+_U = ctypes.c_ulonglong
 
 # name -> (restype, argtypes); mirrors include/ppmoe_capi.h
 _SIGNATURES = {
@@ -39,9 +40,9 @@ _SIGNATURES = {
     "ppmoe_gather": (_I, [_P, _I, _I, _I, _P, _I, _P, _P, _I, _P, _P, _P, _P]),
     "ppmoe_chunk_rows": (_I, [_P, _P, _P, _I, _I, _I, _P, _P, _P]),
     "ppmoe_expert_fc1_fwd": (_I, [_I, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P]),
-    "ppmoe_expert_fc2_fwd": (_I, [_I, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _I, _P, _P, _P]),
+    "ppmoe_expert_fc2_fwd": (_I, [_I, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _I, _F, _U, _P, _P, _P]),
     "ppmoe_cast_out": (_I, [_P, _I, _P, _I, _P]),
-    "ppmoe_bwd_dy": (_I, [_I, _P, _P, _P, _I, _I, _I, _P, _P, _I, _P, _P, _P]),
+    "ppmoe_bwd_dy": (_I, [_I, _P, _P, _P, _I, _I, _I, _P, _P, _I, _F, _U, _P, _P, _P]),
     "ppmoe_expert_fc2_dgrad": (_I, [_I, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P]),
     "ppmoe_expert_fc2_wgrad": (_I, [_I, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P]),
     "ppmoe_expert_fc1_dgrad": (_I, [_I, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P]),

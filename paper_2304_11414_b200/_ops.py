@@ -207,10 +207,13 @@ class ExpertFwdState:
     gelu_grad: torch.Tensor
     act: torch.Tensor
     y: torch.Tensor
+    drop_p: float = 0.0
+    seed: int = 0
 
 
 def experts_forward(hidden, pl: Plan, e0: int, el: int, up, down, bias_up, bias_down, k: int, weight_scaling: bool,
-                    out_acc: torch.Tensor, chunks: int = 1, on_chunk=None) -> ExpertFwdState:
+                    out_acc: torch.Tensor, chunks: int = 1, on_chunk=None, drop_p: float = 0.0,
+                    seed: int = 0) -> ExpertFwdState:
     """index-slice gather -> fc1 (+bias, GeLU) -> fc2 (+bias, gate-scaled scatter-add combine)
     for experts [e0, e0+el) (moe.py:294-305).  With chunks > 1 the two GEMMs run per token
     chunk (each expert segment is ascending in token id, so a chunk is a row range) and
@@ -235,7 +238,7 @@ def experts_forward(hidden, pl: Plan, e0: int, el: int, up, down, bias_up, bias_
         call("ppmoe_expert_fc1_fwd", dt, ptr(xs), ptr(up), ptr(bias_up), ptr(seg), el, h, f, rows_cap, ptr(rlo),
              ptr(rhi), ptr(gelu_grad), ptr(act), s)
         call("ppmoe_expert_fc2_fwd", dt, ptr(act), ptr(down), ptr(bias_down), ptr(seg), el, h, f, rows_cap, ptr(rlo),
-             ptr(rhi), ptr(tok_l), ptr(w_l), int(bool(weight_scaling)), ptr(y), ptr(out_acc), s)
+             ptr(rhi), ptr(tok_l), ptr(w_l), int(bool(weight_scaling)), float(drop_p), int(seed), ptr(y), ptr(out_acc), s)
 
     if chunks <= 1:
         gemms(None, None)
@@ -254,12 +257,12 @@ def experts_forward(hidden, pl: Plan, e0: int, el: int, up, down, bias_up, bias_
         pad_lo, pad_hi = rlo[chunks * el:], rhi[chunks * el:]
         call("ppmoe_expert_fc1_fwd", dt, ptr(xs), ptr(up), ptr(bias_up), ptr(seg), el, h, f, rows_cap, ptr(pad_lo),
              ptr(pad_hi), ptr(gelu_grad), ptr(act), s)
-    return ExpertFwdState(e0, el, rows_cap, seg, xs, tok_l, w_l, gelu_grad, act, y)
+    return ExpertFwdState(e0, el, rows_cap, seg, xs, tok_l, w_l, gelu_grad, act, y, drop_p, seed)
 
 
 def expert_pipeline(xsrc: torch.Tensor, seg: torch.Tensor, el: int, tok_sorted: torch.Tensor,
                     w_sorted: torch.Tensor | None, rows_cap: int, up, down, bias_up, bias_down, weight_scaling: bool,
-                    out_acc: torch.Tensor) -> ExpertFwdState:
+                    out_acc: torch.Tensor, drop_p: float = 0.0, seed: int = 0) -> ExpertFwdState:
     """gather(xsrc rows by tok_sorted) -> fc1 -> fc2 with the scatter-add into out_acc[tok],
     for an arbitrary padded-segment layout (used by the all-to-all comparator's owner side,
     where tok_sorted maps owner rows to receive-buffer rows)."""
@@ -279,8 +282,8 @@ def expert_pipeline(xsrc: torch.Tensor, seg: torch.Tensor, el: int, tok_sorted: 
     call("ppmoe_expert_fc1_fwd", dt, ptr(xs), ptr(up), ptr(bias_up), ptr(seg), el, h, f, rows_cap, None, None,
          ptr(gelu_grad), ptr(act), s)
     call("ppmoe_expert_fc2_fwd", dt, ptr(act), ptr(down), ptr(bias_down), ptr(seg), el, h, f, rows_cap, None, None,
-         ptr(tok_l), ptr(w_l), int(bool(weight_scaling)), ptr(y), ptr(out_acc), s)
-    return ExpertFwdState(0, el, rows_cap, seg, xs, tok_l, w_l, gelu_grad, act, y)
+         ptr(tok_l), ptr(w_l), int(bool(weight_scaling)), float(drop_p), int(seed), ptr(y), ptr(out_acc), s)
+    return ExpertFwdState(0, el, rows_cap, seg, xs, tok_l, w_l, gelu_grad, act, y, drop_p, seed)
 
 
 def a2a_compact(pl: Plan, idx: torch.Tensor, num_experts: int):
@@ -323,7 +326,7 @@ def experts_backward_data(grad_out, st: ExpertFwdState, up, down, weight_scaling
     dy = _act((rows_cap, h), grad_out.dtype, dev)
     dw = _act(rows_cap, torch.float32, dev)
     call("ppmoe_bwd_dy", dt, ptr(grad_out), ptr(st.y), ptr(st.seg), el, h, rows_cap, ptr(st.tok_l), ptr(st.w_l),
-         int(bool(weight_scaling)), ptr(dy), ptr(dw), s)
+         int(bool(weight_scaling)), float(st.drop_p), int(st.seed), ptr(dy), ptr(dw), s)
     dh = _act((rows_cap, f), grad_out.dtype, dev)
     call("ppmoe_expert_fc2_dgrad", dt, ptr(dy), ptr(down), ptr(st.gelu_grad), ptr(st.seg), el, h, f, rows_cap, ptr(dh), s)
     call("ppmoe_expert_fc1_dgrad", dt, ptr(dh), ptr(up), ptr(st.seg), el, h, f, rows_cap, ptr(st.tok_l), ptr(dx_acc), s)

@@ -35,6 +35,19 @@ __device__ __forceinline__ float gelu_grad_f(float x) {
   return cdf + x * pdf;
 }
 
+// Counter-based dropout keep mask: hash(seed, row, col) -> uniform in [0,1); keep if >= p.
+// The same (seed, local row, column) regenerates the mask in the backward.
+__host__ __device__ __forceinline__ float dropout_uniform(unsigned long long seed, int row, int col) {
+  unsigned long long z = seed ^ (static_cast<unsigned long long>(static_cast<unsigned>(row)) * 0x9E3779B97F4A7C15ull) ^
+                         (static_cast<unsigned long long>(static_cast<unsigned>(col)) * 0xC2B2AE3D27D4EB4Full);
+  z ^= z >> 30;
+  z *= 0xBF58476D1CE4E5B9ull;
+  z ^= z >> 27;
+  z *= 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return static_cast<float>(z >> 40) * (1.0f / 16777216.0f);
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

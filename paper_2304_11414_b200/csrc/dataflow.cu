@@ -130,7 +130,8 @@ __global__ void cast_kernel(const float* __restrict__ src, size_t n, T* __restri
 template <typename T>
 __global__ void bwd_dy_kernel(const T* __restrict__ dOut, const T* __restrict__ Y, const int* __restrict__ seg, int El,
                               int H, const int* __restrict__ tok_local, const float* __restrict__ w_local,
-                              int weight_scaling, T* __restrict__ dY, float* __restrict__ dw) {
+                              int weight_scaling, float drop_p, unsigned long long seed, T* __restrict__ dY,
+                              float* __restrict__ dw) {
   const int rows = seg[El] - seg[0];
   const int lane = threadIdx.x & 31;
   const int wpb = blockDim.x / 32;
@@ -147,7 +148,15 @@ __global__ void bwd_dy_kernel(const T* __restrict__ dOut, const T* __restrict__ 
     const T* g = dOut + static_cast<size_t>(tok) * H;
     const T* y = Y + static_cast<size_t>(r) * H;
     float acc = 0.f;
-    if (vec && sizeof(T) == 2) {
+    if (drop_p > 0.f) {  // Y is the dropped output; dY reaches the expert through the same mask
+      const float inv = 1.f / (1.f - drop_p);
+      for (int j = lane; j < H; j += 32) {
+        const float gv = to_f32(g[j]);
+        acc = fmaf(gv, to_f32(y[j]), acc);
+        const float keep = dropout_uniform(seed, r, j) >= drop_p ? inv : 0.f;
+        dy[j] = from_f32<T>(s * gv * keep);
+      }
+    } else if (vec && sizeof(T) == 2) {
       for (int j = lane * 8; j < H; j += 256) {
         uint4 gu = *reinterpret_cast<const uint4*>(g + j);
         uint4 yu = *reinterpret_cast<const uint4*>(y + j);
@@ -362,7 +371,9 @@ int ppmoe_cast_out(const float* acc, int n, void* out, int dtype, void* stream) 
 }
 
 int ppmoe_bwd_dy(int dtype, const void* dOut, const void* Y, const int* seg, int El, int H, int rows_cap,
-                 const int* tok_local, const float* w_local, int weight_scaling, void* dY, float* dw, void* stream) {
+                 const int* tok_local, const float* w_local, int weight_scaling, float dropout_p,
+                 unsigned long long seed, void* dY, float* dw, void* stream) {
+  PPMOE_REQUIRE(dropout_p >= 0.f && dropout_p < 1.f, "dropout probability must be in [0, 1), got %g", dropout_p);
   PPMOE_REQUIRE(dtype == kBF16 || dtype == kF32, "bad dtype");
   if (rows_cap == 0) return kOk;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -370,10 +381,12 @@ int ppmoe_bwd_dy(int dtype, const void* dOut, const void* Y, const int* seg, int
   if (dtype == kBF16)
     bwd_dy_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(dOut),
                                                       static_cast<const __nv_bfloat16*>(Y), seg, El, H, tok_local,
-                                                      w_local, weight_scaling, static_cast<__nv_bfloat16*>(dY), dw);
+                                                      w_local, weight_scaling, dropout_p, seed,
+                                                      static_cast<__nv_bfloat16*>(dY), dw);
   else
     bwd_dy_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(dOut), static_cast<const float*>(Y), seg, El, H,
-                                              tok_local, w_local, weight_scaling, static_cast<float*>(dY), dw);
+                                              tok_local, w_local, weight_scaling, dropout_p, seed,
+                                              static_cast<float*>(dY), dw);
   return check_launch("bwd_dy_kernel");
 }
 

@@ -143,6 +143,8 @@ struct EpiFc2Fwd {
   int weight_scaling;
   float* out_acc;  // [N*H] fp32, zero-initialised
   int cs;
+  float drop_p;             // inverted dropout on the expert output (tensor.py:315-330)
+  unsigned long long seed;
   template <int W>
   __device__ __forceinline__ void apply(int g, int m, int row, int n0, const float (&v)[W]) const {
     const int valid = min(W, H - n0);
@@ -154,6 +156,11 @@ struct EpiFc2Fwd {
     float x[W];
 #pragma unroll
     for (int j = 0; j < W; ++j) x[j] = v[j] + b[j];
+    if (drop_p > 0.f) {
+      const float inv = 1.f / (1.f - drop_p);
+#pragma unroll
+      for (int j = 0; j < W; ++j) x[j] = dropout_uniform(seed, row, n0 + j) >= drop_p ? x[j] * inv : 0.f;
+    }
     store_row<T, W>(y + static_cast<size_t>(row) * H + n0, x, valid, cs);
     const int t = tok[row];
     if (t >= 0) {

@@ -39,6 +39,8 @@ class _A2ASpec:
     capacity_factor: float
     weight_scaling: bool
     override: torch.Tensor | None
+    dropout_p: float = 0.0
+    seed: int = 0
 
 
 def _a2a(world: World, group: ProcessGroup, out: torch.Tensor, inp: torch.Tensor, out_splits, in_splits,
@@ -101,7 +103,8 @@ class _DPMoEFunction(torch.autograd.Function):
         rows_cap_o = n_recv + 128 * el
         seg_o, rmap = _ops.owner_layout(recv_counts, t, el, rows_cap_o)
         yret = torch.zeros((max(n_recv, 1), h), dtype=torch.float32, device=dev)
-        st = _ops.expert_pipeline(xrecv, seg_o, el, rmap, None, rows_cap_o, up, down, bias_up, bias_down, False, yret)
+        st = _ops.expert_pipeline(xrecv, seg_o, el, rmap, None, rows_cap_o, up, down, bias_up, bias_down, False, yret,
+                                  spec.dropout_p, spec.seed)
         yret_b = _ops.cast_out(yret, hidden.dtype)
         del yret
         yback = torch.empty((max(n_send, 1), h), dtype=hidden.dtype, device=dev)
@@ -129,7 +132,7 @@ class _DPMoEFunction(torch.autograd.Function):
         dy_c = _ops._act((max(n_send, 1), h), hidden.dtype, dev)
         dw_c = _ops._act(max(n_send, 1), torch.float32, dev)
         _ops.call("ppmoe_bwd_dy", _ops.dtype_code(hidden.dtype), _ops.ptr(g_out), _ops.ptr(yback), _ops.ptr(cstart), e,
-                  h, max(n_send, 1), _ops.ptr(tok_c), _ops.ptr(w_c), int(spec.weight_scaling), _ops.ptr(dy_c),
+                  h, max(n_send, 1), _ops.ptr(tok_c), _ops.ptr(w_c), int(spec.weight_scaling), 0.0, 0, _ops.ptr(dy_c),
                   _ops.ptr(dw_c), _ops._stream())
         dy_recv = torch.empty((max(n_recv, 1), h), dtype=hidden.dtype, device=dev)
         _a2a(spec.world, spec.group, dy_recv[:n_recv], dy_c[:n_send], recv_rows, send_rows)
@@ -166,7 +169,7 @@ def dpmoe_forward(world: World, ep_group: ProcessGroup, hidden_per_rank, gate, *
     list whose own entry is used); returns (out, l_aux) of this rank.  A single-rank world
     runs the same path without communication.
     """
-    from .moe import ExpertBank, _bank_of, _override_tensor
+    from .moe import ExpertBank, _bank_of, _dropout_seed, _override_tensor
 
     dp = ep_group.size
     if world.distributed:
@@ -184,8 +187,7 @@ def dpmoe_forward(world: World, ep_group: ProcessGroup, hidden_per_rank, gate, *
         hidden = hidden_per_rank
     if len(experts_by_rank) != dp:
         raise ValueError(f"need hidden and experts for each of {dp} ranks")
-    if dropout_p != 0.0:
-        raise NotImplementedError("dropout_p > 0 is not implemented by the B200 kernels yet")
+    seed = _dropout_seed(dropout_p, rng)
     local: ExpertBank = _bank_of(experts_by_rank[me])
     num_experts = gate.num_experts
     if local.count * dp != num_experts:
@@ -195,7 +197,8 @@ def dpmoe_forward(world: World, ep_group: ProcessGroup, hidden_per_rank, gate, *
         ov = _override_tensor(route_overrides[me] if isinstance(route_overrides, (list, tuple)) and
                               len(route_overrides) == dp else route_overrides,
                               hidden.shape[0], top_k, num_experts, hidden.device)
-    spec = _A2ASpec(world, ep_group, me, dp, local.count, top_k, float(capacity_factor), bool(weight_scaling), ov)
+    spec = _A2ASpec(world, ep_group, me, dp, local.count, top_k, float(capacity_factor), bool(weight_scaling), ov,
+                    float(dropout_p), seed)
     wg = gate.wg if gate.wg.dtype == torch.float32 else gate.wg.float()
     return _DPMoEFunction.apply(hidden.contiguous(), wg, local.up.contiguous(), local.down.contiguous(),
                                 None if local.bias_up is None else local.bias_up.contiguous(),

@@ -420,6 +420,8 @@ class _Spec:
     el: int
     aux_here: bool
     fwd_chunks: int = 1
+    dropout_p: float = 0.0
+    seed: int = 0
 
 
 class _PPMoEFunction(torch.autograd.Function):
@@ -449,14 +451,15 @@ class _PPMoEFunction(torch.autograd.Function):
                     works.append(spec.world.all_reduce_async(spec.group, out[lo:hi], charge=False))
 
             st = _ops.experts_forward(hidden, pl, spec.e0, spec.el, up, down, bias_up, bias_down, spec.k,
-                                      spec.weight_scaling, out_acc, spec.fwd_chunks, on_chunk)
+                                      spec.weight_scaling, out_acc, spec.fwd_chunks, on_chunk, spec.dropout_p,
+                                      spec.seed)
             spec.world.charge_all_reduce(spec.group, out.numel())
             for wk in works:
                 if wk is not None:
                     wk.wait()
         else:
             st = _ops.experts_forward(hidden, pl, spec.e0, spec.el, up, down, bias_up, bias_down, spec.k,
-                                      spec.weight_scaling, out_acc)
+                                      spec.weight_scaling, out_acc, drop_p=spec.dropout_p, seed=spec.seed)
             out = _ops.cast_out(out_acc, hidden.dtype)
             spec.world.all_reduce_(spec.group, out)  # reduce_from_tensor_parallel_region (moe.py:307)
         del out_acc
@@ -495,6 +498,18 @@ class _PPMoEFunction(torch.autograd.Function):
         return dx, dwg, d_up, d_down, d_bu, d_bd, None
 
 
+def _dropout_seed(dropout_p: float, rng) -> int:
+    """Validate dropout arguments like tensor.dropout (tensor.py:315-322) and draw the mask
+    seed from the caller's Rng (every rank of a TP group draws the same value)."""
+    if not 0.0 <= dropout_p < 1.0:
+        raise ValueError(f"dropout probability must be in [0, 1), got {dropout_p}")
+    if dropout_p == 0.0:
+        return 0
+    if rng is None:
+        raise ValueError("dropout with p > 0 requires an rng")
+    return int(rng.integers(0, 2**62, 1)[0])
+
+
 def _as_single(value, what: str):
     """Collapse a replica list to its logical value, checking exact agreement (moe.py:238-248)."""
     if isinstance(value, (list, tuple)):
@@ -529,10 +544,7 @@ def ppmoe_forward(world: World, group: ProcessGroup, hidden, gate, experts_by_ra
     tp = group.size
     if len(experts_by_rank) != tp:
         raise ValueError(f"need one expert list per rank: {len(experts_by_rank)} for group of {tp}")
-    if dropout_p != 0.0:
-        if not 0.0 <= dropout_p < 1.0:
-            raise ValueError(f"dropout probability must be in [0, 1), got {dropout_p}")
-        raise NotImplementedError("dropout_p > 0 is not implemented by the B200 PPMoE kernels yet")
+    seed = _dropout_seed(dropout_p, rng)
     num_experts = gate.num_experts
     if not 1 <= top_k <= num_experts:
         raise ValueError(f"top_k must be in [1, {num_experts}], got {top_k}")
@@ -565,7 +577,8 @@ def ppmoe_forward(world: World, group: ProcessGroup, hidden, gate, experts_by_ra
         chunks = max(1, int(env_chunks))
     else:
         chunks = 1  # token-chunked combine measured slower than one all-reduce
-    spec = _Spec(world, group, top_k, float(capacity_factor), bool(weight_scaling), ov, e0, el, aux_here, chunks)
+    spec = _Spec(world, group, top_k, float(capacity_factor), bool(weight_scaling), ov, e0, el, aux_here, chunks,
+                 float(dropout_p), seed)
     wg = gate.wg if gate.wg.dtype == torch.float32 else gate.wg.float()
     out, l_aux = _PPMoEFunction.apply(hidden.contiguous(), wg, local.up.contiguous(), local.down.contiguous(),
                                       None if local.bias_up is None else local.bias_up.contiguous(),

@@ -311,3 +311,56 @@ def test_dpmoe_single_rank_matches_ppmoe():
     assert scaled_err(x.grad.double().cpu().numpy(), pp["grad_hidden"]) < 1e-2
     for k, g in w.named_grads().items():
         assert scaled_err(g.double().cpu().numpy(), pp["grads"][k]) < 2e-2, k
+
+
+# ------------------------------------------------------------------ dropout (tensor.py:315-330)
+
+
+def _dropout_run(hidden, w, p, seed, dtype=torch.float32, direction=None, gout=None):
+    x = torch.as_tensor(hidden).to("cuda", dtype)
+    if direction is not None:
+        x = x + torch.as_tensor(direction).to("cuda", dtype)
+    x.requires_grad_()
+    out, l_aux = P.ppmoe_forward(P.World(1, 2), P.ProcessGroup(P.EP, (0, 1)), x, w.gate, w.shard(2), top_k=2,
+                                 dropout_p=p, rng=None if p == 0 else P.Rng(seed))
+    loss = (out.double() * torch.as_tensor(gout, device="cuda")).sum() + l_aux
+    return out, loss, x
+
+
+def test_dropout_changes_output_and_needs_rng():
+    layer = oracle_rounded(O.init_layer(128, 4, seed=100), torch.float32)
+    w = device_weights(layer, torch.float32)
+    hidden = np.random.default_rng(1).standard_normal((96, 128))
+    gout = np.ones((96, 128))
+    base, _, _ = _dropout_run(hidden, w, 0.0, 0, gout=gout)
+    dropped, _, _ = _dropout_run(hidden, w, 0.5, 102, gout=gout)
+    again, _, _ = _dropout_run(hidden, w, 0.5, 102, gout=gout)
+    assert dropped.shape == base.shape
+    assert (dropped - base).abs().max().item() > 0
+    assert torch.equal(dropped, again)  # same rng seed -> same mask
+    zero_frac = (dropped == 0).float().mean().item()
+    assert 0.3 < zero_frac < 0.7  # two dropped experts per token at p=0.5: ~25-50 % exact zeros
+    with pytest.raises(ValueError, match="requires an rng"):
+        P.ppmoe_forward(P.World(1, 1), P.ProcessGroup(P.EP, (0,)), torch.zeros(4, 128, device="cuda"), w.gate,
+                        [w.bank], dropout_p=0.5)
+    with pytest.raises(ValueError, match=r"\[0, 1\)"):
+        P.ppmoe_forward(P.World(1, 1), P.ProcessGroup(P.EP, (0,)), torch.zeros(4, 128, device="cuda"), w.gate,
+                        [w.bank], dropout_p=1.0, rng=P.Rng(1))
+
+
+def test_dropout_gradient_directional_finite_difference():
+    """fp32 mode, fixed mask (same rng seed): <dL/dx, v> matches the central difference."""
+    layer = oracle_rounded(O.init_layer(64, 4, seed=85, bias=True), torch.float32)
+    w = device_weights(layer, torch.float32)
+    rng = np.random.default_rng(3)
+    hidden = rng.standard_normal((48, 64))
+    gout = rng.standard_normal((48, 64))
+    v = rng.standard_normal((48, 64))
+    _, loss, x = _dropout_run(hidden, w, 0.3, 7, gout=gout)
+    loss.backward()
+    analytic = float((x.grad.double().cpu() * torch.as_tensor(v)).sum())
+    eps = 1e-3
+    _, lp, _ = _dropout_run(hidden, w, 0.3, 7, direction=eps * v, gout=gout)
+    _, lm, _ = _dropout_run(hidden, w, 0.3, 7, direction=-eps * v, gout=gout)
+    numeric = (float(lp) - float(lm)) / (2 * eps)
+    assert abs(analytic - numeric) <= 2e-3 * max(1.0, abs(numeric)), (analytic, numeric)
