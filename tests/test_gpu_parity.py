@@ -339,7 +339,7 @@ def test_dropout_changes_output_and_needs_rng():
     assert (dropped - base).abs().max().item() > 0
     assert torch.equal(dropped, again)  # same rng seed -> same mask
     zero_frac = (dropped == 0).float().mean().item()
-    assert 0.3 < zero_frac < 0.7  # two dropped experts per token at p=0.5: ~25-50 % exact zeros
+    assert 0.2 < zero_frac < 0.3  # an element is zero when both of its top-2 contributions drop: p^2 = 0.25
     with pytest.raises(ValueError, match="requires an rng"):
         P.ppmoe_forward(P.World(1, 1), P.ProcessGroup(P.EP, (0,)), torch.zeros(4, 128, device="cuda"), w.gate,
                         [w.bank], dropout_p=0.5)
