@@ -18,6 +18,7 @@ from .moe import (
     build_dispatch_plan,
     gate_top1,
     gate_topk,
+    global_batch_equivalence,
     ppmoe_forward,
     sync_gate_gradients,
 )
@@ -29,6 +30,6 @@ __version__ = "0.1.0"
 __all__ = [
     "DP", "EP", "PP", "TP", "ConfigurationError", "GroupSet", "ProcessGroup", "TrafficLedger", "World", "tp_groups",
     "DispatchPlan", "ExpertBank", "ExpertFfn", "GateOutput", "GateParams", "LayerConfig", "MoeLayerWeights",
-    "PPMoELayer", "aux_loss", "build_dispatch_plan", "gate_top1", "gate_topk", "ppmoe_forward",
+    "PPMoELayer", "aux_loss", "build_dispatch_plan", "gate_top1", "gate_topk", "global_batch_equivalence", "ppmoe_forward",
     "sync_gate_gradients", "Rng", "dpmoe_forward", "dpmoe_sync_gradients",
 ]

@@ -657,3 +657,53 @@ class PPMoELayer(torch.nn.Module):
 
     def sync_gate_gradients(self):
         sync_gate_gradients(self.world, self.group, self.weights.gate)
+
+
+def global_batch_equivalence(weights: MoeLayerWeights, global_batch, dp: int, *, tp: int = 1, include_aux: bool = True,
+                             weight_scaling: bool = True, top_k: int = 1):
+    """Gradients of one global batch spanned spatially vs temporally (moe.py:475-533).
+
+    Spatial: the micro-batches as `dp` expert-parallel ranks of the all-to-all layer with the
+    gradient sum of the data-parallel all-reduce (single process: one rank after another on
+    this GPU; the ranks share no state when capacity is unlimited).  Temporal: the same
+    micro-batches one after another through the PPMoE layer on a `tp` group, gradients
+    accumulated, then the gate-gradient sync.  Loss per micro-batch: sum(out) (+ l_aux).
+    Returns (spatial, temporal) dicts of fp64 numpy arrays under the reference's names.
+    """
+    from .dpmoe import dpmoe_forward
+
+    if len(global_batch) != dp:
+        raise ValueError(f"global batch of {len(global_batch)} micro-batches does not span dp={dp}")
+    dev = weights.gate.wg.device
+    dtype = weights.bank.up.dtype
+
+    def snapshot():
+        return {k: v.detach().double().cpu().numpy().copy() for k, v in weights.named_grads().items() if v is not None}
+
+    def as_input(x):
+        return torch.as_tensor(np.asarray(x), dtype=torch.float64).to(device=dev, dtype=dtype).contiguous()
+
+    def loss_of(out, l_aux):
+        term = out.float().sum()
+        return term + l_aux if include_aux else term
+
+    weights.zero_grad()
+    world_s = World(1, 1)
+    for x in global_batch:
+        out, l_aux = dpmoe_forward(world_s, ProcessGroup(EP, (0,)), as_input(x), weights.gate,
+                                   experts_by_rank=weights.shard(1), capacity_factor=math.inf,
+                                   weight_scaling=weight_scaling, top_k=top_k)
+        loss_of(out, l_aux).backward()
+    spatial = snapshot()
+
+    weights.zero_grad()
+    world_t = World(1, tp)
+    group = ProcessGroup(EP, tuple(range(tp)))
+    shards = weights.shard(tp)
+    for x in global_batch:
+        out, l_aux = ppmoe_forward(world_t, group, as_input(x), weights.gate, shards, weight_scaling=weight_scaling,
+                                   top_k=top_k)
+        loss_of(out, l_aux).backward()
+    sync_gate_gradients(world_t, group, weights.gate)
+    temporal = snapshot()
+    return spatial, temporal

@@ -364,3 +364,42 @@ def test_dropout_gradient_directional_finite_difference():
     _, lm, _ = _dropout_run(hidden, w, 0.3, 7, direction=-eps * v, gout=gout)
     numeric = (float(lp) - float(lm)) / (2 * eps)
     assert abs(analytic - numeric) <= 2e-3 * max(1.0, abs(numeric)), (analytic, numeric)
+
+
+# ------------------------------------------------------------------ spatial vs temporal spans (moe.py:475-533)
+
+
+@pytest.mark.parametrize("dtype,tol", [(torch.float32, 1e-5), (torch.bfloat16, 2e-2)])
+def test_global_batch_equivalence_spatial_vs_temporal(dtype, tol):
+    layer = oracle_rounded(O.init_layer(64, 4, seed=78), dtype)
+    w = device_weights(layer, dtype)
+    rng = np.random.default_rng(79)
+    batch = [rng.standard_normal((96, 64)) for _ in range(4)]
+    spatial, temporal = P.global_batch_equivalence(w, batch, dp=4, tp=2)
+    assert set(spatial) == set(temporal)
+    for name in spatial:
+        assert O.rel_err(spatial[name], temporal[name]) < tol, name
+    # and against the oracle: the same span run through the fp64 closed form
+    ref = None
+    for x in batch:
+        r = O.ppmoe_layer(torch.as_tensor(x).to(dtype).double().numpy(), layer)
+        ref = r.grads if ref is None else {k: ref[k] + r.grads[k] for k in ref}
+    for name in ref:
+        assert scaled_err(temporal[name], ref[name]) < TOL[dtype], name
+
+
+def test_layer_config_builds_matching_architectures():
+    """cli._layer_config_check pattern (cli.py:119-151): a LayerConfig drives both layers."""
+    cfg = P.LayerConfig.from_dict({"hidden": 128, "experts": 4, "tp": 2, "capacity_factor": "inf", "seed": 5})
+    layer = P.PPMoELayer(cfg, dtype=torch.float32)
+    x = torch.randn(64, 128, device="cuda")
+    out, l_aux = layer(x)
+    w = layer.weights
+    out2, l_aux2 = P.dpmoe_forward(P.World(1, 1), P.ProcessGroup(P.EP, (0,)), x, w.gate,
+                                   experts_by_rank=w.shard(1))
+    assert (out - out2).abs().max().item() < 1e-5
+    assert abs(float(l_aux) - float(l_aux2)) < 1e-6
+    # weights drawn with the reference's Philox streams (moe.py:120-124)
+    ref = O.init_layer(128, 4, seed=5)
+    assert np.allclose(w.gate.wg.detach().cpu().numpy(), ref.wg.astype(np.float32))
+    assert np.allclose(w.bank.up[1].detach().cpu().numpy(), ref.up[1].astype(np.float32))
