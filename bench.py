@@ -36,30 +36,41 @@ sys.path.insert(0, str(ROOT))
 METRIC = "MoE-layer tokens/sec (fwd+bwd) at 1/2/4/8 B200; % of HBM/tensor roofline"
 UNIT = "tokens/s"
 C2 = {"hidden": 4096, "ffn": 16384, "experts": 8, "top_k": 2, "tokens": 16384}
+# BASELINE.json configs[2] ("C3"): the token count is not given there; 16384 assumed
+C3 = {"hidden": 8192, "ffn": 32768, "experts": 16, "top_k": 2, "tokens": 16384, "capacity_factor": 1.25}
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--config", choices=["c2", "c3"], default="c2", help="BASELINE.json configs[1] or configs[2]")
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--tokens", type=int, default=C2["tokens"])
-    ap.add_argument("--hidden", type=int, default=C2["hidden"])
-    ap.add_argument("--experts", type=int, default=C2["experts"])
-    ap.add_argument("--top-k", type=int, default=C2["top_k"])
-    ap.add_argument("--capacity-factor", type=float, default=math.inf)
+    ap.add_argument("--tokens", type=int, default=None)
+    ap.add_argument("--hidden", type=int, default=None)
+    ap.add_argument("--experts", type=int, default=None)
+    ap.add_argument("--top-k", type=int, default=None)
+    ap.add_argument("--capacity-factor", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-a2a", action="store_true", help="skip the all-to-all (DPMoE) comparator")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU time of the cpu_baseline sample")
-    return ap.parse_args()
+    a = ap.parse_args()
+    base = C3 if a.config == "c3" else C2
+    a.tokens = a.tokens if a.tokens is not None else base["tokens"]
+    a.hidden = a.hidden if a.hidden is not None else base["hidden"]
+    a.experts = a.experts if a.experts is not None else base["experts"]
+    a.top_k = a.top_k if a.top_k is not None else base["top_k"]
+    if a.capacity_factor is None:
+        a.capacity_factor = base.get("capacity_factor", math.inf)
+    return a
 
 
 def config_of(a, n_gpus):
     return {
-        "workload": f"C2 PPMoE layer h={a.hidden} ffn={4 * a.hidden} E={a.experts} top-{a.top_k} "
-                    f"N={a.tokens} bf16, TP={n_gpus}",
+        "workload": f"{a.config.upper()} PPMoE layer h={a.hidden} ffn={4 * a.hidden} E={a.experts} top-{a.top_k} "
+                    f"N={a.tokens} cf={a.capacity_factor} bf16, TP={n_gpus}",
         "hidden": a.hidden, "ffn": 4 * a.hidden, "experts": a.experts, "top_k": a.top_k, "tokens": a.tokens,
         "capacity_factor": "inf" if math.isinf(a.capacity_factor) else a.capacity_factor,
         "tp": n_gpus, "parallelism": f"tp{n_gpus} (experts {a.experts // n_gpus}/GPU)",
@@ -295,8 +306,13 @@ def main():
     peak_src = "MEASURED_PEAKS.json bf16_tflops_sustained" if "bf16_tflops_sustained" in peaks else "fallback 1.4 PF/s"
     gemm_names = ["ppmoe_expert_fc1_fwd", "ppmoe_expert_fc2_fwd", "ppmoe_expert_fc2_dgrad", "ppmoe_expert_fc2_wgrad",
                   "ppmoe_expert_fc1_dgrad", "ppmoe_expert_fc1_wgrad"]
-    pairs = n * k  # kept pairs (no capacity drops at cf=inf); per rank P/tp under balance
-    flop_per_gemm = 2.0 * pairs * h * f / tp
+    # algorithmic work: kept (token, expert) pairs of this rank's experts (capacity may drop some)
+    rt_ = _ops.route(x.detach(), w.gate.wg.detach(), k)
+    pl_ = _ops.plan(rt_.idx, rt_.w, E, _ops.capacity_for(a.capacity_factor, n, k, E))
+    kept_all = pl_.kept.cpu()
+    pairs = int(kept_all.sum())
+    local_pairs = int(kept_all[rank * el:(rank + 1) * el].sum())
+    flop_per_gemm = 2.0 * local_pairs * h * f
     gemm_ms = sum(ksum.get(nm, {}).get("ms", 0.0) for nm in gemm_names) / a.steps
     gemm_launches = sum(ksum.get(nm, {}).get("launches", 0) for nm in gemm_names) / a.steps
     achieved = 6 * flop_per_gemm / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
@@ -312,7 +328,8 @@ def main():
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                 "kernel": "grouped_gemm_sm100 (6 launches/step: fc1/fc2 fwd, dgrad, wgrad)",
-                "algorithmic": f"12*P*h*f/TP flop per step, P={pairs} pairs; {gemm_ms:.3f} ms of GEMM per step",
+                "algorithmic": f"12*P_r*h*f flop per step on this rank, P_r={local_pairs} of P={pairs} kept pairs; "
+                               f"{gemm_ms:.3f} ms of GEMM per step",
                 "peak_source": peak_src, "gemm_share_of_step": gemm_ms / ms if ms else None}
 
     # ---- end to end: host (pinned) input -> device -> fwd+bwd -> loss back to host

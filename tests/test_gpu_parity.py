@@ -403,3 +403,24 @@ def test_layer_config_builds_matching_architectures():
     ref = O.init_layer(128, 4, seed=5)
     assert np.allclose(w.gate.wg.detach().cpu().numpy(), ref.wg.astype(np.float32))
     assert np.allclose(w.bank.up[1].detach().cpu().numpy(), ref.up[1].astype(np.float32))
+
+
+def test_c3_shape_routing_capacity_and_step():
+    """BASELINE configs[2] shape (h 8192, ffn 32768, 16 experts, top-2, cf 1.25) at 2048 tokens:
+    routing bit-exact vs the fp64 oracle, capacity bound respected, finite fwd+bwd."""
+    h, e, n, k, cf = 8192, 16, 2048, 2, 1.25
+    w = P.MoeLayerWeights.random(h, e, seed=3, device="cuda")
+    x = torch.randn(n, h, device="cuda").bfloat16()
+    g = P.gate_topk(x, w.gate, k)
+    ref = O.gate_topk(x.double().cpu().numpy(), w.gate.wg.detach().double().cpu().numpy(), k)
+    assert np.array_equal(g.indices.cpu().numpy(), ref.indices)
+    cap = int(np.ceil(cf * k * n / e))
+    lists, kept, counts = O.dispatch_plan(ref.indices, e, cap)
+    plan = P.build_dispatch_plan(g.indices, e, capacity=cap)
+    assert plan.per_expert == lists and max(len(r) for r in lists) <= cap
+    x.requires_grad_()
+    out, l_aux = P.ppmoe_forward(P.World(1, 1), P.ProcessGroup(P.EP, (0,)), x, w.gate, [w.bank], top_k=k,
+                                 capacity_factor=cf)
+    (out.float().sum() + l_aux).backward()
+    assert torch.isfinite(out).all() and torch.isfinite(x.grad).all()
+    assert torch.isfinite(w.bank.up.grad).all() and torch.isfinite(w.gate.wg.grad).all()
