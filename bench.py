@@ -318,7 +318,7 @@ def main():
     achieved = 6 * flop_per_gemm / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
     traffic = None
     tfile = ROOT / "profiles" / "ncu_traffic.json"
-    if tfile.exists():
+    if tfile.exists() and a.config == "c2" and tp == 1:
         try:
             traffic = json.loads(tfile.read_text()).get("grouped_gemm_sm100_bytes_per_launch")
         except Exception:
@@ -404,7 +404,7 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world_size, "steps": a.steps,
                 "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-                "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights of the C2 layer, N(0,1) tokens)",
+                "vs_baseline": None, "dtype": "bf16", "data": f"synthetic (random-init weights of the {a.config.upper()} layer, N(0,1) tokens)",
                 "config": config_of(a, world_size), "roofline": roofline, "cpu_baseline": cb, "e2e": e2e,
                 "gpu_launches": int(launches), "clocks": clk.summary(), "a2a_comparator": a2a, "kernels": per_kernel,
                 "gemm_launches_per_step": gemm_launches}

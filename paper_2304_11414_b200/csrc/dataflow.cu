@@ -255,12 +255,45 @@ __global__ void chunk_rows_kernel(const int* __restrict__ tok_local, const int* 
 
 constexpr int kGradTC = 128;  // tokens per chunk of the dWg partials
 
-template <typename T, int EB>
+template <typename T, int CPT>
+__device__ __forceinline__ void load_cols(const T* p, float (&v)[CPT]) {
+  if constexpr (sizeof(T) == 2 && CPT == 4) {
+    const uint2 u = *reinterpret_cast<const uint2*>(p);
+    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+    const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+  } else if constexpr (sizeof(T) == 4 && CPT == 4) {
+    const float4 f = *reinterpret_cast<const float4*>(p);
+    v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+  } else {
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) v[c] = to_f32(p[c]);
+  }
+}
+
+template <typename T, int CPT>
+__device__ __forceinline__ void store_cols(T* p, const float (&v)[CPT]) {
+  if constexpr (sizeof(T) == 2 && CPT == 4) {
+    uint2 u;
+    u.x = pack_bf16x2(v[0], v[1]);
+    u.y = pack_bf16x2(v[2], v[3]);
+    *reinterpret_cast<uint2*>(p) = u;
+  } else if constexpr (sizeof(T) == 4 && CPT == 4) {
+    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  } else {
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) p[c] = from_f32<T>(v[c]);
+  }
+}
+
+// Thread = CPT adjacent hidden columns; the token loop is unrolled by 4 with all loads of
+// a group issued before the FMAs (enough bytes in flight to stream at HBM rate).
+template <typename T, int EB, int CPT>
 __global__ void __launch_bounds__(256)
     gate_grads_kernel(const float* __restrict__ dx_acc, const T* __restrict__ X, const float* __restrict__ dL,
                       const float* __restrict__ Wg, int N, int H, int E, T* __restrict__ dX, float* __restrict__ part) {
   __shared__ float sdl[kGradTC][EB];
-  const int j = blockIdx.x * 256 + threadIdx.x;
+  const int j0 = (blockIdx.x * 256 + threadIdx.x) * CPT;
   const int c = blockIdx.y;
   const int t0 = c * kGradTC;
   for (int i = threadIdx.x; i < kGradTC * EB; i += 256) {
@@ -269,33 +302,58 @@ __global__ void __launch_bounds__(256)
     sdl[tt][e] = (t < N && e < E) ? dL[static_cast<size_t>(t) * E + e] : 0.f;
   }
   __syncthreads();
-  if (j >= H) return;
-  float wg[EB], acc[EB];
+  if (j0 >= H) return;
+  float wg[CPT][EB], acc[CPT][EB];
 #pragma unroll
-  for (int e = 0; e < EB; ++e) {
-    wg[e] = e < E ? Wg[static_cast<size_t>(j) * E + e] : 0.f;
-    acc[e] = 0.f;
-  }
-  const int tn = min(kGradTC, N - t0);
-  for (int tt = 0; tt < tn; ++tt) {
-    const size_t o = static_cast<size_t>(t0 + tt) * H + j;
-    if (dX) {
-      float v = dx_acc ? dx_acc[o] : 0.f;
+  for (int q = 0; q < CPT; ++q)
 #pragma unroll
-      for (int e = 0; e < EB; ++e) v = fmaf(sdl[tt][e], wg[e], v);
-      dX[o] = from_f32<T>(v);
+    for (int e = 0; e < EB; ++e) {
+      wg[q][e] = e < E ? Wg[static_cast<size_t>(j0 + q) * E + e] : 0.f;
+      acc[q][e] = 0.f;
     }
-    if (part) {
-      const float x = to_f32(X[o]);
+  const int tn = min(kGradTC, N - t0);
+  constexpr int U = 4;
+  for (int tt = 0; tt < tn; tt += U) {
+    float dxv[U][CPT], xv[U][CPT];
 #pragma unroll
-      for (int e = 0; e < EB; ++e) acc[e] = fmaf(x, sdl[tt][e], acc[e]);
+    for (int u = 0; u < U; ++u) {
+      const size_t o = static_cast<size_t>(t0 + tt + u) * H + j0;
+      const bool ok = tt + u < tn;
+#pragma unroll
+      for (int q = 0; q < CPT; ++q) dxv[u][q] = 0.f, xv[u][q] = 0.f;
+      if (ok && dX && dx_acc) load_cols<float, CPT>(dx_acc + o, dxv[u]);
+      if (ok && part) load_cols<T, CPT>(X + o, xv[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (tt + u >= tn) break;
+      const float* d = sdl[tt + u];
+      if (dX) {
+        float v[CPT];
+#pragma unroll
+        for (int q = 0; q < CPT; ++q) {
+          v[q] = dxv[u][q];
+#pragma unroll
+          for (int e = 0; e < EB; ++e) v[q] = fmaf(d[e], wg[q][e], v[q]);
+        }
+        store_cols<T, CPT>(dX + static_cast<size_t>(t0 + tt + u) * H + j0, v);
+      }
+      if (part) {
+#pragma unroll
+        for (int q = 0; q < CPT; ++q)
+#pragma unroll
+          for (int e = 0; e < EB; ++e) acc[q][e] = fmaf(xv[u][q], d[e], acc[q][e]);
+      }
     }
   }
   if (part) {
-    float* p = part + (static_cast<size_t>(c) * H + j) * E;
 #pragma unroll
-    for (int e = 0; e < EB; ++e)
-      if (e < E) p[e] = acc[e];
+    for (int q = 0; q < CPT; ++q) {
+      float* p = part + (static_cast<size_t>(c) * H + j0 + q) * E;
+#pragma unroll
+      for (int e = 0; e < EB; ++e)
+        if (e < E) p[e] = acc[q][e];
+    }
   }
 }
 
@@ -415,24 +473,29 @@ int ppmoe_gate_grads(const float* dx_acc, const void* X, int dtype, const float*
   PPMOE_REQUIRE(!dWg || ws_bytes >= ppmoe_gate_grad_workspace_bytes(N, H, E), "gate-grad workspace too small");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int C = (N + kGradTC - 1) / kGradTC;
-  dim3 grid((H + 255) / 256, C);
   float* part = dWg ? static_cast<float*>(ws) : nullptr;
-#define PPMOE_GG(T, EB)                                                                                            \
-  gate_grads_kernel<T, EB><<<grid, 256, 0, s>>>(dx_acc, static_cast<const T*>(X), dL, Wg, N, H, E, static_cast<T*>(dX), \
-                                                part)
-  if (dtype == kBF16) {
-    using T = __nv_bfloat16;
-    if (E <= 8) PPMOE_GG(T, 8);
-    else if (E <= 16) PPMOE_GG(T, 16);
-    else if (E <= 32) PPMOE_GG(T, 32);
-    else PPMOE_GG(T, 64);
-  } else {
-    using T = float;
-    if (E <= 8) PPMOE_GG(T, 8);
-    else if (E <= 16) PPMOE_GG(T, 16);
-    else if (E <= 32) PPMOE_GG(T, 32);
-    else PPMOE_GG(T, 64);
-  }
+  const int cpt = (H % 4 == 0 && E <= 16) ? 4 : 1;
+  dim3 grid((H + 256 * cpt - 1) / (256 * cpt), C);
+#define PPMOE_GG(T, EB, CPT)                                                                                    \
+  gate_grads_kernel<T, EB, CPT><<<grid, 256, 0, s>>>(dx_acc, static_cast<const T*>(X), dL, Wg, N, H, E,         \
+                                                     static_cast<T*>(dX), part)
+#define PPMOE_GG_E(T)                                   \
+  do {                                                  \
+    if (E <= 8) {                                       \
+      if (cpt == 4) PPMOE_GG(T, 8, 4);                  \
+      else PPMOE_GG(T, 8, 1);                           \
+    } else if (E <= 16) {                               \
+      if (cpt == 4) PPMOE_GG(T, 16, 4);                 \
+      else PPMOE_GG(T, 16, 1);                          \
+    } else if (E <= 32) {                               \
+      PPMOE_GG(T, 32, 1);                               \
+    } else {                                            \
+      PPMOE_GG(T, 64, 1);                               \
+    }                                                   \
+  } while (0)
+  if (dtype == kBF16) PPMOE_GG_E(__nv_bfloat16);
+  else PPMOE_GG_E(float);
+#undef PPMOE_GG_E
 #undef PPMOE_GG
   if (int rc = check_launch("gate_grads_kernel")) return rc;
   if (dWg) {
