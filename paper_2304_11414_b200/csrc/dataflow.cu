@@ -257,7 +257,15 @@ constexpr int kGradTC = 128;  // tokens per chunk of the dWg partials
 
 template <typename T, int CPT>
 __device__ __forceinline__ void load_cols(const T* p, float (&v)[CPT]) {
-  if constexpr (sizeof(T) == 2 && CPT == 4) {
+  if constexpr (sizeof(T) == 2 && CPT == 2) {
+    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(p));
+    v[0] = a.x;
+    v[1] = a.y;
+  } else if constexpr (sizeof(T) == 4 && CPT == 2) {
+    const float2 f = *reinterpret_cast<const float2*>(p);
+    v[0] = f.x;
+    v[1] = f.y;
+  } else if constexpr (sizeof(T) == 2 && CPT == 4) {
     const uint2 u = *reinterpret_cast<const uint2*>(p);
     const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
     const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
@@ -273,7 +281,11 @@ __device__ __forceinline__ void load_cols(const T* p, float (&v)[CPT]) {
 
 template <typename T, int CPT>
 __device__ __forceinline__ void store_cols(T* p, const float (&v)[CPT]) {
-  if constexpr (sizeof(T) == 2 && CPT == 4) {
+  if constexpr (sizeof(T) == 2 && CPT == 2) {
+    *reinterpret_cast<uint32_t*>(p) = pack_bf16x2(v[0], v[1]);
+  } else if constexpr (sizeof(T) == 4 && CPT == 2) {
+    *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
+  } else if constexpr (sizeof(T) == 2 && CPT == 4) {
     uint2 u;
     u.x = pack_bf16x2(v[0], v[1]);
     u.y = pack_bf16x2(v[2], v[3]);
@@ -474,7 +486,7 @@ int ppmoe_gate_grads(const float* dx_acc, const void* X, int dtype, const float*
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int C = (N + kGradTC - 1) / kGradTC;
   float* part = dWg ? static_cast<float*>(ws) : nullptr;
-  const int cpt = (H % 4 == 0 && E <= 16) ? 4 : 1;
+  const int cpt = (H % 2 == 0 && E <= 16) ? 2 : 1;
   dim3 grid((H + 256 * cpt - 1) / (256 * cpt), C);
 #define PPMOE_GG(T, EB, CPT)                                                                                    \
   gate_grads_kernel<T, EB, CPT><<<grid, 256, 0, s>>>(dx_acc, static_cast<const T*>(X), dL, Wg, N, H, E,         \
@@ -482,10 +494,10 @@ int ppmoe_gate_grads(const float* dx_acc, const void* X, int dtype, const float*
 #define PPMOE_GG_E(T)                                   \
   do {                                                  \
     if (E <= 8) {                                       \
-      if (cpt == 4) PPMOE_GG(T, 8, 4);                  \
+      if (cpt == 2) PPMOE_GG(T, 8, 2);                  \
       else PPMOE_GG(T, 8, 1);                           \
     } else if (E <= 16) {                               \
-      if (cpt == 4) PPMOE_GG(T, 16, 4);                 \
+      if (cpt == 2) PPMOE_GG(T, 16, 2);                 \
       else PPMOE_GG(T, 16, 1);                          \
     } else if (E <= 32) {                               \
       PPMOE_GG(T, 32, 1);                               \

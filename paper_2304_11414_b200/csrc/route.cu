@@ -21,9 +21,9 @@
 namespace ppmoe {
 
 constexpr int kRouteThreads = 256;
-constexpr int kRouteTB = 64;    // tokens per block
+constexpr int kRouteTB = 32;    // tokens per block (512 blocks at 16K tokens: >3 per SM)
 constexpr int kRouteTPT = 2;    // tokens per thread (each staged Wg value feeds 2 tokens)
-constexpr int kRouteKS = 8;     // hidden-dimension splits per token (threads per token pair)
+constexpr int kRouteKS = 16;    // hidden-dimension splits per token (threads per token pair)
 constexpr int kRouteHC = 512;   // hidden chunk of Wg staged as fp64 in shared memory
 constexpr int kChunk = 256;     // tokens per plan chunk (one thread per token)
 constexpr int kMaxE = 128;
@@ -119,8 +119,8 @@ __global__ void __launch_bounds__(kRouteThreads, 2) router_kernel(const T* __res
   double* lg = wsm + kRouteHC * EB;                            // [TB][E]
   double* stat = lg + kRouteTB * E;                            // [TB][2]
   const int tid = threadIdx.x;
-  const int ks = tid >> 5;                  // warp = one hidden split
-  const int tl0 = tid & 31, tl1 = tl0 + 32;  // the thread's two tokens (block-local)
+  const int ks = tid >> 4;                  // half-warp = one hidden split
+  const int tl0 = tid & 15, tl1 = tl0 + 16;  // the thread's two tokens (block-local)
   const int t0 = blockIdx.x * kRouteTB;
   const bool ok0 = t0 + tl0 < N, ok1 = t0 + tl1 < N;
   const bool vec = (H % (8 * kRouteKS)) == 0;
