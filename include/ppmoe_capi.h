@@ -66,12 +66,14 @@ unsigned long long ppmoe_kernel_launches(void);
  *   scores   [N x E] fp32    out: full softmax scores
  *   l_aux    [2] fp64        out: {l_aux, sum_e frac_e (== 1)}
  *   counts_top1 [E] int32    out: tokens whose slot-0 expert is e (or NULL)
+ *   score_sums  [E] fp64     out: sum over the N tokens of each expert's score (or NULL);
+ *                            with counts_top1 it lets token slices be combined across ranks
  *   ws       workspace of ppmoe_route_workspace_bytes(N, E, K) bytes
  */
 size_t ppmoe_route_workspace_bytes(int N, int E, int K);
 int ppmoe_route(const void* X, int dtype, const float* Wg, int N, int H, int E, int K, const int* route_override,
-                int* idx, float* w, float* scores, double* l_aux, int* counts_top1, void* ws, size_t ws_bytes,
-                void* stream);
+                int* idx, float* w, float* scores, double* l_aux, int* counts_top1, double* score_sums, void* ws,
+                size_t ws_bytes, void* stream);
 
 /* Dispatch plan with capacity: replaces build_dispatch_plan (moe.py:226-235)
  * and _capacity_mask (moe.py:345-360).  Stable counting sort of the (token,

@@ -71,13 +71,31 @@ __device__ __forceinline__ uint4 ldg16(const T* p) {
 
 template <typename T>
 __device__ __forceinline__ void widen8(const uint4* u, double* dst);
+// Branch-free exact widening of 8 bf16 values; zero handled by a select.  Subnormal and
+// inf/nan inputs (exponent field 0 with a nonzero mantissa, or 255) are detected once per
+// group and redone with F2F on a warp-uniform slow path (they never occur for finite
+// activations, but exactness must not depend on that).
 template <>
 __device__ __forceinline__ void widen8<__nv_bfloat16>(const uint4* u, double* dst) {
   const uint32_t w[4] = {u->x, u->y, u->z, u->w};
+  uint32_t special = 0;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    dst[2 * i] = bf16bits_to_f64(w[i] & 0xFFFFu);
-    dst[2 * i + 1] = bf16bits_to_f64(w[i] >> 16);
+#pragma unroll
+    for (int hlf = 0; hlf < 2; ++hlf) {
+      const uint32_t b = hlf ? (w[i] >> 16) : (w[i] & 0xFFFFu);
+      const uint32_t m = b & 0x7FFFu;
+      special |= (m - 1u < 0x7Fu) | (m >= 0x7F80u);
+      const uint32_t mag = m ? (m << 13) + 0x38000000u : 0u;
+      dst[2 * i + hlf] = __hiloint2double(static_cast<int>(((b & 0x8000u) << 16) | mag), 0);
+    }
+  }
+  if (__any_sync(__activemask(), special)) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      dst[2 * i] = static_cast<double>(__uint_as_float(w[i] << 16));
+      dst[2 * i + 1] = static_cast<double>(__uint_as_float(w[i] & 0xFFFF0000u));
+    }
   }
 }
 template <>
@@ -107,7 +125,7 @@ __host__ inline size_t route_smem_bytes(int E) {
 // splits); experts in register passes of EB.  Every lane of a warp reads the same
 // staged Wg value (shared-memory broadcast).
 template <typename T, int EB>
-__global__ void __launch_bounds__(kRouteThreads, 2) router_kernel(const T* __restrict__ X, const float* __restrict__ Wg,
+__global__ void __launch_bounds__(kRouteThreads, EB == 8 ? 2 : 1) router_kernel(const T* __restrict__ X, const float* __restrict__ Wg,
                                                                int N, int H, int E, int K, const int* __restrict__ ovr,
                                                                int* __restrict__ idx, float* __restrict__ w,
                                                                float* __restrict__ scores, double* __restrict__ ssum,
@@ -123,60 +141,87 @@ __global__ void __launch_bounds__(kRouteThreads, 2) router_kernel(const T* __res
   const int tl0 = tid & 15, tl1 = tl0 + 16;  // the thread's two tokens (block-local)
   const int t0 = blockIdx.x * kRouteTB;
   const bool ok0 = t0 + tl0 < N, ok1 = t0 + tl1 < N;
-  const bool vec = (H % (8 * kRouteKS)) == 0;
   const T* x0 = X + static_cast<size_t>(ok0 ? t0 + tl0 : 0) * H;
   const T* x1 = X + static_cast<size_t>(ok1 ? t0 + tl1 : 0) * H;
 
+  const bool fast = (H % kRouteHC) == 0;  // whole chunks: software-pipelined path
   for (int e0 = 0; e0 < E; e0 += EB) {
     double a0[EB], a1[EB];
 #pragma unroll
     for (int j = 0; j < EB; ++j) a0[j] = a1[j] = 0.0;
-    for (int h0 = 0; h0 < H; h0 += kRouteHC) {
-      const int hc = min(kRouteHC, H - h0);
-      __syncthreads();
-      for (int i = tid; i < hc * EB; i += kRouteThreads) {
-        const int c = i / EB, j = i % EB;
-        wsm[i] = e0 + j < E ? static_cast<double>(Wg[static_cast<size_t>(h0 + c) * E + e0 + j]) : 0.0;
-      }
-      __syncthreads();
-      if (vec) {
-        const int span = hc / kRouteKS;  // multiple of 8
-        const int c_lo = ks * span;
-        constexpr int kU = sizeof(T) == 2 ? 1 : 2;  // uint4 per 8 values
-        for (int c0 = c_lo; c0 < c_lo + span; c0 += 32) {
-          const int nsub = min(4, (c_lo + span - c0) / 8);
-          uint4 ua[4][kU], ub[4][kU];
+    if (fast) {
+      // Each thread owns kSpan hidden columns of every chunk (kG groups of 8).  The x loads
+      // of chunk c+1 and its Wg values are issued while chunk c computes, so HBM latency
+      // overlaps the FP64 FMAs instead of draining at every chunk barrier.
+      constexpr int kSpan = kRouteHC / kRouteKS;
+      constexpr int kG = kSpan / 8;
+      constexpr int kU = sizeof(T) == 2 ? 1 : 2;  // uint4 per 8 values
+      constexpr int kWPer = kRouteHC * EB / kRouteThreads;
+      const int nch = H / kRouteHC;
+      uint4 sa[kG][kU], sb[kG][kU];
+      float wnext[kWPer];
+      auto load_x = [&](int c) {
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            if (u < nsub) {
+        for (int u = 0; u < kG; ++u)
 #pragma unroll
-              for (int q = 0; q < kU; ++q) {
-                ua[u][q] = ok0 ? ldg16(x0 + h0 + c0 + 8 * u + 4 * q) : make_uint4(0, 0, 0, 0);
-                ub[u][q] = ok1 ? ldg16(x1 + h0 + c0 + 8 * u + 4 * q) : make_uint4(0, 0, 0, 0);
-              }
+          for (int q = 0; q < kU; ++q) {
+            const int off = c * kRouteHC + ks * kSpan + 8 * u + 4 * q;
+            sa[u][q] = ok0 ? ldg16(x0 + off) : make_uint4(0, 0, 0, 0);
+            sb[u][q] = ok1 ? ldg16(x1 + off) : make_uint4(0, 0, 0, 0);
+          }
+      };
+      auto load_w = [&](int c) {
+#pragma unroll
+        for (int r = 0; r < kWPer; ++r) {
+          const int i = tid + r * kRouteThreads;
+          const int cc = i / EB, j = i % EB;
+          wnext[r] = e0 + j < E ? __ldg(Wg + static_cast<size_t>(c * kRouteHC + cc) * E + e0 + j) : 0.f;
+        }
+      };
+      load_x(0);
+      load_w(0);
+      for (int c = 0; c < nch; ++c) {
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < kWPer; ++r) wsm[tid + r * kRouteThreads] = static_cast<double>(wnext[r]);
+        __syncthreads();
+        if (c + 1 < nch) load_w(c + 1);
+#pragma unroll
+        for (int u = 0; u < kG; ++u) {
+          double xa[8], xb[8];
+          widen8<T>(sa[u], xa);
+          widen8<T>(sb[u], xb);
+          if (c + 1 < nch) {  // refill this slot with the next chunk's group
+#pragma unroll
+            for (int q = 0; q < kU; ++q) {
+              const int off = (c + 1) * kRouteHC + ks * kSpan + 8 * u + 4 * q;
+              sa[u][q] = ok0 ? ldg16(x0 + off) : make_uint4(0, 0, 0, 0);
+              sb[u][q] = ok1 ? ldg16(x1 + off) : make_uint4(0, 0, 0, 0);
             }
           }
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            if (u >= nsub) break;
-            double xa[8], xb[8];
-            widen8<T>(ua[u], xa);
-            widen8<T>(ub[u], xb);
+          for (int i = 0; i < 8; ++i) {
+            const double* wr = wsm + (ks * kSpan + 8 * u + i) * EB;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const double* wr = wsm + (c0 + 8 * u + i) * EB;
-#pragma unroll
-              for (int j = 0; j < EB; j += 2) {
-                const double2 wv = *reinterpret_cast<const double2*>(wr + j);
-                a0[j] = fma(xa[i], wv.x, a0[j]);
-                a0[j + 1] = fma(xa[i], wv.y, a0[j + 1]);
-                a1[j] = fma(xb[i], wv.x, a1[j]);
-                a1[j + 1] = fma(xb[i], wv.y, a1[j + 1]);
-              }
+            for (int j = 0; j < EB; j += 2) {
+              const double2 wv = *reinterpret_cast<const double2*>(wr + j);
+              a0[j] = fma(xa[i], wv.x, a0[j]);
+              a0[j + 1] = fma(xa[i], wv.y, a0[j + 1]);
+              a1[j] = fma(xb[i], wv.x, a1[j]);
+              a1[j + 1] = fma(xb[i], wv.y, a1[j + 1]);
             }
           }
         }
-      } else {
+      }
+    } else {
+      for (int h0 = 0; h0 < H; h0 += kRouteHC) {
+        const int hc = min(kRouteHC, H - h0);
+        __syncthreads();
+        for (int i = tid; i < hc * EB; i += kRouteThreads) {
+          const int c = i / EB, j = i % EB;
+          wsm[i] = e0 + j < E ? static_cast<double>(Wg[static_cast<size_t>(h0 + c) * E + e0 + j]) : 0.0;
+        }
+        __syncthreads();
         for (int c = ks; c < hc; c += kRouteKS) {
           const double xa = ok0 ? static_cast<double>(to_f32(x0[h0 + c])) : 0.0;
           const double xb = ok1 ? static_cast<double>(to_f32(x1[h0 + c])) : 0.0;
@@ -255,17 +300,28 @@ __global__ void __launch_bounds__(kRouteThreads, 2) router_kernel(const T* __res
 }
 
 // l_aux = E * sum_e frac_e * mean_t s[t,e]  with frac from the top-1 choice (moe.py:221-223)
-__global__ void route_finalize_kernel(const double* __restrict__ ssum, int nblocks, const int* __restrict__ cnt_top1,
-                                      int N, int E, double* __restrict__ l_aux) {
+__global__ void __launch_bounds__(256) route_finalize_kernel(const double* __restrict__ ssum, int nblocks,
+                                                             const int* __restrict__ cnt_top1, int N, int E,
+                                                             double* __restrict__ l_aux,
+                                                             double* __restrict__ score_sums) {
+  __shared__ double red[256];
   __shared__ double part[kMaxE];
-  const int e = threadIdx.x;
-  if (e < E) {
+  for (int e = 0; e < E; ++e) {
     double s = 0.0;
-    for (int b = 0; b < nblocks; ++b) s += ssum[static_cast<size_t>(b) * E + e];
-    part[e] = s * (static_cast<double>(cnt_top1[e]) / N);
+    for (int b = threadIdx.x; b < nblocks; b += 256) s += ssum[static_cast<size_t>(b) * E + e];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {  // fixed-shape tree: deterministic
+      if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      part[e] = red[0] * (static_cast<double>(cnt_top1[e]) / N);
+      if (score_sums) score_sums[e] = red[0];
+    }
+    __syncthreads();
   }
-  __syncthreads();
-  if (e == 0) {
+  if (threadIdx.x == 0) {
     double tot = 0.0, fr = 0.0;
     for (int j = 0; j < E; ++j) {
       tot += part[j];
@@ -498,8 +554,8 @@ size_t ppmoe_route_workspace_bytes(int N, int E, int K) {
 }
 
 int ppmoe_route(const void* X, int dtype, const float* Wg, int N, int H, int E, int K, const int* route_override,
-                int* idx, float* w, float* scores, double* l_aux, int* counts_top1, void* ws, size_t ws_bytes,
-                void* stream) {
+                int* idx, float* w, float* scores, double* l_aux, int* counts_top1, double* score_sums, void* ws,
+                size_t ws_bytes, void* stream) {
   PPMOE_REQUIRE(dtype == kBF16 || dtype == kF32, "dtype must be 0 (bf16) or 1 (fp32)");
   PPMOE_REQUIRE(N >= 1, "aux_loss of zero tokens is undefined (N=%d)", N);
   PPMOE_REQUIRE(H >= 1 && E >= 1 && E <= kMaxE, "router needs 1 <= E <= %d, got E=%d H=%d", kMaxE, E, H);
@@ -518,7 +574,7 @@ int ppmoe_route(const void* X, int dtype, const float* Wg, int N, int H, int E, 
     rc = E <= 8 ? launch_router<float, 8>(X, Wg, N, H, E, K, route_override, idx, w, scores, ssum, cnt, s)
                 : launch_router<float, 16>(X, Wg, N, H, E, K, route_override, idx, w, scores, ssum, cnt, s);
   if (rc) return rc;
-  route_finalize_kernel<<<1, kMaxE, 0, s>>>(ssum, nb, cnt, N, E, l_aux);
+  route_finalize_kernel<<<1, 256, 0, s>>>(ssum, nb, cnt, N, E, l_aux, score_sums);
   if (int rc2 = check_launch("route_finalize_kernel")) return rc2;
   if (counts_top1) PPMOE_CUDA(cudaMemcpyAsync(counts_top1, cnt, static_cast<size_t>(E) * 4, cudaMemcpyDeviceToDevice, s));
   return kOk;

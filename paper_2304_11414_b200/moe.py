@@ -282,6 +282,7 @@ class LayerConfig:
     weight_scaling: bool = True
     dropout_p: float = 0.0
     seed: int = 0
+    sliced_router: bool = False
     top_k: int = 1
 
     _FIELDS = ("hidden", "experts", "tp", "capacity_factor", "weight_scaling", "dropout_p", "seed", "top_k")
@@ -433,7 +434,10 @@ class _PPMoEFunction(torch.autograd.Function):
     def forward(ctx, hidden, wg, up, down, bias_up, bias_down, spec: _Spec):
         n, h = hidden.shape
         e = wg.shape[1]
-        rt = _ops.route(hidden, wg, spec.k, spec.override)
+        if spec.sliced_router:
+            rt = _ops.route_sliced(spec.world, spec.group, hidden, wg, spec.k, spec.override)
+        else:
+            rt = _ops.route(hidden, wg, spec.k, spec.override)
         cap = _ops.capacity_for(spec.capacity_factor, n, spec.k, e)
         pl = _ops.plan(rt.idx, rt.w, e, cap)
         out_acc = torch.zeros((n, h), dtype=torch.float32, device=hidden.device)
@@ -577,8 +581,10 @@ def ppmoe_forward(world: World, group: ProcessGroup, hidden, gate, experts_by_ra
         chunks = max(1, int(env_chunks))
     else:
         chunks = 1  # token-chunked combine measured slower than one all-reduce
+    sliced = (world.distributed and tp > 1 and hidden.shape[0] % tp == 0
+              and os.environ.get("PPMOE_SLICED_ROUTER", "1") != "0")
     spec = _Spec(world, group, top_k, float(capacity_factor), bool(weight_scaling), ov, e0, el, aux_here, chunks,
-                 float(dropout_p), seed)
+                 float(dropout_p), seed, sliced)
     wg = gate.wg if gate.wg.dtype == torch.float32 else gate.wg.float()
     out, l_aux = _PPMoEFunction.apply(hidden.contiguous(), wg, local.up.contiguous(), local.down.contiguous(),
                                       None if local.bias_up is None else local.bias_up.contiguous(),

@@ -45,9 +45,9 @@ def test_workspace_queries_are_host_only():
 def test_invalid_arguments_raise_value_error_without_gpu():
     # argument validation happens before any CUDA call
     with pytest.raises(ValueError, match="top-k"):
-        _lib.call("ppmoe_route", None, 0, None, 8, 16, 4, 5, None, None, None, None, None, None, None, 0, None)
+        _lib.call("ppmoe_route", None, 0, None, 8, 16, 4, 5, None, None, None, None, None, None, None, None, 0, None)
     with pytest.raises(ValueError, match="zero tokens"):
-        _lib.call("ppmoe_route", None, 0, None, 0, 16, 4, 1, None, None, None, None, None, None, None, 0, None)
+        _lib.call("ppmoe_route", None, 0, None, 0, 16, 4, 1, None, None, None, None, None, None, None, None, 0, None)
     with pytest.raises(ValueError, match="divisible by 8"):
         _lib.call("ppmoe_expert_fc1_fwd", 0, None, None, None, None, 2, 12, 48, 128, None, None, None, None, None)
 
