@@ -282,7 +282,6 @@ class LayerConfig:
     weight_scaling: bool = True
     dropout_p: float = 0.0
     seed: int = 0
-    sliced_router: bool = False
     top_k: int = 1
 
     _FIELDS = ("hidden", "experts", "tp", "capacity_factor", "weight_scaling", "dropout_p", "seed", "top_k")
@@ -423,6 +422,7 @@ class _Spec:
     fwd_chunks: int = 1
     dropout_p: float = 0.0
     seed: int = 0
+    sliced_router: bool = False
 
 
 class _PPMoEFunction(torch.autograd.Function):

@@ -3,6 +3,8 @@ simulated world: same outputs and gradients (the reference's T-rank semantics,
 moe.py:254-313).  Needs >= 2 GPUs; skipped otherwise."""
 
 import os
+import queue as _queue
+import time
 
 import numpy as np
 import pytest
@@ -10,6 +12,26 @@ import torch
 import torch.multiprocessing as mp
 
 pytestmark = pytest.mark.gpu
+
+
+def _collect(q, procs, timeout=240):
+    """Results from the worker processes; fail fast if one of them dies."""
+    got, t0 = {}, time.time()
+    while len(got) < len(procs):
+        try:
+            r, res = q.get(timeout=2)
+            got[r] = res
+        except _queue.Empty:
+            dead = [p.exitcode for p in procs if p.exitcode not in (None, 0)]
+            if dead:
+                for p in procs:
+                    p.kill()
+                raise AssertionError(f"worker process failed with exit code {dead}")
+            if time.time() - t0 > timeout:
+                for p in procs:
+                    p.kill()
+                raise AssertionError("timed out waiting for the worker processes")
+    return got
 
 
 def _worker(rank, world, port, q, k, cf):
@@ -60,7 +82,7 @@ def test_tp_nccl_matches_simulated(world, k, cf):
     procs = [ctx.Process(target=_worker, args=(r, world, port, q, k, cf)) for r in range(world)]
     for p in procs:
         p.start()
-    got = dict(q.get(timeout=300) for _ in procs)
+    got = _collect(q, procs)
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
@@ -139,7 +161,7 @@ def test_a2a_comparator_matches_ppmoe_on_global_batch(world, k, cf):
     procs = [ctx.Process(target=_dp_worker, args=(r, world, port, q, k, cf)) for r in range(world)]
     for p in procs:
         p.start()
-    got = dict(q.get(timeout=300) for _ in procs)
+    got = _collect(q, procs)
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
