@@ -136,26 +136,32 @@ int ppmoe_cast_out(const float* acc, int n, void* out, int dtype, void* stream);
 
 /* Backward of scale_rows + index_assign + dropout (tensor.py:190-194, 264-270, 326-328):
  * dY[row] = w*dOut[tok] (times the forward's dropout mask / (1-p)),
- * dw[row] = <dOut[tok], Y[row]>; zero for padding.                          */
+ * dw[row] = <dOut[tok], Y[row]>; zero for padding.  dy_colsum_part (optional, bf16 and
+ * H % 256 == 0): [rows/32 x H] fp32 per-32-row-block column sums of dY, consumed by
+ * ppmoe_expert_fc2_wgrad for the bias_down gradient.                        */
 int ppmoe_bwd_dy(int dtype, const void* dOut, const void* Y, const int* seg, int El, int H, int rows_cap,
                  const int* tok_local, const float* w_local, int weight_scaling, float dropout_p,
-                 unsigned long long seed, void* dY, float* dw, void* stream);
+                 unsigned long long seed, void* dY, float* dw, float* dy_colsum_part, void* stream);
 
-/* dH = (dY*down_g^T) .* GeluGrad   (matmul/gelu backward, tensor.py:134-138, 204-207) */
+/* dH = (dY*down_g^T) .* GeluGrad   (matmul/gelu backward, tensor.py:134-138, 204-207).
+ * dh_colsum_part (optional, bf16 path): [rows/32 x F] fp32 column sums of dH per 32-row
+ * block, produced in the epilogue for ppmoe_expert_fc1_wgrad's bias_up gradient.      */
 int ppmoe_expert_fc2_dgrad(int dtype, const void* dY, const void* down, const void* GeluGrad, const int* seg, int El,
-                           int H, int F, int rows_cap, void* dH, void* stream);
+                           int H, int F, int rows_cap, void* dH, float* dh_colsum_part, void* stream);
 
-/* dDown_g = Act_g^T * dY_g  [El x F x H]; dbias_down_g = colsum(dY_g) (may be NULL). */
+/* dDown_g = Act_g^T * dY_g  [El x F x H]; dbias_down_g = colsum(dY_g) (may be NULL), reduced
+ * from dy_colsum_part when given (else by a pass over dY).                              */
 int ppmoe_expert_fc2_wgrad(int dtype, const void* Act, const void* dY, const int* seg, int El, int H, int F,
-                           int rows_cap, void* dDown, void* dBiasDown, void* stream);
+                           int rows_cap, void* dDown, void* dBiasDown, const float* dy_colsum_part, void* stream);
 
 /* dX_acc[tok] += dH*up_g^T  (index_select backward scatter-add, tensor.py:235-239). */
 int ppmoe_expert_fc1_dgrad(int dtype, const void* dH, const void* up, const int* seg, int El, int H, int F,
                            int rows_cap, const int* tok_local, float* dx_acc, void* stream);
 
-/* dUp_g = Xs_g^T * dH_g  [El x H x F]; dbias_up_g = colsum(dH_g) (may be NULL). */
+/* dUp_g = Xs_g^T * dH_g  [El x H x F]; dbias_up_g = colsum(dH_g) (may be NULL), reduced from
+ * dh_colsum_part when given.                                                            */
 int ppmoe_expert_fc1_wgrad(int dtype, const void* Xs, const void* dH, const int* seg, int El, int H, int F,
-                           int rows_cap, void* dUp, void* dBiasUp, void* stream);
+                           int rows_cap, void* dUp, void* dBiasUp, const float* dh_colsum_part, void* stream);
 
 /* Gate backward (gather_rowwise, softmax and aux_loss backward, tensor.py:218-221,
  * 287-291, moe.py:211-223): dL[t,e] = s*(dS - sum(dS*s)) with

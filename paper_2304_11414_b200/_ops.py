@@ -358,40 +358,54 @@ def scatter_rows(src: torch.Tensor, nrows: torch.Tensor, tok: torch.Tensor, w: t
          _stream())
 
 
-def experts_backward_data(grad_out, st: ExpertFwdState, up, down, weight_scaling: bool, dx_acc: torch.Tensor):
+def _fused_colsums(dt: int, h: int) -> bool:
+    """Bias-gradient column sums produced by bwd_dy / the fc2 dgrad epilogue (bf16 path)."""
+    return dt == 0 and h % 256 == 0 and os.environ.get("PPMOE_FUSED_COLSUM", "1") != "0"
+
+
+def experts_backward_data(grad_out, st: ExpertFwdState, up, down, weight_scaling: bool, dx_acc: torch.Tensor,
+                          has_bias: bool = True):
     """Data-gradient half of the experts' backward: dY/dw (scale_rows + index_assign backward),
-    dH = dY·downᵀ ⊙ GeLU', and dX_acc[tok] += dH·upᵀ.  Returns (dy, dh, dw)."""
+    dH = dY·downᵀ ⊙ GeLU', and dX_acc[tok] += dH·upᵀ.  Returns (dy, dh, dw, parts) where parts
+    are the per-32-row column-sum partials of dY and dH (bias gradients) or None."""
     h = grad_out.shape[1]
     f = up.shape[2]
     el, rows_cap = st.el, st.rows_cap
     dt = dtype_code(grad_out.dtype)
     dev = grad_out.device
     s = _stream()
+    fused = has_bias and _fused_colsums(dt, h)
+    dy_part = torch.empty((max(rows_cap // 32, 1), h), dtype=torch.float32, device=dev) if fused else None
+    dh_part = torch.empty((max(rows_cap // 32, 1), f), dtype=torch.float32, device=dev) if fused else None
     dy = _act((rows_cap, h), grad_out.dtype, dev)
     dw = _act(rows_cap, torch.float32, dev)
     call("ppmoe_bwd_dy", dt, ptr(grad_out), ptr(st.y), ptr(st.seg), el, h, rows_cap, ptr(st.tok_l), ptr(st.w_l),
-         int(bool(weight_scaling)), float(st.drop_p), int(st.seed), ptr(dy), ptr(dw), s)
+         int(bool(weight_scaling)), float(st.drop_p), int(st.seed), ptr(dy), ptr(dw), ptr(dy_part), s)
     dh = _act((rows_cap, f), grad_out.dtype, dev)
-    call("ppmoe_expert_fc2_dgrad", dt, ptr(dy), ptr(down), ptr(st.gelu_grad), ptr(st.seg), el, h, f, rows_cap, ptr(dh), s)
+    call("ppmoe_expert_fc2_dgrad", dt, ptr(dy), ptr(down), ptr(st.gelu_grad), ptr(st.seg), el, h, f, rows_cap, ptr(dh),
+         ptr(dh_part), s)
     call("ppmoe_expert_fc1_dgrad", dt, ptr(dh), ptr(up), ptr(st.seg), el, h, f, rows_cap, ptr(st.tok_l), ptr(dx_acc), s)
-    return dy, dh, dw
+    return dy, dh, dw, (dy_part, dh_part)
 
 
-def experts_backward_weights(st: ExpertFwdState, dy, dh, up, down, has_bias: bool):
+def experts_backward_weights(st: ExpertFwdState, dy, dh, up, down, has_bias: bool, parts=(None, None)):
     """Weight-gradient half: d down = Actᵀ·dY, d up = Xsᵀ·dH (variable-K grouped GEMMs) and
-    the bias column sums.  Independent of dX, so it overlaps the dX all-reduce."""
+    the bias gradients.  Independent of dX, so it overlaps the dX all-reduce."""
     h = dy.shape[1]
     f = up.shape[2]
     el, rows_cap = st.el, st.rows_cap
     dt = dtype_code(dy.dtype)
     dev = dy.device
     s = _stream()
+    dy_part, dh_part = parts
     d_down = torch.empty_like(down)
     d_bd = torch.empty((el, h), dtype=dy.dtype, device=dev) if has_bias else None
-    call("ppmoe_expert_fc2_wgrad", dt, ptr(st.act), ptr(dy), ptr(st.seg), el, h, f, rows_cap, ptr(d_down), ptr(d_bd), s)
+    call("ppmoe_expert_fc2_wgrad", dt, ptr(st.act), ptr(dy), ptr(st.seg), el, h, f, rows_cap, ptr(d_down), ptr(d_bd),
+         ptr(dy_part), s)
     d_up = torch.empty_like(up)
     d_bu = torch.empty((el, f), dtype=dy.dtype, device=dev) if has_bias else None
-    call("ppmoe_expert_fc1_wgrad", dt, ptr(st.xs), ptr(dh), ptr(st.seg), el, h, f, rows_cap, ptr(d_up), ptr(d_bu), s)
+    call("ppmoe_expert_fc1_wgrad", dt, ptr(st.xs), ptr(dh), ptr(st.seg), el, h, f, rows_cap, ptr(d_up), ptr(d_bu),
+         ptr(dh_part), s)
     return d_up, d_down, d_bu, d_bd
 
 

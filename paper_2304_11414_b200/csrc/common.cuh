@@ -54,6 +54,23 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
+// Warp transpose-reduction: lane L holds 32 values v[c] (one row, 32 columns); on return
+// v[0] of lane L is the sum over the 32 lanes of column L.  31 shuffles, fixed order.
+__device__ __forceinline__ float warp_column_sums32(float (&v)[32]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 16, n = 32; o >= 1; o >>= 1, n >>= 1) {
+    const bool upper = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < n / 2; ++i) {
+      const float send = upper ? v[i] : v[i + n / 2];
+      const float keep = upper ? v[i + n / 2] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  return v[0];
+}
+
 __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
   __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&v);

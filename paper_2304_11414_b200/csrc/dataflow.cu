@@ -186,6 +186,73 @@ __global__ void bwd_dy_kernel(const T* __restrict__ dOut, const T* __restrict__ 
   }
 }
 
+// Warp per 32-row block: dY and dw like bwd_dy_kernel, plus the per-block column sums of
+// dY (the bias_down gradient partials) -- so the bias gradient needs no second pass over dY.
+// Lane L handles 8 columns of every 256-wide slice; rows of the block are walked in order.
+__global__ void __launch_bounds__(256)
+    bwd_dy_block_kernel(const __nv_bfloat16* __restrict__ dOut, const __nv_bfloat16* __restrict__ Y,
+                        const int* __restrict__ seg, int El, int H, const int* __restrict__ tok_local,
+                        const float* __restrict__ w_local, int weight_scaling, float drop_p,
+                        unsigned long long seed, __nv_bfloat16* __restrict__ dY, float* __restrict__ dw,
+                        float* __restrict__ part) {
+  const int rows = seg[El] - seg[0];
+  const int lane = threadIdx.x & 31;
+  const int wpb = blockDim.x / 32;
+  const int nblk = rows >> 5;
+  const float inv = drop_p > 0.f ? 1.f / (1.f - drop_p) : 1.f;
+  for (int b = blockIdx.x * wpb + (threadIdx.x >> 5); b < nblk; b += gridDim.x * wpb) {
+    const int r0 = b << 5;
+    const int my_tok = tok_local[r0 + lane];
+    const float my_w = weight_scaling ? w_local[r0 + lane] : 1.f;
+    float dwp[32];
+#pragma unroll
+    for (int r = 0; r < 32; ++r) dwp[r] = 0.f;
+    for (int c0 = lane * 8; c0 < H; c0 += 256) {
+      float colacc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+      for (int r = 0; r < 32; ++r) {
+        const int t = __shfl_sync(0xffffffffu, my_tok, r);
+        const float sw = __shfl_sync(0xffffffffu, my_w, r);
+        __nv_bfloat16* dyr = dY + static_cast<size_t>(r0 + r) * H + c0;
+        if (t < 0) {
+          *reinterpret_cast<uint4*>(dyr) = make_uint4(0, 0, 0, 0);
+          continue;
+        }
+        const uint4 gu = *reinterpret_cast<const uint4*>(dOut + static_cast<size_t>(t) * H + c0);
+        const uint4 yu = *reinterpret_cast<const uint4*>(Y + static_cast<size_t>(r0 + r) * H + c0);
+        const __nv_bfloat162* gh = reinterpret_cast<const __nv_bfloat162*>(&gu);
+        const __nv_bfloat162* yh = reinterpret_cast<const __nv_bfloat162*>(&yu);
+        uint4 out;
+        uint32_t* o = reinterpret_cast<uint32_t*>(&out);
+        float acc = 0.f;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 gf = __bfloat1622float2(gh[i]);
+          const float2 yf = __bfloat1622float2(yh[i]);
+          acc = fmaf(gf.x, yf.x, acc);
+          acc = fmaf(gf.y, yf.y, acc);
+          float d0 = sw * gf.x, d1 = sw * gf.y;
+          if (drop_p > 0.f) {
+            d0 *= dropout_uniform(seed, r0 + r, c0 + 2 * i) >= drop_p ? inv : 0.f;
+            d1 *= dropout_uniform(seed, r0 + r, c0 + 2 * i + 1) >= drop_p ? inv : 0.f;
+          }
+          o[i] = pack_bf16x2(d0, d1);
+          const float2 back = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&o[i]));
+          colacc[2 * i] += back.x;
+          colacc[2 * i + 1] += back.y;
+        }
+        *reinterpret_cast<uint4*>(dyr) = out;
+        dwp[r] += acc;
+      }
+      float* pp = part + static_cast<size_t>(b) * H + c0;
+      *reinterpret_cast<float4*>(pp) = make_float4(colacc[0], colacc[1], colacc[2], colacc[3]);
+      *reinterpret_cast<float4*>(pp + 4) = make_float4(colacc[4], colacc[5], colacc[6], colacc[7]);
+    }
+    const float dwr = warp_column_sums32(dwp);  // lane r: sum over lanes of row r's partial
+    dw[r0 + lane] = (weight_scaling && my_tok >= 0) ? dwr : 0.f;
+  }
+}
+
 // ------------------------------------------------------------------ gate backward
 
 __global__ void gate_bwd_kernel(const float* __restrict__ scores, const int* __restrict__ idx,
@@ -442,8 +509,17 @@ int ppmoe_cast_out(const float* acc, int n, void* out, int dtype, void* stream) 
 
 int ppmoe_bwd_dy(int dtype, const void* dOut, const void* Y, const int* seg, int El, int H, int rows_cap,
                  const int* tok_local, const float* w_local, int weight_scaling, float dropout_p,
-                 unsigned long long seed, void* dY, float* dw, void* stream) {
+                 unsigned long long seed, void* dY, float* dw, float* dy_colsum_part, void* stream) {
   PPMOE_REQUIRE(dropout_p >= 0.f && dropout_p < 1.f, "dropout probability must be in [0, 1), got %g", dropout_p);
+  if (dy_colsum_part) {
+    PPMOE_REQUIRE(dtype == kBF16 && H % 256 == 0,
+                  "dY column-sum partials need the bf16 path and hidden %% 256 == 0 (H=%d)", H);
+    if (rows_cap == 0) return kOk;
+    bwd_dy_block_kernel<<<num_sms() * 4, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const __nv_bfloat16*>(dOut), static_cast<const __nv_bfloat16*>(Y), seg, El, H, tok_local,
+        w_local, weight_scaling, dropout_p, seed, static_cast<__nv_bfloat16*>(dY), dw, dy_colsum_part);
+    return check_launch("bwd_dy_block_kernel");
+  }
   PPMOE_REQUIRE(dtype == kBF16 || dtype == kF32, "bad dtype");
   if (rows_cap == 0) return kOk;
   cudaStream_t s = static_cast<cudaStream_t>(stream);

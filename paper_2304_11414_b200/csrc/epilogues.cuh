@@ -178,6 +178,9 @@ struct EpiFc2Dgrad {
   int F;
   const int* seg;
   int cs;
+  // Optional [rows/32 x F] fp32 partial column sums of dH (bias_up gradient, tensor.py:154)
+  // per 32-row block: needs the 32 lanes of a warp on 32 consecutive rows (tcgen05 kernels).
+  float* colsum_part;
   template <int W>
   __device__ __forceinline__ void apply(int g, int m, int row, int n0, const float (&v)[W]) const {
     const int valid = min(W, F - n0);
@@ -188,6 +191,16 @@ struct EpiFc2Dgrad {
 #pragma unroll
     for (int j = 0; j < W; ++j) x[j] = v[j] * gd[j];
     store_row<T, W>(dh + off, x, valid, cs);
+    if constexpr (W == 32) {
+      if (colsum_part) {
+        // the column sums use the bf16-rounded dH, exactly what the colsum pass would read
+#pragma unroll
+        for (int j = 0; j < W; ++j) x[j] = to_f32(from_f32<T>(x[j]));
+        const float cs_val = warp_column_sums32(x);
+        const int lane = threadIdx.x & 31;
+        if (lane < valid) colsum_part[static_cast<size_t>(row >> 5) * F + n0 + lane] = cs_val;
+      }
+    }
   }
 };
 

@@ -154,6 +154,33 @@ static int stream_stores() {
   return v;
 }
 
+// Bias gradient from per-32-row-block column partials: out[g][c] = sum of the blocks of
+// segment g, in block order (deterministic).
+template <typename T>
+__global__ void colsum_parts_kernel(const float* __restrict__ part, const int* __restrict__ seg, int N,
+                                    T* __restrict__ out) {
+  const int g = blockIdx.y;
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= N) return;
+  const int b0 = (seg[g] - seg[0]) >> 5, b1 = (seg[g + 1] - seg[0]) >> 5;
+  float a0 = 0.f, a1 = 0.f;
+  int b = b0;
+  for (; b + 2 <= b1; b += 2) {
+    a0 += part[static_cast<size_t>(b) * N + col];
+    a1 += part[static_cast<size_t>(b + 1) * N + col];
+  }
+  if (b < b1) a0 += part[static_cast<size_t>(b) * N + col];
+  out[static_cast<size_t>(g) * N + col] = from_f32<T>(a0 + a1);
+}
+
+template <typename T>
+static int colsum_parts(const float* part, const int* seg, int G, int N, void* out, cudaStream_t s) {
+  if (!out) return kOk;
+  dim3 grid((N + 255) / 256, G);
+  colsum_parts_kernel<T><<<grid, 256, 0, s>>>(part, seg, N, static_cast<T*>(out));
+  return check_launch("colsum_parts");
+}
+
 static GroupGeom geom(int G, int N, int M_fixed, int K_fixed, const int* seg, int a_seg, int a_stride, int b_seg,
                       int b_stride) {
   GroupGeom g;
@@ -236,7 +263,7 @@ int ppmoe_expert_fc2_fwd(int dtype, const void* Act, const void* down, const voi
 }
 
 int ppmoe_expert_fc2_dgrad(int dtype, const void* dY, const void* down, const void* GeluGrad, const int* seg, int El, int H,
-                           int F, int rows_cap, void* dH, void* stream) {
+                           int F, int rows_cap, void* dH, float* dh_colsum_part, void* stream) {
   if (int rc = check_common(dtype, El, H, F, rows_cap)) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   GroupGeom geo = geom(El, F, 0, H, seg, 1, 0, 0, F);
@@ -245,10 +272,12 @@ int ppmoe_expert_fc2_dgrad(int dtype, const void* dY, const void* down, const vo
     CUtensorMap ta, tb;
     if (int rc = tmap_kmajor(&ta, dY, H, rows_cap, kBM)) return rc;
     if (int rc = tmap_kmajor(&tb, down, H, static_cast<uint64_t>(El) * F, b_box_rows())) return rc;
-    EpiFc2Dgrad<bf16> epi{static_cast<bf16*>(dH), static_cast<const bf16*>(GeluGrad), F, seg, stream_stores()};
+    EpiFc2Dgrad<bf16> epi{static_cast<bf16*>(dH), static_cast<const bf16*>(GeluGrad), F, seg, stream_stores(),
+                          dh_colsum_part};
     return launch_tc<false, false>(ta, tb, geo, epi, s);
   }
-  EpiFc2Dgrad<float> epi{static_cast<float*>(dH), static_cast<const float*>(GeluGrad), F, seg, 0};
+  PPMOE_REQUIRE(dh_colsum_part == nullptr, "column-sum partials are produced by the bf16 tcgen05 path only");
+  EpiFc2Dgrad<float> epi{static_cast<float*>(dH), static_cast<const float*>(GeluGrad), F, seg, 0, nullptr};
   return launch_simt<float, false, false>(static_cast<const float*>(dY), H, static_cast<const float*>(down), H, geo,
                                           rows_cap, epi, s);
 }
@@ -273,7 +302,7 @@ int ppmoe_expert_fc1_dgrad(int dtype, const void* dH, const void* up, const int*
 }
 
 int ppmoe_expert_fc2_wgrad(int dtype, const void* Act, const void* dY, const int* seg, int El, int H, int F,
-                           int rows_cap, void* dDown, void* dBiasDown, void* stream) {
+                           int rows_cap, void* dDown, void* dBiasDown, const float* dy_colsum_part, void* stream) {
   if (int rc = check_common(dtype, El, H, F, rows_cap)) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   GroupGeom geo = geom(El, H, F, 0, seg, 1, 0, 1, 0);
@@ -287,6 +316,7 @@ int ppmoe_expert_fc2_wgrad(int dtype, const void* Act, const void* dY, const int
     } else {
       PPMOE_CUDA(cudaMemsetAsync(dDown, 0, static_cast<size_t>(El) * F * H * 2, s));
     }
+    if (dy_colsum_part) return colsum_parts<bf16>(dy_colsum_part, seg, El, H, dBiasDown, s);
     return colsum<bf16>(dY, H, seg, El, H, dBiasDown, s);
   }
   EpiWgrad<float> epi{static_cast<float*>(dDown), F, H, 0};
@@ -297,7 +327,7 @@ int ppmoe_expert_fc2_wgrad(int dtype, const void* Act, const void* dY, const int
 }
 
 int ppmoe_expert_fc1_wgrad(int dtype, const void* Xs, const void* dH, const int* seg, int El, int H, int F,
-                           int rows_cap, void* dUp, void* dBiasUp, void* stream) {
+                           int rows_cap, void* dUp, void* dBiasUp, const float* dh_colsum_part, void* stream) {
   if (int rc = check_common(dtype, El, H, F, rows_cap)) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   GroupGeom geo = geom(El, F, H, 0, seg, 1, 0, 1, 0);
@@ -311,6 +341,7 @@ int ppmoe_expert_fc1_wgrad(int dtype, const void* Xs, const void* dH, const int*
     } else {
       PPMOE_CUDA(cudaMemsetAsync(dUp, 0, static_cast<size_t>(El) * H * F * 2, s));
     }
+    if (dh_colsum_part) return colsum_parts<bf16>(dh_colsum_part, seg, El, F, dBiasUp, s);
     return colsum<bf16>(dH, F, seg, El, F, dBiasUp, s);
   }
   EpiWgrad<float> epi{static_cast<float*>(dUp), H, F, 0};

@@ -133,18 +133,18 @@ class _DPMoEFunction(torch.autograd.Function):
         dw_c = _ops._act(max(n_send, 1), torch.float32, dev)
         _ops.call("ppmoe_bwd_dy", _ops.dtype_code(hidden.dtype), _ops.ptr(g_out), _ops.ptr(yback), _ops.ptr(cstart), e,
                   h, max(n_send, 1), _ops.ptr(tok_c), _ops.ptr(w_c), int(spec.weight_scaling), 0.0, 0, _ops.ptr(dy_c),
-                  _ops.ptr(dw_c), _ops._stream())
+                  _ops.ptr(dw_c), None, _ops._stream())
         dy_recv = torch.empty((max(n_recv, 1), h), dtype=hidden.dtype, device=dev)
         _a2a(spec.world, spec.group, dy_recv[:n_recv], dy_c[:n_send], recv_rows, send_rows)
         # owner: data gradients (dY gathered to owner rows by the receive map), dX rows per receive row
         dx_recv = torch.zeros((max(n_recv, 1), h), dtype=torch.float32, device=dev)
-        dy, dh, _ = _ops.experts_backward_data(dy_recv, st, up, down, False, dx_recv)
+        dy, dh, _, parts = _ops.experts_backward_data(dy_recv, st, up, down, False, dx_recv, has_bias)
         dx_recv_b = _ops.cast_out(dx_recv, hidden.dtype)
         del dx_recv
         dx_back = torch.empty((max(n_send, 1), h), dtype=hidden.dtype, device=dev)
         work = _a2a(spec.world, spec.group, dx_back[:n_send], dx_recv_b[:n_recv], send_rows, recv_rows, async_op=True)
         with _ops.sm_budget(_ops.overlap_sm_budget() if work is not None else 0):
-            d_up, d_down, d_bu, d_bd = _ops.experts_backward_weights(st, dy, dh, up, down, has_bias)
+            d_up, d_down, d_bu, d_bd = _ops.experts_backward_weights(st, dy, dh, up, down, has_bias, parts)
         if work is not None:
             work.wait()
         # source: dX rows back to token order + the gate path

@@ -485,7 +485,7 @@ class _PPMoEFunction(torch.autograd.Function):
             aux = g_aux.detach().to(torch.float32).reshape(1).contiguous()
         dx_acc = torch.zeros((n, h), dtype=torch.float32, device=hidden.device)
         # data gradients first: dX can go on the wire while the weight gradients compute
-        dy, dh, dw = _ops.experts_backward_data(g_out, st, up, down, spec.weight_scaling, dx_acc)
+        dy, dh, dw, parts = _ops.experts_backward_data(g_out, st, up, down, spec.weight_scaling, dx_acc, has_bias)
         dl = _ops.gate_backward(rt, pl, st, dw, aux)
         need_dx = ctx.needs_input_grad[0]
         need_dwg = ctx.needs_input_grad[1]
@@ -495,7 +495,7 @@ class _PPMoEFunction(torch.autograd.Function):
         if need_dx:  # copy_to_tensor_parallel_region backward (collectives.py:215-221)
             work = spec.world.all_reduce_async(spec.group, dx)
         with _ops.sm_budget(_ops.overlap_sm_budget() if work is not None else 0):
-            d_up, d_down, d_bu, d_bd = _ops.experts_backward_weights(st, dy, dh, up, down, has_bias)
+            d_up, d_down, d_bu, d_bd = _ops.experts_backward_weights(st, dy, dh, up, down, has_bias, parts)
         if work is not None:
             work.wait()  # stream-ordered: the compute stream waits for the NCCL stream
         ctx.state = None

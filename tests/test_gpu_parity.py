@@ -424,3 +424,21 @@ def test_c3_shape_routing_capacity_and_step():
     (out.float().sum() + l_aux).backward()
     assert torch.isfinite(out).all() and torch.isfinite(x.grad).all()
     assert torch.isfinite(w.bank.up.grad).all() and torch.isfinite(w.gate.wg.grad).all()
+
+
+def test_fused_bias_colsums_match_separate_pass(monkeypatch):
+    """Bias gradients from the fused column-sum partials (bwd_dy / fc2 dgrad epilogue) equal
+    the separate column-sum pass (both sum the same bf16 dY / dH values)."""
+    layer = oracle_rounded(O.init_layer(256, 8, seed=21), torch.bfloat16)
+    hidden = torch.randn(1800, 256).bfloat16().double().numpy()
+    monkeypatch.setenv("PPMOE_FUSED_COLSUM", "0")
+    a = run_cuda_layer(hidden, device_weights(layer, torch.bfloat16), k=2)
+    monkeypatch.setenv("PPMOE_FUSED_COLSUM", "1")
+    b = run_cuda_layer(hidden, device_weights(layer, torch.bfloat16), k=2)
+    for e in range(8):
+        for nm in ("bias_up", "bias_down"):
+            key = f"expert{e}.{nm}"
+            assert scaled_err(b["grads"][key], a["grads"][key]) < 1e-2, key
+    for key in a["grads"]:
+        if "bias" not in key:
+            assert np.array_equal(a["grads"][key], b["grads"][key]), key

@@ -46,12 +46,12 @@ dy = torch.empty(st.rows_cap, h, device=dev, dtype=torch.bfloat16)
 dw = torch.empty(st.rows_cap, device=dev)
 timeit("bwd_dy", lambda: _lib.call("ppmoe_bwd_dy", 0, _ops.ptr(g_out), _ops.ptr(st.y), _ops.ptr(st.seg), E, h,
                                    st.rows_cap, _ops.ptr(st.tok_l), _ops.ptr(st.w_l), 1, 0.0, 0, _ops.ptr(dy),
-                                   _ops.ptr(dw), _ops._stream()), rows * h * 6)
+                                   _ops.ptr(dw), None, _ops._stream()), rows * h * 6)
+part = torch.empty(st.rows_cap // 32, h, device=dev)
+timeit("bwd_dy (+dY colsum parts)", lambda: _lib.call("ppmoe_bwd_dy", 0, _ops.ptr(g_out), _ops.ptr(st.y),
+                                   _ops.ptr(st.seg), E, h, st.rows_cap, _ops.ptr(st.tok_l), _ops.ptr(st.w_l), 1, 0.0,
+                                   0, _ops.ptr(dy), _ops.ptr(dw), _ops.ptr(part), _ops._stream()), rows * h * 6)
 aux = torch.ones(1, device=dev)
 dl = _ops.gate_backward(rt, pl, st, dw, aux)
 timeit("gate_bwd", lambda: _ops.gate_backward(rt, pl, st, dw, aux))
 timeit("gate_grads (dX + dWg)", lambda: _ops.gate_grads(dx_acc, x, dl, wg, True, True), n * h * 8)
-dbd = torch.empty(E, h, device=dev, dtype=torch.bfloat16)
-timeit("colsum dY (bias_down)", lambda: _lib.call("ppmoe_expert_fc2_wgrad", 0, _ops.ptr(st.act), _ops.ptr(dy),
-                                                  _ops.ptr(st.seg), E, h, 4 * h, 0, _ops.ptr(w.bank.down), _ops.ptr(dbd),
-                                                  _ops._stream()), rows * h * 2)
