@@ -186,9 +186,9 @@ __global__ void bwd_dy_kernel(const T* __restrict__ dOut, const T* __restrict__ 
   }
 }
 
-// Warp per 32-row block: dY and dw like bwd_dy_kernel, plus the per-block column sums of
-// dY (the bias_down gradient partials) -- so the bias gradient needs no second pass over dY.
-// Lane L handles 8 columns of every 256-wide slice; rows of the block are walked in order.
+// CTA per 32-row block: phase 1 is bwd_dy_kernel's warp-per-row pass (8 warps x 4 rows);
+// phase 2 re-reads the block's freshly written dY rows (L2-hot) column-wise and writes the
+// block's column sums (the bias_down gradient partials) -- no DRAM pass over dY.
 __global__ void __launch_bounds__(256)
     bwd_dy_block_kernel(const __nv_bfloat16* __restrict__ dOut, const __nv_bfloat16* __restrict__ Y,
                         const int* __restrict__ seg, int El, int H, const int* __restrict__ tok_local,
@@ -196,35 +196,32 @@ __global__ void __launch_bounds__(256)
                         unsigned long long seed, __nv_bfloat16* __restrict__ dY, float* __restrict__ dw,
                         float* __restrict__ part) {
   const int rows = seg[El] - seg[0];
-  const int lane = threadIdx.x & 31;
-  const int wpb = blockDim.x / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nblk = rows >> 5;
   const float inv = drop_p > 0.f ? 1.f / (1.f - drop_p) : 1.f;
-  for (int b = blockIdx.x * wpb + (threadIdx.x >> 5); b < nblk; b += gridDim.x * wpb) {
+  for (int b = blockIdx.x; b < nblk; b += gridDim.x) {
     const int r0 = b << 5;
-    const int my_tok = tok_local[r0 + lane];
-    const float my_w = weight_scaling ? w_local[r0 + lane] : 1.f;
-    float dwp[32];
-#pragma unroll
-    for (int r = 0; r < 32; ++r) dwp[r] = 0.f;
-    for (int c0 = lane * 8; c0 < H; c0 += 256) {
-      float colacc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int rr = warp; rr < 32; rr += 8) {
+      const int r = r0 + rr;
+      const int tok = tok_local[r];
+      __nv_bfloat16* dy = dY + static_cast<size_t>(r) * H;
+      if (tok < 0) {
+        for (int j = lane * 8; j < H; j += 256) *reinterpret_cast<uint4*>(dy + j) = make_uint4(0, 0, 0, 0);
+        if (lane == 0) dw[r] = 0.f;
+        continue;
+      }
+      const float sw = weight_scaling ? w_local[r] : 1.f;
+      const __nv_bfloat16* g = dOut + static_cast<size_t>(tok) * H;
+      const __nv_bfloat16* y = Y + static_cast<size_t>(r) * H;
+      float acc = 0.f;
 #pragma unroll 4
-      for (int r = 0; r < 32; ++r) {
-        const int t = __shfl_sync(0xffffffffu, my_tok, r);
-        const float sw = __shfl_sync(0xffffffffu, my_w, r);
-        __nv_bfloat16* dyr = dY + static_cast<size_t>(r0 + r) * H + c0;
-        if (t < 0) {
-          *reinterpret_cast<uint4*>(dyr) = make_uint4(0, 0, 0, 0);
-          continue;
-        }
-        const uint4 gu = *reinterpret_cast<const uint4*>(dOut + static_cast<size_t>(t) * H + c0);
-        const uint4 yu = *reinterpret_cast<const uint4*>(Y + static_cast<size_t>(r0 + r) * H + c0);
+      for (int j = lane * 8; j < H; j += 256) {
+        const uint4 gu = *reinterpret_cast<const uint4*>(g + j);
+        const uint4 yu = *reinterpret_cast<const uint4*>(y + j);
         const __nv_bfloat162* gh = reinterpret_cast<const __nv_bfloat162*>(&gu);
         const __nv_bfloat162* yh = reinterpret_cast<const __nv_bfloat162*>(&yu);
         uint4 out;
         uint32_t* o = reinterpret_cast<uint32_t*>(&out);
-        float acc = 0.f;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const float2 gf = __bfloat1622float2(gh[i]);
@@ -233,23 +230,29 @@ __global__ void __launch_bounds__(256)
           acc = fmaf(gf.y, yf.y, acc);
           float d0 = sw * gf.x, d1 = sw * gf.y;
           if (drop_p > 0.f) {
-            d0 *= dropout_uniform(seed, r0 + r, c0 + 2 * i) >= drop_p ? inv : 0.f;
-            d1 *= dropout_uniform(seed, r0 + r, c0 + 2 * i + 1) >= drop_p ? inv : 0.f;
+            d0 *= dropout_uniform(seed, r, j + 2 * i) >= drop_p ? inv : 0.f;
+            d1 *= dropout_uniform(seed, r, j + 2 * i + 1) >= drop_p ? inv : 0.f;
           }
           o[i] = pack_bf16x2(d0, d1);
-          const float2 back = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&o[i]));
-          colacc[2 * i] += back.x;
-          colacc[2 * i + 1] += back.y;
         }
-        *reinterpret_cast<uint4*>(dyr) = out;
-        dwp[r] += acc;
+        *reinterpret_cast<uint4*>(dy + j) = out;
       }
-      float* pp = part + static_cast<size_t>(b) * H + c0;
-      *reinterpret_cast<float4*>(pp) = make_float4(colacc[0], colacc[1], colacc[2], colacc[3]);
-      *reinterpret_cast<float4*>(pp + 4) = make_float4(colacc[4], colacc[5], colacc[6], colacc[7]);
+      acc = warp_sum(acc);
+      if (lane == 0) dw[r] = weight_scaling ? acc : 0.f;
     }
-    const float dwr = warp_column_sums32(dwp);  // lane r: sum over lanes of row r's partial
-    dw[r0 + lane] = (weight_scaling && my_tok >= 0) ? dwr : 0.f;
+    __syncthreads();  // the block's dY rows are visible to the whole CTA
+    for (int c = threadIdx.x * 2; c < H; c += 512) {
+      float s0 = 0.f, s1 = 0.f;
+#pragma unroll 8
+      for (int rr = 0; rr < 32; ++rr) {
+        const float2 v = __bfloat1622float2(
+            *reinterpret_cast<const __nv_bfloat162*>(dY + static_cast<size_t>(r0 + rr) * H + c));
+        s0 += v.x;
+        s1 += v.y;
+      }
+      *reinterpret_cast<float2*>(part + static_cast<size_t>(b) * H + c) = make_float2(s0, s1);
+    }
+    __syncthreads();
   }
 }
 
@@ -515,7 +518,7 @@ int ppmoe_bwd_dy(int dtype, const void* dOut, const void* Y, const int* seg, int
     PPMOE_REQUIRE(dtype == kBF16 && H % 256 == 0,
                   "dY column-sum partials need the bf16 path and hidden %% 256 == 0 (H=%d)", H);
     if (rows_cap == 0) return kOk;
-    bwd_dy_block_kernel<<<num_sms() * 4, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+    bwd_dy_block_kernel<<<num_sms() * 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(
         static_cast<const __nv_bfloat16*>(dOut), static_cast<const __nv_bfloat16*>(Y), seg, El, H, tok_local,
         w_local, weight_scaling, dropout_p, seed, static_cast<__nv_bfloat16*>(dY), dw, dy_colsum_part);
     return check_launch("bwd_dy_block_kernel");
