@@ -442,3 +442,46 @@ def test_fused_bias_colsums_match_separate_pass(monkeypatch):
     for key in a["grads"]:
         if "bias" not in key:
             assert np.array_equal(a["grads"][key], b["grads"][key]), key
+
+
+# ------------------------------------------------------------------ edge cases
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("n,h,e,k,tp,cf,ov", [
+    (1, 64, 4, 1, 1, math.inf, None),          # a single token
+    (5, 64, 4, 4, 2, math.inf, None),          # top-k == E
+    (130, 128, 8, 2, 4, math.inf, "one"),      # every token routed to expert 3 (others empty)
+    (257, 64, 1, 1, 1, math.inf, None),        # one expert: dense FFN
+    (300, 128, 6, 3, 3, 0.5, None),            # capacity drops with k=3, odd E/T
+    (64, 256, 16, 2, 8, 0.25, None),           # heavy drops, 2 experts per rank
+])
+def test_layer_edge_cases_vs_oracle(dtype, n, h, e, k, tp, cf, ov):
+    layer = oracle_rounded(O.init_layer(h, e, seed=n + e), dtype)
+    hidden = torch.randn(n, h, generator=torch.Generator().manual_seed(n)).to(dtype).double().numpy()
+    override = None
+    if ov == "one":
+        override = np.full((n, k), -1)
+        override[:, 0] = 3
+        for s in range(1, k):
+            override[:, s] = (3 + s) % e
+    ref = O.ppmoe_layer(hidden, layer, k=k, capacity_factor=cf, route_override=override)
+    res = run_cuda_layer(hidden, device_weights(layer, dtype), tp=tp, k=k, capacity_factor=cf, dtype=dtype,
+                         route_override=None if override is None else torch.tensor(override))
+    _compare(res, ref.out, ref.grad_hidden, ref.grads, dtype, name=f"edge n{n} e{e} k{k}")
+
+
+def test_zero_tokens_and_bad_override():
+    layer = oracle_rounded(O.init_layer(64, 4, seed=2), torch.bfloat16)
+    w = device_weights(layer, torch.bfloat16)
+    world, g = P.World(1, 1), P.ProcessGroup(P.EP, (0,))
+    with pytest.raises(ValueError, match="zero tokens"):
+        P.ppmoe_forward(world, g, torch.zeros(0, 64, device="cuda").bfloat16(), w.gate, [w.bank])
+    with pytest.raises(ValueError, match="out of range"):
+        P.ppmoe_forward(world, g, torch.zeros(3, 64, device="cuda").bfloat16(), w.gate, [w.bank],
+                        route_override=[0, 4, 1])
+    with pytest.raises(ValueError, match="one expert id per token"):
+        P.ppmoe_forward(world, g, torch.zeros(3, 64, device="cuda").bfloat16(), w.gate, [w.bank],
+                        route_override=[0, 1])
+    with pytest.raises(ValueError, match="hidden dtype"):
+        P.ppmoe_forward(world, g, torch.zeros(3, 64, device="cuda"), w.gate, [w.bank])

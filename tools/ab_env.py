@@ -1,0 +1,47 @@
+"""Dev tool: interleaved A/B of environment-switched code paths on the C2 step, one process.
+usage: python tools/ab_env.py VAR=val1,val2 [VAR2=...]  (values applied per round-robin arm)"""
+import os, statistics, sys
+sys.path.insert(0, ".")
+import torch
+import paper_2304_11414_b200 as P
+
+h, E, k, n = 4096, 8, 2, 16384
+dev = torch.device("cuda", 0)
+w = P.MoeLayerWeights.random(h, E, seed=0, device=dev)
+x = torch.randn(n, h, device=dev).bfloat16().requires_grad_()
+g_out = torch.ones(n, h, device=dev, dtype=torch.bfloat16)
+g_aux = torch.ones((), device=dev)
+world, group = P.World(1, 1), P.ProcessGroup(P.EP, (0,))
+var, vals = sys.argv[1].split("=")
+vals = vals.split(",")
+
+
+def step():
+    for p in w.leaf_parameters():
+        p.grad = None
+    x.grad = None
+    out, l_aux = P.ppmoe_forward(world, group, x, w.gate, [w.bank], top_k=k)
+    torch.autograd.backward([out, l_aux], [g_out, g_aux])
+
+
+res = {v: [] for v in vals}
+for v in vals:
+    os.environ[var] = v
+    for _ in range(2):
+        step()
+torch.cuda.synchronize()
+for rnd in range(6):
+    for v in vals:
+        os.environ[var] = v
+        step()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(5):
+            step()
+        e1.record()
+        torch.cuda.synchronize()
+        res[v].append(e0.elapsed_time(e1) / 5)
+for v in vals:
+    ms = statistics.median(res[v])
+    print(f"{var}={v:6s} median {ms:.3f} ms/step  {n / ms * 1e3:,.0f} tok/s   all={[round(t, 2) for t in res[v]]}")
