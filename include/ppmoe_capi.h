@@ -124,11 +124,31 @@ int ppmoe_expert_fc1_fwd(int dtype, const void* Xs, const void* up, const void* 
  * Y = Dropout(Act*down_g + bias_down) (stored, pre-scale), out_acc[tok] += w*Y
  * (moe.py:104-107, scale_rows tensor.py:184-196, index_assign 244-272, dropout
  * tensor.py:315-330 with a counter-based mask hash(seed, local row, column)).
- * out_acc [N x H] fp32 must be zeroed by the caller.                       */
+ * out_acc [N x H] fp32 must be zeroed by the caller; NULL = store Y only (for ppmoe_combine). */
 int ppmoe_expert_fc2_fwd(int dtype, const void* Act, const void* down, const void* bias_down, const int* seg,
                          int El, int H, int F, int rows_cap, const int* row_lo, const int* row_hi,
                          const int* tok_local, const float* w_local, int weight_scaling, float dropout_p,
                          unsigned long long seed, void* Y, float* out_acc, void* stream);
+
+/* Gather-combine over this rank's pairs, in slot order (deterministic):
+ *   out[t] = sum_s w[t,s] * R[pair_pos[t,s] - seg[0]]  (+ dL[t,:] . Wg^T when dL != NULL)
+ * summing the slots whose sorted row lies in this rank's rows [seg[0], seg[El]); w NULL = 1.
+ * Forward: R = the fc2 outputs Y (ppmoe_expert_fc2_fwd with out_acc NULL), the top-k
+ * combine (scale_rows + index_assign, tensor.py:184-272).  The optional gate term takes
+ * dL [N x E] fp32 and Wg [H x E] fp32 (see ppmoe_input_grads).  out [N x H] in dtype.  */
+int ppmoe_combine(int dtype, const void* R, const int* seg, int El, const int* pair_pos, const float* w, int N, int K,
+                  int H, const float* dL, const float* Wg, int E, void* out, void* stream);
+
+/* The layer's input gradients in one pass over the tokens (index_select + gate matmul
+ * backward, tensor.py:134-138, 235-239):
+ *   dX[t] = sum_s dXs[pair_pos[t,s] - seg[0]] + dL[t,:] . Wg^T     (dtype; NULL = skip)
+ *   dWg   = X^T dL                                                   (fp32 [H x E]; NULL = skip)
+ * dXs = the per-row dX of ppmoe_expert_fc1_dgrad; pair sums in slot order, dWg partials
+ * reduced in a fixed order (deterministic).  ws of ppmoe_input_grads_workspace_bytes.  */
+size_t ppmoe_input_grads_workspace_bytes(int dtype, int N, int H, int E);
+int ppmoe_input_grads(int dtype, const void* dXs, const int* seg, int El, const int* pair_pos, int N, int K, int H,
+                      const void* X, const float* dL, const float* Wg, int E, void* dX, float* dWg, void* ws,
+                      size_t ws_bytes, void* stream);
 
 /* out = out_acc cast to dtype (the replicated [N x H] layer output before or
  * after the TP all-reduce, collectives.py:135-153).                         */
@@ -154,9 +174,11 @@ int ppmoe_expert_fc2_dgrad(int dtype, const void* dY, const void* down, const vo
 int ppmoe_expert_fc2_wgrad(int dtype, const void* Act, const void* dY, const int* seg, int El, int H, int F,
                            int rows_cap, void* dDown, void* dBiasDown, const float* dy_colsum_part, void* stream);
 
-/* dX_acc[tok] += dH*up_g^T  (index_select backward scatter-add, tensor.py:235-239). */
+/* dH*up_g^T per local row: scatter-added into dx_acc[tok] (fp32, index_select backward
+ * tensor.py:235-239) or stored per row into dXs [rows x H] (dtype) for the deterministic
+ * gather-combine in ppmoe_gate_grads.  Exactly one of dx_acc / dXs.                   */
 int ppmoe_expert_fc1_dgrad(int dtype, const void* dH, const void* up, const int* seg, int El, int H, int F,
-                           int rows_cap, const int* tok_local, float* dx_acc, void* stream);
+                           int rows_cap, const int* tok_local, float* dx_acc, void* dXs, void* stream);
 
 /* dUp_g = Xs_g^T * dH_g  [El x H x F]; dbias_up_g = colsum(dH_g) (may be NULL), reduced from
  * dh_colsum_part when given.                                                            */
@@ -173,7 +195,8 @@ int ppmoe_gate_bwd(const float* scores, const int* idx, const int* pair_pos, con
 
 /* dX = dx_acc + dL*Wg^T (cast to dtype) and the per-chunk partials of
  * dWg = X^T*dL, reduced deterministically into dWg [H x E] fp32.  Either of
- * dX / dWg may be NULL.  ws of ppmoe_gate_grad_workspace_bytes(N,H,E).     */
+ * dX / dWg may be NULL (with dXs rows, dX comes from ppmoe_combine instead).
+ * ws of ppmoe_gate_grad_workspace_bytes(N,H,E).                            */
 size_t ppmoe_gate_grad_workspace_bytes(int N, int H, int E);
 int ppmoe_gate_grads(const float* dx_acc, const void* X, int dtype, const float* dL, const float* Wg, int N, int H,
                      int E, void* dX, float* dWg, void* ws, size_t ws_bytes, void* stream);

@@ -41,11 +41,14 @@ _SIGNATURES = {
     "ppmoe_chunk_rows": (_I, [_P, _P, _P, _I, _I, _I, _P, _P, _P]),
     "ppmoe_expert_fc1_fwd": (_I, [_I, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P]),
     "ppmoe_expert_fc2_fwd": (_I, [_I, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _I, _F, _U, _P, _P, _P]),
+    "ppmoe_combine": (_I, [_I, _P, _P, _I, _P, _P, _I, _I, _I, _P, _P, _I, _P, _P]),
+    "ppmoe_input_grads_workspace_bytes": (_S, [_I, _I, _I, _I]),
+    "ppmoe_input_grads": (_I, [_I, _P, _P, _I, _P, _I, _I, _I, _P, _P, _P, _I, _P, _P, _P, _S, _P]),
     "ppmoe_cast_out": (_I, [_P, _I, _P, _I, _P]),
     "ppmoe_bwd_dy": (_I, [_I, _P, _P, _P, _I, _I, _I, _P, _P, _I, _F, _U, _P, _P, _P, _P]),
     "ppmoe_expert_fc2_dgrad": (_I, [_I, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P]),
     "ppmoe_expert_fc2_wgrad": (_I, [_I, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P]),
-    "ppmoe_expert_fc1_dgrad": (_I, [_I, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P]),
+    "ppmoe_expert_fc1_dgrad": (_I, [_I, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P]),
     "ppmoe_expert_fc1_wgrad": (_I, [_I, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P]),
     "ppmoe_gate_bwd": (_I, [_P, _P, _P, _P, _P, _I, _P, _I, _I, _I, _P, _P, _P]),
     "ppmoe_gate_grad_workspace_bytes": (_S, [_I, _I, _I]),

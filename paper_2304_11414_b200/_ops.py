@@ -259,7 +259,8 @@ def experts_forward(hidden, pl: Plan, e0: int, el: int, up, down, bias_up, bias_
                     out_acc: torch.Tensor, chunks: int = 1, on_chunk=None, drop_p: float = 0.0,
                     seed: int = 0) -> ExpertFwdState:
     """index-slice gather -> fc1 (+bias, GeLU) -> fc2 (+bias, gate-scaled scatter-add combine)
-    for experts [e0, e0+el) (moe.py:294-305).  With chunks > 1 the two GEMMs run per token
+    for experts [e0, e0+el) (moe.py:294-305).  out_acc None: fc2 only stores Y and the
+    combine is done by ``combine`` (gather, no atomics).  With chunks > 1 the two GEMMs run per token
     chunk (each expert segment is ascending in token id, so a chunk is a row range) and
     ``on_chunk(c)`` is called once chunk c's rows of out_acc are final on this rank."""
     n, h = hidden.shape
@@ -330,6 +331,25 @@ def expert_pipeline(xsrc: torch.Tensor, seg: torch.Tensor, el: int, tok_sorted: 
     return ExpertFwdState(0, el, rows_cap, seg, xs, tok_l, w_l, gelu_grad, act, y, drop_p, seed)
 
 
+def gather_combine() -> bool:
+    """Top-k combine and dX reduction as row gathers (default) or fp32 scatter-adds
+    (PPMOE_COMBINE=scatter, kept for A/B measurement)."""
+    return os.environ.get("PPMOE_COMBINE", "gather") != "scatter"
+
+
+def combine(rows: torch.Tensor, st: ExpertFwdState, pl: Plan, w: torch.Tensor | None, out: torch.Tensor,
+            dl: torch.Tensor | None = None, wg: torch.Tensor | None = None) -> torch.Tensor:
+    """out[t] = sum over t's local pairs (slot order) of w·rows[row] (+ dl[t]·wgᵀ): the top-k
+    combine of Y (scale_rows + index_assign, tensor.py:184-272), or with the per-row dX and
+    the gate term the input gradient, as a deterministic gather."""
+    n, h = out.shape
+    k = pl.pair_pos.shape[1]
+    e = wg.shape[1] if wg is not None else 0
+    call("ppmoe_combine", dtype_code(out.dtype), ptr(rows), ptr(st.seg), st.el, ptr(pl.pair_pos), ptr(w), n, k, h,
+         ptr(dl), ptr(wg), e, ptr(out), _stream())
+    return out
+
+
 def a2a_compact(pl: Plan, idx: torch.Tensor, num_experts: int):
     """Compact expert-major layout of the kept pairs: (cstart [E+1], tok_c, w_c, pair_pos_c)."""
     dev = idx.device
@@ -363,10 +383,11 @@ def _fused_colsums(dt: int, h: int) -> bool:
     return dt == 0 and h % 256 == 0 and os.environ.get("PPMOE_FUSED_COLSUM", "1") != "0"
 
 
-def experts_backward_data(grad_out, st: ExpertFwdState, up, down, weight_scaling: bool, dx_acc: torch.Tensor,
-                          has_bias: bool = True):
+def experts_backward_data(grad_out, st: ExpertFwdState, up, down, weight_scaling: bool, dx_acc: torch.Tensor | None,
+                          has_bias: bool = True, dxs: torch.Tensor | None = None):
     """Data-gradient half of the experts' backward: dY/dw (scale_rows + index_assign backward),
-    dH = dY·downᵀ ⊙ GeLU', and dX_acc[tok] += dH·upᵀ.  Returns (dy, dh, dw, parts) where parts
+    dH = dY·downᵀ ⊙ GeLU', and dX_acc[tok] += dH·upᵀ (or, with ``dxs``, the per-row dH·upᵀ
+    stored for the gather in ``gate_grads``).  Returns (dy, dh, dw, parts) where parts
     are the per-32-row column-sum partials of dY and dH (bias gradients) or None."""
     h = grad_out.shape[1]
     f = up.shape[2]
@@ -384,7 +405,8 @@ def experts_backward_data(grad_out, st: ExpertFwdState, up, down, weight_scaling
     dh = _act((rows_cap, f), grad_out.dtype, dev)
     call("ppmoe_expert_fc2_dgrad", dt, ptr(dy), ptr(down), ptr(st.gelu_grad), ptr(st.seg), el, h, f, rows_cap, ptr(dh),
          ptr(dh_part), s)
-    call("ppmoe_expert_fc1_dgrad", dt, ptr(dh), ptr(up), ptr(st.seg), el, h, f, rows_cap, ptr(st.tok_l), ptr(dx_acc), s)
+    call("ppmoe_expert_fc1_dgrad", dt, ptr(dh), ptr(up), ptr(st.seg), el, h, f, rows_cap, ptr(st.tok_l), ptr(dx_acc),
+         ptr(dxs), s)
     return dy, dh, dw, (dy_part, dh_part)
 
 
@@ -417,6 +439,22 @@ def gate_backward(rt: Route, pl: Plan, st: ExpertFwdState, dw: torch.Tensor, aux
     call("ppmoe_gate_bwd", ptr(rt.scores), ptr(rt.idx), ptr(pl.pair_pos), ptr(dw), ptr(st.seg), st.el,
          ptr(rt.top1_counts), n, e, k, ptr(aux_grad), ptr(dl), _stream())
     return dl
+
+
+def input_grads(dxs, st: ExpertFwdState, pl: Plan, hidden, dl, wg, want_dx: bool, want_dwg: bool):
+    """dX = gather of the token's per-row dX (slot order) + dL Wgᵀ and dWg = Xᵀ dL, one pass."""
+    n, h = hidden.shape
+    e = wg.shape[1]
+    k = pl.pair_pos.shape[1]
+    dt = dtype_code(hidden.dtype)
+    dev = hidden.device
+    dx = torch.empty_like(hidden) if want_dx else None
+    dwg = torch.empty((h, e), dtype=torch.float32, device=dev) if want_dwg else None
+    lib = _lib.load()
+    ws = _ws(lib.ppmoe_input_grads_workspace_bytes(dt, n, h, e) if want_dwg else 0, dev)
+    call("ppmoe_input_grads", dt, ptr(dxs), ptr(st.seg), st.el, ptr(pl.pair_pos), n, k, h, ptr(hidden), ptr(dl),
+         ptr(wg), e, ptr(dx), ptr(dwg), ptr(ws), ws.numel(), _stream())
+    return dx, dwg
 
 
 def gate_grads(dx_acc, hidden, dl, wg, want_dx: bool, want_dwg: bool):

@@ -11,6 +11,8 @@
 //                        tensor.py:218-221, 287-291, moe.py:211-223).
 //   gate_grads_kernel    dX = dx_acc + dL Wg^T and per-chunk X^T dL partials
 //                        (matmul backward of the gate projection, tensor.py:134-138).
+#include <algorithm>
+
 #include "../../include/ppmoe_capi.h"
 #include "common.cuh"
 #include "host.h"
@@ -256,6 +258,343 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// ------------------------------------------------------------------ gather-combine
+
+// out[t] = sum_s w[t,s] * R[pair_pos[t,s] - row_lo]  (+ dL[t] . Wg^T)
+// over the slots whose sorted row is one of this rank's rows [seg[0], seg[El]).  Forward:
+// the top-k combine of the expert outputs (scale_rows + index_assign, tensor.py:184-272);
+// backward: the index_select backward of the experts' per-row dX plus the gate
+// projection's dX (matmul backward, tensor.py:134-138).  A deterministic gather in slot
+// order replaces the fp32 scatter-add accumulator.  Tokens with no local pair get only the
+// gate term (or zero).
+//
+// bf16, H % CW == 0: a thread owns CW consecutive columns for all tokens of its block, so
+// the gate weights of those columns (CW x EB fp32) stay in registers.  U tokens are
+// processed together: their pair positions are loaded first, then all U*KS row loads
+// are issued before any is consumed (memory-level parallelism of a gather).
+template <int CW> struct ColVec;
+template <> struct ColVec<8> { using type = uint4; };
+template <> struct ColVec<4> { using type = uint2; };
+
+template <int EB, int CW, int U, int KT>
+__global__ void __launch_bounds__(256)
+    combine_rows_bf16_kernel(const __nv_bfloat16* __restrict__ R, const int* __restrict__ seg, int El,
+                             const int* __restrict__ pair_pos, const float* __restrict__ w, int N, int Kr, int H,
+                             const float* __restrict__ dL, const float* __restrict__ Wg, int E,
+                             __nv_bfloat16* __restrict__ out) {
+  using V = typename ColVec<CW>::type;
+  constexpr int KS = KT > 0 ? KT : 1;  // slots loaded per batch
+  const int K = KT > 0 ? KT : Kr;
+  const int row_lo = seg[0], row_hi = seg[El];
+  const int j = (blockIdx.x * blockDim.x + threadIdx.x) * CW;
+  if (j >= H) return;
+  float wg[EB > 0 ? CW : 1][EB > 0 ? EB : 1];
+  if constexpr (EB > 0) {
+#pragma unroll
+    for (int q = 0; q < CW; ++q)
+#pragma unroll
+      for (int e = 0; e < EB; ++e) wg[q][e] = e < E ? Wg[static_cast<size_t>(j + q) * E + e] : 0.f;
+  }
+  for (int t0 = blockIdx.y * U; t0 < N; t0 += gridDim.y * U) {
+    float acc[U][CW];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int q = 0; q < CW; ++q) acc[u][q] = 0.f;
+    for (int sb = 0; sb < K; sb += KS) {
+      int rows[U][KS];
+      float ws[U][KS];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int s = 0; s < KS; ++s) {
+          const int t = t0 + u, sl = sb + s;
+          rows[u][s] = -1;
+          ws[u][s] = 0.f;
+          if (t < N) {
+            const int p = pair_pos[static_cast<size_t>(t) * K + sl];
+            if (p >= row_lo && p < row_hi) {
+              rows[u][s] = p - row_lo;
+              ws[u][s] = w ? w[static_cast<size_t>(t) * K + sl] : 1.f;
+            }
+          }
+        }
+      V v[U][KS];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int s = 0; s < KS; ++s) {
+          if (rows[u][s] >= 0) v[u][s] = *reinterpret_cast<const V*>(R + static_cast<size_t>(rows[u][s]) * H + j);
+          else memset(&v[u][s], 0, sizeof(V));
+        }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int s = 0; s < KS; ++s) {
+          const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&v[u][s]);
+#pragma unroll
+          for (int i = 0; i < CW / 2; ++i) {
+            const float2 f = __bfloat1622float2(hv[i]);
+            acc[u][2 * i] = fmaf(ws[u][s], f.x, acc[u][2 * i]);
+            acc[u][2 * i + 1] = fmaf(ws[u][s], f.y, acc[u][2 * i + 1]);
+          }
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int t = t0 + u;
+      if (t >= N) break;
+      if constexpr (EB > 0) {
+#pragma unroll
+        for (int e = 0; e < EB; ++e) {
+          const float d = e < E ? dL[static_cast<size_t>(t) * E + e] : 0.f;
+#pragma unroll
+          for (int q = 0; q < CW; ++q) acc[u][q] = fmaf(d, wg[q][e], acc[u][q]);
+        }
+      }
+      V r;
+      uint32_t* rw = reinterpret_cast<uint32_t*>(&r);
+#pragma unroll
+      for (int i = 0; i < CW / 2; ++i) rw[i] = pack_bf16x2(acc[u][2 * i], acc[u][2 * i + 1]);
+      *reinterpret_cast<V*>(out + static_cast<size_t>(t) * H + j) = r;
+    }
+  }
+}
+
+// Input gradient of the layer in one pass over the tokens (bf16, E <= EB, k = KT):
+//   dX[t]  = sum_s dXs[pair_pos[t,s] - row_lo] + dL[t,:] . Wg^T      (index_select + matmul bwd)
+//   part[blockIdx.y] += X[t]^T dL[t,:]                               (dWg partials, tensor.py:134-138)
+// A CTA owns a slab of kIgSlab columns and a contiguous token range.  A producer warp
+// stages, per token, the X row slab, the slab of every local pair's dXs row and dL[t] into
+// a shared-memory ring with 1-D bulk copies (bytes in flight independent of registers);
+// the 8 consumer warps own 4 columns per thread, whose Wg rows and dWg partial sums stay in
+// registers.  Pair sums in slot order: deterministic.
+constexpr int kIgSlab = 1024;    // columns per CTA
+constexpr int kIgConsumers = 256;
+constexpr int kIgTok = 2;        // tokens per ring stage (amortises the barrier handshake)
+constexpr int kIgRingBytes = 96 * 1024;
+
+template <int KT>
+struct alignas(16) IgStage {  // per-stage control block (rows live in a separate byte ring)
+  float dl[kIgTok][16];
+  int valid[kIgTok][KT];
+};
+
+template <int KT>
+__host__ __device__ constexpr int ig_tok_bytes() { return (KT + 1) * kIgSlab * 2; }
+template <int KT>
+__host__ __device__ constexpr int ig_stage_bytes() { return kIgTok * ig_tok_bytes<KT>(); }
+template <int KT>
+__host__ __device__ constexpr int ig_stages() { return kIgRingBytes / ig_stage_bytes<KT>(); }
+
+template <int EB, int KT, int MINB>
+__global__ void __launch_bounds__(kIgConsumers + 32, MINB)
+    input_grads_ring_kernel(const __nv_bfloat16* __restrict__ dXs, const int* __restrict__ seg, int El,
+                            const int* __restrict__ pair_pos, int N, int H, const __nv_bfloat16* __restrict__ X,
+                            const float* __restrict__ dL, const float* __restrict__ Wg, int E,
+                            __nv_bfloat16* __restrict__ dX, float* __restrict__ part) {
+  constexpr int S = ig_stages<KT>();
+  constexpr int SB = ig_stage_bytes<KT>();
+  constexpr int TB = ig_tok_bytes<KT>();
+  extern __shared__ __align__(128) unsigned char sm[];
+  unsigned char* ring = sm;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + S * SB);
+  uint64_t* empty = full + S;
+  IgStage<KT>* ctl = reinterpret_cast<IgStage<KT>*>(empty + S);
+
+  const int c0 = blockIdx.x * kIgSlab;
+  const int ncols = min(kIgSlab, H - c0);
+  const uint32_t slab_bytes = static_cast<uint32_t>(ncols) * 2;
+  const int per = (N + gridDim.y - 1) / gridDim.y;
+  const int tb = blockIdx.y * per, te = min(N, tb + per);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kIgConsumers / 32);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (threadIdx.x >= kIgConsumers) {  // ---------------- producer warp
+    const int lane = threadIdx.x & 31;
+    const int row_lo = seg[0], row_hi = seg[El];
+    for (int b = tb; b < te; b += 32) {  // b - tb is a multiple of kIgTok
+      // one coalesced round trip for the routing of 32 tokens
+      const int t = b + lane;
+      int rows[KT];
+      float d[EB];
+#pragma unroll
+      for (int s = 0; s < KT; ++s) rows[s] = -1;
+#pragma unroll
+      for (int e = 0; e < EB; ++e) d[e] = 0.f;
+      if (t < te) {
+        if (dX) {
+#pragma unroll
+          for (int s = 0; s < KT; ++s) {
+            const int p = pair_pos[static_cast<size_t>(t) * KT + s];
+            rows[s] = (p >= row_lo && p < row_hi) ? p - row_lo : -1;
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < EB; ++e)
+          if (e < E) d[e] = dL[static_cast<size_t>(t) * E + e];
+      }
+      const int nb = min(32, te - b);
+      // every lane writes its token's control entry; the stage's first lane posts the bytes
+      for (int l0 = 0; l0 < nb; l0 += kIgTok) {
+        const int i = b - tb + l0;  // first token of the stage
+        const int st = (i / kIgTok) % S;
+        const int it = i / kIgTok / S;
+        if (lane == l0 && it > 0) mbar_wait(&empty[st], (it - 1) & 1);
+        __syncwarp();
+        const int u = lane - l0;
+        uint32_t bytes = 0;
+        if (u >= 0 && u < kIgTok && lane < nb) {
+          IgStage<KT>& c = ctl[st];
+#pragma unroll
+          for (int e = 0; e < EB; ++e) c.dl[u][e] = d[e];
+          bytes = part ? slab_bytes : 0;
+#pragma unroll
+          for (int s = 0; s < KT; ++s) {
+            c.valid[u][s] = rows[s] >= 0;
+            if (rows[s] >= 0) bytes += slab_bytes;
+          }
+        }
+        // total bytes of the stage's tokens, to the stage's first lane
+#pragma unroll
+        for (int o = 1; o < kIgTok; o <<= 1) bytes += __shfl_down_sync(0xffffffffu, bytes, o);
+        __syncwarp();
+        if (lane == l0) mbar_arrive_expect_tx(&full[st], bytes);
+        __syncwarp();
+        if (u >= 0 && u < kIgTok && lane < nb) {
+          unsigned char* stg = ring + static_cast<size_t>(st) * SB + u * TB;
+          if (part) bulk_load(stg, X + static_cast<size_t>(t) * H + c0, slab_bytes, &full[st]);
+#pragma unroll
+          for (int s = 0; s < KT; ++s)
+            if (rows[s] >= 0)
+              bulk_load(stg + (s + 1) * kIgSlab * 2, dXs + static_cast<size_t>(rows[s]) * H + c0, slab_bytes,
+                        &full[st]);
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------------------------------------------- consumer warps
+  const int jl = threadIdx.x * 4;  // local column
+  const bool active = jl < ncols;
+  const int j = c0 + jl;
+  float2 wg[2][EB];          // (Wg[j+2p][e], Wg[j+2p+1][e])
+  float2 pacc[4][EB / 2];    // (dWg[j+q][e], dWg[j+q][e+1])
+#pragma unroll
+  for (int p = 0; p < 2; ++p)
+#pragma unroll
+    for (int e = 0; e < EB; ++e) {
+      const bool ok = active && dX && e < E;
+      wg[p][e] = make_float2(ok ? Wg[static_cast<size_t>(j + 2 * p) * E + e] : 0.f,
+                             ok ? Wg[static_cast<size_t>(j + 2 * p + 1) * E + e] : 0.f);
+    }
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int e = 0; e < EB / 2; ++e) pacc[q][e] = make_float2(0.f, 0.f);
+  for (int i0 = 0; i0 < te - tb; i0 += kIgTok) {
+    const int st = (i0 / kIgTok) % S;
+    mbar_wait(&full[st], (i0 / kIgTok / S) & 1);
+    const IgStage<KT>& c = ctl[st];
+    if (active) {
+#pragma unroll
+      for (int u = 0; u < kIgTok; ++u) {
+        const int t = tb + i0 + u;
+        if (t >= te) break;
+        const unsigned char* stg = ring + static_cast<size_t>(st) * SB + u * TB;
+        float d[EB];
+#pragma unroll
+        for (int e = 0; e < EB; e += 4) {
+          const float4 f = *reinterpret_cast<const float4*>(&c.dl[u][e]);
+          d[e] = f.x, d[e + 1] = f.y, d[e + 2] = f.z, d[e + 3] = f.w;
+        }
+        if (dX) {
+          float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+          for (int s = 0; s < KT; ++s) {
+            if (c.valid[u][s]) {
+              const uint2 v = *reinterpret_cast<const uint2*>(stg + (s + 1) * kIgSlab * 2 + jl * 2);
+              acc[0] = __fadd2_rn(acc[0], __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.x)));
+              acc[1] = __fadd2_rn(acc[1], __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.y)));
+            }
+          }
+#pragma unroll
+          for (int e = 0; e < EB; ++e) {
+            const float2 dd = make_float2(d[e], d[e]);
+            acc[0] = __ffma2_rn(dd, wg[0][e], acc[0]);
+            acc[1] = __ffma2_rn(dd, wg[1][e], acc[1]);
+          }
+          uint2 o;
+          o.x = pack_bf16x2(acc[0].x, acc[0].y);
+          o.y = pack_bf16x2(acc[1].x, acc[1].y);
+          *reinterpret_cast<uint2*>(dX + static_cast<size_t>(t) * H + j) = o;
+        }
+        if (part) {
+          const uint2 v = *reinterpret_cast<const uint2*>(stg + jl * 2);
+          const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.x));
+          const float2 bb = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.y));
+          const float x[4] = {a.x, a.y, bb.x, bb.y};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float2 xx = make_float2(x[q], x[q]);
+#pragma unroll
+            for (int e = 0; e < EB / 2; ++e) pacc[q][e] = __ffma2_rn(xx, make_float2(d[2 * e], d[2 * e + 1]), pacc[q][e]);
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[st]);
+  }
+  if (part && active) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float* p = part + (static_cast<size_t>(blockIdx.y) * H + j + q) * E;
+#pragma unroll
+      for (int e = 0; e < EB / 2; ++e) {
+        if (2 * e < E) p[2 * e] = pacc[q][e].x;
+        if (2 * e + 1 < E) p[2 * e + 1] = pacc[q][e].y;
+      }
+    }
+  }
+}
+
+template <int KT>
+constexpr size_t ig_smem_bytes() {
+  return static_cast<size_t>(ig_stages<KT>()) * ig_stage_bytes<KT>() + ig_stages<KT>() * 16 +
+         ig_stages<KT>() * sizeof(IgStage<KT>);
+}
+
+// Generic form (fp32, odd widths, many experts): thread per column, gate weights from L1.
+template <typename T>
+__global__ void __launch_bounds__(256)
+    combine_rows_kernel(const T* __restrict__ R, const int* __restrict__ seg, int El, const int* __restrict__ pair_pos,
+                        const float* __restrict__ w, int N, int K, int H, const float* __restrict__ dL,
+                        const float* __restrict__ Wg, int E, T* __restrict__ out) {
+  const int row_lo = seg[0], row_hi = seg[El];
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= H) return;
+  for (int t = blockIdx.y; t < N; t += gridDim.y) {
+    float acc = 0.f;
+    for (int sl = 0; sl < K; ++sl) {
+      const int p = pair_pos[static_cast<size_t>(t) * K + sl];
+      if (p >= row_lo && p < row_hi)
+        acc = fmaf(w ? w[static_cast<size_t>(t) * K + sl] : 1.f, to_f32(R[static_cast<size_t>(p - row_lo) * H + j]),
+                   acc);
+    }
+    if (dL)
+      for (int e = 0; e < E; ++e) acc = fmaf(dL[static_cast<size_t>(t) * E + e], Wg[static_cast<size_t>(j) * E + e], acc);
+    out[static_cast<size_t>(t) * H + j] = from_f32<T>(acc);
+  }
+}
+
 // ------------------------------------------------------------------ gate backward
 
 __global__ void gate_bwd_kernel(const float* __restrict__ scores, const int* __restrict__ idx,
@@ -447,6 +786,29 @@ __global__ void dwg_reduce_kernel(const float* __restrict__ part, int C, int HE,
   dWg[i] = s;
 }
 
+static int input_grads_chunks(int N, int H, int E) {
+  const int gx = (H + kIgSlab - 1) / kIgSlab;
+  const int per_sm = E <= 8 ? 2 : 1;
+  return max(1, min(N, num_sms() * per_sm / gx));
+}
+
+static bool input_grads_fused(int dtype, int H, int K, int E) {
+  return dtype == kBF16 && H % 8 == 0 && K >= 1 && K <= 4 && E <= 16;
+}
+
+template <int EB, int KT, int MINB>
+static int launch_input_grads(dim3 grid, cudaStream_t s, const void* dXs, const int* seg, int El, const int* pair_pos,
+                              int N, int H, const void* X, const float* dL, const float* Wg, int E, void* dX,
+                              float* part) {
+  constexpr size_t smem = ig_smem_bytes<KT>();
+  auto kern = input_grads_ring_kernel<EB, KT, MINB>;
+  PPMOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  kern<<<grid, kIgConsumers + 32, smem, s>>>(static_cast<const __nv_bfloat16*>(dXs), seg, El, pair_pos, N, H,
+                                             static_cast<const __nv_bfloat16*>(X), dL, Wg, E,
+                                             static_cast<__nv_bfloat16*>(dX), part);
+  return check_launch("input_grads_ring_kernel");
+}
+
 }  // namespace ppmoe
 
 using namespace ppmoe;
@@ -498,6 +860,90 @@ int ppmoe_chunk_rows(const int* tok_local, const int* seg, const int* kept, int 
   const int n = (C + 1) * El;
   chunk_rows_kernel<<<(n + 127) / 128, 128, 0, s>>>(tok_local, seg, kept, El, N, C, row_lo, row_hi);
   return check_launch("chunk_rows_kernel");
+}
+
+int ppmoe_combine(int dtype, const void* R, const int* seg, int El, const int* pair_pos, const float* w, int N, int K,
+                  int H, const float* dL, const float* Wg, int E, void* out, void* stream) {
+  PPMOE_REQUIRE(dtype == kBF16 || dtype == kF32, "bad dtype");
+  PPMOE_REQUIRE(N >= 0 && H >= 1 && K >= 1 && El >= 1, "bad combine shape N=%d H=%d K=%d El=%d", N, H, K, El);
+  PPMOE_REQUIRE(!dL || (Wg && E >= 1), "the gate term needs Wg and E >= 1");
+  if (N == 0) return kOk;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int ctas = num_sms() * 4;
+  auto launch_bf16 = [&](auto kern, int cw, int u) {
+    const int gx = (H / cw + 255) / 256;
+    dim3 grid(gx, max(1, min((N + u - 1) / u, ctas / gx)));
+    kern<<<grid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(R), seg, El, pair_pos, w, N, K, H, dL, Wg, E,
+                              static_cast<__nv_bfloat16*>(out));
+    return check_launch("combine_rows_bf16_kernel");
+  };
+  if (dtype == kBF16 && !dL && H % 8 == 0) {
+    if (K == 2) return launch_bf16(combine_rows_bf16_kernel<0, 8, 4, 2>, 8, 4);
+    if (K == 1) return launch_bf16(combine_rows_bf16_kernel<0, 8, 8, 1>, 8, 8);
+    return launch_bf16(combine_rows_bf16_kernel<0, 8, 8, 0>, 8, 8);
+  }
+  const int gx = (H + 255) / 256;
+  dim3 grid(gx, max(1, min(N, ctas / gx)));
+  if (dtype == kBF16)
+    combine_rows_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(R), seg, El, pair_pos, w,
+                                                            N, K, H, dL, Wg, E, static_cast<__nv_bfloat16*>(out));
+  else
+    combine_rows_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(R), seg, El, pair_pos, w, N, K, H, dL, Wg,
+                                                    E, static_cast<float*>(out));
+  return check_launch("combine_rows_kernel");
+}
+
+size_t ppmoe_input_grads_workspace_bytes(int dtype, int N, int H, int E) {
+  // fused-path partials for any k, or the gate_grads fallback's, whichever is larger
+  const size_t fused = static_cast<size_t>(input_grads_chunks(N, H, E)) * H * E * 4;
+  return dtype == kBF16 ? std::max(fused, ppmoe_gate_grad_workspace_bytes(N, H, E))
+                        : ppmoe_gate_grad_workspace_bytes(N, H, E);
+}
+
+int ppmoe_input_grads(int dtype, const void* dXs, const int* seg, int El, const int* pair_pos, int N, int K, int H,
+                      const void* X, const float* dL, const float* Wg, int E, void* dX, float* dWg, void* ws,
+                      size_t ws_bytes, void* stream) {
+  PPMOE_REQUIRE(dtype == kBF16 || dtype == kF32, "bad dtype");
+  PPMOE_REQUIRE(N >= 1 && H >= 1 && K >= 1 && El >= 1 && E >= 1 && E <= 64, "bad input-grad shape N=%d H=%d K=%d E=%d",
+                N, H, K, E);
+  PPMOE_REQUIRE(!dWg || ws_bytes >= ppmoe_input_grads_workspace_bytes(dtype, N, H, E), "input-grad workspace too small");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (!input_grads_fused(dtype, H, K, E)) {
+    if (dX)
+      if (int rc = ppmoe_combine(dtype, dXs, seg, El, pair_pos, nullptr, N, K, H, dL, Wg, E, dX, stream)) return rc;
+    if (!dWg) return kOk;
+    return ppmoe_gate_grads(nullptr, X, dtype, dL, Wg, N, H, E, nullptr, dWg, ws, ws_bytes, stream);
+  }
+  if (!dX && !dWg) return kOk;
+  const int C = input_grads_chunks(N, H, E);
+  dim3 grid((H + kIgSlab - 1) / kIgSlab, C);
+  float* part = dWg ? static_cast<float*>(ws) : nullptr;
+  int rc;
+#define PPMOE_IG(EB, KT, MINB) \
+  rc = launch_input_grads<EB, KT, MINB>(grid, s, dXs, seg, El, pair_pos, N, H, X, dL, Wg, E, dX, part)
+  if (E <= 8) {
+    switch (K) {
+      case 1: PPMOE_IG(8, 1, 2); break;
+      case 2: PPMOE_IG(8, 2, 2); break;
+      case 3: PPMOE_IG(8, 3, 2); break;
+      default: PPMOE_IG(8, 4, 2); break;
+    }
+  } else {
+    switch (K) {
+      case 1: PPMOE_IG(16, 1, 1); break;
+      case 2: PPMOE_IG(16, 2, 1); break;
+      case 3: PPMOE_IG(16, 3, 1); break;
+      default: PPMOE_IG(16, 4, 1); break;
+    }
+  }
+#undef PPMOE_IG
+  if (rc) return rc;
+  if (dWg) {
+    const int HE = H * E;
+    dwg_reduce_kernel<<<(HE + 255) / 256, 256, 0, s>>>(part, C, HE, dWg);
+    return check_launch("dwg_reduce_kernel");
+  }
+  return kOk;
 }
 
 int ppmoe_cast_out(const float* acc, int n, void* out, int dtype, void* stream) {

@@ -162,6 +162,7 @@ struct EpiFc2Fwd {
       for (int j = 0; j < W; ++j) x[j] = dropout_uniform(seed, row, n0 + j) >= drop_p ? x[j] * inv : 0.f;
     }
     store_row<T, W>(y + static_cast<size_t>(row) * H + n0, x, valid, cs);
+    if (!out_acc) return;  // gather-combine mode: ppmoe_combine reads Y afterwards
     const int t = tok[row];
     if (t >= 0) {
       const float s = weight_scaling ? w[row] : 1.f;
@@ -208,15 +209,21 @@ struct EpiFc2Dgrad {
 // (index_select backward, tensor.py:235-239).
 template <typename T>
 struct EpiFc1Dgrad {
-  float* dx_acc;  // [N*H] fp32
+  float* dx_acc;  // [N*H] fp32 scatter-add target, or
+  T* dxs;         // [rows*H] per-row store (gather-combined later by ppmoe_gate_grads)
   int H;
   const int* seg;
   const int* tok;
+  int cs;
   template <int W>
   __device__ __forceinline__ void apply(int g, int m, int row, int n0, const float (&v)[W]) const {
+    const int valid = min(W, H - n0);
+    if (dxs) {
+      store_row<T, W>(dxs + static_cast<size_t>(row) * H + n0, v, valid, cs);
+      return;
+    }
     const int t = tok[row];
     if (t < 0) return;
-    const int valid = min(W, H - n0);
     scatter_add_row<W>(dx_acc + static_cast<size_t>(t) * H + n0, v, 1.f, valid);
   }
 };

@@ -283,7 +283,8 @@ int ppmoe_expert_fc2_dgrad(int dtype, const void* dY, const void* down, const vo
 }
 
 int ppmoe_expert_fc1_dgrad(int dtype, const void* dH, const void* up, const int* seg, int El, int H, int F,
-                           int rows_cap, const int* tok_local, float* dx_acc, void* stream) {
+                           int rows_cap, const int* tok_local, float* dx_acc, void* dXs, void* stream) {
+  PPMOE_REQUIRE((dx_acc == nullptr) != (dXs == nullptr), "give exactly one of dx_acc (scatter-add) or dXs (rows)");
   if (int rc = check_common(dtype, El, H, F, rows_cap)) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   LongKScope long_k(F);
@@ -293,10 +294,10 @@ int ppmoe_expert_fc1_dgrad(int dtype, const void* dH, const void* up, const int*
     CUtensorMap ta, tb;
     if (int rc = tmap_kmajor(&ta, dH, F, rows_cap, kBM)) return rc;
     if (int rc = tmap_kmajor(&tb, up, F, static_cast<uint64_t>(El) * H, b_box_rows())) return rc;
-    EpiFc1Dgrad<bf16> epi{dx_acc, H, seg, tok_local};
+    EpiFc1Dgrad<bf16> epi{dx_acc, static_cast<bf16*>(dXs), H, seg, tok_local, stream_stores()};
     return launch_tc<false, false>(ta, tb, geo, epi, s);
   }
-  EpiFc1Dgrad<float> epi{dx_acc, H, seg, tok_local};
+  EpiFc1Dgrad<float> epi{dx_acc, static_cast<float*>(dXs), H, seg, tok_local, 0};
   return launch_simt<float, false, false>(static_cast<const float*>(dH), F, static_cast<const float*>(up), F, geo,
                                           rows_cap, epi, s);
 }

@@ -440,8 +440,8 @@ class _PPMoEFunction(torch.autograd.Function):
             rt = _ops.route(hidden, wg, spec.k, spec.override)
         cap = _ops.capacity_for(spec.capacity_factor, n, spec.k, e)
         pl = _ops.plan(rt.idx, rt.w, e, cap)
-        out_acc = torch.zeros((n, h), dtype=torch.float32, device=hidden.device)
         if spec.fwd_chunks > 1:
+            out_acc = torch.zeros((n, h), dtype=torch.float32, device=hidden.device)
             # combine all-reduce pipelined by token chunk: chunk c goes on the wire while the
             # expert GEMMs of chunk c+1 run (reduce_from_tensor_parallel_region, moe.py:307)
             out = torch.empty((n, h), dtype=hidden.dtype, device=hidden.device)
@@ -461,12 +461,20 @@ class _PPMoEFunction(torch.autograd.Function):
             for wk in works:
                 if wk is not None:
                     wk.wait()
+            del out_acc
+        elif _ops.gather_combine():
+            # fc2 stores Y; the combine gathers each token's local pairs (no fp32 accumulator)
+            st = _ops.experts_forward(hidden, pl, spec.e0, spec.el, up, down, bias_up, bias_down, spec.k,
+                                      spec.weight_scaling, None, drop_p=spec.dropout_p, seed=spec.seed)
+            out = _ops.combine(st.y, st, pl, rt.w if spec.weight_scaling else None, torch.empty_like(hidden))
+            spec.world.all_reduce_(spec.group, out)  # reduce_from_tensor_parallel_region (moe.py:307)
         else:
+            out_acc = torch.zeros((n, h), dtype=torch.float32, device=hidden.device)
             st = _ops.experts_forward(hidden, pl, spec.e0, spec.el, up, down, bias_up, bias_down, spec.k,
                                       spec.weight_scaling, out_acc, drop_p=spec.dropout_p, seed=spec.seed)
             out = _ops.cast_out(out_acc, hidden.dtype)
+            del out_acc
             spec.world.all_reduce_(spec.group, out)  # reduce_from_tensor_parallel_region (moe.py:307)
-        del out_acc
         ctx.save_for_backward(hidden, wg, up, down)
         ctx.state = (rt, pl, st, bias_up is not None, spec)
         l_aux = rt.l_aux[0].to(torch.float32)
@@ -483,14 +491,21 @@ class _PPMoEFunction(torch.autograd.Function):
         aux = None
         if spec.aux_here and g_aux is not None:
             aux = g_aux.detach().to(torch.float32).reshape(1).contiguous()
-        dx_acc = torch.zeros((n, h), dtype=torch.float32, device=hidden.device)
-        # data gradients first: dX can go on the wire while the weight gradients compute
-        dy, dh, dw, parts = _ops.experts_backward_data(g_out, st, up, down, spec.weight_scaling, dx_acc, has_bias)
+        # data gradients first: dX can go on the wire while the weight gradients compute.
+        # fc1 dgrad stores per-row dX; gate_grads gathers them per token (no fp32 scatter)
+        if _ops.gather_combine():
+            dx_acc, dxs = None, _ops._act((st.rows_cap, h), hidden.dtype, hidden.device)
+        else:
+            dx_acc, dxs = torch.zeros((n, h), dtype=torch.float32, device=hidden.device), None
+        dy, dh, dw, parts = _ops.experts_backward_data(g_out, st, up, down, spec.weight_scaling, dx_acc, has_bias, dxs)
         dl = _ops.gate_backward(rt, pl, st, dw, aux)
         need_dx = ctx.needs_input_grad[0]
         need_dwg = ctx.needs_input_grad[1]
-        dx, dwg = _ops.gate_grads(dx_acc, hidden, dl, wg, need_dx, need_dwg)
-        del dx_acc
+        if dxs is not None:
+            dx, dwg = _ops.input_grads(dxs, st, pl, hidden, dl, wg, need_dx, need_dwg)
+        else:
+            dx, dwg = _ops.gate_grads(dx_acc, hidden, dl, wg, need_dx, need_dwg)
+        del dx_acc, dxs
         work = None
         if need_dx:  # copy_to_tensor_parallel_region backward (collectives.py:215-221)
             work = spec.world.all_reduce_async(spec.group, dx)

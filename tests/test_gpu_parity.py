@@ -260,10 +260,12 @@ def test_deterministic_bit_identical_runs(monkeypatch):
 
 @pytest.mark.parametrize("chunks", [2, 3, 5])
 def test_token_chunked_forward_bit_identical(chunks, monkeypatch):
-    """The all-reduce pipelining path (fc1/fc2 per token chunk) gives bit-identical results."""
+    """The all-reduce pipelining path (fc1/fc2 per token chunk) gives bit-identical results
+    to the unchunked scatter-add combine it pipelines."""
     layer = oracle_rounded(O.init_layer(256, 8, seed=9), torch.bfloat16)
     hidden = torch.randn(1500, 256).bfloat16().double().numpy()
     monkeypatch.setenv("PPMOE_POISON", "1")
+    monkeypatch.setenv("PPMOE_COMBINE", "scatter")
     base = run_cuda_layer(hidden, device_weights(layer, torch.bfloat16), k=2, capacity_factor=1.1)
     monkeypatch.setenv("PPMOE_FWD_CHUNKS", str(chunks))
     got = run_cuda_layer(hidden, device_weights(layer, torch.bfloat16), k=2, capacity_factor=1.1)
@@ -271,6 +273,29 @@ def test_token_chunked_forward_bit_identical(chunks, monkeypatch):
     assert np.array_equal(base["grad_hidden"], got["grad_hidden"])
     for k in base["grads"]:
         assert np.array_equal(base["grads"][k], got["grads"][k]), k
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("hidden_size,experts", [(256, 8), (264, 16), (128, 32)])
+def test_gather_combine_matches_scatter(dtype, hidden_size, experts, monkeypatch):
+    """The gather combine (fc2 stores Y, ppmoe_combine sums the token's pairs; fc1 dgrad
+    stores per-row dX, gathered with the gate term) agrees with the fp32 scatter-add
+    accumulator path, and is bitwise reproducible run to run."""
+    layer = oracle_rounded(O.init_layer(hidden_size, experts, seed=4), dtype)
+    hidden = torch.randn(700, hidden_size).to(dtype).double().numpy()
+    monkeypatch.setenv("PPMOE_POISON", "1")
+    monkeypatch.setenv("PPMOE_COMBINE", "scatter")
+    ref = run_cuda_layer(hidden, device_weights(layer, dtype), k=2, capacity_factor=1.25, tp=2, dtype=dtype)
+    monkeypatch.setenv("PPMOE_COMBINE", "gather")
+    got = run_cuda_layer(hidden, device_weights(layer, dtype), k=2, capacity_factor=1.25, tp=2, dtype=dtype)
+    again = run_cuda_layer(hidden, device_weights(layer, dtype), k=2, capacity_factor=1.25, tp=2, dtype=dtype)
+    tol = TOL[dtype]
+    assert scaled_err(got["out"], ref["out"]) < tol
+    assert scaled_err(got["grad_hidden"], ref["grad_hidden"]) < tol
+    for k in ref["grads"]:
+        assert scaled_err(got["grads"][k], ref["grads"][k]) < tol, k
+    assert np.array_equal(got["out"], again["out"])
+    assert np.array_equal(got["grad_hidden"], again["grad_hidden"])
 
 
 # ------------------------------------------------------------------ all-to-all comparator (DPMoE)

@@ -55,3 +55,7 @@ aux = torch.ones(1, device=dev)
 dl = _ops.gate_backward(rt, pl, st, dw, aux)
 timeit("gate_bwd", lambda: _ops.gate_backward(rt, pl, st, dw, aux))
 timeit("gate_grads (dX + dWg)", lambda: _ops.gate_grads(dx_acc, x, dl, wg, True, True), n * h * 8)
+outb = torch.empty_like(x)
+timeit("combine fwd (Y gather, w)", lambda: _ops.combine(st.y, st, pl, rt.w, outb), n * h * 6)
+timeit("input_grads (dX + dWg)", lambda: _ops.input_grads(st.y, st, pl, x, dl, wg, True, True), n * h * 8)
+timeit("input_grads (dX only)", lambda: _ops.input_grads(st.y, st, pl, x, dl, wg, True, False), n * h * 6)
