@@ -82,60 +82,88 @@ def config_of(a, n_gpus):
 
 
 class ClockSampler:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    """SM clock / throttle-reason sampling during the timed region (B200_PROFILING.md clocks
+    line): NVML every 10 ms from a thread (nvidia-smi -lms as the fallback)."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap"}
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, period_s: float = 0.01):
         self.index = index
+        self.period = period_s
+        self.sm, self.smax, self.reasons = [], [], set()
+        self.stop = threading.Event()
+        self.thread = None
         self.proc = None
-        self.lines = []
+
+    def _nvml_handle(self):
+        import pynvml
+        import torch
+
+        pynvml.nvmlInit()
+        p = torch.cuda.get_device_properties(self.index)
+        bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+        return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode())
+
+    def _nvml_loop(self, nv, hd):
+        while True:
+            try:
+                self.sm.append(float(nv.nvmlDeviceGetClockInfo(hd, nv.NVML_CLOCK_SM)))
+                self.smax.append(float(nv.nvmlDeviceGetMaxClockInfo(hd, nv.NVML_CLOCK_SM)))
+                bits = nv.nvmlDeviceGetCurrentClocksEventReasons(hd)
+                self.reasons.update(nm for b, nm in self.REASONS.items() if bits & b)
+            except Exception:
+                pass
+            if self.stop.wait(self.period):
+                return
+
+    def _smi_read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            try:
+                self.sm.append(float(parts[0]))
+                self.smax.append(float(parts[1]))
+            except (ValueError, IndexError):
+                continue
+            for nm, v in zip(["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"], parts[3:7]):
+                if v.lower().startswith("active"):
+                    self.reasons.add(nm)
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+            nv, hd = self._nvml_handle()
+            self.thread = threading.Thread(target=self._nvml_loop, args=(nv, hd), daemon=True)
+        except Exception:
+            fields = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+                      "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                      "clocks_event_reasons.sw_power_cap")
+            try:
+                self.proc = subprocess.Popen(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={fields}", "--format=csv,noheader,nounits",
+                     "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                self.thread = threading.Thread(target=self._smi_read, daemon=True)
+            except OSError:
+                self.thread = None
+        if self.thread is not None:
             self.thread.start()
-        except OSError:
-            self.proc = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
     def __exit__(self, *exc):
+        self.stop.set()
         if self.proc is not None:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
+        if self.thread is not None:
+            self.thread.join(timeout=5)
         return False
 
     def summary(self):
-        sm, smax, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 7:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                smax.append(float(parts[1]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[3:7]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
-        if not sm:
+        if not self.sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
-                "samples": len(sm)}
+        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": max(self.smax), "reasons": sorted(self.reasons),
+                "samples": len(self.sm), "sm_mhz_min": min(self.sm)}
 
 
 # ----------------------------------------------------------------------------- CPU baseline
@@ -336,33 +364,39 @@ def main():
     e2e = None
     if not a.no_e2e:
         x_host = torch.randn(n, h, generator=torch.Generator().manual_seed(1234)).to(torch.bfloat16).pin_memory()
-        x_dev = torch.empty(n, h, device=dev, dtype=torch.bfloat16)
         loss_host = torch.empty(1, dtype=torch.float32).pin_memory()
+        # each rank copies its 1/T row slice over PCIe, NCCL all_gather replicates it; the next
+        # batch's copy overlaps this batch's compute (P.ReplicatedFeed)
+        feed = P.ReplicatedFeed(world, group, (n, h), torch.bfloat16, dev)
 
-        def e2e_step():
-            x_dev.copy_(x_host, non_blocking=True)
-            xin = x_dev.detach().requires_grad_()
-            out, l_aux = step(xin)
-            loss = out.float().sum() + l_aux
-            loss_host.copy_(loss.reshape(1), non_blocking=True)
-            torch.cuda.current_stream().synchronize()
-            return float(loss_host[0])
+        def e2e_run(steps):
+            feed.submit(x_host)
+            for i in range(steps):
+                xin = feed.take().detach().requires_grad_()
+                if i + 1 < steps:
+                    feed.submit(x_host)
+                out, l_aux = step(xin)
+                loss = out.float().sum() + l_aux
+                loss_host.copy_(loss.detach().reshape(1), non_blocking=True)
+                torch.cuda.current_stream().synchronize()
+                float(loss_host[0])
 
-        for _ in range(2):
-            e2e_step()
+        e2e_run(2)
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        for _ in range(a.steps):
-            e2e_step()
+        e2e_run(a.steps)
         e1.record()
         barrier()
         ems = e0.elapsed_time(e1) / a.steps
         te = torch.tensor([ems], device=dev, dtype=torch.float64)
         if distributed:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": n / (float(te) / 1e3), "unit": UNIT, "h2d_bytes_per_step": n * h * 2, "d2h_bytes_per_step": 4,
-               "ms_per_step": float(te), "path": "paper_2304_11414_b200.ppmoe_forward + backward (C-ABI) from pinned host"}
+        e2e = {"value": n / (float(te) / 1e3), "unit": UNIT, "h2d_bytes_per_step": feed.h2d_bytes,
+               "d2h_bytes_per_step": 4, "ms_per_step": float(te),
+               "h2d_scope": "per rank: its 1/T row slice of the pinned [N,H] bf16 batch, replicated by an NCCL "
+                            "all_gather; the next batch's copy overlaps this batch's compute",
+               "path": "paper_2304_11414_b200.ReplicatedFeed + ppmoe_forward + backward (C-ABI) from pinned host"}
 
     # ---- conventional all-to-all expert-parallel layer (DPMoE) at the same global N:
     # each rank routes its own N/T tokens and exchanges rows with two all-to-alls per pass

@@ -23,6 +23,7 @@ from .moe import (
     sync_gate_gradients,
 )
 from .dpmoe import dpmoe_forward, dpmoe_sync_gradients
+from .feed import ReplicatedFeed
 from .rng import Rng
 
 __version__ = "0.1.0"
@@ -31,5 +32,5 @@ __all__ = [
     "DP", "EP", "PP", "TP", "ConfigurationError", "GroupSet", "ProcessGroup", "TrafficLedger", "World", "tp_groups",
     "DispatchPlan", "ExpertBank", "ExpertFfn", "GateOutput", "GateParams", "LayerConfig", "MoeLayerWeights",
     "PPMoELayer", "aux_loss", "build_dispatch_plan", "gate_top1", "gate_topk", "global_batch_equivalence", "ppmoe_forward",
-    "sync_gate_gradients", "Rng", "dpmoe_forward", "dpmoe_sync_gradients",
+    "sync_gate_gradients", "Rng", "dpmoe_forward", "dpmoe_sync_gradients", "ReplicatedFeed",
 ]

@@ -1,0 +1,65 @@
+"""Host -> device feed of the replicated PPMoE activations.
+
+Every rank of a PPMoE tensor-parallel group holds the same [N, H] hidden states (the
+input of copy_to_tensor_parallel_region, collectives.py:205-228).  Copying the whole
+batch over PCIe on every rank moves T times the bytes the group needs, so
+``ReplicatedFeed`` splits it: each rank copies its 1/T row slice of the pinned host
+batch (host -> device on a side stream) and one NCCL all_gather over NVLink rebuilds the
+replicated tensor.  Batches are double-buffered: ``submit`` of batch i+1 overlaps the
+layer's compute on batch i, and ``take`` orders the current stream after the copy and
+the gather.  With T = 1 it is a prefetching pinned copy.
+"""
+
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+from .collectives import ProcessGroup, World
+
+
+class ReplicatedFeed:
+    def __init__(self, world: World, group: ProcessGroup, shape, dtype, device, depth: int = 2):
+        n = shape[0]
+        self.world, self.group = world, group
+        self.tp = group.size if world.distributed else 1
+        if n % self.tp:
+            raise ValueError(f"{n} rows do not split over a tensor group of {self.tp}")
+        self.rank = world.rank_in(group) if world.distributed else 0
+        self.rows = n // self.tp
+        self.bufs = [torch.empty(shape, dtype=dtype, device=device) for _ in range(depth)]
+        self.stream = torch.cuda.Stream(device=device)
+        self.pending: list = []
+        self.next = 0
+
+    @property
+    def h2d_bytes(self) -> int:
+        """Host -> device bytes one batch costs this rank."""
+        b = self.bufs[0]
+        return self.rows * b[0].numel() * b.element_size()
+
+    def submit(self, host: torch.Tensor) -> None:
+        """Start moving `host` (pinned, the full [N, H] batch) to the device."""
+        buf = self.bufs[self.next]
+        self.next = (self.next + 1) % len(self.bufs)
+        lo = self.rank * self.rows
+        mine = buf[lo:lo + self.rows]
+        # the buffer was last read by work queued on the current stream
+        self.stream.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(self.stream):
+            mine.copy_(host[lo:lo + self.rows], non_blocking=True)
+            work = None
+            if self.tp > 1:
+                work = dist.all_gather_into_tensor(buf, mine, group=self.world.torch_group(self.group),
+                                                   async_op=True)
+            done = torch.cuda.Event()
+            done.record(self.stream)
+        self.pending.append((buf, work, done))
+
+    def take(self) -> torch.Tensor:
+        """The oldest submitted batch, replicated on this rank; the current stream waits for it."""
+        buf, work, done = self.pending.pop(0)
+        torch.cuda.current_stream().wait_event(done)
+        if work is not None:
+            work.wait()
+        return buf

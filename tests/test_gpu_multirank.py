@@ -184,3 +184,50 @@ def test_a2a_comparator_matches_ppmoe_on_global_batch(world, k, cf):
         assert err(res["dwg"], full.gate.wg.grad.cpu().numpy()) < 2e-2
         assert err(res["dup"], full.bank.up.grad[r * el:(r + 1) * el].float().cpu().numpy()) < 2e-2
         assert res["a2a"] == 5
+
+
+def _feed_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    import paper_2304_11414_b200 as P
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    try:
+        n, h = 1024, 384
+        hosts = [torch.randn(n, h, generator=torch.Generator().manual_seed(s)).bfloat16().pin_memory() for s in range(3)]
+        feed = P.ReplicatedFeed(P.World(1, world), P.ProcessGroup(P.EP, tuple(range(world))), (n, h),
+                                torch.bfloat16, "cuda")
+        ok = []
+        feed.submit(hosts[0])
+        for i in range(3):
+            x = feed.take()
+            if i + 1 < 3:
+                feed.submit(hosts[i + 1])
+            ok.append(bool(torch.equal(x.cpu(), hosts[i])))
+            torch.cuda.synchronize()
+        q.put((rank, {"ok": ok, "h2d": feed.h2d_bytes}))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_replicated_feed_rebuilds_batch():
+    """Each rank copies 1/T of the host batch; the all_gather replicates it exactly."""
+    world = 2
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29800 + os.getpid() % 100
+    procs = [ctx.Process(target=_feed_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = _collect(q, procs)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for r in range(world):
+        assert got[r]["ok"] == [True, True, True]
+        assert got[r]["h2d"] == 1024 * 384 * 2 // world

@@ -298,6 +298,20 @@ def test_gather_combine_matches_scatter(dtype, hidden_size, experts, monkeypatch
     assert np.array_equal(got["grad_hidden"], again["grad_hidden"])
 
 
+def test_replicated_feed_single_gpu():
+    """T = 1: the feed is a double-buffered pinned copy of the whole batch."""
+    n, h = 300, 128
+    hosts = [torch.randn(n, h, generator=torch.Generator().manual_seed(s)).bfloat16().pin_memory() for s in range(3)]
+    feed = P.ReplicatedFeed(P.World(1, 1), P.ProcessGroup(P.EP, (0,)), (n, h), torch.bfloat16, "cuda")
+    feed.submit(hosts[0])
+    for i in range(3):
+        x = feed.take()
+        if i + 1 < 3:
+            feed.submit(hosts[i + 1])
+        assert torch.equal(x.cpu(), hosts[i])
+    assert feed.h2d_bytes == n * h * 2
+
+
 # ------------------------------------------------------------------ all-to-all comparator (DPMoE)
 
 
