@@ -124,11 +124,12 @@ int ppmoe_expert_fc1_fwd(int dtype, const void* Xs, const void* up, const void* 
  * Y = Dropout(Act*down_g + bias_down) (stored, pre-scale), out_acc[tok] += w*Y
  * (moe.py:104-107, scale_rows tensor.py:184-196, index_assign 244-272, dropout
  * tensor.py:315-330 with a counter-based mask hash(seed, local row, column)).
- * out_acc [N x H] fp32 must be zeroed by the caller; NULL = store Y only (for ppmoe_combine). */
+ * out_acc [N x H] fp32 must be zeroed by the caller; NULL = store Y only (for ppmoe_combine).
+ * Y2 (optional) receives a second copy of Y (the peer-visible rows of ppmoe_nvl_owner_gather). */
 int ppmoe_expert_fc2_fwd(int dtype, const void* Act, const void* down, const void* bias_down, const int* seg,
                          int El, int H, int F, int rows_cap, const int* row_lo, const int* row_hi,
                          const int* tok_local, const float* w_local, int weight_scaling, float dropout_p,
-                         unsigned long long seed, void* Y, float* out_acc, void* stream);
+                         unsigned long long seed, void* Y, void* Y2, float* out_acc, void* stream);
 
 /* Gather-combine over this rank's pairs, in slot order (deterministic):
  *   out[t] = sum_s w[t,s] * R[pair_pos[t,s] - seg[0]]  (+ dL[t,:] . Wg^T when dL != NULL)
@@ -217,6 +218,38 @@ int ppmoe_a2a_owner_layout(const int* recv_counts, int T, int El, int rows_cap, 
  * tok < 0 skipped, w NULL = 1 (index_assign back to token order, moe.py:461-467).   */
 int ppmoe_scatter_rows(const void* src, int dtype, int H, const int* nrows, const int* tok, const float* w, float* dst,
                        void* stream);
+
+/* Tensor-parallel exchange over NVLink peer memory (replaces the [N x H] all-reduces of
+ * reduce_from_tensor_parallel_region moe.py:307 and tp_region backward
+ * collectives.py:205-228, whose partials are k/T-sparse by token) ------------------ */
+/* CUDA IPC: device buffer + handle (ppmoe_ipc_handle_bytes() bytes), open a peer's handle. */
+size_t ppmoe_ipc_handle_bytes(void);
+int ppmoe_ipc_alloc(size_t bytes, void** ptr, void* handle);
+int ppmoe_ipc_open(const void* handle, void** ptr);
+int ppmoe_ipc_close(void* ptr);
+int ppmoe_ipc_free(void* ptr);
+/* Barrier of T ranks on channel ch: writes `epoch` (release, system scope) into every
+ * peer's signal pad (pads = device array of T pad pointers, ppmoe_nvl_pad_bytes() each),
+ * then waits until all T flags of this rank's pad reach `epoch`.  A spin longer than
+ * timeout_cycles sets *err = 1 and returns instead of hanging.                       */
+size_t ppmoe_nvl_pad_bytes(void);
+int ppmoe_nvl_barrier(void* const* pads, int T, int rank, int ch, unsigned int epoch, int* err,
+                      long long timeout_cycles, void* stream);
+/* Owner gather for this rank's tokens [t0, t1) = [rank*N/T, (rank+1)*N/T):
+ *   out[t] = sum_s w[t,s] * rows[q][pair_pos[t,s] - seg[q*El]]   q = idx[t,s] / El
+ *            (+ dl[t - t0, :] . Wg^T when dl != NULL)
+ * in slot order; rows = device array of T peer row buffers (bf16 [rows x H]; Y forward,
+ * per-row dX backward), dl = this rank's summed dL rows [t1-t0 x E] fp32 (from
+ * ppmoe_nvl_sum_rows).  Writes the owned rows of out (local [N x H]) and of out_sym (this
+ * rank's peer-visible copy).                                                             */
+int ppmoe_nvl_owner_gather(const void* const* rows, const int* seg, int El, const int* idx, const int* pair_pos,
+                           const float* w, int N, int K, int H, int T, int rank, const float* dl, const float* Wg,
+                           int E, void* out, void* out_sym, void* stream);
+/* out [t1-t0 x C] = sum over q (rank order) of srcs[q] rows [t0, t1) (fp32 [N x C]): the
+ * owned rows of the ranks' partial gate-logit gradients.                               */
+int ppmoe_nvl_sum_rows(const void* const* srcs, int T, int rank, int N, int C, float* out, void* stream);
+/* All-gather by pull: out rows of every other owner q's block from srcs[q] (its out_sym). */
+int ppmoe_nvl_pull_blocks(const void* const* srcs, int T, int rank, int N, int H, void* out, void* stream);
 
 /* Self-test entry: plain grouped GEMM D_g = A_g * B_g through the tcgen05 path
  * (use_tc=1) or the CUDA-core path (use_tc=0).  mode 0: A [rows x K] K-major

@@ -21,6 +21,8 @@ _F = ctypes.c_float
 _D = ctypes.c_double
 _S = ctypes.c_size_t
 _U = ctypes.c_ulonglong
+_UI = ctypes.c_uint
+_LL = ctypes.c_longlong
 
 # name -> (restype, argtypes); mirrors include/ppmoe_capi.h
 _SIGNATURES = {
@@ -40,11 +42,21 @@ _SIGNATURES = {
     "ppmoe_gather": (_I, [_P, _I, _I, _I, _P, _I, _P, _P, _I, _P, _P, _P, _P]),
     "ppmoe_chunk_rows": (_I, [_P, _P, _P, _I, _I, _I, _P, _P, _P]),
     "ppmoe_expert_fc1_fwd": (_I, [_I, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P]),
-    "ppmoe_expert_fc2_fwd": (_I, [_I, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _I, _F, _U, _P, _P, _P]),
+    "ppmoe_expert_fc2_fwd": (_I, [_I, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _I, _F, _U, _P, _P, _P, _P]),
     "ppmoe_combine": (_I, [_I, _P, _P, _I, _P, _P, _I, _I, _I, _P, _P, _I, _P, _P]),
     "ppmoe_input_grads_workspace_bytes": (_S, [_I, _I, _I, _I]),
     "ppmoe_input_grads": (_I, [_I, _P, _P, _I, _P, _I, _I, _I, _P, _P, _P, _I, _P, _P, _P, _S, _P]),
     "ppmoe_cast_out": (_I, [_P, _I, _P, _I, _P]),
+    "ppmoe_ipc_handle_bytes": (_S, []),
+    "ppmoe_ipc_alloc": (_I, [_S, _P, _P]),
+    "ppmoe_ipc_open": (_I, [_P, _P]),
+    "ppmoe_ipc_close": (_I, [_P]),
+    "ppmoe_ipc_free": (_I, [_P]),
+    "ppmoe_nvl_pad_bytes": (_S, []),
+    "ppmoe_nvl_barrier": (_I, [_P, _I, _I, _I, _UI, _P, _LL, _P]),
+    "ppmoe_nvl_owner_gather": (_I, [_P, _P, _I, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _I, _P, _P, _P]),
+    "ppmoe_nvl_pull_blocks": (_I, [_P, _I, _I, _I, _I, _P, _P]),
+    "ppmoe_nvl_sum_rows": (_I, [_P, _I, _I, _I, _I, _P, _P]),
     "ppmoe_bwd_dy": (_I, [_I, _P, _P, _P, _I, _I, _I, _P, _P, _I, _F, _U, _P, _P, _P, _P]),
     "ppmoe_expert_fc2_dgrad": (_I, [_I, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P]),
     "ppmoe_expert_fc2_wgrad": (_I, [_I, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P]),

@@ -257,7 +257,7 @@ class ExpertFwdState:
 
 def experts_forward(hidden, pl: Plan, e0: int, el: int, up, down, bias_up, bias_down, k: int, weight_scaling: bool,
                     out_acc: torch.Tensor, chunks: int = 1, on_chunk=None, drop_p: float = 0.0,
-                    seed: int = 0) -> ExpertFwdState:
+                    seed: int = 0, y_mirror: torch.Tensor | None = None) -> ExpertFwdState:
     """index-slice gather -> fc1 (+bias, GeLU) -> fc2 (+bias, gate-scaled scatter-add combine)
     for experts [e0, e0+el) (moe.py:294-305).  out_acc None: fc2 only stores Y and the
     combine is done by ``combine`` (gather, no atomics).  With chunks > 1 the two GEMMs run per token
@@ -283,7 +283,8 @@ def experts_forward(hidden, pl: Plan, e0: int, el: int, up, down, bias_up, bias_
         call("ppmoe_expert_fc1_fwd", dt, ptr(xs), ptr(up), ptr(bias_up), ptr(seg), el, h, f, rows_cap, ptr(rlo),
              ptr(rhi), ptr(gelu_grad), ptr(act), s)
         call("ppmoe_expert_fc2_fwd", dt, ptr(act), ptr(down), ptr(bias_down), ptr(seg), el, h, f, rows_cap, ptr(rlo),
-             ptr(rhi), ptr(tok_l), ptr(w_l), int(bool(weight_scaling)), float(drop_p), int(seed), ptr(y), ptr(out_acc), s)
+             ptr(rhi), ptr(tok_l), ptr(w_l), int(bool(weight_scaling)), float(drop_p), int(seed), ptr(y), ptr(y_mirror),
+             ptr(out_acc), s)
 
     if chunks <= 1:
         gemms(None, None)
@@ -327,7 +328,7 @@ def expert_pipeline(xsrc: torch.Tensor, seg: torch.Tensor, el: int, tok_sorted: 
     call("ppmoe_expert_fc1_fwd", dt, ptr(xs), ptr(up), ptr(bias_up), ptr(seg), el, h, f, rows_cap, None, None,
          ptr(gelu_grad), ptr(act), s)
     call("ppmoe_expert_fc2_fwd", dt, ptr(act), ptr(down), ptr(bias_down), ptr(seg), el, h, f, rows_cap, None, None,
-         ptr(tok_l), ptr(w_l), int(bool(weight_scaling)), float(drop_p), int(seed), ptr(y), ptr(out_acc), s)
+         ptr(tok_l), ptr(w_l), int(bool(weight_scaling)), float(drop_p), int(seed), ptr(y), None, ptr(out_acc), s)
     return ExpertFwdState(0, el, rows_cap, seg, xs, tok_l, w_l, gelu_grad, act, y, drop_p, seed)
 
 
@@ -431,11 +432,12 @@ def experts_backward_weights(st: ExpertFwdState, dy, dh, up, down, has_bias: boo
     return d_up, d_down, d_bu, d_bd
 
 
-def gate_backward(rt: Route, pl: Plan, st: ExpertFwdState, dw: torch.Tensor, aux_grad: torch.Tensor | None) -> torch.Tensor:
+def gate_backward(rt: Route, pl: Plan, st: ExpertFwdState, dw: torch.Tensor, aux_grad: torch.Tensor | None,
+                  out: torch.Tensor | None = None) -> torch.Tensor:
     """dL = d(loss)/d(logits) from the local pairs' dw and (on one rank) the aux loss."""
     n, e = rt.scores.shape
     k = rt.idx.shape[1]
-    dl = torch.empty((n, e), dtype=torch.float32, device=rt.scores.device)
+    dl = out if out is not None else torch.empty((n, e), dtype=torch.float32, device=rt.scores.device)
     call("ppmoe_gate_bwd", ptr(rt.scores), ptr(rt.idx), ptr(pl.pair_pos), ptr(dw), ptr(st.seg), st.el,
          ptr(rt.top1_counts), n, e, k, ptr(aux_grad), ptr(dl), _stream())
     return dl
@@ -455,6 +457,22 @@ def input_grads(dxs, st: ExpertFwdState, pl: Plan, hidden, dl, wg, want_dx: bool
     call("ppmoe_input_grads", dt, ptr(dxs), ptr(st.seg), st.el, ptr(pl.pair_pos), n, k, h, ptr(hidden), ptr(dl),
          ptr(wg), e, ptr(dx), ptr(dwg), ptr(ws), ws.numel(), _stream())
     return dx, dwg
+
+
+def gate_weight_grad(hidden_rows: torch.Tensor, dl_rows: torch.Tensor, wg: torch.Tensor,
+                     out: torch.Tensor | None = None) -> torch.Tensor:
+    """dWg = Xᵀ dL over the given token rows (fp32 [H x E]; deterministic partials)."""
+    n, h = hidden_rows.shape
+    e = wg.shape[1]
+    dt = dtype_code(hidden_rows.dtype)
+    dwg = out if out is not None else torch.empty((h, e), dtype=torch.float32, device=hidden_rows.device)
+    if n == 0:
+        return dwg.zero_()
+    lib = _lib.load()
+    ws = _ws(lib.ppmoe_input_grads_workspace_bytes(dt, n, h, e), hidden_rows.device)
+    call("ppmoe_input_grads", dt, None, None, 1, None, n, 1, h, ptr(hidden_rows), ptr(dl_rows), ptr(wg), e, None,
+         ptr(dwg), ptr(ws), ws.numel(), _stream())
+    return dwg
 
 
 def gate_grads(dx_acc, hidden, dl, wg, want_dx: bool, want_dwg: bool):

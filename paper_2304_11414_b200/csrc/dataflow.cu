@@ -418,7 +418,7 @@ __global__ void __launch_bounds__(kIgConsumers + 32, MINB)
 
   if (threadIdx.x >= kIgConsumers) {  // ---------------- producer warp
     const int lane = threadIdx.x & 31;
-    const int row_lo = seg[0], row_hi = seg[El];
+    const int row_lo = dX ? seg[0] : 0, row_hi = dX ? seg[El] : 0;
     for (int b = tb; b < te; b += 32) {  // b - tb is a multiple of kIgTok
       // one coalesced round trip for the routing of 32 tokens
       const int t = b + lane;

@@ -135,6 +135,7 @@ struct EpiFc1Fwd {
 template <typename T>
 struct EpiFc2Fwd {
   T* y;
+  T* y2;          // optional second copy of Y (peer-visible buffer of the NVLink exchange)
   const T* bias;  // [G*H] or null
   int H;
   const int* seg;
@@ -162,6 +163,7 @@ struct EpiFc2Fwd {
       for (int j = 0; j < W; ++j) x[j] = dropout_uniform(seed, row, n0 + j) >= drop_p ? x[j] * inv : 0.f;
     }
     store_row<T, W>(y + static_cast<size_t>(row) * H + n0, x, valid, cs);
+    if (y2) store_row<T, W>(y2 + static_cast<size_t>(row) * H + n0, x, valid, 0);
     if (!out_acc) return;  // gather-combine mode: ppmoe_combine reads Y afterwards
     const int t = tok[row];
     if (t >= 0) {

@@ -237,10 +237,9 @@ int ppmoe_expert_fc1_fwd(int dtype, const void* Xs, const void* up, const void* 
 int ppmoe_expert_fc2_fwd(int dtype, const void* Act, const void* down, const void* bias_down, const int* seg, int El,
                          int H, int F, int rows_cap, const int* row_lo, const int* row_hi, const int* tok_local,
                          const float* w_local, int weight_scaling, float dropout_p, unsigned long long seed,
-                         void* Y, float* out_acc, void* stream) {
+                         void* Y, void* Y2, float* out_acc, void* stream) {
   if (int rc = check_common(dtype, El, H, F, rows_cap)) return rc;
   PPMOE_REQUIRE((row_lo == nullptr) == (row_hi == nullptr), "row_lo and row_hi must both be given or both be NULL");
-  PPMOE_REQUIRE(dropout_p >= 0.f && dropout_p < 1.f, "dropout probability must be in [0, 1), got %g", dropout_p);
   PPMOE_REQUIRE(dropout_p >= 0.f && dropout_p < 1.f, "dropout probability must be in [0, 1), got %g", dropout_p);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   LongKScope long_k(F);
@@ -252,12 +251,12 @@ int ppmoe_expert_fc2_fwd(int dtype, const void* Act, const void* down, const voi
     CUtensorMap ta, tb;
     if (int rc = tmap_kmajor(&ta, Act, F, rows_cap, kBM)) return rc;
     if (int rc = tmap_mnmajor(&tb, down, H, static_cast<uint64_t>(El) * F)) return rc;
-    EpiFc2Fwd<bf16> epi{static_cast<bf16*>(Y), static_cast<const bf16*>(bias_down), H, seg, tok_local, w_local,
-                        weight_scaling, out_acc, stream_stores(), dropout_p, seed};
+    EpiFc2Fwd<bf16> epi{static_cast<bf16*>(Y), static_cast<bf16*>(Y2), static_cast<const bf16*>(bias_down), H, seg,
+                        tok_local, w_local, weight_scaling, out_acc, stream_stores(), dropout_p, seed};
     return launch_tc<false, true>(ta, tb, geo, epi, s);
   }
-  EpiFc2Fwd<float> epi{static_cast<float*>(Y), static_cast<const float*>(bias_down), H, seg, tok_local, w_local,
-                       weight_scaling, out_acc, 0, dropout_p, seed};
+  EpiFc2Fwd<float> epi{static_cast<float*>(Y), static_cast<float*>(Y2), static_cast<const float*>(bias_down), H, seg,
+                       tok_local, w_local, weight_scaling, out_acc, 0, dropout_p, seed};
   return launch_simt<float, false, true>(static_cast<const float*>(Act), F, static_cast<const float*>(down), H, geo,
                                          rows_cap, epi, s);
 }

@@ -1,0 +1,307 @@
+// PPMoE tensor-parallel exchange over NVLink / NVSwitch peer memory.
+//
+// The reference sums the T ranks' [N x H] partial outputs with one all-reduce per pass
+// (reduce_from_tensor_parallel_region, moe.py:307; dX in tp_region backward,
+// collectives.py:205-228).  Those partials are sparse by token: token t has at most k
+// nonzero contributions, each produced by the rank owning the pair's expert.  So instead
+// of a generic all-reduce this file implements the exchange as
+//   1. barrier (every rank's expert rows are final),
+//   2. owner gather: rank r owns tokens [r N/T, (r+1) N/T) and sums, in slot order, the k
+//      expert rows of each owned token straight out of the peers' memory (P2P loads),
+//   3. barrier, then every rank pulls the other owners' finished rows (all-gather).
+// Deterministic (slot order, no atomics), no fp32 [N x H] accumulator, and the bytes on
+// NVLink are k/T-sparse reads plus one all-gather instead of a dense all-reduce.
+//
+// Peer buffers come from cudaIpc handles exchanged by the host (paper_2304_11414_b200/
+// nvlink.py).  Barriers are flag writes with release/acquire at system scope into a
+// signal pad on every peer, with a bounded spin (a stuck peer reports an error instead
+// of hanging the GPU).
+#include <algorithm>
+#include <cstring>
+
+#include "../../include/ppmoe_capi.h"
+#include "common.cuh"
+#include "host.h"
+
+namespace ppmoe {
+
+constexpr int kNvlMaxRanks = 8;
+constexpr int kNvlChannels = 8;
+
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// pads[q] = rank q's signal pad ([kNvlChannels][kNvlMaxRanks] uint32, mapped here).
+__global__ void nvl_barrier_kernel(uint32_t* const* __restrict__ pads, int T, int rank, int ch, uint32_t epoch,
+                                   int* __restrict__ err, long long timeout_cycles) {
+  const int q = threadIdx.x;
+  if (q < T) {
+    __threadfence_system();  // everything this GPU wrote before the barrier is visible to peers
+    st_release_sys(pads[q] + ch * kNvlMaxRanks + rank, epoch);
+    const uint32_t* mine = pads[rank] + ch * kNvlMaxRanks + q;
+    const long long t0 = clock64();
+    while (static_cast<int>(ld_acquire_sys(mine) - epoch) < 0) {
+      if (clock64() - t0 > timeout_cycles) {
+        atomicExch(err, 1);
+        break;
+      }
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void acc_bf16x8(float (&acc)[8], const uint4& u, float s) {
+  const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 f = __bfloat1622float2(hv[i]);
+    acc[2 * i] = fmaf(s, f.x, acc[2 * i]);
+    acc[2 * i + 1] = fmaf(s, f.y, acc[2 * i + 1]);
+  }
+}
+
+__device__ __forceinline__ uint4 pack_bf16x8(const float (&a)[8]) {
+  uint4 r;
+  r.x = pack_bf16x2(a[0], a[1]);
+  r.y = pack_bf16x2(a[2], a[3]);
+  r.z = pack_bf16x2(a[4], a[5]);
+  r.w = pack_bf16x2(a[6], a[7]);
+  return r;
+}
+
+// Owner gather.  rows[q] = rank q's expert-row buffer (Y forward, dX_s backward), local
+// row = sorted position - seg[q*El].  Owned tokens [t0, t1), processed in tiles of kOgTile
+// tokens: the (source row, weight) of every (token, slot) and the gate-term dL rows are
+// resolved once per tile into shared memory, then every thread streams its 8 columns of
+// U tokens x K slots with all loads in flight before the first use.  Optional gate term
+// (backward): + dl[t - t0, :] . Wg^T, dl = this rank's summed dL rows [t1-t0 x E] fp32,
+// Wg [H x E] fp32 with the thread's 8 columns held in registers.
+constexpr int kOgTile = 32;
+
+template <int EB, int U, int KT>  // KT = k (1, 2) or 0: any k <= 8 read at run time
+__global__ void __launch_bounds__(256)
+    nvl_owner_gather_kernel(const __nv_bfloat16* const* __restrict__ rows, const int* __restrict__ seg, int El,
+                            const int* __restrict__ idx, const int* __restrict__ pair_pos,
+                            const float* __restrict__ w, int Kr, int H, int t0, int t1,
+                            const float* __restrict__ dl, const float* __restrict__ Wg, int E,
+                            __nv_bfloat16* __restrict__ out, __nv_bfloat16* __restrict__ out_sym) {
+  constexpr int KS = KT > 0 ? KT : 8;
+  const int K = KT > 0 ? KT : Kr;
+  __shared__ const __nv_bfloat16* src[kOgTile][KS];
+  __shared__ float sw[kOgTile][KS];
+  __shared__ float sdl[kOgTile][EB > 0 ? EB : 1];
+  const int j = (blockIdx.y * blockDim.x + threadIdx.x) * 8;
+  const bool active = j < H;
+  float wg[EB > 0 ? 8 : 1][EB > 0 ? EB : 1];
+  if constexpr (EB > 0) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+#pragma unroll
+      for (int e = 0; e < EB; ++e) wg[c][e] = (active && e < E) ? Wg[static_cast<size_t>(j + c) * E + e] : 0.f;
+  }
+  for (int tb = t0 + blockIdx.x * kOgTile; tb < t1; tb += gridDim.x * kOgTile) {
+    const int nt = min(kOgTile, t1 - tb);
+    __syncthreads();  // previous tile's shared entries are consumed
+    for (int i = threadIdx.x; i < kOgTile * KS; i += blockDim.x) {
+      const int u = i / KS, s = i % KS;
+      const __nv_bfloat16* p_src = nullptr;
+      float ws = 0.f;
+      if (u < nt && s < K) {
+        const size_t pi = static_cast<size_t>(tb + u) * K + s;
+        const int p = pair_pos[pi];
+        if (p >= 0) {
+          const int q = idx[pi] / El;
+          p_src = rows[q] + static_cast<size_t>(p - seg[q * El]) * H;
+          ws = w ? w[pi] : 1.f;
+        }
+      }
+      src[u][s] = p_src;
+      sw[u][s] = ws;
+    }
+    if constexpr (EB > 0) {
+      for (int i = threadIdx.x; i < kOgTile * EB; i += blockDim.x) {
+        const int u = i / EB, e = i % EB;
+        sdl[u][e] = (u < nt && e < E) ? dl[static_cast<size_t>(tb - t0 + u) * E + e] : 0.f;
+      }
+    }
+    __syncthreads();
+    if (!active) continue;
+    for (int u0 = 0; u0 < nt; u0 += U) {
+      uint4 v[U][KS];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int s = 0; s < KS; ++s) {
+          const __nv_bfloat16* p = (s < K && u0 + u < nt) ? src[u0 + u][s] : nullptr;
+          v[u][s] = p ? *reinterpret_cast<const uint4*>(p + j) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (u0 + u >= nt) break;
+        float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int s = 0; s < KS; ++s)
+          if (s < K) acc_bf16x8(acc, v[u][s], sw[u0 + u][s]);
+        if constexpr (EB > 0) {
+#pragma unroll
+          for (int e = 0; e < EB; ++e) {
+            const float d = sdl[u0 + u][e];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) acc[c] = fmaf(d, wg[c][e], acc[c]);
+          }
+        }
+        const uint4 o = pack_bf16x8(acc);
+        const size_t off = static_cast<size_t>(tb + u0 + u) * H + j;
+        *reinterpret_cast<uint4*>(out + off) = o;
+        *reinterpret_cast<uint4*>(out_sym + off) = o;
+      }
+    }
+  }
+}
+
+// Sum over the T ranks (rank order) of rows [t0, t1) of a [N x C] fp32 buffer (the partial
+// gate-logit gradients dL): out [t1-t0 x C].
+__global__ void nvl_sum_rows_kernel(const float* const* __restrict__ srcs, int T, int C, int t0, int t1,
+                                    float* __restrict__ out) {
+  const size_t n = static_cast<size_t>(t1 - t0) * C;
+  const size_t base = static_cast<size_t>(t0) * C;
+  for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    float acc = 0.f;
+    for (int q = 0; q < T; ++q) acc += srcs[q][base + i];
+    out[i] = acc;
+  }
+}
+
+// All-gather (pull): out rows of every other owner's block, read from its out_sym.
+__global__ void __launch_bounds__(256)
+    nvl_pull_blocks_kernel(const __nv_bfloat16* const* __restrict__ srcs, int T, int rank, int N, int H,
+                           __nv_bfloat16* __restrict__ out) {
+  const size_t row_vecs = static_cast<size_t>(H) / 8;
+  for (int q0 = 1; q0 < T; ++q0) {
+    const int q = (rank + q0) % T;  // stagger the sources across ranks
+    const size_t lo = static_cast<size_t>(q) * N / T, hi = static_cast<size_t>(q + 1) * N / T;
+    const uint4* src = reinterpret_cast<const uint4*>(srcs[q]) + lo * row_vecs;
+    uint4* dst = reinterpret_cast<uint4*>(out) + lo * row_vecs;
+    const size_t n = (hi - lo) * row_vecs;
+    const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+    size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    for (; i + 3 * stride < n; i += 4 * stride) {
+      const uint4 a = src[i], b = src[i + stride], c = src[i + 2 * stride], d = src[i + 3 * stride];
+      dst[i] = a;
+      dst[i + stride] = b;
+      dst[i + 2 * stride] = c;
+      dst[i + 3 * stride] = d;
+    }
+    for (; i < n; i += stride) dst[i] = src[i];
+  }
+}
+
+}  // namespace ppmoe
+
+using namespace ppmoe;
+
+extern "C" {
+
+size_t ppmoe_ipc_handle_bytes(void) { return sizeof(cudaIpcMemHandle_t); }
+
+int ppmoe_ipc_alloc(size_t bytes, void** ptr, void* handle) {
+  PPMOE_REQUIRE(ptr && handle && bytes > 0, "bad ipc_alloc arguments");
+  PPMOE_CUDA(cudaMalloc(ptr, bytes));
+  PPMOE_CUDA(cudaMemset(*ptr, 0, bytes));
+  PPMOE_CUDA(cudaDeviceSynchronize());
+  PPMOE_CUDA(cudaIpcGetMemHandle(static_cast<cudaIpcMemHandle_t*>(handle), *ptr));
+  return kOk;
+}
+
+int ppmoe_ipc_open(const void* handle, void** ptr) {
+  PPMOE_REQUIRE(ptr && handle, "bad ipc_open arguments");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  PPMOE_CUDA(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return kOk;
+}
+
+int ppmoe_ipc_close(void* ptr) {
+  PPMOE_CUDA(cudaIpcCloseMemHandle(ptr));
+  return kOk;
+}
+
+int ppmoe_ipc_free(void* ptr) {
+  PPMOE_CUDA(cudaFree(ptr));
+  return kOk;
+}
+
+size_t ppmoe_nvl_pad_bytes(void) { return sizeof(uint32_t) * kNvlChannels * kNvlMaxRanks; }
+
+int ppmoe_nvl_barrier(void* const* pads, int T, int rank, int ch, unsigned int epoch, int* err,
+                      long long timeout_cycles, void* stream) {
+  PPMOE_REQUIRE(T >= 1 && T <= kNvlMaxRanks && rank >= 0 && rank < T, "bad barrier group T=%d rank=%d", T, rank);
+  PPMOE_REQUIRE(ch >= 0 && ch < kNvlChannels, "barrier channel %d out of range", ch);
+  nvl_barrier_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<uint32_t* const*>(pads), T, rank, ch, static_cast<uint32_t>(epoch), err, timeout_cycles);
+  return check_launch("nvl_barrier_kernel");
+}
+
+int ppmoe_nvl_owner_gather(const void* const* rows, const int* seg, int El, const int* idx, const int* pair_pos,
+                           const float* w, int N, int K, int H, int T, int rank, const float* dl, const float* Wg,
+                           int E, void* out, void* out_sym, void* stream) {
+  PPMOE_REQUIRE(T >= 1 && T <= kNvlMaxRanks && rank >= 0 && rank < T, "bad group T=%d rank=%d", T, rank);
+  PPMOE_REQUIRE(K >= 1 && K <= 8 && H % 8 == 0 && El >= 1, "owner gather needs 1 <= k <= 8 and hidden %% 8 == 0");
+  PPMOE_REQUIRE(!dl || (Wg && E >= 1 && E <= 16), "the gate term supports 1 <= E <= 16");
+  const int t0 = static_cast<int>(static_cast<long long>(rank) * N / T);
+  const int t1 = static_cast<int>(static_cast<long long>(rank + 1) * N / T);
+  if (t1 <= t0) return kOk;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int gy = (H / 8 + 255) / 256;
+  const int tiles = (t1 - t0 + kOgTile - 1) / kOgTile;
+  dim3 grid(max(1, min(tiles, num_sms() * 3 / gy)), gy);
+  auto R = reinterpret_cast<const __nv_bfloat16* const*>(rows);
+  auto O = static_cast<__nv_bfloat16*>(out);
+  auto OS = static_cast<__nv_bfloat16*>(out_sym);
+#define PPMOE_OG(EB, U, KT)                                                                                 \
+  nvl_owner_gather_kernel<EB, U, KT><<<grid, 256, 0, s>>>(R, seg, El, idx, pair_pos, w, K, H, t0, t1, dl, Wg, E, O, \
+                                                          OS)
+  if (!dl) {
+    if (K == 2) PPMOE_OG(0, 4, 2);
+    else if (K == 1) PPMOE_OG(0, 8, 1);
+    else PPMOE_OG(0, 1, 0);
+  } else if (E <= 8) {
+    if (K == 2) PPMOE_OG(8, 2, 2);
+    else if (K == 1) PPMOE_OG(8, 4, 1);
+    else PPMOE_OG(8, 1, 0);
+  } else {
+    PPMOE_OG(16, 1, 0);
+  }
+#undef PPMOE_OG
+  return check_launch("nvl_owner_gather_kernel");
+}
+
+int ppmoe_nvl_sum_rows(const void* const* srcs, int T, int rank, int N, int C, float* out, void* stream) {
+  PPMOE_REQUIRE(T >= 1 && T <= kNvlMaxRanks && rank >= 0 && rank < T && C >= 1, "bad sum_rows arguments");
+  const int t0 = static_cast<int>(static_cast<long long>(rank) * N / T);
+  const int t1 = static_cast<int>(static_cast<long long>(rank + 1) * N / T);
+  if (t1 <= t0) return kOk;
+  const size_t n = static_cast<size_t>(t1 - t0) * C;
+  const int grid = static_cast<int>(std::min<size_t>((n + 255) / 256, static_cast<size_t>(num_sms()) * 4));
+  nvl_sum_rows_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const float* const*>(srcs), T, C, t0, t1, out);
+  return check_launch("nvl_sum_rows_kernel");
+}
+
+int ppmoe_nvl_pull_blocks(const void* const* srcs, int T, int rank, int N, int H, void* out, void* stream) {
+  PPMOE_REQUIRE(T >= 1 && T <= kNvlMaxRanks && rank >= 0 && rank < T, "bad group T=%d rank=%d", T, rank);
+  PPMOE_REQUIRE(H % 8 == 0, "pull needs hidden %% 8 == 0");
+  if (T == 1 || N == 0) return kOk;
+  nvl_pull_blocks_kernel<<<num_sms() * 4, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const __nv_bfloat16* const*>(srcs), T, rank, N, H, static_cast<__nv_bfloat16*>(out));
+  return check_launch("nvl_pull_blocks_kernel");
+}
+
+}  // extern "C"

@@ -22,7 +22,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-from . import _ops
+from . import _ops, nvlink
 from .collectives import EP, ProcessGroup, World
 from .rng import Rng
 
@@ -462,6 +462,17 @@ class _PPMoEFunction(torch.autograd.Function):
                 if wk is not None:
                     wk.wait()
             del out_acc
+        elif nvlink.enabled(spec.world, spec.group, hidden.dtype, h):
+            # fc2 also mirrors Y into peer-visible memory; every rank sums its owned tokens'
+            # expert rows straight from the peers and the owners' blocks are all-gathered
+            # (replaces reduce_from_tensor_parallel_region's all-reduce, moe.py:307)
+            ar = nvlink.arena(spec.world, spec.group)
+            ym = ar.tensor("y", (_ops.local_rows_cap(n, spec.k, spec.el, cap), h), hidden.dtype)
+            st = _ops.experts_forward(hidden, pl, spec.e0, spec.el, up, down, bias_up, bias_down, spec.k,
+                                      spec.weight_scaling, None, drop_p=spec.dropout_p, seed=spec.seed, y_mirror=ym)
+            out = nvlink.exchange(ar, "y", pl.seg, spec.el, rt.idx, pl.pair_pos,
+                                  rt.w if spec.weight_scaling else None, n, h, torch.empty_like(hidden))
+            spec.world.charge_all_reduce(spec.group, out.numel())
         elif _ops.gather_combine():
             # fc2 stores Y; the combine gathers each token's local pairs (no fp32 accumulator)
             st = _ops.experts_forward(hidden, pl, spec.e0, spec.el, up, down, bias_up, bias_down, spec.k,
@@ -492,6 +503,40 @@ class _PPMoEFunction(torch.autograd.Function):
         if spec.aux_here and g_aux is not None:
             aux = g_aux.detach().to(torch.float32).reshape(1).contiguous()
         # data gradients first: dX can go on the wire while the weight gradients compute.
+        need_dx = ctx.needs_input_grad[0]
+        need_dwg = ctx.needs_input_grad[1]
+        if nvlink.enabled(spec.world, spec.group, hidden.dtype, h) and need_dx:
+            # per-row dX and dL into peer-visible memory; owners gather them (+ the gate term)
+            # and the blocks are all-gathered (replaces tp_region's dX all-reduce)
+            ar = nvlink.arena(spec.world, spec.group)
+            dxs = ar.tensor("dxs", (st.rows_cap, h), hidden.dtype)
+            dy, dh, dw, parts = _ops.experts_backward_data(g_out, st, up, down, spec.weight_scaling, None, has_bias,
+                                                           dxs)
+            e = wg.shape[1]
+            _ops.gate_backward(rt, pl, st, dw, aux, out=ar.tensor("dl", (n, e), torch.float32))
+            t0, t1 = nvlink.owned_range(ar, n)
+            dx = torch.empty_like(hidden)
+            dwg = torch.empty((h, e), dtype=torch.float32, device=hidden.device) if need_dwg else None
+            main = torch.cuda.current_stream()
+            side = ar.stream
+            side.wait_stream(main)
+            for t in (dx, dwg, hidden, wg, dy, dh):
+                if t is not None:
+                    t.record_stream(side)
+            with torch.cuda.stream(side):
+                # the exchange runs beside the weight-gradient GEMMs (their SM budget leaves room)
+                ar.barrier(0)  # every rank's dX rows and dL partials are published
+                dl_own = nvlink.sum_owned_rows(ar, "dl", n, e)
+                if need_dwg:  # dWg over the owned tokens; sync_gate_gradients sums the ranks' shares
+                    _ops.gate_weight_grad(hidden[t0:t1], dl_own, wg, out=dwg)
+                nvlink.exchange(ar, "dxs", pl.seg, spec.el, rt.idx, pl.pair_pos, None, n, h, dx, dl_own, wg,
+                                barrier_first=False)
+            spec.world.charge_all_reduce(spec.group, dx.numel())
+            with _ops.sm_budget(_ops.overlap_sm_budget()):
+                d_up, d_down, d_bu, d_bd = _ops.experts_backward_weights(st, dy, dh, up, down, has_bias, parts)
+            main.wait_stream(side)
+            ctx.state = None
+            return dx, dwg, d_up, d_down, d_bu, d_bd, None
         # fc1 dgrad stores per-row dX; gate_grads gathers them per token (no fp32 scatter)
         if _ops.gather_combine():
             dx_acc, dxs = None, _ops._act((st.rows_cap, h), hidden.dtype, hidden.device)
@@ -499,8 +544,6 @@ class _PPMoEFunction(torch.autograd.Function):
             dx_acc, dxs = torch.zeros((n, h), dtype=torch.float32, device=hidden.device), None
         dy, dh, dw, parts = _ops.experts_backward_data(g_out, st, up, down, spec.weight_scaling, dx_acc, has_bias, dxs)
         dl = _ops.gate_backward(rt, pl, st, dw, aux)
-        need_dx = ctx.needs_input_grad[0]
-        need_dwg = ctx.needs_input_grad[1]
         if dxs is not None:
             dx, dwg = _ops.input_grads(dxs, st, pl, hidden, dl, wg, need_dx, need_dwg)
         else:

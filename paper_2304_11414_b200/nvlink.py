@@ -1,0 +1,180 @@
+"""Peer-memory arena of a tensor-parallel group: the NVLink exchange of the PPMoE layer.
+
+``NvlArena`` owns, per (World, ProcessGroup), a set of device buffers that every rank
+of the group can address directly (CUDA IPC handles exchanged once through
+torch.distributed), a signal pad per rank for the cross-GPU barriers, and the epoch
+counters of those barriers.  The kernels that use it live in csrc/nvlink.cu
+(ppmoe_nvl_barrier / ppmoe_nvl_owner_gather / ppmoe_nvl_pull_blocks); moe.py calls
+``exchange_forward`` / ``exchange_backward`` in place of the two [N x H] all-reduces of
+the reference (moe.py:307, collectives.py:205-228).
+
+Buffers are allocated collectively: every rank requests the same names and sizes in the
+same order (the sizes are functions of the layer shape only), so the arenas stay in
+lock-step.  A buffer grows by re-allocation when a larger shape arrives.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from ._lib import ptr
+from ._ops import call  # event-timed under _ops.KernelProfile
+
+_ARENAS: dict = {}
+# ~2 s at 2 GHz: a barrier that waits longer reports an error instead of hanging the GPU
+_TIMEOUT_CYCLES = int(os.environ.get("PPMOE_NVL_TIMEOUT_CYCLES", str(4_000_000_000)))
+
+
+class _CudaArray:
+    """__cuda_array_interface__ view of a raw device pointer (wrapped by torch.as_tensor)."""
+
+    def __init__(self, p: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (p, False),
+                                         "version": 3, "strides": None, "stream": None}
+
+
+def _wrap(p: int, shape, dtype: torch.dtype, device) -> torch.Tensor:
+    if dtype == torch.bfloat16:
+        t = torch.as_tensor(_CudaArray(p, shape, "<i2"), device=device)
+        return t.view(torch.bfloat16)
+    typestr = {torch.float32: "<f4", torch.int32: "<i4", torch.uint8: "|u1"}[dtype]
+    return torch.as_tensor(_CudaArray(p, shape, typestr), device=device)
+
+
+class _PeerBuffer:
+    def __init__(self, arena: "NvlArena", nbytes: int):
+        lib = _lib.load()
+        hsize = lib.ppmoe_ipc_handle_bytes()
+        local = ctypes.c_void_p()
+        handle = ctypes.create_string_buffer(hsize)
+        _lib.call("ppmoe_ipc_alloc", nbytes, ctypes.byref(local), handle)
+        handles = [None] * arena.tp
+        dist.all_gather_object(handles, handle.raw, group=arena.torch_group)
+        self.local = local.value
+        self.nbytes = nbytes
+        self.opened = []
+        ptrs = []
+        for q, hb in enumerate(handles):
+            if q == arena.rank:
+                ptrs.append(self.local)
+                continue
+            peer = ctypes.c_void_p()
+            _lib.call("ppmoe_ipc_open", ctypes.create_string_buffer(hb, hsize), ctypes.byref(peer))
+            self.opened.append(peer.value)
+            ptrs.append(peer.value)
+        self.ptrs = ptrs
+        self.table = torch.tensor(ptrs, dtype=torch.int64, device=arena.device)  # device array of T pointers
+
+    def release(self):
+        for p in self.opened:
+            _lib.call("ppmoe_ipc_close", ctypes.c_void_p(p))
+        _lib.call("ppmoe_ipc_free", ctypes.c_void_p(self.local))
+        self.opened = []
+
+
+class NvlArena:
+    """Peer buffers, signal pads and barrier epochs of one tensor-parallel group."""
+
+    def __init__(self, world, group):
+        if not world.distributed:
+            raise RuntimeError("the NVLink arena needs a distributed world (one process per GPU)")
+        self.world, self.group = world, group
+        self.tp = group.size
+        self.rank = world.rank_in(group)
+        self.device = torch.device("cuda", torch.cuda.current_device())
+        self.torch_group = world.torch_group(group)
+        lib = _lib.load()
+        self.pads = _PeerBuffer(self, lib.ppmoe_nvl_pad_bytes())
+        self.err = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.epoch = [0] * 8
+        self.bufs: dict = {}
+        self.stream = torch.cuda.Stream(device=self.device)  # exchange beside the weight-gradient GEMMs
+
+    # ------------------------------------------------------------------ buffers
+
+    def buffer(self, name: str, nbytes: int) -> _PeerBuffer:
+        b = self.bufs.get(name)
+        if b is None or b.nbytes < nbytes:
+            if b is not None:
+                torch.cuda.synchronize()
+                dist.barrier(group=self.torch_group)  # no peer still reads the old buffer
+                b.release()
+            b = _PeerBuffer(self, nbytes)
+            self.bufs[name] = b
+        return b
+
+    def tensor(self, name: str, shape, dtype: torch.dtype) -> torch.Tensor:
+        n = 1
+        for s in shape:
+            n *= s
+        nbytes = max(n * torch.empty((), dtype=dtype).element_size(), 16)
+        return _wrap(self.buffer(name, nbytes).local, shape, dtype, self.device)
+
+    def table(self, name: str) -> torch.Tensor:
+        return self.bufs[name].table
+
+    # ------------------------------------------------------------------ sync
+
+    def barrier(self, ch: int) -> None:
+        self.epoch[ch] = (self.epoch[ch] + 1) & 0xFFFFFFFF
+        call("ppmoe_nvl_barrier", ptr(self.pads.table), self.tp, self.rank, ch, self.epoch[ch], ptr(self.err),
+             _TIMEOUT_CYCLES, _lib.stream_ptr())
+
+    def check(self) -> None:
+        """Raise if any barrier of this arena timed out (synchronises the device)."""
+        if int(self.err.item()) != 0:
+            raise RuntimeError("NVLink barrier timed out: a peer of the tensor group stopped responding")
+
+
+def arena(world, group) -> NvlArena:
+    key = (id(world), group.members)
+    a = _ARENAS.get(key)
+    if a is None:
+        a = NvlArena(world, group)
+        _ARENAS[key] = a
+    return a
+
+
+def enabled(world, group, dtype: torch.dtype, hidden: int) -> bool:
+    """NVLink exchange for distributed bf16 groups of 2..8 ranks (PPMOE_TP_COMM=nccl opts out)."""
+    if os.environ.get("PPMOE_TP_COMM", "nvl") != "nvl":
+        return False
+    return (world.distributed and 1 < group.size <= 8 and dtype == torch.bfloat16 and hidden % 8 == 0)
+
+
+def owned_range(ar: NvlArena, n: int) -> tuple[int, int]:
+    """Tokens [t0, t1) this rank owns in the exchange (contiguous blocks in rank order)."""
+    return ar.rank * n // ar.tp, (ar.rank + 1) * n // ar.tp
+
+
+def sum_owned_rows(ar: NvlArena, name: str, n: int, c: int) -> torch.Tensor:
+    """Sum over the group (rank order) of this rank's owned rows of the fp32 [n x c] peer
+    buffer `name`; call after a barrier that published it."""
+    t0, t1 = owned_range(ar, n)
+    out = torch.empty((t1 - t0, c), dtype=torch.float32, device=ar.device)
+    call("ppmoe_nvl_sum_rows", ptr(ar.table(name)), ar.tp, ar.rank, n, c, ptr(out), _lib.stream_ptr())
+    return out
+
+
+def exchange(ar: NvlArena, rows_name: str, seg, el: int, idx, pair_pos, w, n: int, h: int, out: torch.Tensor,
+             dl_own: torch.Tensor | None = None, wg: torch.Tensor | None = None,
+             barrier_first: bool = True) -> torch.Tensor:
+    """out = the replicated sum over the group of every token's expert rows (+ the gate term
+    dl_own . Wg^T of the owned rows), see nvlink.cu: barrier -> owner gather (P2P reads) ->
+    barrier -> pull the other owners' blocks."""
+    k = pair_pos.shape[1]
+    xch = ar.tensor("xch", (n, h), torch.bfloat16)
+    s = _lib.stream_ptr()
+    if barrier_first:
+        ar.barrier(0)
+    e = wg.shape[1] if wg is not None else 0
+    call("ppmoe_nvl_owner_gather", ptr(ar.table(rows_name)), ptr(seg), el, ptr(idx), ptr(pair_pos), ptr(w), n, k, h,
+         ar.tp, ar.rank, ptr(dl_own), ptr(wg), e, ptr(out), ptr(xch), s)
+    ar.barrier(1)
+    call("ppmoe_nvl_pull_blocks", ptr(ar.table("xch")), ar.tp, ar.rank, n, h, ptr(out), s)
+    return out
