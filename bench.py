@@ -83,72 +83,55 @@ def config_of(a, n_gpus):
 
 class ClockSampler:
     """SM clock / throttle-reason sampling during the timed region (B200_PROFILING.md clocks
-    line): NVML every 10 ms from a thread (nvidia-smi -lms as the fallback)."""
+    line).  One `nvidia-smi -lms` process started by rank 0 samples every GPU of the job:
+    in-process NVML polling on every rank stalled the CUDA launch path often enough to
+    skew the barrier-coupled ranks."""
 
-    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap"}
+    FIELDS = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
-    def __init__(self, index: int, period_s: float = 0.01):
-        self.index = index
-        self.period = period_s
+    def __init__(self, indices, period_ms: int = 50, active: bool = True):
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        if vis:  # local ordinals -> the ids nvidia-smi knows (ints or UUIDs)
+            ids = [v.strip() for v in vis.split(",") if v.strip()]
+            indices = [ids[i] if i < len(ids) else str(i) for i in indices]
+        self.indices = list(indices)
+        self.period = period_ms
+        self.active = active and os.environ.get("PPMOE_CLOCKS", "smi") != "off"
         self.sm, self.smax, self.reasons = [], [], set()
-        self.stop = threading.Event()
-        self.thread = None
         self.proc = None
+        self.thread = None
 
-    def _nvml_handle(self):
-        import pynvml
-        import torch
-
-        pynvml.nvmlInit()
-        p = torch.cuda.get_device_properties(self.index)
-        bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
-        return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode())
-
-    def _nvml_loop(self, nv, hd):
-        while True:
-            try:
-                self.sm.append(float(nv.nvmlDeviceGetClockInfo(hd, nv.NVML_CLOCK_SM)))
-                self.smax.append(float(nv.nvmlDeviceGetMaxClockInfo(hd, nv.NVML_CLOCK_SM)))
-                bits = nv.nvmlDeviceGetCurrentClocksEventReasons(hd)
-                self.reasons.update(nm for b, nm in self.REASONS.items() if bits & b)
-            except Exception:
-                pass
-            if self.stop.wait(self.period):
-                return
-
-    def _smi_read(self):
+    def _read(self):
         for line in self.proc.stdout:
             parts = [x.strip() for x in line.split(",")]
             try:
-                self.sm.append(float(parts[0]))
-                self.smax.append(float(parts[1]))
+                self.sm.append(float(parts[1]))
+                self.smax.append(float(parts[2]))
             except (ValueError, IndexError):
                 continue
-            for nm, v in zip(["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"], parts[3:7]):
+            for nm, v in zip(self.NAMES, parts[3:7]):
                 if v.lower().startswith("active"):
                     self.reasons.add(nm)
 
     def __enter__(self):
+        if not self.active:
+            return self
         try:
-            nv, hd = self._nvml_handle()
-            self.thread = threading.Thread(target=self._nvml_loop, args=(nv, hd), daemon=True)
-        except Exception:
-            fields = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-                      "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-                      "clocks_event_reasons.sw_power_cap")
-            try:
-                self.proc = subprocess.Popen(
-                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={fields}", "--format=csv,noheader,nounits",
-                     "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-                self.thread = threading.Thread(target=self._smi_read, daemon=True)
-            except OSError:
-                self.thread = None
-        if self.thread is not None:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", ",".join(str(i) for i in self.indices), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", str(self.period)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            time.sleep(0.3)  # first sample lands before the timed region starts
+        except OSError:
+            self.proc = None
         return self
 
     def __exit__(self, *exc):
-        self.stop.set()
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -163,7 +146,7 @@ class ClockSampler:
         if not self.sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": max(self.smax), "reasons": sorted(self.reasons),
-                "samples": len(self.sm), "sm_mhz_min": min(self.sm)}
+                "samples": len(self.sm), "sm_mhz_min": min(self.sm), "gpus": len(self.indices)}
 
 
 # ----------------------------------------------------------------------------- CPU baseline
@@ -312,7 +295,7 @@ def main():
     lib = _lib.load()
     launches0 = lib.ppmoe_kernel_launches()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local_rank) as clk, _ops.KernelProfile() as prof:
+    with ClockSampler(range(world_size), active=(rank == 0)) as clk, _ops.KernelProfile() as prof:
         barrier()
         ev0.record()
         for _ in range(a.steps):

@@ -90,7 +90,8 @@ __global__ void __launch_bounds__(256)
                             const int* __restrict__ idx, const int* __restrict__ pair_pos,
                             const float* __restrict__ w, int Kr, int H, int t0, int t1,
                             const float* __restrict__ dl, const float* __restrict__ Wg, int E,
-                            __nv_bfloat16* __restrict__ out, __nv_bfloat16* __restrict__ out_sym) {
+                            __nv_bfloat16* __restrict__ out, __nv_bfloat16* __restrict__ out_sym,
+                            __nv_bfloat16* const* __restrict__ push, int T) {
   constexpr int KS = KT > 0 ? KT : 8;
   const int K = KT > 0 ? KT : Kr;
   __shared__ const __nv_bfloat16* src[kOgTile][KS];
@@ -159,7 +160,11 @@ __global__ void __launch_bounds__(256)
         const uint4 o = pack_bf16x8(acc);
         const size_t off = static_cast<size_t>(tb + u0 + u) * H + j;
         *reinterpret_cast<uint4*>(out + off) = o;
-        *reinterpret_cast<uint4*>(out_sym + off) = o;
+        if (push) {  // the owned row straight into every rank's exchange buffer (P2P stores)
+          for (int q = 0; q < T; ++q) *reinterpret_cast<uint4*>(push[q] + off) = o;
+        } else {
+          *reinterpret_cast<uint4*>(out_sym + off) = o;
+        }
       }
     }
   }
@@ -251,7 +256,7 @@ int ppmoe_nvl_barrier(void* const* pads, int T, int rank, int ch, unsigned int e
 
 int ppmoe_nvl_owner_gather(const void* const* rows, const int* seg, int El, const int* idx, const int* pair_pos,
                            const float* w, int N, int K, int H, int T, int rank, const float* dl, const float* Wg,
-                           int E, void* out, void* out_sym, void* stream) {
+                           int E, void* out, void* out_sym, void* const* push, void* stream) {
   PPMOE_REQUIRE(T >= 1 && T <= kNvlMaxRanks && rank >= 0 && rank < T, "bad group T=%d rank=%d", T, rank);
   PPMOE_REQUIRE(K >= 1 && K <= 8 && H % 8 == 0 && El >= 1, "owner gather needs 1 <= k <= 8 and hidden %% 8 == 0");
   PPMOE_REQUIRE(!dl || (Wg && E >= 1 && E <= 16), "the gate term supports 1 <= E <= 16");
@@ -265,9 +270,10 @@ int ppmoe_nvl_owner_gather(const void* const* rows, const int* seg, int El, cons
   auto R = reinterpret_cast<const __nv_bfloat16* const*>(rows);
   auto O = static_cast<__nv_bfloat16*>(out);
   auto OS = static_cast<__nv_bfloat16*>(out_sym);
+  auto P = reinterpret_cast<__nv_bfloat16* const*>(push);
 #define PPMOE_OG(EB, U, KT)                                                                                 \
   nvl_owner_gather_kernel<EB, U, KT><<<grid, 256, 0, s>>>(R, seg, El, idx, pair_pos, w, K, H, t0, t1, dl, Wg, E, O, \
-                                                          OS)
+                                                          OS, P, T)
   if (!dl) {
     if (K == 2) PPMOE_OG(0, 4, 2);
     else if (K == 1) PPMOE_OG(0, 8, 1);

@@ -518,11 +518,10 @@ class _PPMoEFunction(torch.autograd.Function):
             dx = torch.empty_like(hidden)
             dwg = torch.empty((h, e), dtype=torch.float32, device=hidden.device) if need_dwg else None
             main = torch.cuda.current_stream()
-            side = ar.stream
+            side = ar.stream if os.environ.get("PPMOE_NVL_OVERLAP", "1") == "1" else main
             side.wait_stream(main)
-            for t in (dx, dwg, hidden, wg, dy, dh):
-                if t is not None:
-                    t.record_stream(side)
+            # no record_stream: every tensor the side stream touches outlives the
+            # main.wait_stream(side) below (inputs are saved tensors, outputs are returned)
             with torch.cuda.stream(side):
                 # the exchange runs beside the weight-gradient GEMMs (their SM budget leaves room)
                 ar.barrier(0)  # every rank's dX rows and dL partials are published

@@ -118,6 +118,13 @@ class NvlArena:
     def table(self, name: str) -> torch.Tensor:
         return self.bufs[name].table
 
+    def local_table(self, name: str) -> torch.Tensor:
+        """A T-entry pointer table that names this rank's own copy of `name` T times."""
+        b = self.bufs[name]
+        if getattr(b, "local_tab", None) is None:
+            b.local_tab = torch.tensor([b.local] * self.tp, dtype=torch.int64, device=self.device)
+        return b.local_tab
+
     # ------------------------------------------------------------------ sync
 
     def barrier(self, ch: int) -> None:
@@ -173,8 +180,11 @@ def exchange(ar: NvlArena, rows_name: str, seg, el: int, idx, pair_pos, w, n: in
     if barrier_first:
         ar.barrier(0)
     e = wg.shape[1] if wg is not None else 0
+    push = os.environ.get("PPMOE_NVL_PUSH", "0") == "1"
     call("ppmoe_nvl_owner_gather", ptr(ar.table(rows_name)), ptr(seg), el, ptr(idx), ptr(pair_pos), ptr(w), n, k, h,
-         ar.tp, ar.rank, ptr(dl_own), ptr(wg), e, ptr(out), ptr(xch), s)
+         ar.tp, ar.rank, ptr(dl_own), ptr(wg), e, ptr(out), ptr(xch), ptr(ar.table("xch")) if push else None, s)
     ar.barrier(1)
-    call("ppmoe_nvl_pull_blocks", ptr(ar.table("xch")), ar.tp, ar.rank, n, h, ptr(out), s)
+    # push: every block already sits in the local exchange buffer; pull: read the owners'
+    src = ar.local_table("xch") if push else ar.table("xch")
+    call("ppmoe_nvl_pull_blocks", ptr(src), ar.tp, ar.rank, n, h, ptr(out), s)
     return out
