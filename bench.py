@@ -347,12 +347,15 @@ def main():
     e2e = None
     if not a.no_e2e:
         x_host = torch.randn(n, h, generator=torch.Generator().manual_seed(1234)).to(torch.bfloat16).pin_memory()
-        loss_host = torch.empty(1, dtype=torch.float32).pin_memory()
+        loss_host = [torch.empty(1, dtype=torch.float32).pin_memory() for _ in range(2)]
+        loss_ev = [torch.cuda.Event() for _ in range(2)]
         # each rank copies its 1/T row slice over PCIe, NCCL all_gather replicates it; the next
-        # batch's copy overlaps this batch's compute (P.ReplicatedFeed)
+        # batch's copy overlaps this batch's compute (P.ReplicatedFeed).  Step i's loss is read
+        # on the host while step i+1 is already queued, so the device never idles on the host.
         feed = P.ReplicatedFeed(world, group, (n, h), torch.bfloat16, dev)
 
         def e2e_run(steps):
+            losses = []
             feed.submit(x_host)
             for i in range(steps):
                 xin = feed.take().detach().requires_grad_()
@@ -360,9 +363,14 @@ def main():
                     feed.submit(x_host)
                 out, l_aux = step(xin)
                 loss = out.float().sum() + l_aux
-                loss_host.copy_(loss.detach().reshape(1), non_blocking=True)
-                torch.cuda.current_stream().synchronize()
-                float(loss_host[0])
+                loss_host[i % 2].copy_(loss.detach().reshape(1), non_blocking=True)
+                loss_ev[i % 2].record()
+                if i > 0:
+                    loss_ev[(i - 1) % 2].synchronize()
+                    losses.append(float(loss_host[(i - 1) % 2][0]))
+            loss_ev[(steps - 1) % 2].synchronize()
+            losses.append(float(loss_host[(steps - 1) % 2][0]))
+            return losses
 
         e2e_run(2)
         barrier()

@@ -228,8 +228,10 @@ int ppmoe_ipc_alloc(size_t bytes, void** ptr, void* handle);
 int ppmoe_ipc_open(const void* handle, void** ptr);
 int ppmoe_ipc_close(void* ptr);
 int ppmoe_ipc_free(void* ptr);
-/* Barrier of T ranks on channel ch: writes `epoch` (release, system scope) into every
- * peer's signal pad (pads = device array of T pad pointers, ppmoe_nvl_pad_bytes() each),
+/* Pointer sets (pads, rows, push, srcs) are HOST arrays of T device pointers (passed to
+ * the kernels by value; T <= 8), entry q = rank q's buffer as mapped in this process.
+ * Barrier of T ranks on channel ch: writes `epoch` (release, system scope) into every
+ * peer's signal pad (ppmoe_nvl_pad_bytes() each),
  * then waits until all T flags of this rank's pad reach `epoch`.  A spin longer than
  * timeout_cycles sets *err = 1 and returns instead of hanging.                       */
 size_t ppmoe_nvl_pad_bytes(void);
@@ -238,11 +240,12 @@ int ppmoe_nvl_barrier(void* const* pads, int T, int rank, int ch, unsigned int e
 /* Owner gather for this rank's tokens [t0, t1) = [rank*N/T, (rank+1)*N/T):
  *   out[t] = sum_s w[t,s] * rows[q][pair_pos[t,s] - seg[q*El]]   q = idx[t,s] / El
  *            (+ dl[t - t0, :] . Wg^T when dl != NULL)
- * in slot order; rows = device array of T peer row buffers (bf16 [rows x H]; Y forward,
- * per-row dX backward), dl = this rank's summed dL rows [t1-t0 x E] fp32 (from
- * ppmoe_nvl_sum_rows).  Writes the owned rows of out (local [N x H]) and either of out_sym
- * (this rank's peer-visible copy, push NULL: peers pull) or of every rank's exchange
- * buffer push[q] (device array of T pointers: P2P stores, then a local pull).            */
+ * in slot order; rows = the T ranks' row buffers (bf16 [rows x H]; Y forward, per-row dX
+ * backward), dl = this rank's summed dL rows [t1-t0 x E] fp32 (from ppmoe_nvl_sum_rows;
+ * E <= 128).  Writes the owned rows of out (local [N x H]) and either of out_sym (this
+ * rank's peer-visible copy, push NULL: peers pull; may be NULL) or of every rank's
+ * exchange buffer push[q] (P2P stores, then a local pull).  With T = 1 it is the
+ * single-GPU top-k combine / input-gradient gather.                                     */
 int ppmoe_nvl_owner_gather(const void* const* rows, const int* seg, int El, const int* idx, const int* pair_pos,
                            const float* w, int N, int K, int H, int T, int rank, const float* dl, const float* Wg,
                            int E, void* out, void* out_sym, void* const* push, void* stream);

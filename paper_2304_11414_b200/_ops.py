@@ -8,6 +8,7 @@ stays on the device (padded segments) and the GEMM tile schedulers read it.
 
 from __future__ import annotations
 
+import ctypes
 import math
 import os
 from dataclasses import dataclass
@@ -332,10 +333,29 @@ def expert_pipeline(xsrc: torch.Tensor, seg: torch.Tensor, el: int, tok_sorted: 
     return ExpertFwdState(0, el, rows_cap, seg, xs, tok_l, w_l, gelu_grad, act, y, drop_p, seed)
 
 
-def gather_combine() -> bool:
-    """Top-k combine and dX reduction as row gathers (default) or fp32 scatter-adds
-    (PPMOE_COMBINE=scatter, kept for A/B measurement)."""
-    return os.environ.get("PPMOE_COMBINE", "gather") != "scatter"
+def combine_mode(dtype: torch.dtype, hidden: int) -> str:
+    """How one rank sums its tokens' expert rows: "owner" (the owner-gather kernel of the
+    NVLink exchange with a group of one, bf16), "gather" (ppmoe_combine / ppmoe_input_grads)
+    or "scatter" (fp32 scatter-add in the GEMM epilogues).  PPMOE_COMBINE overrides."""
+    mode = os.environ.get("PPMOE_COMBINE")
+    if mode is None:
+        mode = "owner"
+    if mode == "owner" and not (dtype == torch.bfloat16 and hidden % 8 == 0):
+        mode = "gather"
+    return mode
+
+
+def local_combine(rows: torch.Tensor, st: ExpertFwdState, pl: Plan, idx: torch.Tensor, w: torch.Tensor | None,
+                  out: torch.Tensor, dl: torch.Tensor | None = None, wg: torch.Tensor | None = None) -> torch.Tensor:
+    """out[t] = sum over t's pairs (slot order) of w·rows[row] (+ dl[t]·wgᵀ): the owner-gather
+    kernel of csrc/nvlink.cu for a group of one (all experts local, e0 = 0)."""
+    n, h = out.shape
+    k = pl.pair_pos.shape[1]
+    e = wg.shape[1] if wg is not None else 0
+    rows_set = (ctypes.c_void_p * 1)(rows.data_ptr())
+    call("ppmoe_nvl_owner_gather", rows_set, ptr(pl.seg), st.el, ptr(idx), ptr(pl.pair_pos), ptr(w), n, k, h, 1, 0,
+         ptr(dl), ptr(wg), e, ptr(out), None, None, _stream())
+    return out
 
 
 def combine(rows: torch.Tensor, st: ExpertFwdState, pl: Plan, w: torch.Tensor | None, out: torch.Tensor,

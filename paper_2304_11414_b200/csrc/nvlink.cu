@@ -28,6 +28,19 @@ namespace ppmoe {
 constexpr int kNvlMaxRanks = 8;
 constexpr int kNvlChannels = 8;
 
+// The group's peer pointers travel by value in the kernel parameters (no device tables).
+template <typename T>
+struct PeerSet {
+  T* p[kNvlMaxRanks];
+};
+
+template <typename T>
+static PeerSet<T> peer_set(const void* const* host_ptrs, int n) {
+  PeerSet<T> s{};
+  for (int i = 0; i < n && host_ptrs; ++i) s.p[i] = static_cast<T*>(const_cast<void*>(host_ptrs[i]));
+  return s;
+}
+
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -37,14 +50,14 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
   return v;
 }
 
-// pads[q] = rank q's signal pad ([kNvlChannels][kNvlMaxRanks] uint32, mapped here).
-__global__ void nvl_barrier_kernel(uint32_t* const* __restrict__ pads, int T, int rank, int ch, uint32_t epoch,
+// pads.p[q] = rank q's signal pad ([kNvlChannels][kNvlMaxRanks] uint32, mapped here).
+__global__ void nvl_barrier_kernel(const __grid_constant__ PeerSet<uint32_t> pads, int T, int rank, int ch, uint32_t epoch,
                                    int* __restrict__ err, long long timeout_cycles) {
   const int q = threadIdx.x;
   if (q < T) {
     __threadfence_system();  // everything this GPU wrote before the barrier is visible to peers
-    st_release_sys(pads[q] + ch * kNvlMaxRanks + rank, epoch);
-    const uint32_t* mine = pads[rank] + ch * kNvlMaxRanks + q;
+    st_release_sys(pads.p[q] + ch * kNvlMaxRanks + rank, epoch);
+    const uint32_t* mine = pads.p[rank] + ch * kNvlMaxRanks + q;
     const long long t0 = clock64();
     while (static_cast<int>(ld_acquire_sys(mine) - epoch) < 0) {
       if (clock64() - t0 > timeout_cycles) {
@@ -75,28 +88,31 @@ __device__ __forceinline__ uint4 pack_bf16x8(const float (&a)[8]) {
   return r;
 }
 
-// Owner gather.  rows[q] = rank q's expert-row buffer (Y forward, dX_s backward), local
+// Owner gather.  rows.p[q] = rank q's expert-row buffer (Y forward, dX_s backward), local
 // row = sorted position - seg[q*El].  Owned tokens [t0, t1), processed in tiles of kOgTile
 // tokens: the (source row, weight) of every (token, slot) and the gate-term dL rows are
 // resolved once per tile into shared memory, then every thread streams its 8 columns of
 // U tokens x K slots with all loads in flight before the first use.  Optional gate term
 // (backward): + dl[t - t0, :] . Wg^T, dl = this rank's summed dL rows [t1-t0 x E] fp32,
-// Wg [H x E] fp32 with the thread's 8 columns held in registers.
+// Wg [H x E] fp32: EB > 0 holds the thread's 8 columns of Wg in registers (E <= EB);
+// EB < 0 is the any-E form that streams Wg per tile (loads amortised over U tokens).
 constexpr int kOgTile = 32;
+constexpr int kOgMaxE = 128;
 
 template <int EB, int U, int KT>  // KT = k (1, 2) or 0: any k <= 8 read at run time
 __global__ void __launch_bounds__(256)
-    nvl_owner_gather_kernel(const __nv_bfloat16* const* __restrict__ rows, const int* __restrict__ seg, int El,
+    nvl_owner_gather_kernel(const __grid_constant__ PeerSet<const __nv_bfloat16> rows, const int* __restrict__ seg, int El,
                             const int* __restrict__ idx, const int* __restrict__ pair_pos,
                             const float* __restrict__ w, int Kr, int H, int t0, int t1,
                             const float* __restrict__ dl, const float* __restrict__ Wg, int E,
                             __nv_bfloat16* __restrict__ out, __nv_bfloat16* __restrict__ out_sym,
-                            __nv_bfloat16* const* __restrict__ push, int T) {
+                            const __grid_constant__ PeerSet<__nv_bfloat16> push, int T) {
   constexpr int KS = KT > 0 ? KT : 8;
+  constexpr int DLW = EB > 0 ? EB : (EB < 0 ? kOgMaxE : 1);
   const int K = KT > 0 ? KT : Kr;
   __shared__ const __nv_bfloat16* src[kOgTile][KS];
   __shared__ float sw[kOgTile][KS];
-  __shared__ float sdl[kOgTile][EB > 0 ? EB : 1];
+  __shared__ float sdl[kOgTile][DLW];
   const int j = (blockIdx.y * blockDim.x + threadIdx.x) * 8;
   const bool active = j < H;
   float wg[EB > 0 ? 8 : 1][EB > 0 ? EB : 1];
@@ -118,17 +134,17 @@ __global__ void __launch_bounds__(256)
         const int p = pair_pos[pi];
         if (p >= 0) {
           const int q = idx[pi] / El;
-          p_src = rows[q] + static_cast<size_t>(p - seg[q * El]) * H;
+          p_src = rows.p[q] + static_cast<size_t>(p - seg[q * El]) * H;
           ws = w ? w[pi] : 1.f;
         }
       }
       src[u][s] = p_src;
       sw[u][s] = ws;
     }
-    if constexpr (EB > 0) {
-      for (int i = threadIdx.x; i < kOgTile * EB; i += blockDim.x) {
-        const int u = i / EB, e = i % EB;
-        sdl[u][e] = (u < nt && e < E) ? dl[static_cast<size_t>(tb - t0 + u) * E + e] : 0.f;
+    if constexpr (EB != 0) {
+      for (int i = threadIdx.x; i < kOgTile * E; i += blockDim.x) {
+        const int u = i / E, e = i % E;
+        sdl[u][e] = u < nt ? dl[static_cast<size_t>(tb - t0 + u) * E + e] : 0.f;
       }
     }
     __syncthreads();
@@ -142,27 +158,46 @@ __global__ void __launch_bounds__(256)
           const __nv_bfloat16* p = (s < K && u0 + u < nt) ? src[u0 + u][s] : nullptr;
           v[u][s] = p ? *reinterpret_cast<const uint4*>(p + j) : make_uint4(0, 0, 0, 0);
         }
+      float acc[U][8];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc[u][c] = 0.f;
+#pragma unroll
+        for (int s = 0; s < KS; ++s)
+          if (s < K) acc_bf16x8(acc[u], v[u][s], sw[min(u0 + u, kOgTile - 1)][s]);
+      }
+      if constexpr (EB > 0) {
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int e = 0; e < EB; ++e) {
+            const float d = sdl[min(u0 + u, kOgTile - 1)][e];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) acc[u][c] = fmaf(d, wg[c][e], acc[u][c]);
+          }
+      } else if constexpr (EB < 0) {
+        for (int e = 0; e < E; ++e) {
+          float wc[8];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) wc[c] = Wg[static_cast<size_t>(j + c) * E + e];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const float d = sdl[min(u0 + u, kOgTile - 1)][e];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) acc[u][c] = fmaf(d, wc[c], acc[u][c]);
+          }
+        }
+      }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         if (u0 + u >= nt) break;
-        float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-        for (int s = 0; s < KS; ++s)
-          if (s < K) acc_bf16x8(acc, v[u][s], sw[u0 + u][s]);
-        if constexpr (EB > 0) {
-#pragma unroll
-          for (int e = 0; e < EB; ++e) {
-            const float d = sdl[u0 + u][e];
-#pragma unroll
-            for (int c = 0; c < 8; ++c) acc[c] = fmaf(d, wg[c][e], acc[c]);
-          }
-        }
-        const uint4 o = pack_bf16x8(acc);
+        const uint4 o = pack_bf16x8(acc[u]);
         const size_t off = static_cast<size_t>(tb + u0 + u) * H + j;
         *reinterpret_cast<uint4*>(out + off) = o;
-        if (push) {  // the owned row straight into every rank's exchange buffer (P2P stores)
-          for (int q = 0; q < T; ++q) *reinterpret_cast<uint4*>(push[q] + off) = o;
-        } else {
+        if (push.p[0]) {  // the owned row straight into every rank's exchange buffer (P2P stores)
+          for (int q = 0; q < T; ++q) *reinterpret_cast<uint4*>(push.p[q] + off) = o;
+        } else if (out_sym) {
           *reinterpret_cast<uint4*>(out_sym + off) = o;
         }
       }
@@ -172,27 +207,27 @@ __global__ void __launch_bounds__(256)
 
 // Sum over the T ranks (rank order) of rows [t0, t1) of a [N x C] fp32 buffer (the partial
 // gate-logit gradients dL): out [t1-t0 x C].
-__global__ void nvl_sum_rows_kernel(const float* const* __restrict__ srcs, int T, int C, int t0, int t1,
+__global__ void nvl_sum_rows_kernel(const __grid_constant__ PeerSet<const float> srcs, int T, int C, int t0, int t1,
                                     float* __restrict__ out) {
   const size_t n = static_cast<size_t>(t1 - t0) * C;
   const size_t base = static_cast<size_t>(t0) * C;
   for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<size_t>(gridDim.x) * blockDim.x) {
     float acc = 0.f;
-    for (int q = 0; q < T; ++q) acc += srcs[q][base + i];
+    for (int q = 0; q < T; ++q) acc += srcs.p[q][base + i];
     out[i] = acc;
   }
 }
 
 // All-gather (pull): out rows of every other owner's block, read from its out_sym.
 __global__ void __launch_bounds__(256)
-    nvl_pull_blocks_kernel(const __nv_bfloat16* const* __restrict__ srcs, int T, int rank, int N, int H,
+    nvl_pull_blocks_kernel(const __grid_constant__ PeerSet<const __nv_bfloat16> srcs, int T, int rank, int N, int H,
                            __nv_bfloat16* __restrict__ out) {
   const size_t row_vecs = static_cast<size_t>(H) / 8;
   for (int q0 = 1; q0 < T; ++q0) {
     const int q = (rank + q0) % T;  // stagger the sources across ranks
     const size_t lo = static_cast<size_t>(q) * N / T, hi = static_cast<size_t>(q + 1) * N / T;
-    const uint4* src = reinterpret_cast<const uint4*>(srcs[q]) + lo * row_vecs;
+    const uint4* src = reinterpret_cast<const uint4*>(srcs.p[q]) + lo * row_vecs;
     uint4* dst = reinterpret_cast<uint4*>(out) + lo * row_vecs;
     const size_t n = (hi - lo) * row_vecs;
     const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
@@ -250,7 +285,7 @@ int ppmoe_nvl_barrier(void* const* pads, int T, int rank, int ch, unsigned int e
   PPMOE_REQUIRE(T >= 1 && T <= kNvlMaxRanks && rank >= 0 && rank < T, "bad barrier group T=%d rank=%d", T, rank);
   PPMOE_REQUIRE(ch >= 0 && ch < kNvlChannels, "barrier channel %d out of range", ch);
   nvl_barrier_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(
-      reinterpret_cast<uint32_t* const*>(pads), T, rank, ch, static_cast<uint32_t>(epoch), err, timeout_cycles);
+      peer_set<uint32_t>(pads, T), T, rank, ch, static_cast<uint32_t>(epoch), err, timeout_cycles);
   return check_launch("nvl_barrier_kernel");
 }
 
@@ -259,7 +294,7 @@ int ppmoe_nvl_owner_gather(const void* const* rows, const int* seg, int El, cons
                            int E, void* out, void* out_sym, void* const* push, void* stream) {
   PPMOE_REQUIRE(T >= 1 && T <= kNvlMaxRanks && rank >= 0 && rank < T, "bad group T=%d rank=%d", T, rank);
   PPMOE_REQUIRE(K >= 1 && K <= 8 && H % 8 == 0 && El >= 1, "owner gather needs 1 <= k <= 8 and hidden %% 8 == 0");
-  PPMOE_REQUIRE(!dl || (Wg && E >= 1 && E <= 16), "the gate term supports 1 <= E <= 16");
+  PPMOE_REQUIRE(!dl || (Wg && E >= 1 && E <= kOgMaxE), "the gate term supports 1 <= E <= %d", kOgMaxE);
   const int t0 = static_cast<int>(static_cast<long long>(rank) * N / T);
   const int t1 = static_cast<int>(static_cast<long long>(rank + 1) * N / T);
   if (t1 <= t0) return kOk;
@@ -267,10 +302,10 @@ int ppmoe_nvl_owner_gather(const void* const* rows, const int* seg, int El, cons
   const int gy = (H / 8 + 255) / 256;
   const int tiles = (t1 - t0 + kOgTile - 1) / kOgTile;
   dim3 grid(max(1, min(tiles, num_sms() * 3 / gy)), gy);
-  auto R = reinterpret_cast<const __nv_bfloat16* const*>(rows);
+  const auto R = peer_set<const __nv_bfloat16>(rows, T);
   auto O = static_cast<__nv_bfloat16*>(out);
   auto OS = static_cast<__nv_bfloat16*>(out_sym);
-  auto P = reinterpret_cast<__nv_bfloat16* const*>(push);
+  const auto P = peer_set<__nv_bfloat16>(push, push ? T : 0);
 #define PPMOE_OG(EB, U, KT)                                                                                 \
   nvl_owner_gather_kernel<EB, U, KT><<<grid, 256, 0, s>>>(R, seg, El, idx, pair_pos, w, K, H, t0, t1, dl, Wg, E, O, \
                                                           OS, P, T)
@@ -283,7 +318,8 @@ int ppmoe_nvl_owner_gather(const void* const* rows, const int* seg, int El, cons
     else if (K == 1) PPMOE_OG(8, 4, 1);
     else PPMOE_OG(8, 1, 0);
   } else {
-    PPMOE_OG(16, 1, 0);
+    if (K == 2) PPMOE_OG(-1, 4, 2);
+    else PPMOE_OG(-1, 2, 0);
   }
 #undef PPMOE_OG
   return check_launch("nvl_owner_gather_kernel");
@@ -296,8 +332,8 @@ int ppmoe_nvl_sum_rows(const void* const* srcs, int T, int rank, int N, int C, f
   if (t1 <= t0) return kOk;
   const size_t n = static_cast<size_t>(t1 - t0) * C;
   const int grid = static_cast<int>(std::min<size_t>((n + 255) / 256, static_cast<size_t>(num_sms()) * 4));
-  nvl_sum_rows_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      reinterpret_cast<const float* const*>(srcs), T, C, t0, t1, out);
+  nvl_sum_rows_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(peer_set<const float>(srcs, T), T, C, t0,
+                                                                            t1, out);
   return check_launch("nvl_sum_rows_kernel");
 }
 
@@ -306,7 +342,7 @@ int ppmoe_nvl_pull_blocks(const void* const* srcs, int T, int rank, int N, int H
   PPMOE_REQUIRE(H % 8 == 0, "pull needs hidden %% 8 == 0");
   if (T == 1 || N == 0) return kOk;
   nvl_pull_blocks_kernel<<<num_sms() * 4, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      reinterpret_cast<const __nv_bfloat16* const*>(srcs), T, rank, N, H, static_cast<__nv_bfloat16*>(out));
+      peer_set<const __nv_bfloat16>(srcs, T), T, rank, N, H, static_cast<__nv_bfloat16*>(out));
   return check_launch("nvl_pull_blocks_kernel");
 }
 

@@ -473,7 +473,14 @@ class _PPMoEFunction(torch.autograd.Function):
             out = nvlink.exchange(ar, "y", pl.seg, spec.el, rt.idx, pl.pair_pos,
                                   rt.w if spec.weight_scaling else None, n, h, torch.empty_like(hidden))
             spec.world.charge_all_reduce(spec.group, out.numel())
-        elif _ops.gather_combine():
+        elif spec.el == e and _ops.combine_mode(hidden.dtype, h) == "owner":
+            # all experts local: fc2 stores Y, the owner-gather kernel sums every token's rows
+            st = _ops.experts_forward(hidden, pl, spec.e0, spec.el, up, down, bias_up, bias_down, spec.k,
+                                      spec.weight_scaling, None, drop_p=spec.dropout_p, seed=spec.seed)
+            out = _ops.local_combine(st.y, st, pl, rt.idx, rt.w if spec.weight_scaling else None,
+                                     torch.empty_like(hidden))
+            spec.world.all_reduce_(spec.group, out)  # a group of one: ledger only (moe.py:307)
+        elif _ops.combine_mode(hidden.dtype, h) != "scatter":
             # fc2 stores Y; the combine gathers each token's local pairs (no fp32 accumulator)
             st = _ops.experts_forward(hidden, pl, spec.e0, spec.el, up, down, bias_up, bias_down, spec.k,
                                       spec.weight_scaling, None, drop_p=spec.dropout_p, seed=spec.seed)
@@ -536,8 +543,23 @@ class _PPMoEFunction(torch.autograd.Function):
             main.wait_stream(side)
             ctx.state = None
             return dx, dwg, d_up, d_down, d_bu, d_bd, None
+        if spec.el == wg.shape[1] and _ops.combine_mode(hidden.dtype, h) == "owner":
+            # all experts local: per-row dX gathered per token with the gate term (owner gather)
+            dxs = _ops._act((st.rows_cap, h), hidden.dtype, hidden.device)
+            dy, dh, dw, parts = _ops.experts_backward_data(g_out, st, up, down, spec.weight_scaling, None, has_bias,
+                                                           dxs)
+            dl = _ops.gate_backward(rt, pl, st, dw, aux)
+            dx = None
+            if need_dx:
+                dx = _ops.local_combine(dxs, st, pl, rt.idx, None, torch.empty_like(hidden), dl, wg)
+                spec.world.all_reduce_(spec.group, dx)  # a group of one: ledger only
+            dwg = _ops.gate_weight_grad(hidden, dl, wg) if need_dwg else None
+            del dxs
+            d_up, d_down, d_bu, d_bd = _ops.experts_backward_weights(st, dy, dh, up, down, has_bias, parts)
+            ctx.state = None
+            return dx, dwg, d_up, d_down, d_bu, d_bd, None
         # fc1 dgrad stores per-row dX; gate_grads gathers them per token (no fp32 scatter)
-        if _ops.gather_combine():
+        if _ops.combine_mode(hidden.dtype, h) != "scatter":
             dx_acc, dxs = None, _ops._act((st.rows_cap, h), hidden.dtype, hidden.device)
         else:
             dx_acc, dxs = torch.zeros((n, h), dtype=torch.float32, device=hidden.device), None

@@ -30,6 +30,11 @@ _ARENAS: dict = {}
 _TIMEOUT_CYCLES = int(os.environ.get("PPMOE_NVL_TIMEOUT_CYCLES", str(4_000_000_000)))
 
 
+def ptr_set(ptrs):
+    """ctypes host array of device pointers (the C-ABI pointer-set arguments)."""
+    return (ctypes.c_void_p * len(ptrs))(*ptrs)
+
+
 class _CudaArray:
     """__cuda_array_interface__ view of a raw device pointer (wrapped by torch.as_tensor)."""
 
@@ -68,7 +73,7 @@ class _PeerBuffer:
             self.opened.append(peer.value)
             ptrs.append(peer.value)
         self.ptrs = ptrs
-        self.table = torch.tensor(ptrs, dtype=torch.int64, device=arena.device)  # device array of T pointers
+        self.table = ptr_set(ptrs)  # host array of the T ranks' pointers (kernel parameters)
 
     def release(self):
         for p in self.opened:
@@ -115,21 +120,21 @@ class NvlArena:
         nbytes = max(n * torch.empty((), dtype=dtype).element_size(), 16)
         return _wrap(self.buffer(name, nbytes).local, shape, dtype, self.device)
 
-    def table(self, name: str) -> torch.Tensor:
+    def table(self, name: str):
         return self.bufs[name].table
 
-    def local_table(self, name: str) -> torch.Tensor:
-        """A T-entry pointer table that names this rank's own copy of `name` T times."""
+    def local_table(self, name: str):
+        """A T-entry pointer set that names this rank's own copy of `name` T times."""
         b = self.bufs[name]
         if getattr(b, "local_tab", None) is None:
-            b.local_tab = torch.tensor([b.local] * self.tp, dtype=torch.int64, device=self.device)
+            b.local_tab = ptr_set([b.local] * self.tp)
         return b.local_tab
 
     # ------------------------------------------------------------------ sync
 
     def barrier(self, ch: int) -> None:
         self.epoch[ch] = (self.epoch[ch] + 1) & 0xFFFFFFFF
-        call("ppmoe_nvl_barrier", ptr(self.pads.table), self.tp, self.rank, ch, self.epoch[ch], ptr(self.err),
+        call("ppmoe_nvl_barrier", self.pads.table, self.tp, self.rank, ch, self.epoch[ch], ptr(self.err),
              _TIMEOUT_CYCLES, _lib.stream_ptr())
 
     def check(self) -> None:
@@ -164,7 +169,7 @@ def sum_owned_rows(ar: NvlArena, name: str, n: int, c: int) -> torch.Tensor:
     buffer `name`; call after a barrier that published it."""
     t0, t1 = owned_range(ar, n)
     out = torch.empty((t1 - t0, c), dtype=torch.float32, device=ar.device)
-    call("ppmoe_nvl_sum_rows", ptr(ar.table(name)), ar.tp, ar.rank, n, c, ptr(out), _lib.stream_ptr())
+    call("ppmoe_nvl_sum_rows", ar.table(name), ar.tp, ar.rank, n, c, ptr(out), _lib.stream_ptr())
     return out
 
 
@@ -181,10 +186,10 @@ def exchange(ar: NvlArena, rows_name: str, seg, el: int, idx, pair_pos, w, n: in
         ar.barrier(0)
     e = wg.shape[1] if wg is not None else 0
     push = os.environ.get("PPMOE_NVL_PUSH", "0") == "1"
-    call("ppmoe_nvl_owner_gather", ptr(ar.table(rows_name)), ptr(seg), el, ptr(idx), ptr(pair_pos), ptr(w), n, k, h,
-         ar.tp, ar.rank, ptr(dl_own), ptr(wg), e, ptr(out), ptr(xch), ptr(ar.table("xch")) if push else None, s)
+    call("ppmoe_nvl_owner_gather", ar.table(rows_name), ptr(seg), el, ptr(idx), ptr(pair_pos), ptr(w), n, k, h,
+         ar.tp, ar.rank, ptr(dl_own), ptr(wg), e, ptr(out), ptr(xch), ar.table("xch") if push else None, s)
     ar.barrier(1)
     # push: every block already sits in the local exchange buffer; pull: read the owners'
     src = ar.local_table("xch") if push else ar.table("xch")
-    call("ppmoe_nvl_pull_blocks", ptr(src), ar.tp, ar.rank, n, h, ptr(out), s)
+    call("ppmoe_nvl_pull_blocks", src, ar.tp, ar.rank, n, h, ptr(out), s)
     return out

@@ -275,18 +275,19 @@ def test_token_chunked_forward_bit_identical(chunks, monkeypatch):
         assert np.array_equal(base["grads"][k], got["grads"][k]), k
 
 
+@pytest.mark.parametrize("mode", ["gather", "owner"])
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
 @pytest.mark.parametrize("hidden_size,experts", [(256, 8), (264, 16), (128, 32)])
-def test_gather_combine_matches_scatter(dtype, hidden_size, experts, monkeypatch):
-    """The gather combine (fc2 stores Y, ppmoe_combine sums the token's pairs; fc1 dgrad
-    stores per-row dX, gathered with the gate term) agrees with the fp32 scatter-add
-    accumulator path, and is bitwise reproducible run to run."""
+def test_gather_combine_matches_scatter(mode, dtype, hidden_size, experts, monkeypatch):
+    """The gather combines (fc2 stores Y and the token's pairs are summed by ppmoe_combine or
+    the owner-gather kernel; fc1 dgrad stores per-row dX, gathered with the gate term) agree
+    with the fp32 scatter-add accumulator path, and are bitwise reproducible run to run."""
     layer = oracle_rounded(O.init_layer(hidden_size, experts, seed=4), dtype)
     hidden = torch.randn(700, hidden_size).to(dtype).double().numpy()
     monkeypatch.setenv("PPMOE_POISON", "1")
     monkeypatch.setenv("PPMOE_COMBINE", "scatter")
     ref = run_cuda_layer(hidden, device_weights(layer, dtype), k=2, capacity_factor=1.25, tp=2, dtype=dtype)
-    monkeypatch.setenv("PPMOE_COMBINE", "gather")
+    monkeypatch.setenv("PPMOE_COMBINE", mode)
     got = run_cuda_layer(hidden, device_weights(layer, dtype), k=2, capacity_factor=1.25, tp=2, dtype=dtype)
     again = run_cuda_layer(hidden, device_weights(layer, dtype), k=2, capacity_factor=1.25, tp=2, dtype=dtype)
     tol = TOL[dtype]
