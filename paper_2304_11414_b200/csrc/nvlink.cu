@@ -17,6 +17,7 @@
 // signal pad on every peer, with a bounded spin (a stuck peer reports an error instead
 // of hanging the GPU).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "../../include/ppmoe_capi.h"
@@ -99,26 +100,43 @@ __device__ __forceinline__ uint4 pack_bf16x8(const float (&a)[8]) {
 constexpr int kOgTile = 32;
 constexpr int kOgMaxE = 128;
 
-template <int EB, int U, int KT>  // KT = k (1, 2) or 0: any k <= 8 read at run time
+template <int CW> struct OgVec;
+template <> struct OgVec<8> { using type = uint4; };
+template <> struct OgVec<4> { using type = uint2; };
+
+template <int CW>
+__device__ __forceinline__ void acc_bf16(float (&acc)[CW], const typename OgVec<CW>::type& u, float s) {
+  const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < CW / 2; ++i) {
+    const float2 f = __bfloat1622float2(hv[i]);
+    acc[2 * i] = fmaf(s, f.x, acc[2 * i]);
+    acc[2 * i + 1] = fmaf(s, f.y, acc[2 * i + 1]);
+  }
+}
+
+// One CTA per tile of kOgTile owned tokens x (256*CW) columns.  CW columns per thread.
+template <int EB, int U, int KT, int CW>  // KT = k (1, 2) or 0: any k <= 8 read at run time
 __global__ void __launch_bounds__(256)
-    nvl_owner_gather_kernel(const __grid_constant__ PeerSet<const __nv_bfloat16> rows, const int* __restrict__ seg, int El,
-                            const int* __restrict__ idx, const int* __restrict__ pair_pos,
+    nvl_owner_gather_kernel(const __grid_constant__ PeerSet<const __nv_bfloat16> rows, const int* __restrict__ seg,
+                            int El, const int* __restrict__ idx, const int* __restrict__ pair_pos,
                             const float* __restrict__ w, int Kr, int H, int t0, int t1,
                             const float* __restrict__ dl, const float* __restrict__ Wg, int E,
                             __nv_bfloat16* __restrict__ out, __nv_bfloat16* __restrict__ out_sym,
                             const __grid_constant__ PeerSet<__nv_bfloat16> push, int T) {
+  using V = typename OgVec<CW>::type;
   constexpr int KS = KT > 0 ? KT : 8;
   constexpr int DLW = EB > 0 ? EB : (EB < 0 ? kOgMaxE : 1);
   const int K = KT > 0 ? KT : Kr;
   __shared__ const __nv_bfloat16* src[kOgTile][KS];
   __shared__ float sw[kOgTile][KS];
   __shared__ float sdl[kOgTile][DLW];
-  const int j = (blockIdx.y * blockDim.x + threadIdx.x) * 8;
+  const int j = (blockIdx.y * blockDim.x + threadIdx.x) * CW;
   const bool active = j < H;
-  float wg[EB > 0 ? 8 : 1][EB > 0 ? EB : 1];
+  float wg[EB > 0 ? CW : 1][EB > 0 ? EB : 1];
   if constexpr (EB > 0) {
 #pragma unroll
-    for (int c = 0; c < 8; ++c)
+    for (int c = 0; c < CW; ++c)
 #pragma unroll
       for (int e = 0; e < EB; ++e) wg[c][e] = (active && e < E) ? Wg[static_cast<size_t>(j + c) * E + e] : 0.f;
   }
@@ -142,30 +160,33 @@ __global__ void __launch_bounds__(256)
       sw[u][s] = ws;
     }
     if constexpr (EB != 0) {
-      for (int i = threadIdx.x; i < kOgTile * E; i += blockDim.x) {
-        const int u = i / E, e = i % E;
-        sdl[u][e] = u < nt ? dl[static_cast<size_t>(tb - t0 + u) * E + e] : 0.f;
+      constexpr int W = EB > 0 ? EB : 1;
+      const int ew = EB > 0 ? W : E;  // register form reads all EB columns: zero-fill past E
+      for (int i = threadIdx.x; i < kOgTile * ew; i += blockDim.x) {
+        const int u = i / ew, e = i % ew;
+        sdl[u][e] = (u < nt && e < E) ? dl[static_cast<size_t>(tb - t0 + u) * E + e] : 0.f;
       }
     }
     __syncthreads();
     if (!active) continue;
     for (int u0 = 0; u0 < nt; u0 += U) {
-      uint4 v[U][KS];
+      V v[U][KS];
 #pragma unroll
       for (int u = 0; u < U; ++u)
 #pragma unroll
         for (int s = 0; s < KS; ++s) {
           const __nv_bfloat16* p = (s < K && u0 + u < nt) ? src[u0 + u][s] : nullptr;
-          v[u][s] = p ? *reinterpret_cast<const uint4*>(p + j) : make_uint4(0, 0, 0, 0);
+          if (p) v[u][s] = *reinterpret_cast<const V*>(p + j);
+          else memset(&v[u][s], 0, sizeof(V));
         }
-      float acc[U][8];
+      float acc[U][CW];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
 #pragma unroll
-        for (int c = 0; c < 8; ++c) acc[u][c] = 0.f;
+        for (int c = 0; c < CW; ++c) acc[u][c] = 0.f;
 #pragma unroll
         for (int s = 0; s < KS; ++s)
-          if (s < K) acc_bf16x8(acc[u], v[u][s], sw[min(u0 + u, kOgTile - 1)][s]);
+          if (s < K) acc_bf16<CW>(acc[u], v[u][s], sw[min(u0 + u, kOgTile - 1)][s]);
       }
       if constexpr (EB > 0) {
 #pragma unroll
@@ -174,31 +195,34 @@ __global__ void __launch_bounds__(256)
           for (int e = 0; e < EB; ++e) {
             const float d = sdl[min(u0 + u, kOgTile - 1)][e];
 #pragma unroll
-            for (int c = 0; c < 8; ++c) acc[u][c] = fmaf(d, wg[c][e], acc[u][c]);
+            for (int c = 0; c < CW; ++c) acc[u][c] = fmaf(d, wg[c][e], acc[u][c]);
           }
       } else if constexpr (EB < 0) {
         for (int e = 0; e < E; ++e) {
-          float wc[8];
+          float wc[CW];
 #pragma unroll
-          for (int c = 0; c < 8; ++c) wc[c] = Wg[static_cast<size_t>(j + c) * E + e];
+          for (int c = 0; c < CW; ++c) wc[c] = Wg[static_cast<size_t>(j + c) * E + e];
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             const float d = sdl[min(u0 + u, kOgTile - 1)][e];
 #pragma unroll
-            for (int c = 0; c < 8; ++c) acc[u][c] = fmaf(d, wc[c], acc[u][c]);
+            for (int c = 0; c < CW; ++c) acc[u][c] = fmaf(d, wc[c], acc[u][c]);
           }
         }
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         if (u0 + u >= nt) break;
-        const uint4 o = pack_bf16x8(acc[u]);
+        V o;
+        uint32_t* ow = reinterpret_cast<uint32_t*>(&o);
+#pragma unroll
+        for (int i = 0; i < CW / 2; ++i) ow[i] = pack_bf16x2(acc[u][2 * i], acc[u][2 * i + 1]);
         const size_t off = static_cast<size_t>(tb + u0 + u) * H + j;
-        *reinterpret_cast<uint4*>(out + off) = o;
+        *reinterpret_cast<V*>(out + off) = o;
         if (push.p[0]) {  // the owned row straight into every rank's exchange buffer (P2P stores)
-          for (int q = 0; q < T; ++q) *reinterpret_cast<uint4*>(push.p[q] + off) = o;
+          for (int q = 0; q < T; ++q) *reinterpret_cast<V*>(push.p[q] + off) = o;
         } else if (out_sym) {
-          *reinterpret_cast<uint4*>(out_sym + off) = o;
+          *reinterpret_cast<V*>(out_sym + off) = o;
         }
       }
     }
@@ -241,6 +265,15 @@ __global__ void __launch_bounds__(256)
     }
     for (; i < n; i += stride) dst[i] = src[i];
   }
+}
+
+static int og_ctas_per_sm() {
+  static int v = [] { const char* e = getenv("PPMOE_OG_CTAS"); return e ? atoi(e) : 4; }();
+  return v;
+}
+static int og_fwd_cw() {
+  static int v = [] { const char* e = getenv("PPMOE_OG_FWD_CW"); return e ? atoi(e) : 4; }();
+  return v;
 }
 
 }  // namespace ppmoe
@@ -294,32 +327,37 @@ int ppmoe_nvl_owner_gather(const void* const* rows, const int* seg, int El, cons
                            int E, void* out, void* out_sym, void* const* push, void* stream) {
   PPMOE_REQUIRE(T >= 1 && T <= kNvlMaxRanks && rank >= 0 && rank < T, "bad group T=%d rank=%d", T, rank);
   PPMOE_REQUIRE(K >= 1 && K <= 8 && H % 8 == 0 && El >= 1, "owner gather needs 1 <= k <= 8 and hidden %% 8 == 0");
+  PPMOE_REQUIRE(N / T < (1 << 30), "too many tokens");
   PPMOE_REQUIRE(!dl || (Wg && E >= 1 && E <= kOgMaxE), "the gate term supports 1 <= E <= %d", kOgMaxE);
   const int t0 = static_cast<int>(static_cast<long long>(rank) * N / T);
   const int t1 = static_cast<int>(static_cast<long long>(rank + 1) * N / T);
   if (t1 <= t0) return kOk;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int gy = (H / 8 + 255) / 256;
   const int tiles = (t1 - t0 + kOgTile - 1) / kOgTile;
-  dim3 grid(max(1, min(tiles, num_sms() * 3 / gy)), gy);
   const auto R = peer_set<const __nv_bfloat16>(rows, T);
   auto O = static_cast<__nv_bfloat16*>(out);
   auto OS = static_cast<__nv_bfloat16*>(out_sym);
   const auto P = peer_set<__nv_bfloat16>(push, push ? T : 0);
-#define PPMOE_OG(EB, U, KT)                                                                                 \
-  nvl_owner_gather_kernel<EB, U, KT><<<grid, 256, 0, s>>>(R, seg, El, idx, pair_pos, w, K, H, t0, t1, dl, Wg, E, O, \
-                                                          OS, P, T)
+  // persistent-ish grid over the tiles; the gate-term forms use 4 columns per thread to keep
+  // Wg in registers at 3+ CTAs per SM
+#define PPMOE_OG(EB, U, KT, CW)                                                                            \
+  do {                                                                                                     \
+    const int gy_ = (H / CW + 255) / 256;                                                                  \
+    nvl_owner_gather_kernel<EB, U, KT, CW><<<dim3(max(1, min(tiles, num_sms() * og_ctas_per_sm() / gy_)), gy_), 256, 0, s>>>( \
+        R, seg, El, idx, pair_pos, w, K, H, t0, t1, dl, Wg, E, O, OS, P, T);                               \
+  } while (0)
   if (!dl) {
-    if (K == 2) PPMOE_OG(0, 4, 2);
-    else if (K == 1) PPMOE_OG(0, 8, 1);
-    else PPMOE_OG(0, 1, 0);
+    if (K == 2 && og_fwd_cw() == 4) PPMOE_OG(0, 8, 2, 4);
+    else if (K == 2) PPMOE_OG(0, 4, 2, 8);
+    else if (K == 1) PPMOE_OG(0, 8, 1, 8);
+    else PPMOE_OG(0, 1, 0, 8);
   } else if (E <= 8) {
-    if (K == 2) PPMOE_OG(8, 2, 2);
-    else if (K == 1) PPMOE_OG(8, 4, 1);
-    else PPMOE_OG(8, 1, 0);
+    if (K == 2) PPMOE_OG(8, 4, 2, 4);
+    else if (K == 1) PPMOE_OG(8, 8, 1, 4);
+    else PPMOE_OG(8, 1, 0, 4);
   } else {
-    if (K == 2) PPMOE_OG(-1, 4, 2);
-    else PPMOE_OG(-1, 2, 0);
+    if (K == 2) PPMOE_OG(-1, 4, 2, 4);
+    else PPMOE_OG(-1, 2, 0, 4);
   }
 #undef PPMOE_OG
   return check_launch("nvl_owner_gather_kernel");

@@ -59,3 +59,6 @@ outb = torch.empty_like(x)
 timeit("combine fwd (Y gather, w)", lambda: _ops.combine(st.y, st, pl, rt.w, outb), n * h * 6)
 timeit("input_grads (dX + dWg)", lambda: _ops.input_grads(st.y, st, pl, x, dl, wg, True, True), n * h * 8)
 timeit("input_grads (dX only)", lambda: _ops.input_grads(st.y, st, pl, x, dl, wg, True, False), n * h * 6)
+timeit("owner gather fwd (T=1)", lambda: _ops.local_combine(st.y, st, pl, rt.idx, rt.w, outb), n * h * 6)
+timeit("owner gather bwd (T=1, +gate)", lambda: _ops.local_combine(st.y, st, pl, rt.idx, None, outb, dl, wg), n * h * 6)
+timeit("gate_weight_grad (dWg)", lambda: _ops.gate_weight_grad(x, dl, wg), n * h * 2)

@@ -1,6 +1,4 @@
-"""Dev tool: two C2 PPMoE steps (fwd+bwd) for ncu captures; kernel order per step:
-router, finalize, plan x5, gather, fc1_fwd, fc2_fwd, cast, bwd_dy, fc2_dgrad, fc2_wgrad,
-colsum, fc1_dgrad, fc1_wgrad, colsum, gate_bwd, gate_grads, dwg_reduce."""
+"""Dev tool: two C2 PPMoE steps (fwd+bwd) for ncu captures (TP = 1, default combine mode)."""
 import sys
 sys.path.insert(0, ".")
 import torch
