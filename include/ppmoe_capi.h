@@ -252,8 +252,10 @@ int ppmoe_nvl_owner_gather(const void* const* rows, const int* seg, int El, cons
 /* out [t1-t0 x C] = sum over q (rank order) of srcs[q] rows [t0, t1) (fp32 [N x C]): the
  * owned rows of the ranks' partial gate-logit gradients.                               */
 int ppmoe_nvl_sum_rows(const void* const* srcs, int T, int rank, int N, int C, float* out, void* stream);
-/* All-gather by pull: out rows of every other owner q's block from srcs[q] (its out_sym). */
+/* All-gather by pull: out rows of every other owner q's block from srcs[q] (its out_sym),
+ * by SM loads (_blocks) or by copy-engine transfers, one per peer block (_blocks_ce).  */
 int ppmoe_nvl_pull_blocks(const void* const* srcs, int T, int rank, int N, int H, void* out, void* stream);
+int ppmoe_nvl_pull_blocks_ce(const void* const* srcs, int T, int rank, int N, int H, void* out, void* stream);
 
 /* Self-test entry: plain grouped GEMM D_g = A_g * B_g through the tcgen05 path
  * (use_tc=1) or the CUDA-core path (use_tc=0).  mode 0: A [rows x K] K-major

@@ -384,4 +384,18 @@ int ppmoe_nvl_pull_blocks(const void* const* srcs, int T, int rank, int N, int H
   return check_launch("nvl_pull_blocks_kernel");
 }
 
+int ppmoe_nvl_pull_blocks_ce(const void* const* srcs, int T, int rank, int N, int H, void* out, void* stream) {
+  PPMOE_REQUIRE(T >= 1 && T <= kNvlMaxRanks && rank >= 0 && rank < T, "bad group T=%d rank=%d", T, rank);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t row = static_cast<size_t>(H) * 2;
+  for (int q0 = 1; q0 < T; ++q0) {  // one copy-engine transfer per peer block, staggered sources
+    const int q = (rank + q0) % T;
+    const size_t lo = static_cast<size_t>(q) * N / T, hi = static_cast<size_t>(q + 1) * N / T;
+    if (hi > lo)
+      PPMOE_CUDA(cudaMemcpyAsync(static_cast<char*>(out) + lo * row, static_cast<const char*>(srcs[q]) + lo * row,
+                                 (hi - lo) * row, cudaMemcpyDeviceToDevice, s));
+  }
+  return kOk;
+}
+
 }  // extern "C"

@@ -191,5 +191,7 @@ def exchange(ar: NvlArena, rows_name: str, seg, el: int, idx, pair_pos, w, n: in
     ar.barrier(1)
     # push: every block already sits in the local exchange buffer; pull: read the owners'
     src = ar.local_table("xch") if push else ar.table("xch")
-    call("ppmoe_nvl_pull_blocks", src, ar.tp, ar.rank, n, h, ptr(out), s)
+    # copy engines by default: the all-gather then takes no SMs from the overlapped GEMMs
+    pull = "ppmoe_nvl_pull_blocks" if os.environ.get("PPMOE_NVL_PULL", "ce") == "sm" else "ppmoe_nvl_pull_blocks_ce"
+    call(pull, src, ar.tp, ar.rank, n, h, ptr(out), s)
     return out
