@@ -172,3 +172,24 @@ def test_distributed_world_gloo_two_ranks():
         assert part == expect
         assert grad == [[3.0, 3.0]] * 3
         assert cnt == 1
+
+
+def test_schedule_1f1b_matches_reference_order():
+    """The pipeline stack runs the reference's 1F1B op order (pipeline.py:64-82)."""
+    from paper_2304_11414_b200.pipeline import schedule_1f1b
+
+    assert schedule_1f1b(2, 3) == [[("F", 1), ("F", 2), ("B", 1), ("F", 3), ("B", 2), ("B", 3)],
+                                   [("F", 1), ("B", 1), ("F", 2), ("B", 2), ("F", 3), ("B", 3)]]
+    for p, m in [(1, 1), (2, 1), (3, 5), (4, 8), (4, 2)]:
+        sched = schedule_1f1b(p, m)
+        for ops in sched:
+            assert sorted(ops) == sorted([("F", i) for i in range(1, m + 1)] + [("B", i) for i in range(1, m + 1)])
+            assert all(ops.index(("F", i)) < ops.index(("B", i)) for i in range(1, m + 1))
+    try:
+        import sys
+        sys.path.insert(0, "/root/reference/pkg/src")
+        from moesim.pipeline import schedule_1f1b as ref_sched
+    except Exception:
+        return
+    for p, m in [(1, 1), (2, 3), (3, 5), (4, 8), (4, 2), (8, 16)]:
+        assert schedule_1f1b(p, m) == [[(str(k), int(mb)) for k, mb in ops] for ops in ref_sched(p, m)]

@@ -231,3 +231,75 @@ def test_replicated_feed_rebuilds_batch():
     for r in range(world):
         assert got[r]["ok"] == [True, True, True]
         assert got[r]["h2d"] == 1024 * 384 * 2 // world
+
+
+def _pp_worker(rank, world, port, q, stages, tp):
+    import torch.distributed as dist
+
+    import paper_2304_11414_b200 as P
+    from paper_2304_11414_b200.pipeline import PipelineStack, schedule_1f1b
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    try:
+        stack = PipelineStack(P.World(1, world), layers=4, stages=stages, tp=tp, hidden=256, experts=8, top_k=2,
+                              seed=3)
+        done = stack.train_step(3, mb_tokens=384)
+        stack.sync_gate_gradients()
+        torch.cuda.synchronize()
+        grads = {}
+        for j, (dense, moe) in enumerate(stack.blocks):
+            li = stack.first_layer + j
+            grads[f"{li}.dense.up"] = dense.up.grad.float().cpu().numpy()
+            grads[f"{li}.moe.wg"] = moe.gate.wg.grad.cpu().numpy()
+            grads[f"{li}.moe.up"] = moe.bank.up.grad.float().cpu().numpy()
+        q.put((rank, {"done": done, "expected": schedule_1f1b(stages, 3)[stack.stage], "grads": grads,
+                      "stage": stack.stage, "slot": stack.slot}))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("stages,tp", [(2, 1), (2, 2)])
+def test_pipeline_stack_matches_single_gpu(stages, tp):
+    """1F1B over P stages x T tensor ranks (NCCL p2p + the NVLink exchange) gives the
+    gradients of the same 4-block stack run on one GPU (BASELINE configs[3] structure)."""
+    world = stages * tp
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    import paper_2304_11414_b200 as P
+    from paper_2304_11414_b200.pipeline import PipelineStack
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29900 + os.getpid() % 90
+    procs = [ctx.Process(target=_pp_worker, args=(r, world, port, q, stages, tp)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = _collect(q, procs)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    ref = PipelineStack(P.World(1, 1), layers=4, stages=1, tp=1, hidden=256, experts=8, top_k=2, seed=3)
+    ref.train_step(3, mb_tokens=384)
+    torch.cuda.synchronize()
+
+    def err(a, b):
+        return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-30))
+
+    el, fs = 8 // tp, 1024 // tp
+    for r in range(world):
+        res = got[r]
+        assert res["done"] == res["expected"]
+        t = res["slot"]
+        for key, g in res["grads"].items():
+            li, part, name = key.split(".")
+            dense, moe = ref.blocks[int(li)]
+            if part == "dense":
+                want = dense.up.grad[:, t * fs:(t + 1) * fs].float().cpu().numpy()
+            elif name == "wg":
+                want = moe.gate.wg.grad.cpu().numpy()
+            else:
+                want = moe.bank.up.grad[t * el:(t + 1) * el].float().cpu().numpy()
+            assert err(g, want) < 3e-2, (key, err(g, want))
