@@ -233,7 +233,7 @@ def test_replicated_feed_rebuilds_batch():
         assert got[r]["h2d"] == 1024 * 384 * 2 // world
 
 
-def _pp_worker(rank, world, port, q, stages, tp):
+def _pp_worker(rank, world, port, q, stages, tp, dtype):
     import torch.distributed as dist
 
     import paper_2304_11414_b200 as P
@@ -245,7 +245,7 @@ def _pp_worker(rank, world, port, q, stages, tp):
     dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
     try:
         stack = PipelineStack(P.World(1, world), layers=4, stages=stages, tp=tp, hidden=256, experts=8, top_k=2,
-                              seed=3)
+                              seed=3, dtype=dtype)
         done = stack.train_step(3, mb_tokens=384)
         stack.sync_gate_gradients()
         torch.cuda.synchronize()
@@ -261,10 +261,13 @@ def _pp_worker(rank, world, port, q, stages, tp):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("stages,tp", [(2, 1), (2, 2)])
-def test_pipeline_stack_matches_single_gpu(stages, tp):
-    """1F1B over P stages x T tensor ranks (NCCL p2p + the NVLink exchange) gives the
-    gradients of the same 4-block stack run on one GPU (BASELINE configs[3] structure)."""
+@pytest.mark.parametrize("stages,tp,dtype", [(2, 1, torch.bfloat16), (2, 2, torch.float32)])
+def test_pipeline_stack_matches_single_gpu(stages, tp, dtype):
+    """1F1B over P stages x T tensor ranks (NCCL p2p, TP dense FFN, PPMoE exchange) gives the
+    gradients of the same 4-block stack run on one GPU (BASELINE configs[3] structure).
+    With T = 1 the arithmetic is identical (bf16); with T = 2 the sharded dense FFN
+    changes bf16 rounding and, through routing near-ties amplified by the residual stack,
+    whole tokens' gradients, so the tensor-parallel composition is checked in fp32."""
     world = stages * tp
     if torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
@@ -274,14 +277,14 @@ def test_pipeline_stack_matches_single_gpu(stages, tp):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = 29900 + os.getpid() % 90
-    procs = [ctx.Process(target=_pp_worker, args=(r, world, port, q, stages, tp)) for r in range(world)]
+    procs = [ctx.Process(target=_pp_worker, args=(r, world, port, q, stages, tp, dtype)) for r in range(world)]
     for p in procs:
         p.start()
     got = _collect(q, procs)
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
-    ref = PipelineStack(P.World(1, 1), layers=4, stages=1, tp=1, hidden=256, experts=8, top_k=2, seed=3)
+    ref = PipelineStack(P.World(1, 1), layers=4, stages=1, tp=1, hidden=256, experts=8, top_k=2, seed=3, dtype=dtype)
     ref.train_step(3, mb_tokens=384)
     torch.cuda.synchronize()
 
@@ -302,4 +305,4 @@ def test_pipeline_stack_matches_single_gpu(stages, tp):
                 want = moe.gate.wg.grad.cpu().numpy()
             else:
                 want = moe.bank.up.grad[t * el:(t + 1) * el].float().cpu().numpy()
-            assert err(g, want) < 3e-2, (key, err(g, want))
+            assert err(g, want) < (3e-2 if dtype == torch.bfloat16 else 1e-3), (key, err(g, want))
