@@ -193,3 +193,22 @@ def test_schedule_1f1b_matches_reference_order():
         return
     for p, m in [(1, 1), (2, 3), (3, 5), (4, 8), (4, 2), (8, 16)]:
         assert schedule_1f1b(p, m) == [[(str(k), int(mb)) for k, mb in ops] for ops in ref_sched(p, m)]
+
+
+def test_costmodel_formulas_reduce_to_reference():
+    """The recalibrated cost model restates the reference formulas (costmodel.py:181-192)."""
+    from paper_2304_11414_b200 import costmodel as C
+
+    # reference ring all-reduce 2(n-1)(t_s + m/B) is the ring_factor=False form
+    assert abs(C.lat_all_reduce(4, 1e6, 1e9, 1e-6, ring_factor=False) - 2 * 3 * (1e-6 + 1e-3)) < 1e-15
+    assert abs(C.lat_all_reduce(4, 1e6, 1e9) - 2 * 3 * 1e6 / 4 / 1e9) < 1e-15
+    assert C.lat_all_reduce(1, 1e6, 1e9) == 0.0
+    assert abs(C.lat_all_to_all(4, 1e6, 1e9, 0.0) - 3 * 1e6 * 4 / 2e9) < 1e-15
+    assert C.expert_flops(16384, 4096, 2, backward=True) == 12 * 16384 * 2 * 4096 * 16384
+    prof = C.B200Profile(flops=1.35e15, nvlink_bw=6e11, startup=1e-5, hbm_bw=6.5e12)
+    m1 = C.layer_latency("moe_ppmoe", 16384, 4096, 8, 2, 1, prof)
+    m4 = C.layer_latency("moe_ppmoe", 16384, 4096, 8, 2, 4, prof)
+    assert m1["moe_all_reduce"] == 0.0 and m4["moe_all_reduce"] > 0
+    assert abs(m4["expert_compute"] * 4 - m1["expert_compute"]) < 1e-12
+    rows = C.breakdown_rows({"a": 1.0, "b": 3.0, "total": 4.0})
+    assert rows == [("a", 1.0, 25.0), ("b", 3.0, 75.0)]
