@@ -252,6 +252,23 @@ int ppmoe_nvl_owner_gather(const void* const* rows, const int* seg, int El, cons
 /* out [t1-t0 x C] = sum over q (rank order) of srcs[q] rows [t0, t1) (fp32 [N x C]): the
  * owned rows of the ranks' partial gate-logit gradients.                               */
 int ppmoe_nvl_sum_rows(const void* const* srcs, int T, int rank, int N, int C, float* out, void* stream);
+/* Fused forward variant: ppmoe_expert_fc2_fwd_owner's epilogue scatter-adds w*Y of every
+ * row straight into the fp32 accumulator of the rank that owns the row's token (owner_acc
+ * = DEVICE array of T peer pointers, each [owner_rows x H], token t owned by t / owner_rows,
+ * red.global.add over NVLink while the GEMM runs; k <= 2 keeps it order-independent).
+ * After a barrier, ppmoe_nvl_cast_owned turns this rank's accumulator rows into bf16
+ * (out rows and the exchange copy) and zeroes them for the next pass.               */
+/* Owner-slot variant (owner_slots instead of owner_acc): w*Y is stored in bf16 with plain
+ * P2P stores into slot s of the owner's [owner_rows x K x H] buffer (s = the pair's top-k
+ * slot from pair_pos [N x K], K <= 2), and ppmoe_nvl_sum_slots sums the valid slots.   */
+int ppmoe_expert_fc2_fwd_owner(int dtype, const void* Act, const void* down, const void* bias_down, const int* seg,
+                               int El, int H, int F, int rows_cap, const int* tok_local, const float* w_local,
+                               int weight_scaling, float dropout_p, unsigned long long seed, void* Y,
+                               float* const* owner_acc, void* const* owner_slots, const int* pair_pos, int K,
+                               int owner_rows, void* stream);
+int ppmoe_nvl_cast_owned(float* acc, int rows, int H, void* out_rows, void* xch_rows, void* stream);
+int ppmoe_nvl_sum_slots(const void* slots, int rows, int K, int H, int t0, const int* pair_pos, void* out_rows,
+                        void* xch_rows, void* stream);
 /* All-gather by pull: out rows of every other owner q's block from srcs[q] (its out_sym),
  * by SM loads (_blocks) or by copy-engine transfers, one per peer block (_blocks_ce).  */
 int ppmoe_nvl_pull_blocks(const void* const* srcs, int T, int rank, int N, int H, void* out, void* stream);

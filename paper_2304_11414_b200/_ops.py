@@ -258,7 +258,8 @@ class ExpertFwdState:
 
 def experts_forward(hidden, pl: Plan, e0: int, el: int, up, down, bias_up, bias_down, k: int, weight_scaling: bool,
                     out_acc: torch.Tensor, chunks: int = 1, on_chunk=None, drop_p: float = 0.0,
-                    seed: int = 0, y_mirror: torch.Tensor | None = None) -> ExpertFwdState:
+                    seed: int = 0, y_mirror: torch.Tensor | None = None, owner_table: torch.Tensor | None = None,
+                    owner_rows: int = 0, owner_slots: torch.Tensor | None = None) -> ExpertFwdState:
     """index-slice gather -> fc1 (+bias, GeLU) -> fc2 (+bias, gate-scaled scatter-add combine)
     for experts [e0, e0+el) (moe.py:294-305).  out_acc None: fc2 only stores Y and the
     combine is done by ``combine`` (gather, no atomics).  With chunks > 1 the two GEMMs run per token
@@ -283,6 +284,12 @@ def experts_forward(hidden, pl: Plan, e0: int, el: int, up, down, bias_up, bias_
     def gemms(rlo, rhi):
         call("ppmoe_expert_fc1_fwd", dt, ptr(xs), ptr(up), ptr(bias_up), ptr(seg), el, h, f, rows_cap, ptr(rlo),
              ptr(rhi), ptr(gelu_grad), ptr(act), s)
+        if owner_table is not None or owner_slots is not None:
+            # combine fused into the epilogue: rows go to their owners (fp32 accumulators or bf16 slots)
+            call("ppmoe_expert_fc2_fwd_owner", dt, ptr(act), ptr(down), ptr(bias_down), ptr(seg), el, h, f, rows_cap,
+                 ptr(tok_l), ptr(w_l), int(bool(weight_scaling)), float(drop_p), int(seed), ptr(y), ptr(owner_table),
+                 ptr(owner_slots), ptr(pl.pair_pos), k, int(owner_rows), s)
+            return
         call("ppmoe_expert_fc2_fwd", dt, ptr(act), ptr(down), ptr(bias_down), ptr(seg), el, h, f, rows_cap, ptr(rlo),
              ptr(rhi), ptr(tok_l), ptr(w_l), int(bool(weight_scaling)), float(drop_p), int(seed), ptr(y), ptr(y_mirror),
              ptr(out_acc), s)

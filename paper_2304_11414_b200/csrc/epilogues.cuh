@@ -146,6 +146,16 @@ struct EpiFc2Fwd {
   int cs;
   float drop_p;             // inverted dropout on the expert output (tensor.py:315-330)
   unsigned long long seed;
+  // Owner mode (NVLink exchange): the weighted row goes straight into the fp32 accumulator
+  // of the rank owning the token (owner_acc = device table of T peer pointers, each
+  // [owner_rows x H]), over NVLink, tile by tile while the GEMM runs.
+  float* const* owner_acc;
+  int owner_rows;
+  // Owner-slot mode: w*Y (bf16) stored into slot s of the owning rank's [owner_rows x K x H]
+  // buffer with plain P2P stores (slot = the pair's top-k slot, found from pair_pos).
+  T* const* owner_slots;
+  const int* pair_pos;
+  int K;
   template <int W>
   __device__ __forceinline__ void apply(int g, int m, int row, int n0, const float (&v)[W]) const {
     const int valid = min(W, H - n0);
@@ -164,11 +174,28 @@ struct EpiFc2Fwd {
     }
     store_row<T, W>(y + static_cast<size_t>(row) * H + n0, x, valid, cs);
     if (y2) store_row<T, W>(y2 + static_cast<size_t>(row) * H + n0, x, valid, 0);
-    if (!out_acc) return;  // gather-combine mode: ppmoe_combine reads Y afterwards
+    if (!out_acc && !owner_acc && !owner_slots) return;  // gather-combine mode: the combine reads Y afterwards
     const int t = tok[row];
+    if (t >= 0 && owner_slots) {
+      const float s = weight_scaling ? w[row] : 1.f;
+      const int q = t / owner_rows;
+      const int slot = (K == 1 || pair_pos[static_cast<size_t>(t) * K] == row + seg[0]) ? 0 : 1;
+      float xs[W];
+#pragma unroll
+      for (int j = 0; j < W; ++j) xs[j] = s * x[j];
+      store_row<T, W>(owner_slots[q] + (static_cast<size_t>(t - q * owner_rows) * K + slot) * H + n0, xs, valid, 0);
+      return;
+    }
     if (t >= 0) {
       const float s = weight_scaling ? w[row] : 1.f;
-      scatter_add_row<W>(out_acc + static_cast<size_t>(t) * H + n0, x, s, valid);
+      float* dst;
+      if (owner_acc) {
+        const int q = t / owner_rows;
+        dst = owner_acc[q] + static_cast<size_t>(t - q * owner_rows) * H;
+      } else {
+        dst = out_acc + static_cast<size_t>(t) * H;
+      }
+      scatter_add_row<W>(dst + n0, x, s, valid);
     }
   }
 };

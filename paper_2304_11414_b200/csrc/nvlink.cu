@@ -243,6 +243,45 @@ __global__ void nvl_sum_rows_kernel(const __grid_constant__ PeerSet<const float>
   }
 }
 
+// Owned rows of the fp32 owner accumulator -> bf16 (local output and the peer-visible
+// exchange copy), zeroing the accumulator for the next pass.  rows x H, H % 4 == 0.
+__global__ void nvl_cast_owned_kernel(float* __restrict__ acc, size_t n4, __nv_bfloat16* __restrict__ out,
+                                      __nv_bfloat16* __restrict__ xch) {
+  for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    float4* a = reinterpret_cast<float4*>(acc) + i;
+    const float4 v = *a;
+    *a = make_float4(0.f, 0.f, 0.f, 0.f);
+    uint2 o;
+    o.x = pack_bf16x2(v.x, v.y);
+    o.y = pack_bf16x2(v.z, v.w);
+    reinterpret_cast<uint2*>(out)[i] = o;
+    if (xch) reinterpret_cast<uint2*>(xch)[i] = o;
+  }
+}
+
+// Owner-slot sum: out[t] = sum over valid slots s (pair_pos[t,s] >= 0) of slots[t-t0][s],
+// for the owned tokens [t0, t0+rows); writes the local output rows and the exchange copy.
+__global__ void nvl_sum_slots_kernel(const __nv_bfloat16* __restrict__ slots, int rows, int K, int H, int t0,
+                                     const int* __restrict__ pair_pos, __nv_bfloat16* __restrict__ out,
+                                     __nv_bfloat16* __restrict__ xch) {
+  const int hv = H / 8;
+  const size_t n = static_cast<size_t>(rows) * hv;
+  for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(i / hv), c = static_cast<int>(i % hv) * 8;
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int sl = 0; sl < K; ++sl) {
+      if (pair_pos[static_cast<size_t>(t0 + r) * K + sl] < 0) continue;
+      const uint4 u = *reinterpret_cast<const uint4*>(slots + (static_cast<size_t>(r) * K + sl) * H + c);
+      acc_bf16x8(acc, u, 1.f);
+    }
+    const uint4 o = pack_bf16x8(acc);
+    *reinterpret_cast<uint4*>(out + static_cast<size_t>(r) * H + c) = o;
+    *reinterpret_cast<uint4*>(xch + static_cast<size_t>(r) * H + c) = o;
+  }
+}
+
 // All-gather (pull): out rows of every other owner's block, read from its out_sym.
 __global__ void __launch_bounds__(256)
     nvl_pull_blocks_kernel(const __grid_constant__ PeerSet<const __nv_bfloat16> srcs, int T, int rank, int N, int H,
@@ -382,6 +421,28 @@ int ppmoe_nvl_pull_blocks(const void* const* srcs, int T, int rank, int N, int H
   nvl_pull_blocks_kernel<<<num_sms() * 4, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       peer_set<const __nv_bfloat16>(srcs, T), T, rank, N, H, static_cast<__nv_bfloat16*>(out));
   return check_launch("nvl_pull_blocks_kernel");
+}
+
+int ppmoe_nvl_cast_owned(float* acc, int rows, int H, void* out_rows, void* xch_rows, void* stream) {
+  PPMOE_REQUIRE(rows >= 0 && H % 4 == 0, "cast_owned needs hidden %% 4 == 0");
+  const size_t n4 = static_cast<size_t>(rows) * H / 4;
+  if (n4 == 0) return kOk;
+  const int grid = static_cast<int>(std::min<size_t>((n4 + 255) / 256, static_cast<size_t>(num_sms()) * 8));
+  nvl_cast_owned_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      acc, n4, static_cast<__nv_bfloat16*>(out_rows), static_cast<__nv_bfloat16*>(xch_rows));
+  return check_launch("nvl_cast_owned_kernel");
+}
+
+int ppmoe_nvl_sum_slots(const void* slots, int rows, int K, int H, int t0, const int* pair_pos, void* out_rows,
+                        void* xch_rows, void* stream) {
+  PPMOE_REQUIRE(rows >= 0 && K >= 1 && K <= 8 && H % 8 == 0, "bad sum_slots arguments");
+  const size_t n = static_cast<size_t>(rows) * (H / 8);
+  if (n == 0) return kOk;
+  const int grid = static_cast<int>(std::min<size_t>((n + 255) / 256, static_cast<size_t>(num_sms()) * 8));
+  nvl_sum_slots_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const __nv_bfloat16*>(slots), rows, K, H, t0, pair_pos, static_cast<__nv_bfloat16*>(out_rows),
+      static_cast<__nv_bfloat16*>(xch_rows));
+  return check_launch("nvl_sum_slots_kernel");
 }
 
 int ppmoe_nvl_pull_blocks_ce(const void* const* srcs, int T, int rank, int N, int H, void* out, void* stream) {

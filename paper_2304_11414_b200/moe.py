@@ -467,11 +467,30 @@ class _PPMoEFunction(torch.autograd.Function):
             # expert rows straight from the peers and the owners' blocks are all-gathered
             # (replaces reduce_from_tensor_parallel_region's all-reduce, moe.py:307)
             ar = nvlink.arena(spec.world, spec.group)
-            ym = ar.tensor("y", (_ops.local_rows_cap(n, spec.k, spec.el, cap), h), hidden.dtype)
-            st = _ops.experts_forward(hidden, pl, spec.e0, spec.el, up, down, bias_up, bias_down, spec.k,
-                                      spec.weight_scaling, None, drop_p=spec.dropout_p, seed=spec.seed, y_mirror=ym)
-            out = nvlink.exchange(ar, "y", pl.seg, spec.el, rt.idx, pl.pair_pos,
-                                  rt.w if spec.weight_scaling else None, n, h, torch.empty_like(hidden))
+            mode = nvlink.fused_forward_mode(ar, n, spec.k)
+            if mode == "slots":
+                # the fc2 epilogue stores w*Y into the owning rank's slot rows over NVLink
+                # (plain P2P stores, tile by tile during the GEMM); owners sum, then all-gather
+                table, rows = nvlink.owner_slots(ar, n, spec.k, h)
+                st = _ops.experts_forward(hidden, pl, spec.e0, spec.el, up, down, bias_up, bias_down, spec.k,
+                                          spec.weight_scaling, None, drop_p=spec.dropout_p, seed=spec.seed,
+                                          owner_slots=table, owner_rows=rows)
+                out = nvlink.finish_slots_forward(ar, n, spec.k, h, pl.pair_pos, torch.empty_like(hidden))
+            elif mode == "fused":
+                # the fc2 epilogue adds w*Y straight into the owning rank's fp32 accumulator
+                # over NVLink, tile by tile during the GEMM; owners cast, then all-gather
+                table, rows = nvlink.owner_accumulator(ar, n, h)
+                st = _ops.experts_forward(hidden, pl, spec.e0, spec.el, up, down, bias_up, bias_down, spec.k,
+                                          spec.weight_scaling, None, drop_p=spec.dropout_p, seed=spec.seed,
+                                          owner_table=table, owner_rows=rows)
+                out = nvlink.finish_fused_forward(ar, n, h, torch.empty_like(hidden))
+            else:
+                ym = ar.tensor("y", (_ops.local_rows_cap(n, spec.k, spec.el, cap), h), hidden.dtype)
+                st = _ops.experts_forward(hidden, pl, spec.e0, spec.el, up, down, bias_up, bias_down, spec.k,
+                                          spec.weight_scaling, None, drop_p=spec.dropout_p, seed=spec.seed,
+                                          y_mirror=ym)
+                out = nvlink.exchange(ar, "y", pl.seg, spec.el, rt.idx, pl.pair_pos,
+                                      rt.w if spec.weight_scaling else None, n, h, torch.empty_like(hidden))
             spec.world.charge_all_reduce(spec.group, out.numel())
         elif spec.el == e and _ops.combine_mode(hidden.dtype, h) == "owner":
             # all experts local: fc2 stores Y, the owner-gather kernel sums every token's rows

@@ -123,6 +123,13 @@ class NvlArena:
     def table(self, name: str):
         return self.bufs[name].table
 
+    def device_table(self, name: str) -> torch.Tensor:
+        """Device array of the T ranks' pointers to `name` (built once per allocation)."""
+        b = self.bufs[name]
+        if getattr(b, "dtab", None) is None:
+            b.dtab = torch.tensor(b.ptrs, dtype=torch.int64, device=self.device)
+        return b.dtab
+
     def local_table(self, name: str):
         """A T-entry pointer set that names this rank's own copy of `name` T times."""
         b = self.bufs[name]
@@ -170,6 +177,63 @@ def sum_owned_rows(ar: NvlArena, name: str, n: int, c: int) -> torch.Tensor:
     t0, t1 = owned_range(ar, n)
     out = torch.empty((t1 - t0, c), dtype=torch.float32, device=ar.device)
     call("ppmoe_nvl_sum_rows", ar.table(name), ar.tp, ar.rank, n, c, ptr(out), _lib.stream_ptr())
+    return out
+
+
+def fused_forward_mode(ar: NvlArena, n: int, k: int) -> str:
+    """Forward combine over NVLink: "gather" (owner gather after fc2, default), "slots"
+    (fc2 epilogue stores w*Y into the owner's bf16 slot rows with P2P stores) or "fused"
+    (fc2 epilogue red.adds into the owner's fp32 accumulator).  PPMOE_NVL_FWD selects."""
+    mode = os.environ.get("PPMOE_NVL_FWD", "gather")
+    if mode in ("fused", "slots") and (k > 2 or n % ar.tp):
+        mode = "gather"
+    return mode
+
+
+def owner_slots(ar: NvlArena, n: int, k: int, h: int):
+    """(device pointer table, rows per owner) of the bf16 owner slot buffers [rows x k x h]."""
+    rows = n // ar.tp
+    ar.tensor("slots", (rows, k, h), torch.bfloat16)
+    return ar.device_table("slots"), rows
+
+
+def finish_slots_forward(ar: NvlArena, n: int, k: int, h: int, pair_pos, out: torch.Tensor) -> torch.Tensor:
+    """After the owner-slot fc2: barrier -> sum the owned tokens' valid slots -> barrier ->
+    pull the other owners' blocks."""
+    rows = n // ar.tp
+    slots = ar.tensor("slots", (rows, k, h), torch.bfloat16)
+    xch = ar.tensor("xch", (n, h), torch.bfloat16)
+    s = _lib.stream_ptr()
+    ar.barrier(0)
+    t0 = ar.rank * rows
+    call("ppmoe_nvl_sum_slots", ptr(slots), rows, k, h, t0, ptr(pair_pos), ptr(out[t0:t0 + rows]),
+         ptr(xch[t0:t0 + rows]), s)
+    ar.barrier(1)
+    pull = "ppmoe_nvl_pull_blocks" if os.environ.get("PPMOE_NVL_PULL", "ce") == "sm" else "ppmoe_nvl_pull_blocks_ce"
+    call(pull, ar.table("xch"), ar.tp, ar.rank, n, h, ptr(out), s)
+    return out
+
+
+def owner_accumulator(ar: NvlArena, n: int, h: int):
+    """(device pointer table, rows per owner) of the fp32 owner accumulators."""
+    rows = n // ar.tp
+    ar.tensor("acc", (rows, h), torch.float32)
+    return ar.device_table("acc"), rows
+
+
+def finish_fused_forward(ar: NvlArena, n: int, h: int, out: torch.Tensor) -> torch.Tensor:
+    """After the owner-mode fc2: barrier -> owned accumulator rows to bf16 (zeroing them) ->
+    barrier -> pull the other owners' blocks."""
+    rows = n // ar.tp
+    acc = ar.tensor("acc", (rows, h), torch.float32)
+    xch = ar.tensor("xch", (n, h), torch.bfloat16)
+    s = _lib.stream_ptr()
+    ar.barrier(0)
+    t0 = ar.rank * rows
+    call("ppmoe_nvl_cast_owned", ptr(acc), rows, h, ptr(out[t0:t0 + rows]), ptr(xch[t0:t0 + rows]), s)
+    ar.barrier(1)
+    pull = "ppmoe_nvl_pull_blocks" if os.environ.get("PPMOE_NVL_PULL", "ce") == "sm" else "ppmoe_nvl_pull_blocks_ce"
+    call(pull, ar.table("xch"), ar.tp, ar.rank, n, h, ptr(out), s)
     return out
 
 
