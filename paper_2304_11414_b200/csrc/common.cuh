@@ -35,6 +35,24 @@ __device__ __forceinline__ float gelu_grad_f(float x) {
   return cdf + x * pdf;
 }
 
+// GeLU(x) = x Phi(x) and GeLU'(x) = Phi(x) + x phi(x) in one pass for the fc1 epilogue:
+// Phi(x) = erfc(-x/sqrt2)/2 from the Abramowitz-Stegun 7.1.26 rational form
+// erfc(z) = t(a1 + t(a2 + t(a3 + t(a4 + t a5)))) e^{-z^2}, t = 1/(1 + p z), z >= 0
+// (|error| <= 1.5e-7, no cancellation for x << 0), sharing e^{-x^2/2} with phi(x):
+// one MUFU.RCP + one MUFU.EX2 + 12 FMA per element instead of erff's branchy polynomial
+// plus a separate exp -- the fc1 epilogue was the limiter of that GEMM.
+__device__ __forceinline__ void gelu_and_grad(float x, float& act, float& grad) {
+  const float z = fabsf(x) * 0.70710678118654752f;
+  const float t = __fdividef(1.0f, fmaf(0.3275911f, z, 1.0f));
+  const float poly =
+      t * fmaf(t, fmaf(t, fmaf(t, fmaf(t, 1.061405429f, -1.453152027f), 1.421413741f), -0.284496736f), 0.254829592f);
+  const float e = __expf(-0.5f * x * x);
+  const float q = 0.5f * poly * e;  // erfc(|x|/sqrt2) / 2
+  const float cdf = x >= 0.f ? 1.0f - q : q;
+  act = x * cdf;
+  grad = fmaf(x * 0.39894228040143268f, e, cdf);
+}
+
 // Counter-based dropout keep mask: hash(seed, row, col) -> uniform in [0,1); keep if >= p.
 // The same (seed, local row, column) regenerates the mask in the backward.
 __host__ __device__ __forceinline__ float dropout_uniform(unsigned long long seed, int row, int col) {

@@ -118,10 +118,7 @@ struct EpiFc1Fwd {
     float d[W], a[W];
 #pragma unroll
     for (int j = 0; j < W; ++j) {
-      const float x = v[j] + b[j];
-      const float cdf = 0.5f * (1.0f + erff(x * 0.70710678118654752f));
-      a[j] = x * cdf;
-      d[j] = cdf + x * (__expf(-0.5f * x * x) * 0.39894228040143268f);
+      gelu_and_grad(v[j] + b[j], a[j], d[j]);
     }
     const size_t off = static_cast<size_t>(row) * F + n0;
     store_row<T, W>(gelu_grad + off, d, valid, cs);

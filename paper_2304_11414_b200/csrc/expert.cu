@@ -49,7 +49,7 @@ static int launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const GroupGe
     auto kern = grouped_gemm_sm100_pair<kBN, A_MN, B_MN, Epi>;
     constexpr int smem = PairSmem<kBN>::kTotal;
     PPMOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    kern<<<gemm_ctas() / 2 * 2, kGemmThreads, smem, s>>>(ta, tb, geo, epi);
+    kern<<<gemm_ctas() / 2 * 2, kPairThreads, smem, s>>>(ta, tb, geo, epi);
     return check_launch("grouped_gemm_sm100_pair");
   }
   auto kern = grouped_gemm_sm100<kBN, A_MN, B_MN, Epi>;

@@ -312,6 +312,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 //   tmem_empty[a](leader) 8 arrivals: 4 epilogue warps x 2 CTAs
 constexpr int kPairBM = 256;
 constexpr int kPairStages = 6;
+// CTA-pair kernel: warp0 TMA, warp1 MMA, warps 2..9 epilogue (warp2 also allocates TMEM)
+constexpr int kPairEpiWarps = 8;
+constexpr int kPairThreads = 32 * (2 + kPairEpiWarps);
 
 template <int BN>
 struct PairSmem {
@@ -326,7 +329,7 @@ struct PairSmem {
 };
 
 template <int BN, bool A_MN, bool B_MN, class Epi>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     grouped_gemm_sm100_pair(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                             GroupGeom geo, Epi epi) {
   using L = PairSmem<BN>;
@@ -378,7 +381,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tmem_full[a], 1);
-      mbar_init(&tmem_empty[a], 8);
+      mbar_init(&tmem_empty[a], 2 * kPairEpiWarps);  // every epilogue warp of both CTAs
     }
     fence_mbar_init();
   }
@@ -489,9 +492,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       }
     }
     __syncwarp();
-  } else if (warp >= 4) {
+  } else if (warp >= 2) {
     // ------------------------------------------------------------ epilogue (both CTAs)
+    // kPairEpiWarps warps: warp w reads TMEM lane quarter w % 4 (the hardware rule) and
+    // one of the column halves, so two warps per SM sub-partition share each tile's
+    // epilogue (latency of tcgen05.ld / the stores overlaps across them).
     const int q = warp & 3;
+    const int half = (warp - 2) >> 2;
+    constexpr int kChunksPerWarp = BN / 32 / (kPairEpiWarps / 4);
     const int row_in_tile = static_cast<int>(rank) * 128 + q * 32 + lane;
     const uint32_t empty_leader = mapa_shared(&tmem_empty[0], 0);
     int iter = 0;
@@ -508,7 +516,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
       const int m = mt * kPairBM + row_in_tile;
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = half * kChunksPerWarp; c < (half + 1) * kChunksPerWarp; ++c) {
         float v[32];
         tmem_ld32(taddr + c * 32, v);
         if (!has_k) {
