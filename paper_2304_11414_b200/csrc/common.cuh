@@ -275,6 +275,14 @@ __host__ __device__ constexpr uint32_t make_idesc_bf16(int M, int N, bool a_mn_m
 }
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+// One lane of the (fully active) warp, chosen by the hardware.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
 __device__ __forceinline__ int warp_id() { return threadIdx.x >> 5; }
 
 }  // namespace ppmoe

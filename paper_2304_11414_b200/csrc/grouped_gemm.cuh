@@ -453,12 +453,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     __syncwarp();
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (leader only)
-    if (leader && lane == 0) {
+    // The whole warp runs the loop (warp-uniform descriptor math lands in uniform
+    // registers, no per-instruction waterfall) and one elected lane issues each MMA: the
+    // issue stream must keep up with the tensor pipe while two epilogue warps share this
+    // SM sub-partition.
+    if (leader) {
       constexpr uint32_t idesc = make_idesc_bf16(kPairBM, BN, A_MN, B_MN);
       constexpr uint32_t a_lbo = A_MN ? (64 * kBK * 2) : 16;
       constexpr uint32_t b_lbo = B_MN ? (64 * kBK * 2) : 16;
       constexpr uint32_t k_step_a = A_MN ? (kUMMAK * 128) : (kUMMAK * 2);
       constexpr uint32_t k_step_b = B_MN ? (kUMMAK * 128) : (kUMMAK * 2);
+      const bool elected = elect_one();
       int stage = 0;
       uint32_t phase = 0;
       int iter = 0;
@@ -480,15 +485,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           for (int k = 0; k < kBK / kUMMAK; ++k) {
             const uint64_t ad = make_sdesc(sa + k * k_step_a, a_lbo, 1024);
             const uint64_t bd = make_sdesc(sb + k * k_step_b, b_lbo, 1024);
-            umma_bf16_pair(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+            if (elected) umma_bf16_pair(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
           }
-          umma_commit_pair_mc(&empty[stage], 0x3);
+          if (elected) umma_commit_pair_mc(&empty[stage], 0x3);
+          __syncwarp();
           if (++stage == kPairStages) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit_pair_mc(&tmem_full[acc], 0x3);
+        if (elected) umma_commit_pair_mc(&tmem_full[acc], 0x3);
+        __syncwarp();
       }
     }
     __syncwarp();
