@@ -424,7 +424,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           pol_b = (geo.hint && !a_res) ? kL2EvictFirst : kNormal;
         }
         for (int kb = 0; kb < kb_n; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_wait_sleep(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * L::kStageBytes;
           uint8_t* sb = sa + L::kABytes;
           const uint32_t fbar = mapa_shared(&full[stage], 0);
@@ -518,7 +518,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       const bool has_k = tab.k_blocks[g] > 0;
       const int acc = iter & 1;
       const uint32_t acc_phase = (iter >> 1) & 1;
-      mbar_wait(&tmem_full[acc], acc_phase);
+      mbar_wait_sleep(&tmem_full[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
       const int m = mt * kPairBM + row_in_tile;
