@@ -522,16 +522,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       tc_fence_after();
       const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
       const int m = mt * kPairBM + row_in_tile;
+      static_assert(kChunksPerWarp % 2 == 0, "64-column TMEM loads");
 #pragma unroll 1
-      for (int c = half * kChunksPerWarp; c < (half + 1) * kChunksPerWarp; ++c) {
-        float v[32];
-        tmem_ld32(taddr + c * 32, v);
+      for (int c = half * kChunksPerWarp; c < (half + 1) * kChunksPerWarp; c += 2) {
+        float v[64];
+        tmem_ld64(taddr + c * 32, v);
         if (!has_k) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = 0.f;
+          for (int j = 0; j < 64; ++j) v[j] = 0.f;
         }
+        const bool row_ok = m < tab.m_rows[g];
         const int n0 = nt * BN + c * 32;
-        if (n0 < geo.N && m < tab.m_rows[g]) epi.template apply<32>(g, m, tab.row_base[g] + m, n0, v);
+        if (n0 < geo.N && row_ok)
+          epi.template apply<32>(g, m, tab.row_base[g] + m, n0, *reinterpret_cast<const float(*)[32]>(v));
+        if (n0 + 32 < geo.N && row_ok)
+          epi.template apply<32>(g, m, tab.row_base[g] + m, n0 + 32, *reinterpret_cast<const float(*)[32]>(v + 32));
       }
       tc_fence_before();
       __syncwarp();
