@@ -11,10 +11,25 @@
 
 namespace ppmoe {
 
-// `cs`: store with the streaming (evict-first) cache policy.
+// `cs`: 2 = 32-byte stores, 1 = 16-byte stores with the streaming (evict-first) cache
+// policy, 0 = plain 16-byte stores (default: measured fastest in the C2 step).
 template <typename T, int W>
-__device__ __forceinline__ void store_row(T* p, const float (&x)[W], int valid, bool cs = false) {
+__device__ __forceinline__ void store_row(T* p, const float (&x)[W], int valid, int cs = 0) {
   if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+    if (cs == 2 && valid >= W && (W % 16 == 0) && (reinterpret_cast<uintptr_t>(p) & 31) == 0) {
+      // 32-byte stores: every lane writes whole L2 sectors (the lanes of a warp hold
+      // different rows, so 16-byte stores left each sector half written per instruction)
+#pragma unroll
+      for (int j = 0; j < W; j += 16) {
+        uint32_t u[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) u[i] = pack_bf16x2(x[j + 2 * i], x[j + 2 * i + 1]);
+        asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p + j), "r"(u[0]), "r"(u[1]),
+                     "r"(u[2]), "r"(u[3]), "r"(u[4]), "r"(u[5]), "r"(u[6]), "r"(u[7])
+                     : "memory");
+      }
+      return;
+    }
     if (valid >= W && (W % 8 == 0) && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
 #pragma unroll
       for (int j = 0; j < W; j += 8) {
@@ -23,7 +38,7 @@ __device__ __forceinline__ void store_row(T* p, const float (&x)[W], int valid, 
         u.y = pack_bf16x2(x[j + 2], x[j + 3]);
         u.z = pack_bf16x2(x[j + 4], x[j + 5]);
         u.w = pack_bf16x2(x[j + 6], x[j + 7]);
-        if (cs) st_cs_v4(p + j, u);
+        if (cs == 1) st_cs_v4(p + j, u);
         else *reinterpret_cast<uint4*>(p + j) = u;
       }
       return;

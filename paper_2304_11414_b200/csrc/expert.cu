@@ -146,12 +146,14 @@ static int load_hint() {
   }();
   return v;
 }
+// Epilogue store flavour: 0 = plain 16-byte stores (default), 1 = 16-byte evict-first
+// (PPMOE_STORE=cs), 2 = 32-byte stores (PPMOE_STORE=v8; measured 5 % slower in the C2
+// step).  Read per launch (A/B runs).
 static int stream_stores() {
-  static const int v = [] {
-    const char* e = getenv("PPMOE_STORE");
-    return (e && strcmp(e, "cs") == 0) ? 1 : 0;
-  }();
-  return v;
+  const char* e = getenv("PPMOE_STORE");
+  if (e && strcmp(e, "cs") == 0) return 1;
+  if (e && strcmp(e, "v8") == 0) return 2;
+  return 0;
 }
 
 // Bias gradient from per-32-row-block column partials: out[g][c] = sum of the blocks of
