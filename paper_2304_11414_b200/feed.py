@@ -42,8 +42,9 @@ class ReplicatedFeed:
         self.pending: list = []
         self.next = 0
         self.arena = None
-        if (self.tp > 1 and dtype == torch.bfloat16 and os.environ.get("PPMOE_FEED", "nvl") == "nvl"):
-            from . import nvlink
+        from . import nvlink
+        if (self.tp > 1 and os.environ.get("PPMOE_FEED", "nvl") == "nvl"
+                and nvlink.enabled(world, group, dtype, shape[1])):
             self.arena = nvlink.arena(world, group)
             self.bufs = [self.arena.tensor(f"feed{i}", self.shape, dtype) for i in range(depth)]
         else:

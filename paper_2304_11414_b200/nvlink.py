@@ -150,6 +150,9 @@ class NvlArena:
             raise RuntimeError("NVLink barrier timed out: a peer of the tensor group stopped responding")
 
 
+_UNAVAILABLE: set = set()
+
+
 def arena(world, group) -> NvlArena:
     key = (id(world), group.members)
     a = _ARENAS.get(key)
@@ -159,11 +162,37 @@ def arena(world, group) -> NvlArena:
     return a
 
 
+def _probe(world, group) -> bool:
+    """Create the group's arena once; every rank learns whether all of them could map
+    their peers (a MIN all-reduce), so the group takes the same path everywhere."""
+    key = (id(world), group.members)
+    if key in _ARENAS:
+        return True
+    if key in _UNAVAILABLE:
+        return False
+    ok = 1
+    try:
+        arena(world, group)
+    except Exception as exc:  # no P2P / IPC on this box: fall back to NCCL, loudly
+        import warnings
+        warnings.warn(f"NVLink exchange unavailable, using NCCL all-reduces: {exc}")
+        ok = 0
+    flag = torch.tensor([ok], dtype=torch.int32, device=torch.device("cuda", torch.cuda.current_device()))
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=world.torch_group(group))
+    if int(flag.item()) == 0:
+        _UNAVAILABLE.add(key)
+        _ARENAS.pop(key, None)
+        return False
+    return True
+
+
 def enabled(world, group, dtype: torch.dtype, hidden: int) -> bool:
     """NVLink exchange for distributed bf16 groups of 2..8 ranks (PPMOE_TP_COMM=nccl opts out)."""
     if os.environ.get("PPMOE_TP_COMM", "nvl") != "nvl":
         return False
-    return (world.distributed and 1 < group.size <= 8 and dtype == torch.bfloat16 and hidden % 8 == 0)
+    if not (world.distributed and 1 < group.size <= 8 and dtype == torch.bfloat16 and hidden % 8 == 0):
+        return False
+    return _probe(world, group)
 
 
 def owned_range(ar: NvlArena, n: int) -> tuple[int, int]:

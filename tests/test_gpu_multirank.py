@@ -70,7 +70,7 @@ def _worker(rank, world, port, q, k, cf):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,k,cf", [(2, 2, float("inf")), (2, 1, 1.0)])
+@pytest.mark.parametrize("world,k,cf", [(2, 2, float("inf")), (2, 1, 1.0), (4, 2, 1.25)])
 def test_tp_nccl_matches_simulated(world, k, cf):
     if torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
