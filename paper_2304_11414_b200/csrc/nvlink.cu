@@ -449,12 +449,36 @@ int ppmoe_nvl_pull_blocks_ce(const void* const* srcs, int T, int rank, int N, in
   PPMOE_REQUIRE(T >= 1 && T <= kNvlMaxRanks && rank >= 0 && rank < T, "bad group T=%d rank=%d", T, rank);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const size_t row = static_cast<size_t>(H) * 2;
-  for (int q0 = 1; q0 < T; ++q0) {  // one copy-engine transfer per peer block, staggered sources
-    const int q = (rank + q0) % T;
+  // One copy-engine transfer per peer block, each on its own stream so the T-1 transfers
+  // run concurrently on different copy engines (forked from / joined back to `stream`).
+  static thread_local cudaStream_t side[kNvlMaxRanks] = {};
+  static thread_local cudaEvent_t fork = nullptr, join[kNvlMaxRanks] = {};
+  static thread_local int dev_of = -1;
+  int dev = 0;
+  PPMOE_CUDA(cudaGetDevice(&dev));
+  if (dev_of != dev) {
+    for (int i = 0; i < kNvlMaxRanks; ++i) {
+      PPMOE_CUDA(cudaStreamCreateWithFlags(&side[i], cudaStreamNonBlocking));
+      PPMOE_CUDA(cudaEventCreateWithFlags(&join[i], cudaEventDisableTiming));
+    }
+    PPMOE_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    dev_of = dev;
+  }
+  const char* ser = getenv("PPMOE_CE_SERIAL");
+  const bool split = !(ser && ser[0] == '1');
+  if (split) PPMOE_CUDA(cudaEventRecord(fork, s));
+  for (int q0 = 1; q0 < T; ++q0) {
+    const int q = (rank + q0) % T;  // staggered sources
     const size_t lo = static_cast<size_t>(q) * N / T, hi = static_cast<size_t>(q + 1) * N / T;
-    if (hi > lo)
-      PPMOE_CUDA(cudaMemcpyAsync(static_cast<char*>(out) + lo * row, static_cast<const char*>(srcs[q]) + lo * row,
-                                 (hi - lo) * row, cudaMemcpyDeviceToDevice, s));
+    if (hi <= lo) continue;
+    cudaStream_t cs = split ? side[q0] : s;
+    if (split) PPMOE_CUDA(cudaStreamWaitEvent(cs, fork, 0));
+    PPMOE_CUDA(cudaMemcpyAsync(static_cast<char*>(out) + lo * row, static_cast<const char*>(srcs[q]) + lo * row,
+                               (hi - lo) * row, cudaMemcpyDeviceToDevice, cs));
+    if (split) {
+      PPMOE_CUDA(cudaEventRecord(join[q0], cs));
+      PPMOE_CUDA(cudaStreamWaitEvent(s, join[q0], 0));
+    }
   }
   return kOk;
 }
