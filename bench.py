@@ -108,15 +108,16 @@ class ClockSampler:
         for line in self.proc.stdout:
             parts = [x.strip() for x in line.split(",")]
             try:
-                self.sm.append(float(parts[1]))
-                self.smax.append(float(parts[2]))
+                rec = (time.perf_counter(), float(parts[1]), float(parts[2]),
+                       {nm for nm, v in zip(self.NAMES, parts[3:7]) if v.lower().startswith("active")})
             except (ValueError, IndexError):
                 continue
-            for nm, v in zip(self.NAMES, parts[3:7]):
-                if v.lower().startswith("active"):
-                    self.reasons.add(nm)
+            self.samples.append(rec)
 
     def __enter__(self):
+        """Start sampling (before the warm-up: nvidia-smi needs ~0.5 s to its first line);
+        only samples inside mark_start()/mark_end() count."""
+        self.samples, self.t0, self.t1 = [], None, None
         if not self.active:
             return self
         try:
@@ -126,10 +127,20 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
-            time.sleep(0.3)  # first sample lands before the timed region starts
         except OSError:
             self.proc = None
         return self
+
+    def mark_start(self):
+        self.t0 = time.perf_counter()
+
+    def mark_end(self):
+        self.t1 = time.perf_counter()
+        # a timed region shorter than the sampling period still gets the next sample
+        deadline = self.t1 + 4 * self.period / 1e3
+        while self.proc is not None and time.perf_counter() < deadline and not any(
+                r[0] >= self.t1 for r in self.samples):
+            time.sleep(self.period / 4e3)
 
     def __exit__(self, *exc):
         if self.proc is not None:
@@ -143,10 +154,20 @@ class ClockSampler:
         return False
 
     def summary(self):
-        if not self.sm:
+        recs = list(self.samples)
+        if self.t0 is not None and self.t1 is not None:
+            inside = [r for r in recs if self.t0 <= r[0] <= self.t1]
+            if not inside:  # region shorter than the period: the samples bracketing it
+                before = [r for r in recs if r[0] < self.t0][-1:]
+                after = [r for r in recs if r[0] > self.t1][:1]
+                inside = before + after
+            recs = inside
+        if not recs:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": max(self.smax), "reasons": sorted(self.reasons),
-                "samples": len(self.sm), "sm_mhz_min": min(self.sm), "gpus": len(self.indices)}
+        sm = [r[1] for r in recs]
+        reasons = set().union(*(r[3] for r in recs))
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(r[2] for r in recs), "reasons": sorted(reasons),
+                "samples": len(sm), "sm_mhz_min": min(sm), "gpus": len(self.indices)}
 
 
 # ----------------------------------------------------------------------------- CPU baseline
@@ -288,6 +309,8 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    clk = ClockSampler(range(world_size), active=(rank == 0))
+    clk.__enter__()  # sampling starts before the warm-up; only the timed window counts
     for _ in range(a.warmup):
         step(x)
     barrier()
@@ -295,13 +318,16 @@ def main():
     lib = _lib.load()
     launches0 = lib.ppmoe_kernel_launches()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(range(world_size), active=(rank == 0)) as clk, _ops.KernelProfile() as prof:
+    with _ops.KernelProfile() as prof:
         barrier()
+        clk.mark_start()
         ev0.record()
         for _ in range(a.steps):
             step(x)
         ev1.record()
         barrier()
+        clk.mark_end()
+    clk.__exit__(None, None, None)
     launches = lib.ppmoe_kernel_launches() - launches0
     ms = ev0.elapsed_time(ev1) / a.steps
     t = torch.tensor([ms], device=dev, dtype=torch.float64)
