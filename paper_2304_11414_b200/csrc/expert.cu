@@ -133,11 +133,8 @@ static int colsum(const void* src, int ld, const int* seg, int G, int N, void* o
 // banded order) and the epilogue store cache policy (streaming by default;
 // PPMOE_STORE=normal disables it).
 static int banded_order() {
-  static const int v = [] {
-    const char* e = getenv("PPMOE_ORDER");
-    return (e && strcmp(e, "band") == 0) ? 1 : 0;
-  }();
-  return v;
+  const char* e = getenv("PPMOE_ORDER");
+  return (e && strcmp(e, "band") == 0) ? 1 : 0;
 }
 static int load_hint() {
   static const int v = [] {
@@ -189,6 +186,10 @@ static GroupGeom geom(int G, int N, int M_fixed, int K_fixed, const int* seg, in
   g.rlo = nullptr;
   g.rhi = nullptr;
   g.banded = banded_order();
+  {
+    const char* e = getenv("PPMOE_NFAST");
+    g.nfast = e ? atoi(e) : -1;
+  }
   g.hint = load_hint();
   g.G = G;
   g.N = N;

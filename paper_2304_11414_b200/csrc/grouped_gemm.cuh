@@ -42,6 +42,7 @@ struct GroupGeom {
   const int* rlo; // optional [G] local first row of each group (token chunk of a segment)
   const int* rhi; // optional [G] local end row; when set, M_g = rhi - rlo (seg ignored for rows)
   int banded;     // 1: banded 2-D tile order with L2 residency hints, 0: panel order
+  int nfast;      // -1: fast dimension chosen by panel size; 0 / 1: force M / N fast
   int hint;       // panel order: load the streaming operand with evict-first priority
 };
 
@@ -148,7 +149,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       tab.k_blocks[g] = (K + kBK - 1) / kBK;
       tab.a_base[g] = geo.a_seg ? seg_lo : g * geo.a_stride;
       tab.b_base[g] = geo.b_seg ? seg_lo : g * geo.b_stride;
-      tab.n_fast[g] = M > geo.N ? 1 : 0;
+      tab.n_fast[g] = geo.nfast >= 0 ? geo.nfast : (M > geo.N ? 1 : 0);
       tab.m_rows[g] = M;
       tab.row_base[g] = seg_lo;
       acc += tab.m_tiles[g] * n_tiles;
@@ -369,7 +370,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       tab.k_blocks[g] = (K + kBK - 1) / kBK;
       tab.a_base[g] = geo.a_seg ? seg_lo : g * geo.a_stride;
       tab.b_base[g] = geo.b_seg ? seg_lo : g * geo.b_stride;
-      tab.n_fast[g] = M > geo.N ? 1 : 0;
+      tab.n_fast[g] = geo.nfast >= 0 ? geo.nfast : (M > geo.N ? 1 : 0);
       tab.m_rows[g] = M;
       tab.row_base[g] = seg_lo;
       acc += tab.m_tiles[g] * n_tiles;
