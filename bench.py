@@ -388,7 +388,7 @@ def main():
                 if i + 1 < steps:
                     feed.submit(x_host)
                 out, l_aux = step(xin)
-                loss = out.float().sum() + l_aux
+                loss = out.sum(dtype=torch.float32) + l_aux
                 loss_host[i % 2].copy_(loss.detach().reshape(1), non_blocking=True)
                 loss_ev[i % 2].record()
                 if i > 0:

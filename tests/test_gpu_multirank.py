@@ -34,8 +34,10 @@ def _collect(q, procs, timeout=240):
     return got
 
 
-def _worker(rank, world, port, q, k, cf):
+def _worker(rank, world, port, q, k, cf, env=None):
     import torch.distributed as dist
+
+    os.environ.update(env or {})
 
     import paper_2304_11414_b200 as P
 
@@ -70,8 +72,12 @@ def _worker(rank, world, port, q, k, cf):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,k,cf", [(2, 2, float("inf")), (2, 1, 1.0), (4, 2, 1.25)])
-def test_tp_nccl_matches_simulated(world, k, cf):
+@pytest.mark.parametrize("world,k,cf,env", [
+    (2, 2, float("inf"), {}), (2, 1, 1.0, {}), (4, 2, 1.25, {}),
+    (2, 2, 1.25, {"PPMOE_NVL_FWD": "fused"}), (2, 2, float("inf"), {"PPMOE_NVL_FWD": "slots"}),
+    (2, 2, float("inf"), {"PPMOE_TP_COMM": "nccl"}), (2, 2, float("inf"), {"PPMOE_NVL_PUSH": "1", "PPMOE_NVL_PULL": "sm"}),
+])
+def test_tp_nccl_matches_simulated(world, k, cf, env):
     if torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
     import paper_2304_11414_b200 as P
@@ -79,7 +85,7 @@ def test_tp_nccl_matches_simulated(world, k, cf):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = 29600 + os.getpid() % 500
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q, k, cf)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, k, cf, env)) for r in range(world)]
     for p in procs:
         p.start()
     got = _collect(q, procs)
