@@ -4,9 +4,12 @@
 of the group can address directly (CUDA IPC handles exchanged once through
 torch.distributed), a signal pad per rank for the cross-GPU barriers, and the epoch
 counters of those barriers.  The kernels that use it live in csrc/nvlink.cu
-(ppmoe_nvl_barrier / ppmoe_nvl_owner_gather / ppmoe_nvl_pull_blocks); moe.py calls
-``exchange_forward`` / ``exchange_backward`` in place of the two [N x H] all-reduces of
-the reference (moe.py:307, collectives.py:205-228).
+(ppmoe_nvl_barrier / ppmoe_nvl_owner_gather / ppmoe_nvl_pull_blocks[_ce] /
+ppmoe_nvl_sum_rows); moe.py calls ``exchange`` (forward: the experts' Y rows; backward:
+their per-row dX plus the gate term) in place of the two [N x H] all-reduces of the
+reference (moe.py:307, collectives.py:205-228).  Barrier channels 0/1 belong to the
+layer's exchange, 2/3 to the host feed (feed.py).  ``enabled`` probes the group once and
+falls back to NCCL everywhere if any rank cannot map its peers.
 
 Buffers are allocated collectively: every rank requests the same names and sizes in the
 same order (the sizes are functions of the layer shape only), so the arenas stay in
