@@ -244,11 +244,12 @@ int ppmoe_nvl_barrier(void* const* pads, int T, int rank, int ch, unsigned int e
  * backward), dl = this rank's summed dL rows [t1-t0 x E] fp32 (from ppmoe_nvl_sum_rows;
  * E <= 128).  Writes the owned rows of out (local [N x H]) and either of out_sym (this
  * rank's peer-visible copy, push NULL: peers pull; may be NULL) or of every rank's
- * exchange buffer push[q] (P2P stores, then a local pull).  With T = 1 it is the
- * single-GPU top-k combine / input-gradient gather.                                     */
+ * exchange buffer push[q] (P2P stores, then a local pull).  sym_mc = 1: out_sym is an
+ * NVLS multicast address (multimem.st: one store reaches every rank's buffer, then a
+ * local copy).  With T = 1 it is the single-GPU top-k combine / input-gradient gather.  */
 int ppmoe_nvl_owner_gather(const void* const* rows, const int* seg, int El, const int* idx, const int* pair_pos,
                            const float* w, int N, int K, int H, int T, int rank, const float* dl, const float* Wg,
-                           int E, void* out, void* out_sym, void* const* push, void* stream);
+                           int E, void* out, void* out_sym, void* const* push, int sym_mc, void* stream);
 /* out [t1-t0 x C] = sum over q (rank order) of srcs[q] rows [t0, t1) (fp32 [N x C]): the
  * owned rows of the ranks' partial gate-logit gradients.                               */
 int ppmoe_nvl_sum_rows(const void* const* srcs, int T, int rank, int N, int C, float* out, void* stream);

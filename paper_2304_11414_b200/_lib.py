@@ -54,7 +54,7 @@ _SIGNATURES = {
     "ppmoe_ipc_free": (_I, [_P]),
     "ppmoe_nvl_pad_bytes": (_S, []),
     "ppmoe_nvl_barrier": (_I, [_P, _I, _I, _I, _UI, _P, _LL, _P]),
-    "ppmoe_nvl_owner_gather": (_I, [_P, _P, _I, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _I, _P, _P, _P, _P]),
+    "ppmoe_nvl_owner_gather": (_I, [_P, _P, _I, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _I, _P, _P, _P, _I, _P]),
     "ppmoe_nvl_pull_blocks": (_I, [_P, _I, _I, _I, _I, _P, _P]),
     "ppmoe_nvl_sum_rows": (_I, [_P, _I, _I, _I, _I, _P, _P]),
     "ppmoe_nvl_pull_blocks_ce": (_I, [_P, _I, _I, _I, _I, _P, _P]),

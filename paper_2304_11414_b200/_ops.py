@@ -361,7 +361,7 @@ def local_combine(rows: torch.Tensor, st: ExpertFwdState, pl: Plan, idx: torch.T
     e = wg.shape[1] if wg is not None else 0
     rows_set = (ctypes.c_void_p * 1)(rows.data_ptr())
     call("ppmoe_nvl_owner_gather", rows_set, ptr(pl.seg), st.el, ptr(idx), ptr(pl.pair_pos), ptr(w), n, k, h, 1, 0,
-         ptr(dl), ptr(wg), e, ptr(out), None, None, _stream())
+         ptr(dl), ptr(wg), e, ptr(out), None, None, 0, _stream())
     return out
 
 

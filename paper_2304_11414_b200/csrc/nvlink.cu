@@ -100,6 +100,15 @@ __device__ __forceinline__ uint4 pack_bf16x8(const float (&a)[8]) {
 constexpr int kOgTile = 32;
 constexpr int kOgMaxE = 128;
 
+__device__ __forceinline__ void multimem_store(__nv_bfloat16* mc, const uint4& v) {
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(mc), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void multimem_store(__nv_bfloat16* mc, const uint2& v) {
+  asm volatile("multimem.st.relaxed.sys.global.v2.f32 [%0], {%1, %2};" ::"l"(mc), "r"(v.x), "r"(v.y) : "memory");
+}
+
 template <int CW> struct OgVec;
 template <> struct OgVec<8> { using type = uint4; };
 template <> struct OgVec<4> { using type = uint2; };
@@ -123,7 +132,7 @@ __global__ void __launch_bounds__(256)
                             const float* __restrict__ w, int Kr, int H, int t0, int t1,
                             const float* __restrict__ dl, const float* __restrict__ Wg, int E,
                             __nv_bfloat16* __restrict__ out, __nv_bfloat16* __restrict__ out_sym,
-                            const __grid_constant__ PeerSet<__nv_bfloat16> push, int T) {
+                            const __grid_constant__ PeerSet<__nv_bfloat16> push, int T, int sym_mc) {
   using V = typename OgVec<CW>::type;
   constexpr int KS = KT > 0 ? KT : 8;
   constexpr int DLW = EB > 0 ? EB : (EB < 0 ? kOgMaxE : 1);
@@ -221,6 +230,8 @@ __global__ void __launch_bounds__(256)
         *reinterpret_cast<V*>(out + off) = o;
         if (push.p[0]) {  // the owned row straight into every rank's exchange buffer (P2P stores)
           for (int q = 0; q < T; ++q) *reinterpret_cast<V*>(push.p[q] + off) = o;
+        } else if (out_sym && sym_mc) {  // NVLS multicast: one store lands in every rank's buffer
+          multimem_store(out_sym + off, o);
         } else if (out_sym) {
           *reinterpret_cast<V*>(out_sym + off) = o;
         }
@@ -363,9 +374,10 @@ int ppmoe_nvl_barrier(void* const* pads, int T, int rank, int ch, unsigned int e
 
 int ppmoe_nvl_owner_gather(const void* const* rows, const int* seg, int El, const int* idx, const int* pair_pos,
                            const float* w, int N, int K, int H, int T, int rank, const float* dl, const float* Wg,
-                           int E, void* out, void* out_sym, void* const* push, void* stream) {
+                           int E, void* out, void* out_sym, void* const* push, int sym_mc, void* stream) {
   PPMOE_REQUIRE(T >= 1 && T <= kNvlMaxRanks && rank >= 0 && rank < T, "bad group T=%d rank=%d", T, rank);
   PPMOE_REQUIRE(K >= 1 && K <= 8 && H % 8 == 0 && El >= 1, "owner gather needs 1 <= k <= 8 and hidden %% 8 == 0");
+  PPMOE_REQUIRE(!sym_mc || (out_sym && !push), "multicast output needs out_sym and no push set");
   PPMOE_REQUIRE(N / T < (1 << 30), "too many tokens");
   PPMOE_REQUIRE(!dl || (Wg && E >= 1 && E <= kOgMaxE), "the gate term supports 1 <= E <= %d", kOgMaxE);
   const int t0 = static_cast<int>(static_cast<long long>(rank) * N / T);
@@ -383,7 +395,7 @@ int ppmoe_nvl_owner_gather(const void* const* rows, const int* seg, int El, cons
   do {                                                                                                     \
     const int gy_ = (H / CW + 255) / 256;                                                                  \
     nvl_owner_gather_kernel<EB, U, KT, CW><<<dim3(max(1, min(tiles, num_sms() * og_ctas_per_sm() / gy_)), gy_), 256, 0, s>>>( \
-        R, seg, El, idx, pair_pos, w, K, H, t0, t1, dl, Wg, E, O, OS, P, T);                               \
+        R, seg, El, idx, pair_pos, w, K, H, t0, t1, dl, Wg, E, O, OS, P, T, sym_mc);                       \
   } while (0)
   if (!dl) {
     if (K == 2 && og_fwd_cw() == 4) PPMOE_OG(0, 8, 2, 4);

@@ -101,6 +101,8 @@ class NvlArena:
         self.err = torch.zeros(1, dtype=torch.int32, device=self.device)
         self.epoch = [0] * 8
         self.bufs: dict = {}
+        self.mc_bufs: dict = {}
+        self.mc_disabled = False
         self.stream = torch.cuda.Stream(device=self.device)  # exchange beside the weight-gradient GEMMs
 
     # ------------------------------------------------------------------ buffers
@@ -132,6 +134,34 @@ class NvlArena:
         if getattr(b, "dtab", None) is None:
             b.dtab = torch.tensor(b.ptrs, dtype=torch.int64, device=self.device)
         return b.dtab
+
+    def multicast(self, name: str, shape):
+        """(local bf16 tensor, NVLS multicast address) of a symmetric buffer of the group
+        (torch symmetric memory), or None when the box has no multicast; grown collectively."""
+        if self.mc_disabled:
+            return None
+        n = shape[0] * shape[1]
+        cur = self.mc_bufs.get(name)
+        if cur is None or cur[0].numel() < n:
+            ok, entry = 1, None
+            try:
+                import torch.distributed._symmetric_memory as symm_mem
+                t = symm_mem.empty(n, dtype=torch.bfloat16, device=self.device)
+                hdl = symm_mem.rendezvous(t, self.torch_group)
+                mc = int(getattr(hdl, "multicast_ptr", 0) or 0)
+                ok = 1 if mc else 0
+                entry = (t, mc, hdl)
+            except Exception:
+                ok = 0
+            flag = torch.tensor([ok], dtype=torch.int32, device=self.device)
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=self.torch_group)
+            if int(flag.item()) == 0:
+                self.mc_disabled = True
+                return None
+            self.mc_bufs[name] = entry
+            cur = entry
+        t, mc, _ = cur
+        return t[:n].view(shape), mc
 
     def local_table(self, name: str):
         """A T-entry pointer set that names this rank's own copy of `name` T times."""
@@ -274,16 +304,28 @@ def exchange(ar: NvlArena, rows_name: str, seg, el: int, idx, pair_pos, w, n: in
              barrier_first: bool = True) -> torch.Tensor:
     """out = the replicated sum over the group of every token's expert rows (+ the gate term
     dl_own . Wg^T of the owned rows), see nvlink.cu: barrier -> owner gather (P2P reads) ->
-    barrier -> pull the other owners' blocks."""
+    barrier -> all-gather of the owners' blocks: copy-engine pulls of the peers' blocks, or
+    (PPMOE_NVL_MC=1, NVSwitch multicast) an NVLS multimem store from the owner gather that
+    reaches every rank's buffer, then a local copy.  The multicast form is correct but
+    measured slower at T = 4 (the multimem stores make the owner gather 2x slower than the
+    pull they save)."""
     k = pair_pos.shape[1]
-    xch = ar.tensor("xch", (n, h), torch.bfloat16)
     s = _lib.stream_ptr()
     if barrier_first:
         ar.barrier(0)
     e = wg.shape[1] if wg is not None else 0
+    mc = ar.multicast("xchmc", (n, h)) if os.environ.get("PPMOE_NVL_MC", "0") == "1" else None
+    if mc is not None:
+        local, mc_ptr = mc
+        call("ppmoe_nvl_owner_gather", ar.table(rows_name), ptr(seg), el, ptr(idx), ptr(pair_pos), ptr(w), n, k, h,
+             ar.tp, ar.rank, ptr(dl_own), ptr(wg), e, ptr(out), ctypes.c_void_p(mc_ptr), None, 1, s)
+        ar.barrier(1)  # every owner's multicast rows have landed everywhere
+        call("ppmoe_nvl_pull_blocks", ptr_set([local.data_ptr()] * ar.tp), ar.tp, ar.rank, n, h, ptr(out), s)
+        return out
+    xch = ar.tensor("xch", (n, h), torch.bfloat16)
     push = os.environ.get("PPMOE_NVL_PUSH", "0") == "1"
     call("ppmoe_nvl_owner_gather", ar.table(rows_name), ptr(seg), el, ptr(idx), ptr(pair_pos), ptr(w), n, k, h,
-         ar.tp, ar.rank, ptr(dl_own), ptr(wg), e, ptr(out), ptr(xch), ar.table("xch") if push else None, s)
+         ar.tp, ar.rank, ptr(dl_own), ptr(wg), e, ptr(out), ptr(xch), ar.table("xch") if push else None, 0, s)
     ar.barrier(1)
     # push: every block already sits in the local exchange buffer; pull: read the owners'
     src = ar.local_table("xch") if push else ar.table("xch")
