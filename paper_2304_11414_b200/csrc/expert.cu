@@ -43,8 +43,23 @@ struct LongKScope {  // marks a token-segment GEMM with a long reduction dimensi
 static uint32_t b_box_rows() { return use_pair() ? kBN / 2 : kBN; }
 
 template <bool A_MN, bool B_MN, class Epi>
-static int launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const GroupGeom& geo, const Epi& epi,
+static int launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const GroupGeom& geo_in, const Epi& epi,
                      cudaStream_t s) {
+  GroupGeom geo = geo_in;
+  {  // soft wave synchronisation of the fixed-K GEMMs (PPMOE_KSYNC = k-blocks between sync
+     // points, default 64; PPMOE_KSYNC_MINK = smallest K it applies to, default 8192)
+    const char* e = getenv("PPMOE_KSYNC");
+    const int ks = e ? atoi(e) : 64;
+    const char* mk = getenv("PPMOE_KSYNC_MINK");
+    const int min_k = mk ? atoi(mk) : 8192;
+    if (ks > 0 && geo.K_fixed >= min_k && geo.K_fixed > 0) {
+      static unsigned int* ctr = nullptr;
+      if (!ctr) PPMOE_CUDA(cudaMalloc(&ctr, sizeof(unsigned int)));
+      PPMOE_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned int), s));
+      geo.ksync_ctr = ctr;
+      geo.ksync = ks;
+    }
+  }
   if (use_pair()) {
     auto kern = grouped_gemm_sm100_pair<kBN, A_MN, B_MN, Epi>;
     constexpr int smem = PairSmem<kBN>::kTotal;
@@ -190,6 +205,8 @@ static GroupGeom geom(int G, int N, int M_fixed, int K_fixed, const int* seg, in
     const char* e = getenv("PPMOE_NFAST");
     g.nfast = e ? atoi(e) : -1;
   }
+  g.ksync_ctr = nullptr;
+  g.ksync = 0;
   g.hint = load_hint();
   g.G = G;
   g.N = N;

@@ -44,6 +44,11 @@ struct GroupGeom {
   int banded;     // 1: banded 2-D tile order with L2 residency hints, 0: panel order
   int nfast;      // -1: fast dimension chosen by panel size; 0 / 1: force M / N fast
   int hint;       // panel order: load the streaming operand with evict-first priority
+  // Soft wave synchronisation of the TMA producers every `ksync` k-blocks (0 = off; only
+  // with K_fixed > 0): keeps the concurrent tiles' k positions together so the wave's
+  // operand slices are re-used from L2 instead of re-read from DRAM.  Bounded wait.
+  unsigned int* ksync_ctr;
+  int ksync;
 };
 
 template <int BN>
@@ -403,6 +408,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      // soft wave barrier bookkeeping (see GroupGeom::ksync)
+      const bool ksync_on = geo.ksync > 0 && geo.K_fixed > 0 && geo.ksync_ctr != nullptr;
+      const int spt = ksync_on ? (tab.k_blocks[0] + geo.ksync - 1) / geo.ksync : 0;
+      const int base_tiles = total_tiles / num_pairs, extra = total_tiles % num_pairs;
+      const unsigned nctas = gridDim.x;
+      unsigned sp = 0;
       for (int tile = pair; tile < total_tiles; tile += num_pairs) {
         int g, local;
         sched_locate(tab, G, tile, g, local);
@@ -425,6 +436,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           pol_b = (geo.hint && !a_res) ? kL2EvictFirst : kNormal;
         }
         for (int kb = 0; kb < kb_n; ++kb) {
+          if (ksync_on && kb % geo.ksync == 0) {
+            ++sp;
+            const unsigned full_sp = static_cast<unsigned>(base_tiles * spt);
+            const unsigned target = sp <= full_sp ? sp * nctas
+                                                  : full_sp * nctas + (sp - full_sp) * 2u * static_cast<unsigned>(extra);
+            atomicAdd(geo.ksync_ctr, 1u);
+            const long long t0 = clock64();
+            while (*reinterpret_cast<volatile unsigned*>(geo.ksync_ctr) < target && clock64() - t0 < 40000) {
+            }
+          }
           mbar_wait_sleep(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * L::kStageBytes;
           uint8_t* sb = sa + L::kABytes;
