@@ -152,11 +152,8 @@ static int banded_order() {
   return (e && strcmp(e, "band") == 0) ? 1 : 0;
 }
 static int load_hint() {
-  static const int v = [] {
-    const char* e = getenv("PPMOE_HINT");
-    return (e && strcmp(e, "1") == 0) ? 1 : 0;
-  }();
-  return v;
+  const char* e = getenv("PPMOE_HINT");
+  return (e && strcmp(e, "1") == 0) ? 1 : 0;
 }
 // Epilogue store flavour: 0 = plain 16-byte stores (default), 1 = 16-byte evict-first
 // (PPMOE_STORE=cs), 2 = 32-byte stores (PPMOE_STORE=v8; measured 5 % slower in the C2

@@ -431,9 +431,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         if (geo.banded) {
           pol_a = a_res ? kL2EvictLast : kL2EvictFirst;
           pol_b = a_res ? kL2EvictFirst : kL2EvictLast;
-        } else {  // panel order: the fast dimension's operand is shared by the wave, the other streams
-          pol_a = (geo.hint && a_res) ? kL2EvictFirst : kNormal;
-          pol_b = (geo.hint && !a_res) ? kL2EvictFirst : kNormal;
+        } else {  // panel order: the slow dimension's operand is re-read by every wave of the
+                  // group -> keep it (evict-last); the fast one is shared within a wave only
+          pol_a = (geo.hint && !a_res) ? kL2EvictLast : kNormal;
+          pol_b = (geo.hint && a_res) ? kL2EvictLast : kNormal;
         }
         for (int kb = 0; kb < kb_n; ++kb) {
           if (ksync_on && kb % geo.ksync == 0) {
