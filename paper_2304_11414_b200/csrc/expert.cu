@@ -46,19 +46,13 @@ template <bool A_MN, bool B_MN, class Epi>
 static int launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const GroupGeom& geo_in, const Epi& epi,
                      cudaStream_t s) {
   GroupGeom geo = geo_in;
-  {  // soft wave synchronisation of the fixed-K GEMMs (PPMOE_KSYNC = k-blocks between sync
-     // points, default 64; PPMOE_KSYNC_MINK = smallest K it applies to, default 8192)
-    const char* e = getenv("PPMOE_KSYNC");
-    const int ks = e ? atoi(e) : 64;
-    const char* mk = getenv("PPMOE_KSYNC_MINK");
-    const int min_k = mk ? atoi(mk) : 8192;
-    if (ks > 0 && geo.K_fixed >= min_k && geo.K_fixed > 0) {
-      static unsigned int* ctr = nullptr;
-      if (!ctr) PPMOE_CUDA(cudaMalloc(&ctr, sizeof(unsigned int)));
-      PPMOE_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned int), s));
-      geo.ksync_ctr = ctr;
-      geo.ksync = ks;
-    }
+  if (geo.ksync > 0 && geo.K_fixed > 0) {  // soft wave synchronisation (see GroupGeom::ksync)
+    static unsigned int* ctr = nullptr;
+    if (!ctr) PPMOE_CUDA(cudaMalloc(&ctr, sizeof(unsigned int)));
+    PPMOE_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned int), s));
+    geo.ksync_ctr = ctr;
+  } else {
+    geo.ksync = 0;
   }
   if (use_pair()) {
     auto kern = grouped_gemm_sm100_pair<kBN, A_MN, B_MN, Epi>;
@@ -151,6 +145,14 @@ static int banded_order() {
   const char* e = getenv("PPMOE_ORDER");
   return (e && strcmp(e, "band") == 0) ? 1 : 0;
 }
+// k-blocks between the soft wave barriers of the GEMMs that use them (PPMOE_KSYNC, 0 = off).
+// Enabled for fc2 fwd, fc2 dgrad and fc1 dgrad: halves their DRAM traffic, which under the
+// power cap buys clock; fc1 fwd measured slower with it.
+static int ksync_interval() {
+  const char* e = getenv("PPMOE_KSYNC");
+  return e ? atoi(e) : 64;
+}
+
 static int load_hint() {
   const char* e = getenv("PPMOE_HINT");
   return (e && strcmp(e, "1") == 0) ? 1 : 0;
@@ -232,6 +234,7 @@ static int fc2_fwd_impl(int dtype, const void* Act, const void* down, const void
   GroupGeom geo = geom(El, H, 0, F, seg, 1, 0, 0, F);
   geo.rlo = row_lo;
   geo.rhi = row_hi;
+  geo.ksync = ksync_interval();
   if (rows_cap == 0) return kOk;
   if (dtype == kBF16) {
     CUtensorMap ta, tb;
@@ -310,6 +313,7 @@ int ppmoe_expert_fc2_dgrad(int dtype, const void* dY, const void* down, const vo
   if (int rc = check_common(dtype, El, H, F, rows_cap)) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   GroupGeom geo = geom(El, F, 0, H, seg, 1, 0, 0, F);
+  geo.ksync = ksync_interval();
   if (rows_cap == 0) return kOk;
   if (dtype == kBF16) {
     CUtensorMap ta, tb;
@@ -332,6 +336,7 @@ int ppmoe_expert_fc1_dgrad(int dtype, const void* dH, const void* up, const int*
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   LongKScope long_k(F);
   GroupGeom geo = geom(El, H, 0, F, seg, 1, 0, 0, H);
+  geo.ksync = ksync_interval();
   if (rows_cap == 0) return kOk;
   if (dtype == kBF16) {
     CUtensorMap ta, tb;
