@@ -47,10 +47,15 @@ static int launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const GroupGe
                      cudaStream_t s) {
   GroupGeom geo = geo_in;
   if (geo.ksync > 0 && geo.K_fixed > 0) {  // soft wave synchronisation (see GroupGeom::ksync)
-    static unsigned int* ctr = nullptr;
-    if (!ctr) PPMOE_CUDA(cudaMalloc(&ctr, sizeof(unsigned int)));
-    PPMOE_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned int), s));
-    geo.ksync_ctr = ctr;
+    // one counter per device, reset on the launch stream before every synchronised GEMM
+    constexpr int kMaxDevices = 64;
+    static unsigned int* ctr[kMaxDevices] = {};
+    int dev = 0;
+    PPMOE_CUDA(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= kMaxDevices) return set_error(kErrUnsupported, "device ordinal %d out of range", dev);
+    if (!ctr[dev]) PPMOE_CUDA(cudaMalloc(&ctr[dev], sizeof(unsigned int)));
+    PPMOE_CUDA(cudaMemsetAsync(ctr[dev], 0, sizeof(unsigned int), s));
+    geo.ksync_ctr = ctr[dev];
   } else {
     geo.ksync = 0;
   }
