@@ -274,6 +274,9 @@ int ppmoe_nvl_sum_slots(const void* slots, int rows, int K, int H, int t0, const
  * by SM loads (_blocks) or by copy-engine transfers, one per peer block (_blocks_ce).  */
 int ppmoe_nvl_pull_blocks(const void* const* srcs, int T, int rank, int N, int H, void* out, void* stream);
 int ppmoe_nvl_pull_blocks_ce(const void* const* srcs, int T, int rank, int N, int H, void* out, void* stream);
+/* Copy-engine pull of the blocks of owners [q_lo, q_hi) only (token-chunked exchange). */
+int ppmoe_nvl_pull_range_ce(const void* const* srcs, int T, int rank, int N, int H, int q_lo, int q_hi, void* out,
+                            void* stream);
 
 /* Self-test entry: plain grouped GEMM D_g = A_g * B_g through the tcgen05 path
  * (use_tc=1) or the CUDA-core path (use_tc=0).  mode 0: A [rows x K] K-major

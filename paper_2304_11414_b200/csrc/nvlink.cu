@@ -457,6 +457,22 @@ int ppmoe_nvl_sum_slots(const void* slots, int rows, int K, int H, int t0, const
   return check_launch("nvl_sum_slots_kernel");
 }
 
+int ppmoe_nvl_pull_range_ce(const void* const* srcs, int T, int rank, int N, int H, int q_lo, int q_hi, void* out,
+                            void* stream) {
+  PPMOE_REQUIRE(T >= 1 && T <= kNvlMaxRanks && rank >= 0 && rank < T, "bad group T=%d rank=%d", T, rank);
+  PPMOE_REQUIRE(0 <= q_lo && q_lo <= q_hi && q_hi <= T, "bad owner range [%d, %d)", q_lo, q_hi);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t row = static_cast<size_t>(H) * 2;
+  for (int q = q_lo; q < q_hi; ++q) {
+    if (q == rank) continue;
+    const size_t lo = static_cast<size_t>(q) * N / T, hi = static_cast<size_t>(q + 1) * N / T;
+    if (hi > lo)
+      PPMOE_CUDA(cudaMemcpyAsync(static_cast<char*>(out) + lo * row, static_cast<const char*>(srcs[q]) + lo * row,
+                                 (hi - lo) * row, cudaMemcpyDeviceToDevice, s));
+  }
+  return kOk;
+}
+
 int ppmoe_nvl_pull_blocks_ce(const void* const* srcs, int T, int rank, int N, int H, void* out, void* stream) {
   PPMOE_REQUIRE(T >= 1 && T <= kNvlMaxRanks && rank >= 0 && rank < T, "bad group T=%d rank=%d", T, rank);
   cudaStream_t s = static_cast<cudaStream_t>(stream);

@@ -484,6 +484,26 @@ class _PPMoEFunction(torch.autograd.Function):
                                           spec.weight_scaling, None, drop_p=spec.dropout_p, seed=spec.seed,
                                           owner_table=table, owner_rows=rows)
                 out = nvlink.finish_fused_forward(ar, n, h, torch.empty_like(hidden))
+            elif nvlink.forward_chunks(ar, n) > 1:
+                # pipelined: the exchange of token chunk c (its owners' blocks) runs on the side
+                # stream while the expert GEMMs of chunk c+1 compute (SM budget leaves room)
+                chunks = nvlink.forward_chunks(ar, n)
+                ym = ar.tensor("y", (_ops.local_rows_cap(n, spec.k, spec.el, cap), h), hidden.dtype)
+                out = torch.empty_like(hidden)
+                ar.tensor("xch", (n, h), torch.bfloat16)  # allocated before the side stream uses it
+                main, side = torch.cuda.current_stream(), ar.stream
+                wts = rt.w if spec.weight_scaling else None
+
+                def on_chunk(c):
+                    side.wait_stream(main)
+                    with torch.cuda.stream(side):
+                        nvlink.exchange_chunk(ar, c, chunks, "y", pl.seg, spec.el, rt.idx, pl.pair_pos, wts, n, h,
+                                              out)
+
+                st = _ops.experts_forward(hidden, pl, spec.e0, spec.el, up, down, bias_up, bias_down, spec.k,
+                                          spec.weight_scaling, None, chunks, on_chunk, spec.dropout_p, spec.seed,
+                                          y_mirror=ym)
+                main.wait_stream(side)
             else:
                 ym = ar.tensor("y", (_ops.local_rows_cap(n, spec.k, spec.el, cap), h), hidden.dtype)
                 st = _ops.experts_forward(hidden, pl, spec.e0, spec.el, up, down, bias_up, bias_down, spec.k,

@@ -333,3 +333,30 @@ def exchange(ar: NvlArena, rows_name: str, seg, el: int, idx, pair_pos, w, n: in
     pull = "ppmoe_nvl_pull_blocks" if os.environ.get("PPMOE_NVL_PULL", "ce") == "sm" else "ppmoe_nvl_pull_blocks_ce"
     call(pull, src, ar.tp, ar.rank, n, h, ptr(out), s)
     return out
+
+
+def forward_chunks(ar: NvlArena, n: int) -> int:
+    """Token chunks of the pipelined forward exchange (PPMOE_NVL_CHUNKS): chunk c is the
+    token range of owners [c T/C, (c+1) T/C), so C must divide T."""
+    c = int(os.environ.get("PPMOE_NVL_CHUNKS", "1"))
+    if c <= 1 or ar.tp % c or n % ar.tp:
+        return 1
+    return c
+
+
+def exchange_chunk(ar: NvlArena, c: int, chunks: int, rows_name: str, seg, el: int, idx, pair_pos, w, n: int, h: int,
+                   out: torch.Tensor) -> None:
+    """Exchange of token chunk c (its owners' blocks): barrier (every rank's rows of the
+    chunk are final) -> owner gather on the chunk's owners -> barrier -> every rank pulls
+    the chunk's blocks.  Runs on the arena's side stream while the next chunk computes."""
+    k = pair_pos.shape[1]
+    q_lo, q_hi = c * ar.tp // chunks, (c + 1) * ar.tp // chunks
+    ch = 4 + 2 * (c % 2)
+    xch = ar.tensor("xch", (n, h), torch.bfloat16)
+    s = _lib.stream_ptr()
+    ar.barrier(ch)
+    if q_lo <= ar.rank < q_hi:
+        call("ppmoe_nvl_owner_gather", ar.table(rows_name), ptr(seg), el, ptr(idx), ptr(pair_pos), ptr(w), n, k, h,
+             ar.tp, ar.rank, None, None, 0, ptr(out), ptr(xch), None, 0, s)
+    ar.barrier(ch + 1)
+    call("ppmoe_nvl_pull_range_ce", ar.table("xch"), ar.tp, ar.rank, n, h, q_lo, q_hi, ptr(out), s)

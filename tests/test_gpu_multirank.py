@@ -76,7 +76,8 @@ def _worker(rank, world, port, q, k, cf, env=None):
     (2, 2, float("inf"), {}), (2, 1, 1.0, {}), (4, 2, 1.25, {}),
     (2, 2, 1.25, {"PPMOE_NVL_FWD": "fused"}), (2, 2, float("inf"), {"PPMOE_NVL_FWD": "slots"}),
     (2, 2, float("inf"), {"PPMOE_TP_COMM": "nccl"}), (2, 2, float("inf"), {"PPMOE_NVL_PUSH": "1", "PPMOE_NVL_PULL": "sm"}),
-    (2, 2, float("inf"), {"PPMOE_NVL_MC": "1"}),
+    (2, 2, float("inf"), {"PPMOE_NVL_MC": "1"}), (2, 2, 1.25, {"PPMOE_NVL_CHUNKS": "2"}),
+    (4, 2, float("inf"), {"PPMOE_NVL_CHUNKS": "2"}),
 ])
 def test_tp_nccl_matches_simulated(world, k, cf, env):
     if torch.cuda.device_count() < world:
