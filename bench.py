@@ -367,7 +367,10 @@ def main():
                 "kernel": "grouped_gemm_sm100 (6 launches/step: fc1/fc2 fwd, dgrad, wgrad)",
                 "algorithmic": f"12*P_r*h*f flop per step on this rank, P_r={local_pairs} of P={pairs} kept pairs; "
                                f"{gemm_ms:.3f} ms of GEMM per step",
-                "peak_source": peak_src, "gemm_share_of_step": gemm_ms / ms if ms else None}
+                "peak_source": peak_src, "gemm_share_of_step": gemm_ms / ms if ms else None,
+                "frac_of_burst_peak": (achieved / peaks["bf16_tflops"]) if (achieved and "bf16_tflops" in peaks) else None,
+                "peak_note": "peak = cuBLAS bf16 8192^3 back-to-back for 4 s on this pool (power-capped, the regime a "
+                             "long step runs in); frac_of_burst_peak uses the short-burst figure"}
 
     # ---- end to end: host (pinned) input -> device -> fwd+bwd -> loss back to host
     e2e = None
