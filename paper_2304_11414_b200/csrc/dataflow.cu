@@ -24,23 +24,30 @@ __host__ __device__ inline size_t align_to(size_t v, size_t a) { return (v + a -
 // ------------------------------------------------------------------ gather
 
 constexpr int kGatherThreads = 128;
-constexpr int kGatherLag = 2;  // store groups allowed in flight before a slot is recycled
+constexpr int kGatherLag = 8;  // store groups allowed in flight before a slot is recycled
 
 template <typename T>
 __global__ void __launch_bounds__(kGatherThreads)
     gather_bulk_kernel(const T* __restrict__ X, int H, const int* __restrict__ seg, int El,
                        const int* __restrict__ tok_sorted, const float* __restrict__ w_sorted, T* __restrict__ Xs,
-                       int* __restrict__ tok_local, float* __restrict__ w_local, int R) {
+                       int* __restrict__ tok_local, float* __restrict__ w_local, int R, int per) {
   extern __shared__ __align__(128) unsigned char sm[];
   const uint32_t row_bytes = static_cast<uint32_t>(H) * sizeof(T);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm);
   unsigned char* zero = sm + align_to(static_cast<size_t>(R) * 8, 128);
-  unsigned char* slots = zero + align_to(row_bytes, 128);
+  int* stok = reinterpret_cast<int*>(zero + align_to(row_bytes, 128));  // this CTA's source tokens
+  unsigned char* slots = reinterpret_cast<unsigned char*>(stok) + align_to(static_cast<size_t>(per) * 4, 128);
   const int s0 = seg[0];
   const int rows = seg[El] - s0;
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
-    tok_local[r] = tok_sorted[s0 + r];
-    w_local[r] = w_sorted ? w_sorted[s0 + r] : 1.f;
+  // this CTA's contiguous row range; its source token ids are staged in shared memory so the
+  // issuing thread never waits on a global load (it used to, once per row)
+  const int r0 = min(rows, static_cast<int>(blockIdx.x) * per);
+  const int n = min(rows, r0 + per) - r0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int tok = tok_sorted[s0 + r0 + i];
+    stok[i] = tok;
+    tok_local[r0 + i] = tok;
+    w_local[r0 + i] = w_sorted ? w_sorted[s0 + r0 + i] : 1.f;
   }
   for (uint32_t i = threadIdx.x; i < row_bytes / 16; i += blockDim.x) reinterpret_cast<uint4*>(zero)[i] = make_uint4(0, 0, 0, 0);
   if (threadIdx.x == 0) {
@@ -50,11 +57,9 @@ __global__ void __launch_bounds__(kGatherThreads)
   fence_proxy_async_smem();
   __syncthreads();
   if (threadIdx.x != 0) return;
-  const int n = rows > static_cast<int>(blockIdx.x) ? (rows - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-  auto row_of = [&](int i) { return static_cast<int>(blockIdx.x) + i * static_cast<int>(gridDim.x); };
   auto issue = [&](int i) {
     const int slot = i % R;
-    const int tok = tok_sorted[s0 + row_of(i)];
+    const int tok = stok[i];
     if (tok >= 0) {
       mbar_arrive_expect_tx(&bars[slot], row_bytes);
       bulk_load(slots + static_cast<size_t>(slot) * row_bytes, X + static_cast<size_t>(tok) * H, row_bytes, &bars[slot]);
@@ -66,9 +71,9 @@ __global__ void __launch_bounds__(kGatherThreads)
   for (; issued < n && issued <= R - kGatherLag; ++issued) issue(issued);
   for (int i = 0; i < n; ++i) {
     const int slot = i % R;
-    const int tok = tok_sorted[s0 + row_of(i)];
+    const int tok = stok[i];
     mbar_wait(&bars[slot], (i / R) & 1);
-    bulk_store(Xs + static_cast<size_t>(row_of(i)) * H, tok >= 0 ? slots + static_cast<size_t>(slot) * row_bytes : zero,
+    bulk_store(Xs + static_cast<size_t>(r0 + i) * H, tok >= 0 ? slots + static_cast<size_t>(slot) * row_bytes : zero,
                row_bytes);
     bulk_commit();
     if (issued < n) {
@@ -824,22 +829,24 @@ int ppmoe_gather(const void* X, int dtype, int N, int H, const int* seg, int El,
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const size_t esz = dtype == kBF16 ? 2 : 4;
   const size_t row_bytes = static_cast<size_t>(H) * esz;
-  const size_t budget = 200 * 1024;
-  int R = static_cast<int>((budget - align_to(row_bytes, 128) - 512) / row_bytes);
-  if (R > 32) R = 32;
   const int grid = num_sms();
-  if (row_bytes % 16 == 0 && R >= kGatherLag + 2) {
-    const size_t smem = align_to(static_cast<size_t>(R) * 8, 128) + align_to(row_bytes, 128) + R * row_bytes;
+  const int per = (rows_cap + grid - 1) / grid;  // rows per CTA (upper bound)
+  const size_t tok_bytes = align_to(static_cast<size_t>(per) * 4, 128);
+  const size_t budget = 200 * 1024;
+  int R = static_cast<int>((budget - align_to(row_bytes, 128) - 512 - std::min(tok_bytes, budget / 2)) / row_bytes);
+  if (R > 32) R = 32;
+  if (row_bytes % 16 == 0 && R >= kGatherLag + 2 && tok_bytes <= budget / 2) {
+    const size_t smem = align_to(static_cast<size_t>(R) * 8, 128) + align_to(row_bytes, 128) + tok_bytes + R * row_bytes;
     if (dtype == kBF16) {
       auto k = gather_bulk_kernel<__nv_bfloat16>;
       PPMOE_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
       k<<<grid, kGatherThreads, smem, s>>>(static_cast<const __nv_bfloat16*>(X), H, seg, El, tok_sorted, w_sorted,
-                                           static_cast<__nv_bfloat16*>(Xs), tok_local, w_local, R);
+                                           static_cast<__nv_bfloat16*>(Xs), tok_local, w_local, R, per);
     } else {
       auto k = gather_bulk_kernel<float>;
       PPMOE_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
       k<<<grid, kGatherThreads, smem, s>>>(static_cast<const float*>(X), H, seg, El, tok_sorted, w_sorted,
-                                           static_cast<float*>(Xs), tok_local, w_local, R);
+                                           static_cast<float*>(Xs), tok_local, w_local, R, per);
     }
     return check_launch("gather_bulk_kernel");
   }
