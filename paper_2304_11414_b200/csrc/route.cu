@@ -13,6 +13,8 @@
 // Everything is deterministic: integer histograms (exact under atomics), fixed-order
 // fp64 reductions for the aux loss.
 #include <climits>
+#include <cstdlib>
+#include <cstring>
 
 #include "../../include/ppmoe_capi.h"
 #include "common.cuh"
@@ -118,6 +120,62 @@ __host__ inline size_t route_smem_bytes(int E) {
   const int EB = route_eb(E);
   // staged Wg chunk (fp64), reused for the split-K partials (KS*TB == HC)
   return static_cast<size_t>(kRouteHC) * EB * 8 + static_cast<size_t>(kRouteTB) * E * 8 + 2 * kRouteTB * 8;
+}
+
+// Softmax (fp64), top-k and the per-block aux-loss sums of the kRouteTB tokens of this
+// block from their logits lg[TB][E] (shared by the router kernels).
+__device__ __forceinline__ void route_tail(double* lg, double* stat, int t0, int N, int E, int K,
+                                           const int* __restrict__ ovr, int* __restrict__ idx, float* __restrict__ w,
+                                           float* __restrict__ scores, double* __restrict__ ssum,
+                                           int* __restrict__ cnt_top1) {
+  const int tid = threadIdx.x;
+  __syncthreads();
+  // softmax statistics (row max shift, tensor.py:214-216)
+  if (tid < kRouteTB) {
+    const double* l = lg + tid * E;
+    double mx = l[0];
+    for (int j = 1; j < E; ++j) mx = fmax(mx, l[j]);
+    double s = 0.0;
+    for (int j = 0; j < E; ++j) s += exp(l[j] - mx);
+    stat[2 * tid] = mx;
+    stat[2 * tid + 1] = s;
+  }
+  __syncthreads();
+  for (int i = tid; i < kRouteTB * E; i += kRouteThreads) {
+    const int tl = i / E, e = i % E;
+    const double sc = exp(lg[i] - stat[2 * tl]) / stat[2 * tl + 1];
+    lg[i] = sc;
+    if (t0 + tl < N) scores[static_cast<size_t>(t0 + tl) * E + e] = static_cast<float>(sc);
+  }
+  __syncthreads();
+  // top-k selection, one thread per token
+  if (tid < kRouteTB && t0 + tid < N) {
+    const int tt = t0 + tid;
+    const double* sc = lg + tid * E;
+    unsigned long long chosen[2] = {0ull, 0ull};
+    for (int s = 0; s < K; ++s) {
+      int best;
+      if (ovr) {
+        best = ovr[static_cast<size_t>(tt) * K + s];
+      } else {
+        best = -1;
+        for (int j = 0; j < E; ++j) {
+          if ((chosen[j >> 6] >> (j & 63)) & 1ull) continue;
+          if (best < 0 || sc[j] > sc[best]) best = j;
+        }
+        chosen[best >> 6] |= 1ull << (best & 63);
+      }
+      idx[static_cast<size_t>(tt) * K + s] = best;
+      w[static_cast<size_t>(tt) * K + s] = static_cast<float>(sc[best]);
+      if (s == 0) atomicAdd(&cnt_top1[best], 1);
+    }
+  }
+  // per-block expert score sums in token order (deterministic aux-loss reduction)
+  for (int e = tid; e < E; e += kRouteThreads) {
+    double s = 0.0;
+    for (int r = 0; r < kRouteTB && t0 + r < N; ++r) s += lg[r * E + e];
+    ssum[static_cast<size_t>(blockIdx.x) * E + e] = s;
+  }
 }
 
 // Gate logits X*Wg in fp64 (bf16/fp32 x fp32 products are exact in fp64), softmax,
@@ -250,53 +308,7 @@ __global__ void __launch_bounds__(kRouteThreads, EB == 8 ? 2 : 1) router_kernel(
     }
     __syncthreads();  // the next expert pass restages Wg over the partials
   }
-  __syncthreads();
-  // softmax statistics (row max shift, tensor.py:214-216)
-  if (tid < kRouteTB) {
-    const double* l = lg + tid * E;
-    double mx = l[0];
-    for (int j = 1; j < E; ++j) mx = fmax(mx, l[j]);
-    double s = 0.0;
-    for (int j = 0; j < E; ++j) s += exp(l[j] - mx);
-    stat[2 * tid] = mx;
-    stat[2 * tid + 1] = s;
-  }
-  __syncthreads();
-  for (int i = tid; i < kRouteTB * E; i += kRouteThreads) {
-    const int tl = i / E, e = i % E;
-    const double sc = exp(lg[i] - stat[2 * tl]) / stat[2 * tl + 1];
-    lg[i] = sc;
-    if (t0 + tl < N) scores[static_cast<size_t>(t0 + tl) * E + e] = static_cast<float>(sc);
-  }
-  __syncthreads();
-  // top-k selection, one thread per token
-  if (tid < kRouteTB && t0 + tid < N) {
-    const int tt = t0 + tid;
-    const double* sc = lg + tid * E;
-    unsigned long long chosen[2] = {0ull, 0ull};
-    for (int s = 0; s < K; ++s) {
-      int best;
-      if (ovr) {
-        best = ovr[static_cast<size_t>(tt) * K + s];
-      } else {
-        best = -1;
-        for (int j = 0; j < E; ++j) {
-          if ((chosen[j >> 6] >> (j & 63)) & 1ull) continue;
-          if (best < 0 || sc[j] > sc[best]) best = j;
-        }
-        chosen[best >> 6] |= 1ull << (best & 63);
-      }
-      idx[static_cast<size_t>(tt) * K + s] = best;
-      w[static_cast<size_t>(tt) * K + s] = static_cast<float>(sc[best]);
-      if (s == 0) atomicAdd(&cnt_top1[best], 1);
-    }
-  }
-  // per-block expert score sums in token order (deterministic aux-loss reduction)
-  for (int e = tid; e < E; e += kRouteThreads) {
-    double s = 0.0;
-    for (int r = 0; r < kRouteTB && t0 + r < N; ++r) s += lg[r * E + e];
-    ssum[static_cast<size_t>(blockIdx.x) * E + e] = s;
-  }
+  route_tail(lg, stat, t0, N, E, K, ovr, idx, w, scores, ssum, cnt_top1);
 }
 
 // l_aux = E * sum_e frac_e * mean_t s[t,e]  with frac from the top-1 choice (moe.py:221-223)
