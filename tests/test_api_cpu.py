@@ -212,3 +212,24 @@ def test_costmodel_formulas_reduce_to_reference():
     assert abs(m4["expert_compute"] * 4 - m1["expert_compute"]) < 1e-12
     rows = C.breakdown_rows({"a": 1.0, "b": 3.0, "total": 4.0})
     assert rows == [("a", 1.0, 25.0), ("b", 3.0, 75.0)]
+
+
+def test_bench_reference_arm_contract():
+    """`bench.py --impl reference` (the CPU oracle arm the driver runs) prints one JSON line
+    with the contract keys, on a small shape so the CPU suite stays fast."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    out = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "2", "--warmup", "1",
+                          "--hidden", "256", "--experts", "4", "--cpu-seconds", "0.5"],
+                         cwd=root, capture_output=True, text=True, timeout=300, check=True).stdout
+    line = json.loads(out.strip().splitlines()[-1])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "config",
+                "cpu_baseline", "e2e"):
+        assert key in line, key
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
