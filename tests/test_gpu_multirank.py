@@ -34,7 +34,7 @@ def _collect(q, procs, timeout=240):
     return got
 
 
-def _worker(rank, world, port, q, k, cf, env=None):
+def _worker(rank, world, port, q, k, cf, env=None, e=8):
     import torch.distributed as dist
 
     os.environ.update(env or {})
@@ -46,7 +46,7 @@ def _worker(rank, world, port, q, k, cf, env=None):
     torch.cuda.set_device(rank)
     dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
     try:
-        h, e, n = 512, 8, 1024
+        h, n = 512, 1024
         el = e // world
         full = P.MoeLayerWeights.random(h, e, seed=11, device="cuda")  # identical on every rank
         local = P.MoeLayerWeights(P.GateParams(full.gate.wg.detach().clone().requires_grad_()),
@@ -72,6 +72,13 @@ def _worker(rank, world, port, q, k, cf, env=None):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("world,k,cf,env,e", [(2, 2, float("inf"), {}, 2), (4, 2, 1.25, {}, 4), (4, 1, 1.0, {}, 4)])
+def test_tp_one_expert_per_rank(world, k, cf, env, e):
+    """E = T: one expert per rank (the C2 layout at T = 8), single-group GEMMs and the
+    exchange with E < 8 gate columns."""
+    test_tp_nccl_matches_simulated(world, k, cf, env, e)
+
+
 @pytest.mark.parametrize("world,k,cf,env", [
     (2, 2, float("inf"), {}), (2, 1, 1.0, {}), (4, 2, 1.25, {}),
     (2, 2, 1.25, {"PPMOE_NVL_FWD": "fused"}), (2, 2, float("inf"), {"PPMOE_NVL_FWD": "slots"}),
@@ -79,7 +86,7 @@ def _worker(rank, world, port, q, k, cf, env=None):
     (2, 2, float("inf"), {"PPMOE_NVL_MC": "1"}), (2, 2, 1.25, {"PPMOE_NVL_CHUNKS": "2"}),
     (4, 2, float("inf"), {"PPMOE_NVL_CHUNKS": "2"}),
 ])
-def test_tp_nccl_matches_simulated(world, k, cf, env):
+def test_tp_nccl_matches_simulated(world, k, cf, env, e=8):
     if torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
     import paper_2304_11414_b200 as P
@@ -87,7 +94,7 @@ def test_tp_nccl_matches_simulated(world, k, cf, env):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = 29600 + os.getpid() % 500
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q, k, cf, env)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, k, cf, env, e)) for r in range(world)]
     for p in procs:
         p.start()
     got = _collect(q, procs)
@@ -95,7 +102,7 @@ def test_tp_nccl_matches_simulated(world, k, cf, env):
         p.join(timeout=120)
         assert p.exitcode == 0
     # single-process reference: simulated TP world on GPU 0
-    h, e, n = 512, 8, 1024
+    h, n = 512, 1024
     full = P.MoeLayerWeights.random(h, e, seed=11, device="cuda")
     x = torch.randn(n, h, device="cuda", generator=torch.Generator(device="cuda").manual_seed(5)).bfloat16()
     x.requires_grad_()
