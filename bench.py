@@ -322,8 +322,10 @@ def main():
         barrier()
         clk.mark_start()
         ev0.record()
+        h0 = time.perf_counter()
         for _ in range(a.steps):
             step(x)
+        host_ms = (time.perf_counter() - h0) * 1e3 / a.steps  # host enqueue time (the step never syncs)
         ev1.record()
         barrier()
         clk.mark_end()
@@ -461,6 +463,7 @@ def main():
                 "vs_baseline": None, "dtype": "bf16", "data": f"synthetic (random-init weights of the {a.config.upper()} layer, N(0,1) tokens)",
                 "config": config_of(a, world_size), "roofline": roofline, "cpu_baseline": cb, "e2e": e2e,
                 "gpu_launches": int(launches), "clocks": clk.summary(), "a2a_comparator": a2a, "kernels": per_kernel,
+                "host_enqueue_ms_per_step": round(host_ms, 3),
                 "gemm_launches_per_step": gemm_launches}
         print(json.dumps(line), flush=True)
     if distributed:
