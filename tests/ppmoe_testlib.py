@@ -63,3 +63,37 @@ def oracle_rounded(layer: O.OracleLayer, dtype) -> O.OracleLayer:
 
     return O.OracleLayer(np.asarray(layer.wg, dtype=np.float32).astype(np.float64), [r(u) for u in layer.up],
                          [r(d) for d in layer.down], [r(b) for b in layer.bias_up], [r(b) for b in layer.bias_down])
+
+
+def per_token_oracle(x64, wg64, bank, tokens, k, n_all, route):
+    """out[t] and dX[t] of the C2 layer for the sampled tokens t, in fp64, from the closed
+    form of oracle.ppmoe_layer (dOut = ones, aux gradient 1) restricted to one token:
+    out[t] = sum_e w_te FFN_e(x_t); dX[t] = sum_e (w_te (1 down_e^T) * GeLU'(a)) up_e^T
+    + dL_t Wg^T, with dS[t,e] = sum_j Y_e(x_t)_j + (E/N) frac_e."""
+    e_count = wg64.shape[1]
+    h = x64.shape[1]
+    out = np.zeros((len(tokens), h))
+    dx = np.zeros((len(tokens), h))
+    ds = np.zeros((len(tokens), e_count))
+    for e in range(e_count):
+        sel = [(i, s) for i, t in enumerate(tokens) for s in range(k) if route.indices[t, s] == e]
+        if not sel:
+            continue
+        up = bank.up[e].detach().double().cpu().numpy()
+        down = bank.down[e].detach().double().cpu().numpy()
+        bu = bank.bias_up[e].detach().double().cpu().numpy()
+        bd = bank.bias_down[e].detach().double().cpu().numpy()
+        rows = np.array([i for i, _ in sel])
+        wt = np.array([route.weights[tokens[i], s] for i, s in sel])
+        a = x64[tokens[rows]] @ up + bu
+        y = O.gelu(a) @ down + bd
+        out[rows] += wt[:, None] * y
+        ds[rows, e] += y.sum(axis=1)
+        da = wt[:, None] * down.sum(axis=1)[None, :] * O.gelu_grad(a)
+        dx[rows] += da @ up.T
+    frac = route.top1_counts / n_all
+    ds += (e_count / n_all) * frac[None, :]
+    s = route.scores[tokens]
+    dl = s * (ds - (ds * s).sum(axis=1, keepdims=True))
+    dx += dl @ wg64.T
+    return out, dx

@@ -321,3 +321,67 @@ def test_pipeline_stack_matches_single_gpu(stages, tp, dtype):
             else:
                 want = moe.bank.up.grad[t * el:(t + 1) * el].float().cpu().numpy()
             assert err(g, want) < (3e-2 if dtype == torch.bfloat16 else 1e-3), (key, err(g, want))
+
+
+def _full_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    import paper_2304_11414_b200 as P
+    from oracle import ppmoe_oracle as O
+    from ppmoe_testlib import per_token_oracle, scaled_err
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    try:
+        h, e, n, k = 4096, 8, 16384, 2
+        el = e // world
+        full = P.MoeLayerWeights.random(h, e, seed=0, device="cuda")  # identical on every rank
+        gate = P.GateParams(full.gate.wg.detach().clone().requires_grad_())
+        bank = P.ExpertBank(*(t.detach()[rank * el:(rank + 1) * el].clone().requires_grad_()
+                              for t in (full.bank.up, full.bank.down, full.bank.bias_up, full.bank.bias_down)),
+                            first=rank * el)
+        x = torch.randn(n, h, device="cuda", generator=torch.Generator(device="cuda").manual_seed(1)).bfloat16()
+        x.requires_grad_()
+        wd = P.World(1, world)
+        g = P.ProcessGroup(P.EP, tuple(range(world)))
+        out, l_aux = P.ppmoe_forward(wd, g, x, gate, [bank if r == rank else None for r in range(world)], top_k=k)
+        torch.autograd.backward([out, l_aux], [torch.ones_like(out), torch.ones_like(l_aux)])
+        P.sync_gate_gradients(wd, g, gate)
+        torch.cuda.synchronize()
+        x64 = x.detach().double().cpu().numpy()
+        wg64 = gate.wg.detach().double().cpu().numpy()
+        route = O.gate_topk(x64, wg64, k)
+        # every rank checks its own sample of tokens of the replicated out / dX
+        tokens = np.random.default_rng(rank).choice(n, size=24, replace=False)
+        ref_out, ref_dx = per_token_oracle(x64, wg64, full.bank, tokens, k, n, route)
+        sel = torch.as_tensor(tokens, device="cuda")
+        res = {"out": scaled_err(out.detach()[sel].double().cpu().numpy(), ref_out),
+               "dx": scaled_err(x.grad[sel].double().cpu().numpy(), ref_dx),
+               "l_aux": abs(float(l_aux.detach()) - route.l_aux),
+               "digest": float(out.detach().float().sum())}
+        q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_tp_full_size_c2():
+    """BASELINE configs[1] at full size over the NVLink exchange (T = 4, or 2): each rank's
+    replicated out and dX on sampled tokens against the per-token closed form."""
+    world = 4 if torch.cuda.device_count() >= 4 else 2
+    if torch.cuda.device_count() < world:
+        pytest.skip("needs >= 2 GPUs")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29600 + (os.getpid() + 7) % 500
+    procs = [ctx.Process(target=_full_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = _collect(q, procs, timeout=400)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for r in range(world):
+        assert got[r]["out"] < 2e-2 and got[r]["dx"] < 2e-2 and got[r]["l_aux"] < 1e-5, (r, got[r])
+    assert len({got[r]["digest"] for r in range(world)}) == 1  # identical replicas

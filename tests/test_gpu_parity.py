@@ -14,7 +14,7 @@ import torch
 import paper_2304_11414_b200 as P
 from golden_util import golden_inputs, load, unpack_lists
 from oracle import ppmoe_oracle as O
-from ppmoe_testlib import TOL, device_weights, oracle_rounded, run_cuda_layer, scaled_err
+from ppmoe_testlib import TOL, device_weights, oracle_rounded, per_token_oracle, run_cuda_layer, scaled_err
 
 pytestmark = pytest.mark.gpu
 
@@ -527,40 +527,6 @@ def test_zero_tokens_and_bad_override():
         P.ppmoe_forward(world, g, torch.zeros(3, 64, device="cuda"), w.gate, [w.bank])
 
 
-def _per_token_oracle(x64, wg64, w, tokens, k, n_all, route):
-    """out[t] and dX[t] of the C2 layer for the sampled tokens t, in fp64, from the closed
-    form of oracle.ppmoe_layer (dOut = ones, aux gradient 1) restricted to one token:
-    out[t] = sum_e w_te FFN_e(x_t); dX[t] = sum_e (w_te (1 down_e^T) * GeLU'(a)) up_e^T
-    + dL_t Wg^T, with dS[t,e] = sum_j Y_e(x_t)_j + (E/N) frac_e."""
-    e_count = wg64.shape[1]
-    h = x64.shape[1]
-    out = np.zeros((len(tokens), h))
-    dx = np.zeros((len(tokens), h))
-    ds = np.zeros((len(tokens), e_count))
-    for e in range(e_count):
-        sel = [(i, s) for i, t in enumerate(tokens) for s in range(k) if route.indices[t, s] == e]
-        if not sel:
-            continue
-        up = w.bank.up[e].detach().double().cpu().numpy()
-        down = w.bank.down[e].detach().double().cpu().numpy()
-        bu = w.bank.bias_up[e].detach().double().cpu().numpy()
-        bd = w.bank.bias_down[e].detach().double().cpu().numpy()
-        rows = np.array([i for i, _ in sel])
-        wt = np.array([route.weights[tokens[i], s] for i, s in sel])
-        a = x64[tokens[rows]] @ up + bu
-        y = O.gelu(a) @ down + bd
-        out[rows] += wt[:, None] * y
-        ds[rows, e] += y.sum(axis=1)
-        da = wt[:, None] * down.sum(axis=1)[None, :] * O.gelu_grad(a)
-        dx[rows] += da @ up.T
-    frac = route.top1_counts / n_all
-    ds += (e_count / n_all) * frac[None, :]
-    s = route.scores[tokens]
-    dl = s * (ds - (ds * s).sum(axis=1, keepdims=True))
-    dx += dl @ wg64.T
-    return out, dx
-
-
 def test_c2_full_size_sampled_tokens_vs_oracle():
     """BASELINE configs[1] at full size (N 16384, h 4096, ffn 16384, E 8, top-2, bf16),
     fwd+bwd through the public API.  The oracle can't run the whole layer in seconds, so
@@ -579,7 +545,7 @@ def test_c2_full_size_sampled_tokens_vs_oracle():
     route = O.gate_topk(x64, wg64, k)
     assert abs(float(l_aux.detach()) - route.l_aux) < 1e-5
     tokens = np.random.default_rng(0).choice(n, size=48, replace=False)
-    ref_out, ref_dx = _per_token_oracle(x64, wg64, w, tokens, k, n, route)
+    ref_out, ref_dx = per_token_oracle(x64, wg64, w.bank, tokens, k, n, route)
     tol = TOL[torch.bfloat16]
     got_out = out.detach()[torch.as_tensor(tokens, device="cuda")].double().cpu().numpy()
     got_dx = x.grad[torch.as_tensor(tokens, device="cuda")].double().cpu().numpy()
