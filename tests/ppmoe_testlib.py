@@ -65,18 +65,20 @@ def oracle_rounded(layer: O.OracleLayer, dtype) -> O.OracleLayer:
                          [r(d) for d in layer.down], [r(b) for b in layer.bias_up], [r(b) for b in layer.bias_down])
 
 
-def per_token_oracle(x64, wg64, bank, tokens, k, n_all, route):
+def per_token_oracle(x64, wg64, bank, tokens, k, n_all, route, kept=None):
     """out[t] and dX[t] of the C2 layer for the sampled tokens t, in fp64, from the closed
     form of oracle.ppmoe_layer (dOut = ones, aux gradient 1) restricted to one token:
     out[t] = sum_e w_te FFN_e(x_t); dX[t] = sum_e (w_te (1 down_e^T) * GeLU'(a)) up_e^T
-    + dL_t Wg^T, with dS[t,e] = sum_j Y_e(x_t)_j + (E/N) frac_e."""
+    + dL_t Wg^T, with dS[t,e] = sum_j Y_e(x_t)_j + (E/N) frac_e.  `kept` [N, k] drops the
+    pairs capacity removed (they contribute neither output nor expert gradient)."""
     e_count = wg64.shape[1]
     h = x64.shape[1]
     out = np.zeros((len(tokens), h))
     dx = np.zeros((len(tokens), h))
     ds = np.zeros((len(tokens), e_count))
     for e in range(e_count):
-        sel = [(i, s) for i, t in enumerate(tokens) for s in range(k) if route.indices[t, s] == e]
+        sel = [(i, s) for i, t in enumerate(tokens) for s in range(k)
+               if route.indices[t, s] == e and (kept is None or kept[t, s])]
         if not sel:
             continue
         up = bank.up[e].detach().double().cpu().numpy()

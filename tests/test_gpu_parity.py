@@ -556,3 +556,28 @@ def test_c2_full_size_sampled_tokens_vs_oracle():
     np.add.at(wsum, route.indices.ravel(), route.weights.ravel())
     gbd = w.bank.bias_down.grad.double().cpu().numpy()
     assert scaled_err(gbd, np.broadcast_to(wsum[:, None], gbd.shape)) < tol
+
+
+def test_c3_full_size_sampled_tokens_vs_oracle():
+    """BASELINE configs[2] at full size (N 16384, h 8192, ffn 32768, E 16, top-2, cf 1.25,
+    17 GB of bf16 experts) on one GPU: out and dX of sampled tokens against the per-token
+    closed form with the oracle's capacity mask, l_aux."""
+    h, e, n, k, cf = 8192, 16, 16384, 2, 1.25
+    w = P.MoeLayerWeights.random(h, e, seed=0, device="cuda")
+    x = torch.randn(n, h, device="cuda", generator=torch.Generator(device="cuda").manual_seed(2)).bfloat16()
+    x.requires_grad_()
+    out, l_aux = P.ppmoe_forward(P.World(1, 1), P.ProcessGroup(P.EP, (0,)), x, w.gate, [w.bank], top_k=k,
+                                 capacity_factor=cf)
+    torch.autograd.backward([out, l_aux], [torch.ones_like(out), torch.ones_like(l_aux)])
+    torch.cuda.synchronize()
+    x64 = x.detach().double().cpu().numpy()
+    wg64 = w.gate.wg.detach().double().cpu().numpy()
+    route = O.gate_topk(x64, wg64, k)
+    assert abs(float(l_aux.detach()) - route.l_aux) < 1e-5
+    _, kept, _ = O.dispatch_plan(route.indices, e, O.capacity_of(cf, n, k, e))
+    tokens = np.random.default_rng(1).choice(n, size=32, replace=False)
+    ref_out, ref_dx = per_token_oracle(x64, wg64, w.bank, tokens, k, n, route, kept)
+    sel = torch.as_tensor(tokens, device="cuda")
+    tol = TOL[torch.bfloat16]
+    assert scaled_err(out.detach()[sel].double().cpu().numpy(), ref_out) < tol
+    assert scaled_err(x.grad[sel].double().cpu().numpy(), ref_dx) < tol
