@@ -279,7 +279,8 @@ int ppmoe_nvl_pull_range_ce(const void* const* srcs, int T, int rank, int N, int
                             void* stream);
 
 /* Self-test entry: plain grouped GEMM D_g = A_g * B_g through the tcgen05 path
- * (use_tc=1) or the CUDA-core path (use_tc=0).  mode 0: A [rows x K] K-major
+ * (use_tc=1 default, 2 1-CTA, 3 CTA pair 256x256, 4 CTA pair 256x512) or the
+ * CUDA-core path (use_tc=0).  mode 0: A [rows x K] K-major
  * per segment, B [G*K x N] MN-major, D [rows x N]; mode 1: K from segments,
  * A [rows x M] MN-major, B [rows x N] MN-major, D [G x M x N];
  * mode 2: A K-major segments, B [G*N x K] K-major, D [rows x N].           */

@@ -39,8 +39,21 @@ struct LongKScope {  // marks a token-segment GEMM with a long reduction dimensi
   ~LongKScope() { g_long_k = 0; }
 };
 
-// Rows of a K-major B box: the pair kernel stages half of the 256-wide N tile per CTA.
+// Rows of a K-major B box: the pair kernel stages half of each 256-wide MMA per CTA.
 static uint32_t b_box_rows() { return use_pair() ? kBN / 2 : kBN; }
+
+// Pair-kernel tile width: 256 x 512 ("wide", two MMAs per k-step, 25 % fewer L2 -> SM
+// bytes, epilogue not overlapped) or 256 x 256 (double-buffered TMEM).  PPMOE_WIDE:
+// 0 = never, 1 = every GEMM, long = the long-K token GEMMs (fc2 fwd, fc1 dgrad).  Read per
+// launch (A/B runs).
+static thread_local int g_force_wide = -1;
+static bool use_wide() {
+  if (g_force_wide >= 0) return g_force_wide != 0;
+  const char* e = getenv("PPMOE_WIDE");
+  if (!e) return false;
+  if (strcmp(e, "long") == 0) return g_long_k != 0;
+  return atoi(e) != 0;
+}
 
 template <bool A_MN, bool B_MN, class Epi>
 static int launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const GroupGeom& geo_in, const Epi& epi,
@@ -60,6 +73,13 @@ static int launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const GroupGe
     geo.ksync = 0;
   }
   if (use_pair()) {
+    if (use_wide()) {
+      auto kern = grouped_gemm_sm100_pair<2 * kBN, A_MN, B_MN, Epi>;
+      constexpr int smem = PairSmem<2 * kBN>::kTotal;
+      PPMOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      kern<<<gemm_ctas() / 2 * 2, kPairThreads, smem, s>>>(ta, tb, geo, epi);
+      return check_launch("grouped_gemm_sm100_pair");
+    }
     auto kern = grouped_gemm_sm100_pair<kBN, A_MN, B_MN, Epi>;
     constexpr int smem = PairSmem<kBN>::kTotal;
     PPMOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -409,11 +429,18 @@ int ppmoe_gemm_selftest(int mode, int use_tc, int dtype, const void* A, const vo
                         int N, int K, int rows_cap, void* D, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   PPMOE_REQUIRE(mode >= 0 && mode <= 2, "mode must be 0..2");
-  PPMOE_REQUIRE(use_tc >= 0 && use_tc <= 3, "use_tc: 0 CUDA cores, 1 default tcgen05, 2 1-CTA, 3 CTA pair");
+  PPMOE_REQUIRE(use_tc >= 0 && use_tc <= 4,
+                "use_tc: 0 CUDA cores, 1 default tcgen05, 2 1-CTA, 3 CTA pair 256x256, 4 CTA pair 256x512");
   struct ForceGuard {
-    explicit ForceGuard(int m) { g_force_mode = m; }
-    ~ForceGuard() { g_force_mode = 0; }
-  } guard(use_tc >= 2 ? use_tc - 1 : 0);
+    explicit ForceGuard(int m, int w) {
+      g_force_mode = m;
+      g_force_wide = w;
+    }
+    ~ForceGuard() {
+      g_force_mode = 0;
+      g_force_wide = -1;
+    }
+  } guard(use_tc >= 2 ? (use_tc >= 3 ? 2 : 1) : 0, use_tc == 4 ? 1 : (use_tc == 3 ? 0 : -1));
   PPMOE_REQUIRE(G >= 1 && G <= kMaxGroups, "bad group count %d", G);
   PPMOE_REQUIRE(!use_tc || dtype == kBF16, "tcgen05 path is bf16 only");
   if (mode == 0) {  // D[seg rows x N] = A[seg rows x K] * B_g[K x N] (B MN-major)

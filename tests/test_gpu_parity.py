@@ -36,7 +36,7 @@ def _segments(counts):
     return seg
 
 
-@pytest.mark.parametrize("use_tc", [3, 2, 0])
+@pytest.mark.parametrize("use_tc", [4, 3, 2, 0])
 @pytest.mark.parametrize("mode,counts,M,N,K", [
     (0, [128], 0, 256, 64), (0, [100, 300, 0, 5], 0, 512, 256), (0, [700, 64], 0, 768, 448),
     (2, [128], 0, 256, 64), (2, [200, 33], 0, 512, 320),

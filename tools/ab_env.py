@@ -30,7 +30,7 @@ for v in vals:
     for _ in range(2):
         step()
 torch.cuda.synchronize()
-for rnd in range(6):
+for rnd in range(int(os.environ.get("AB_ROUNDS", "6"))):
     for v in vals:
         os.environ[var] = v
         step()
