@@ -3,7 +3,7 @@
 NVCC      ?= /usr/local/cuda/bin/nvcc
 ARCH      := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS   := $(ARCH) -O3 -std=c++17 -lineinfo -Xcompiler -fPIC -Xcompiler -Wall \
-             --expt-relaxed-constexpr -Iinclude
+             --expt-relaxed-constexpr -Iinclude $(EXTRA)
 SRC_DIR   := paper_2304_11414_b200/csrc
 OBJ_DIR   := build/obj
 LIB       := paper_2304_11414_b200/lib/libppmoe.so

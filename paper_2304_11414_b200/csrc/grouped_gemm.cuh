@@ -508,17 +508,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int iter = 0;
+#ifdef PPMOE_GEMM_STATS
+      long long st_empty = 0, st_full = 0, st_t0 = clock64(), st_a;
+#endif
       for (int tile = pair; tile < total_tiles; tile += num_pairs, ++iter) {
         int g, local;
         sched_locate(tab, G, tile, g, local);
         const int kb_n = tab.k_blocks[g];
         const int acc = iter % kAcc;
         const uint32_t acc_phase = (iter / kAcc) & 1;
+#ifdef PPMOE_GEMM_STATS
+        st_a = clock64();
+#endif
         mbar_wait_cluster(&tmem_empty[acc], acc_phase ^ 1);
+#ifdef PPMOE_GEMM_STATS
+        st_empty += clock64() - st_a;
+#endif
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = 0; kb < kb_n; ++kb) {
+#ifdef PPMOE_GEMM_STATS
+          st_a = clock64();
+#endif
           mbar_wait_sleep(&full[stage], phase);
+#ifdef PPMOE_GEMM_STATS
+          st_full += clock64() - st_a;
+#endif
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + stage * L::kStageBytes);
           const uint32_t sb = sa + L::kABytes;
@@ -541,6 +556,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         if (elected) umma_commit_pair_mc(&tmem_full[acc], 0x3);
         __syncwarp();
       }
+#ifdef PPMOE_GEMM_STATS
+      if (lane == 0 && (pair % 16) == 0)
+        printf("gemm BN=%d pair %d: tiles %d cycles %lld wait tmem_empty %lld (%.1f%%) wait full %lld (%.1f%%)\n", BN,
+               pair, iter, clock64() - st_t0, st_empty, 100.0 * st_empty / (clock64() - st_t0), st_full,
+               100.0 * st_full / (clock64() - st_t0));
+#endif
     }
     __syncwarp();
   } else if (warp >= 2) {
