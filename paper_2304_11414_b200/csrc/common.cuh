@@ -12,6 +12,10 @@
 
 namespace ppmoe {
 
+// Row stride (bytes) of the per-warp epilogue staging area: 64 B of bf16 + 16 B pad, so
+// the 16-byte shared-memory phases of a warp are bank-conflict free.
+constexpr int kStageStride = 80;
+
 enum DType : int { kBF16 = 0, kF32 = 1 };
 
 // ----------------------------------------------------------------- numerics

@@ -111,6 +111,39 @@ __device__ __forceinline__ void scatter_add_row(float* p, const float (&x)[W], f
     if (j < valid) atomicAdd(p + j, s * x[j]);
 }
 
+// Warp-cooperative row store through a per-warp shared-memory staging area (32 rows x
+// kStageStride bytes).  The tcgen05 epilogue holds one output row per lane, so a plain
+// store instruction touches 32 rows; staging turns each 32-column chunk into four
+// instructions of 8 rows x 64 contiguous bytes (4x fewer L1 store wavefronts).  Every lane
+// of the warp must call it (convergent); `p` = this lane's destination or null.
+__device__ __forceinline__ void stage_store32(uint8_t* buf, __nv_bfloat16* p, const float (&x)[32], int valid) {
+  const int lane = threadIdx.x & 31;
+  if (valid < 32) {  // ragged last chunk of a row (N % 32 != 0): direct stores
+    if (p) store_row<__nv_bfloat16, 32>(p, x, valid);
+    return;
+  }
+  uint4* mine = reinterpret_cast<uint4*>(buf + lane * kStageStride);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    uint4 u;
+    u.x = pack_bf16x2(x[8 * j], x[8 * j + 1]);
+    u.y = pack_bf16x2(x[8 * j + 2], x[8 * j + 3]);
+    u.z = pack_bf16x2(x[8 * j + 4], x[8 * j + 5]);
+    u.w = pack_bf16x2(x[8 * j + 6], x[8 * j + 7]);
+    mine[j] = u;
+  }
+  const unsigned long long pp = reinterpret_cast<unsigned long long>(p);
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = 8 * i + (lane >> 2), seg = lane & 3;
+    const unsigned long long q = __shfl_sync(0xffffffffu, pp, r);
+    const uint4 u = *reinterpret_cast<const uint4*>(buf + r * kStageStride + seg * 16);
+    if (q) *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(q) + seg * 8) = u;
+  }
+  __syncwarp();
+}
+
 // fc1 forward: a = X_e * up_e + bias_up ; Act = GeLU(a), and GeLU'(a) saved for the
 // backward so the fc2 data-gradient epilogue is a plain multiply (moe.py:101-104,
 // tensor.py:199-207).
@@ -168,6 +201,29 @@ struct EpiFc2Fwd {
   T* const* owner_slots;
   const int* pair_pos;
   int K;
+  // staged-store interface (plain Y / Y2 row stores only)
+  static constexpr bool kStageable = std::is_same<T, __nv_bfloat16>::value;
+  __device__ __forceinline__ bool stage_ok() const { return !out_acc && !owner_acc && !owner_slots; }
+  __device__ __forceinline__ int stage_n() const { return H; }
+  __device__ __forceinline__ void stage_values(int g, int row, int n0, const float (&v)[32], float (&x)[32]) const {
+    float b[32];
+    if (bias) load_row<T, 32>(bias + static_cast<size_t>(g) * H + n0, b, min(32, H - n0));
+    else
+#pragma unroll
+      for (int j = 0; j < 32; ++j) b[j] = 0.f;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] = v[j] + b[j];
+    if (drop_p > 0.f) {
+      const float inv = 1.f / (1.f - drop_p);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) x[j] = dropout_uniform(seed, row, n0 + j) >= drop_p ? x[j] * inv : 0.f;
+    }
+  }
+  __device__ __forceinline__ T* stage_dst(int g, int m, int row, int n0, int which) const {
+    T* base = which == 0 ? y : y2;
+    return base ? base + static_cast<size_t>(row) * H + n0 : nullptr;
+  }
+  __device__ __forceinline__ bool stage_second() const { return y2 != nullptr; }
   template <int W>
   __device__ __forceinline__ void apply(int g, int m, int row, int n0, const float (&v)[W]) const {
     const int valid = min(W, H - n0);
@@ -256,6 +312,17 @@ struct EpiFc1Dgrad {
   const int* seg;
   const int* tok;
   int cs;
+  static constexpr bool kStageable = std::is_same<T, __nv_bfloat16>::value;
+  __device__ __forceinline__ bool stage_ok() const { return dxs != nullptr; }
+  __device__ __forceinline__ int stage_n() const { return H; }
+  __device__ __forceinline__ void stage_values(int, int, int, const float (&v)[32], float (&x)[32]) const {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] = v[j];
+  }
+  __device__ __forceinline__ T* stage_dst(int, int, int row, int n0, int) const {
+    return dxs + static_cast<size_t>(row) * H + n0;
+  }
+  __device__ __forceinline__ bool stage_second() const { return false; }
   template <int W>
   __device__ __forceinline__ void apply(int g, int m, int row, int n0, const float (&v)[W]) const {
     const int valid = min(W, H - n0);
@@ -276,6 +343,17 @@ struct EpiWgrad {
   int M;
   int N;
   int cs;
+  static constexpr bool kStageable = std::is_same<T, __nv_bfloat16>::value;
+  __device__ __forceinline__ bool stage_ok() const { return true; }
+  __device__ __forceinline__ int stage_n() const { return N; }
+  __device__ __forceinline__ void stage_values(int, int, int, const float (&v)[32], float (&x)[32]) const {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] = v[j];
+  }
+  __device__ __forceinline__ T* stage_dst(int g, int m, int, int n0, int) const {
+    return m < M ? out + (static_cast<size_t>(g) * M + m) * N + n0 : nullptr;
+  }
+  __device__ __forceinline__ bool stage_second() const { return false; }
   template <int W>
   __device__ __forceinline__ void apply(int g, int m, int row, int n0, const float (&v)[W]) const {
     if (m >= M) return;

@@ -47,6 +47,14 @@ static uint32_t b_box_rows() { return use_pair() ? kBN / 2 : kBN; }
 // 0 = never, 1 = every GEMM, long = the long-K token GEMMs (fc2 fwd, fc1 dgrad).  Read per
 // launch (A/B runs).
 static thread_local int g_force_wide = -1;
+// Warp-cooperative staged epilogue stores (PPMOE_STAGE: 0 off, 1 on, unset = on for the
+// wide tile, whose epilogue is exposed; off for the 256-wide tile, whose epilogue overlaps
+// the next tile's mainloop).  Read per launch.
+static int staged_stores(bool wide) {
+  const char* e = getenv("PPMOE_STAGE");
+  if (!e) return wide ? 1 : 0;
+  return atoi(e) != 0;
+}
 static bool use_wide() {
   if (g_force_wide >= 0) return g_force_wide != 0;
   const char* e = getenv("PPMOE_WIDE");
@@ -73,6 +81,7 @@ static int launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const GroupGe
     geo.ksync = 0;
   }
   if (use_pair()) {
+    geo.stage = staged_stores(use_wide());
     if (use_wide()) {
       auto kern = grouped_gemm_sm100_pair<2 * kBN, A_MN, B_MN, Epi>;
       constexpr int smem = PairSmem<2 * kBN>::kTotal;
@@ -231,6 +240,7 @@ static GroupGeom geom(int G, int N, int M_fixed, int K_fixed, const int* seg, in
   }
   g.ksync_ctr = nullptr;
   g.ksync = 0;
+  g.stage = 0;
   g.hint = load_hint();
   g.G = G;
   g.N = N;

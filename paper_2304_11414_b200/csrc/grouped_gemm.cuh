@@ -49,6 +49,17 @@ struct GroupGeom {
   // operand slices are re-used from L2 instead of re-read from DRAM.  Bounded wait.
   unsigned int* ksync_ctr;
   int ksync;
+  int stage;      // pair kernel: warp-cooperative staged row stores for stageable epilogues
+};
+
+// Epilogues that can hand their bf16 rows to the staged (coalesced) store path.
+template <class E, class = void>
+struct StageTrait {
+  static constexpr bool value = false;
+};
+template <class E>
+struct StageTrait<E, std::void_t<decltype(E::kStageable)>> {
+  static constexpr bool value = E::kStageable;
 };
 
 template <int BN>
@@ -341,7 +352,9 @@ struct PairSmem {
   static constexpr int kBarBytes = (2 * kStages + 4) * 8 + 16;
   static constexpr int kSchedOffset = kBarOffset + kBarBytes;
   static constexpr int kSchedBytes = (kMaxGroups + 1) * 4 * 8;
-  static constexpr int kTotal = kSchedOffset + kSchedBytes + 1024;
+  static constexpr int kStageBufOffset = (kSchedOffset + kSchedBytes + 15) / 16 * 16;
+  static constexpr int kStageBufBytes = kPairEpiWarps * 32 * kStageStride;
+  static constexpr int kTotal = kStageBufOffset + kStageBufBytes + 1024;
 };
 
 template <int BN, bool A_MN, bool B_MN, class Epi>
@@ -574,6 +587,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     constexpr int kChunksPerWarp = BN / 32 / (kPairEpiWarps / 4);
     const int row_in_tile = static_cast<int>(rank) * 128 + q * 32 + lane;
     const uint32_t empty_leader = mapa_shared(&tmem_empty[0], 0);
+    constexpr bool kCanStage = StageTrait<Epi>::value;
+    uint8_t* stage_buf = smem + L::kStageBufOffset + (warp - 2) * 32 * kStageStride;
+    bool staged = false;
+    if constexpr (kCanStage) staged = geo.stage && epi.stage_ok();
     int iter = 0;
     for (int tile = pair; tile < total_tiles; tile += num_pairs, ++iter) {
       int g, local;
@@ -598,6 +615,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         }
         const bool row_ok = m < tab.m_rows[g];
         const int n0 = nt * BN + c * 32;
+        if constexpr (kCanStage) {
+          if (staged) {  // warp-uniform
+            const int row = tab.row_base[g] + m;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int nn = n0 + 32 * h;
+              if (nn >= geo.N) break;
+              float x[32];
+              if (row_ok) epi.stage_values(g, row, nn, *reinterpret_cast<const float(*)[32]>(v + 32 * h), x);
+              const int valid = min(32, epi.stage_n() - nn);
+              stage_store32(stage_buf, row_ok ? epi.stage_dst(g, m, row, nn, 0) : nullptr, x, valid);
+              if (epi.stage_second())
+                stage_store32(stage_buf, row_ok ? epi.stage_dst(g, m, row, nn, 1) : nullptr, x, valid);
+            }
+            continue;
+          }
+        }
         if (n0 < geo.N && row_ok)
           epi.template apply<32>(g, m, tab.row_base[g] + m, n0, *reinterpret_cast<const float(*)[32]>(v));
         if (n0 + 32 < geo.N && row_ok)

@@ -466,6 +466,28 @@ def test_c3_shape_routing_capacity_and_step():
     assert torch.isfinite(w.bank.up.grad).all() and torch.isfinite(w.gate.wg.grad).all()
 
 
+@pytest.mark.parametrize("hidden_size", [256, 264])
+@pytest.mark.parametrize("wide,stage", [("0", "1"), ("1", "0"), ("1", "1"), ("long", "1")])
+def test_wide_tile_and_staged_stores_bit_identical(hidden_size, wide, stage, monkeypatch):
+    """The 256x512 pair tile (PPMOE_WIDE) and the shared-memory staged epilogue stores
+    (PPMOE_STAGE) keep each output element's k order and values, so the layer's outputs and
+    gradients are bit-identical to the default 256x256 tile with direct stores (h = 264
+    exercises the ragged last 32-column chunk)."""
+    layer = oracle_rounded(O.init_layer(hidden_size, 8, seed=31), torch.bfloat16)
+    hidden = torch.randn(1700, hidden_size).bfloat16().double().numpy()
+    monkeypatch.setenv("PPMOE_POISON", "1")
+    monkeypatch.setenv("PPMOE_WIDE", "0")
+    monkeypatch.setenv("PPMOE_STAGE", "0")
+    base = run_cuda_layer(hidden, device_weights(layer, torch.bfloat16), k=2, capacity_factor=1.25)
+    monkeypatch.setenv("PPMOE_WIDE", wide)
+    monkeypatch.setenv("PPMOE_STAGE", stage)
+    got = run_cuda_layer(hidden, device_weights(layer, torch.bfloat16), k=2, capacity_factor=1.25)
+    assert np.array_equal(base["out"], got["out"])
+    assert np.array_equal(base["grad_hidden"], got["grad_hidden"])
+    for key in base["grads"]:
+        assert np.array_equal(base["grads"][key], got["grads"][key]), key
+
+
 def test_fused_bias_colsums_match_separate_pass(monkeypatch):
     """Bias gradients from the fused column-sum partials (bwd_dy / fc2 dgrad epilogue) equal
     the separate column-sum pass (both sum the same bf16 dY / dH values)."""

@@ -1,5 +1,6 @@
 """Dev tool: interleaved A/B of environment-switched code paths on the C2 step, one process.
-usage: python tools/ab_env.py VAR=val1,val2 [VAR2=...]  (values applied per round-robin arm)"""
+usage: python tools/ab_env.py VAR=val1,val2          (one variable, one arm per value)
+       python tools/ab_env.py A=x+B=y C=z+D=w ...    (one arm per argument, '+'-joined settings)"""
 import os, statistics, sys
 sys.path.insert(0, ".")
 import torch
@@ -12,8 +13,20 @@ x = torch.randn(n, h, device=dev).bfloat16().requires_grad_()
 g_out = torch.ones(n, h, device=dev, dtype=torch.bfloat16)
 g_aux = torch.ones((), device=dev)
 world, group = P.World(1, 1), P.ProcessGroup(P.EP, (0,))
-var, vals = sys.argv[1].split("=")
-vals = vals.split(",")
+if len(sys.argv) > 2 or "+" in sys.argv[1]:
+    var, vals = "arm", sys.argv[1:]
+else:
+    var, vals = sys.argv[1].split("=")
+    vals = vals.split(",")
+
+
+def set_arm(v):
+    if var != "arm":
+        os.environ[var] = v
+        return
+    for kv in v.split("+"):
+        k_, v_ = kv.split("=")
+        os.environ[k_] = v_
 
 
 def step():
@@ -26,13 +39,13 @@ def step():
 
 res = {v: [] for v in vals}
 for v in vals:
-    os.environ[var] = v
+    set_arm(v)
     for _ in range(2):
         step()
 torch.cuda.synchronize()
 for rnd in range(int(os.environ.get("AB_ROUNDS", "6"))):
     for v in vals:
-        os.environ[var] = v
+        set_arm(v)
         step()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -44,4 +57,4 @@ for rnd in range(int(os.environ.get("AB_ROUNDS", "6"))):
         res[v].append(e0.elapsed_time(e1) / 5)
 for v in vals:
     ms = statistics.median(res[v])
-    print(f"{var}={v:6s} median {ms:.3f} ms/step  {n / ms * 1e3:,.0f} tok/s   all={[round(t, 2) for t in res[v]]}")
+    print(f"{var}={v} median {ms:.3f} ms/step  {n / ms * 1e3:,.0f} tok/s   all={[round(t, 2) for t in res[v]]}")
