@@ -440,7 +440,8 @@ def experts_backward_data(grad_out, st: ExpertFwdState, up, down, weight_scaling
 
 def experts_backward_weights(st: ExpertFwdState, dy, dh, up, down, has_bias: bool, parts=(None, None)):
     """Weight-gradient half: d down = Actᵀ·dY, d up = Xsᵀ·dH (variable-K grouped GEMMs) and
-    the bias gradients.  Independent of dX, so it overlaps the dX all-reduce."""
+    the bias gradients.  Independent of dX, so it overlaps the dX all-reduce: under an
+    `sm_budget` only the first GEMM leaves SMs free for it (PPMOE_BUDGET_SPLIT=0: both)."""
     h = dy.shape[1]
     f = up.shape[2]
     el, rows_cap = st.el, st.rows_cap
@@ -452,6 +453,10 @@ def experts_backward_weights(st: ExpertFwdState, dy, dh, up, down, has_bias: boo
     d_bd = torch.empty((el, h), dtype=dy.dtype, device=dev) if has_bias else None
     call("ppmoe_expert_fc2_wgrad", dt, ptr(st.act), ptr(dy), ptr(st.seg), el, h, f, rows_cap, ptr(d_down), ptr(d_bd),
          ptr(dy_part), s)
+    if os.environ.get("PPMOE_BUDGET_SPLIT", "1") == "1":
+        # the collective beside us finishes within the first GEMM: the second takes every SM
+        # (T = 4: 5.82 vs 5.93 ms per step, T = 2: 10.79 vs 11.05; profiles/r01_sm_budget.md)
+        call("ppmoe_set_gemm_sm_budget", 0)
     d_up = torch.empty_like(up)
     d_bu = torch.empty((el, f), dtype=dy.dtype, device=dev) if has_bias else None
     call("ppmoe_expert_fc1_wgrad", dt, ptr(st.xs), ptr(dh), ptr(st.seg), el, h, f, rows_cap, ptr(d_up), ptr(d_bu),
