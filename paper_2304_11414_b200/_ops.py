@@ -53,15 +53,26 @@ class sm_budget:
     def __init__(self, sms: int):
         self.sms = int(sms)
 
+    active = 0  # the budget in force (0 = none)
+
     def __enter__(self):
         if self.sms:
             _lib.call("ppmoe_set_gemm_sm_budget", self.sms)
+            sm_budget.active = self.sms
         return self
 
     def __exit__(self, *exc):
         if self.sms:
             _lib.call("ppmoe_set_gemm_sm_budget", 0)
+            sm_budget.active = 0
         return False
+
+    @staticmethod
+    def release():
+        """Drop the budget early (the rest of the block runs on every SM)."""
+        if sm_budget.active:
+            _lib.call("ppmoe_set_gemm_sm_budget", 0)
+            sm_budget.active = 0
 
 
 def overlap_sm_budget() -> int:
@@ -456,7 +467,7 @@ def experts_backward_weights(st: ExpertFwdState, dy, dh, up, down, has_bias: boo
     if os.environ.get("PPMOE_BUDGET_SPLIT", "1") == "1":
         # the collective beside us finishes within the first GEMM: the second takes every SM
         # (T = 4: 5.82 vs 5.93 ms per step, T = 2: 10.79 vs 11.05; profiles/r01_sm_budget.md)
-        call("ppmoe_set_gemm_sm_budget", 0)
+        sm_budget.release()
     d_up = torch.empty_like(up)
     d_bu = torch.empty((el, f), dtype=dy.dtype, device=dev) if has_bias else None
     call("ppmoe_expert_fc1_wgrad", dt, ptr(st.xs), ptr(dh), ptr(st.seg), el, h, f, rows_cap, ptr(d_up), ptr(d_bu),
