@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-a2a", action="store_true", help="skip the all-to-all (DPMoE) comparator")
+    ap.add_argument("--upstream", choices=["ones", "normal"], default="ones",
+                    help="upstream gradient dOut: ones (loss = sum(out) + l_aux, test_moe.py:400; SURVEY 8(d)) "
+                         "or N(0,1) bf16; the other one is timed as well and reported under upstream_alt")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU time of the cpu_baseline sample")
     a = ap.parse_args()
     base = C3 if a.config == "c3" else C2
@@ -75,6 +78,7 @@ def config_of(a, n_gpus):
         "capacity_factor": "inf" if math.isinf(a.capacity_factor) else a.capacity_factor,
         "tp": n_gpus, "parallelism": f"tp{n_gpus} (experts {a.experts // n_gpus}/GPU)",
         "l2": "per-step working set (weights 2.1 GB + activations) >> 126 MB L2; no flush needed",
+        "upstream_grad": getattr(a, "upstream", "ones"),
     }
 
 
@@ -290,7 +294,11 @@ def main():
         group = P.ProcessGroup(P.EP, (0,))
     gen = torch.Generator(device=dev).manual_seed(1234)  # same hidden on every rank (replicated activation)
     x = torch.randn(n, h, device=dev, generator=gen).to(torch.bfloat16).requires_grad_()
-    g_out = torch.ones(n, h, device=dev, dtype=torch.bfloat16)
+    # dOut: all ones gives constant-per-row dY (low tensor-core switching power, so ~3 % more
+    # clock under the power cap than a random gradient); both are timed (upstream_alt)
+    g_ones = torch.ones(n, h, device=dev, dtype=torch.bfloat16)
+    g_normal = torch.randn(n, h, device=dev, generator=torch.Generator(device=dev).manual_seed(99)).bfloat16()
+    g_out = g_ones if a.upstream == "ones" else g_normal
     g_aux = torch.ones((), device=dev, dtype=torch.float32)
     params = w.leaf_parameters()
 
@@ -338,6 +346,22 @@ def main():
     ms = float(t)
     value = n / (ms / 1e3)
     ksum = prof.summary()
+
+    # ---- the same step with the other upstream gradient (untimed warm-up step first)
+    alt_name = "normal" if a.upstream == "ones" else "ones"
+    g_out = g_normal if a.upstream == "ones" else g_ones
+    step(x)
+    barrier()
+    ev0.record()
+    for _ in range(a.steps):
+        step(x)
+    ev1.record()
+    barrier()
+    t = torch.tensor([ev0.elapsed_time(ev1) / a.steps], device=dev, dtype=torch.float64)
+    if distributed:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    upstream_alt = {"upstream_grad": alt_name, "value": n / (float(t) / 1e3), "ms_per_step": float(t)}
+    g_out = g_ones if a.upstream == "ones" else g_normal
 
     # ---- roofline of the dominant kernel: the grouped expert GEMM (six launches per step)
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
@@ -463,7 +487,7 @@ def main():
                 "vs_baseline": None, "dtype": "bf16", "data": f"synthetic (random-init weights of the {a.config.upper()} layer, N(0,1) tokens)",
                 "config": config_of(a, world_size), "roofline": roofline, "cpu_baseline": cb, "e2e": e2e,
                 "gpu_launches": int(launches), "clocks": clk.summary(), "a2a_comparator": a2a, "kernels": per_kernel,
-                "host_enqueue_ms_per_step": round(host_ms, 3),
+                "host_enqueue_ms_per_step": round(host_ms, 3), "upstream_alt": upstream_alt,
                 "gemm_launches_per_step": gemm_launches}
         print(json.dumps(line), flush=True)
     if distributed:

@@ -10,7 +10,8 @@ h, E, k, n = 4096, 8, 2, 16384
 dev = torch.device("cuda", 0)
 w = P.MoeLayerWeights.random(h, E, seed=0, device=dev)
 x = torch.randn(n, h, device=dev).bfloat16().requires_grad_()
-g_out = torch.ones(n, h, device=dev, dtype=torch.bfloat16)
+g_ones = torch.ones(n, h, device=dev, dtype=torch.bfloat16)
+g_normal = torch.randn(n, h, device=dev).bfloat16()  # AB_UPSTREAM=normal (arm setting)
 g_aux = torch.ones((), device=dev)
 world, group = P.World(1, 1), P.ProcessGroup(P.EP, (0,))
 if len(sys.argv) > 2 or "+" in sys.argv[1]:
@@ -34,6 +35,7 @@ def step():
         p.grad = None
     x.grad = None
     out, l_aux = P.ppmoe_forward(world, group, x, w.gate, [w.bank], top_k=k)
+    g_out = g_normal if os.environ.get("AB_UPSTREAM") == "normal" else g_ones
     torch.autograd.backward([out, l_aux], [g_out, g_aux])
 
 
