@@ -35,6 +35,17 @@ def test_library_exports_every_header_symbol():
     assert lib.ppmoe_version() == 1
 
 
+def test_missing_library_fails_loudly(monkeypatch):
+    """No CPU fallback: with the CUDA library absent every product entry point raises."""
+    monkeypatch.setattr(_lib, "_lib", None)
+    monkeypatch.setattr(_lib, "LIB_PATH", ROOT / "no_such_dir" / "libppmoe.so")
+    with pytest.raises(ImportError, match="no CPU fallback"):
+        _lib.call("ppmoe_version")
+    w = P.MoeLayerWeights.random(64, 4, seed=0, device="cpu")
+    with pytest.raises(ImportError, match="no CPU fallback"):
+        P.ppmoe_forward(P.World(1, 1), P.ProcessGroup(P.EP, (0,)), torch.zeros(8, 64).bfloat16(), w.gate, [w.bank])
+
+
 def test_workspace_queries_are_host_only():
     lib = _lib.load()
     assert lib.ppmoe_route_workspace_bytes(16384, 8, 2) > 0
