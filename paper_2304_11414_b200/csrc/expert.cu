@@ -47,9 +47,9 @@ static uint32_t b_box_rows() { return use_pair() ? kBN / 2 : kBN; }
 // 0 = never, 1 = every GEMM, long = the long-K token GEMMs (fc2 fwd, fc1 dgrad).  Read per
 // launch (A/B runs).
 static thread_local int g_force_wide = -1;
-// Warp-cooperative staged epilogue stores (PPMOE_STAGE: 0 off, 1 on, unset = on for the
-// wide tile, whose epilogue is exposed; off for the 256-wide tile, whose epilogue overlaps
-// the next tile's mainloop).  Read per launch.
+// Warp-cooperative staged epilogue stores for the wide tile (PPMOE_STAGE: 0 off, 1 on,
+// unset = on); its epilogue is exposed.  The 256-wide tile has no staging buffer (its
+// epilogue overlaps the next tile's mainloop) and ignores the switch.  Read per launch.
 static int staged_stores(bool wide) {
   const char* e = getenv("PPMOE_STAGE");
   if (!e) return wide ? 1 : 0;

@@ -353,7 +353,10 @@ struct PairSmem {
   static constexpr int kSchedOffset = kBarOffset + kBarBytes;
   static constexpr int kSchedBytes = (kMaxGroups + 1) * 4 * 8;
   static constexpr int kStageBufOffset = (kSchedOffset + kSchedBytes + 15) / 16 * 16;
-  static constexpr int kStageBufBytes = kPairEpiWarps * 32 * kStageStride;
+  // staged epilogue stores exist only for the wide tile: 20 KB more shared memory on the
+  // 256-wide tile shrinks its L1 carveout and cost 2-5 points of tensor-pipe activity
+  static constexpr bool kHasStageBuf = BN > 256;
+  static constexpr int kStageBufBytes = kHasStageBuf ? kPairEpiWarps * 32 * kStageStride : 0;
   static constexpr int kTotal = kStageBufOffset + kStageBufBytes + 1024;
 };
 
@@ -587,7 +590,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     constexpr int kChunksPerWarp = BN / 32 / (kPairEpiWarps / 4);
     const int row_in_tile = static_cast<int>(rank) * 128 + q * 32 + lane;
     const uint32_t empty_leader = mapa_shared(&tmem_empty[0], 0);
-    constexpr bool kCanStage = StageTrait<Epi>::value;
+    constexpr bool kCanStage = StageTrait<Epi>::value && L::kHasStageBuf;
     uint8_t* stage_buf = smem + L::kStageBufOffset + (warp - 2) * 32 * kStageStride;
     bool staged = false;
     if constexpr (kCanStage) staged = geo.stage && epi.stage_ok();
