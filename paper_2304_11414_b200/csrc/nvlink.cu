@@ -142,12 +142,16 @@ __global__ void __launch_bounds__(256)
   __shared__ float sdl[kOgTile][DLW];
   const int j = (blockIdx.y * blockDim.x + threadIdx.x) * CW;
   const bool active = j < H;
-  float wg[EB > 0 ? CW : 1][EB > 0 ? EB : 1];
+  // gate-term form: this CTA's Wg columns in shared memory, [c][e][thread] so a warp's
+  // reads are conflict-free (in registers they cost 32 per thread and halved the resident
+  // CTAs, which left too few row loads in flight for HBM)
+  __shared__ float swg[EB > 0 ? CW * EB * 256 : 1];
   if constexpr (EB > 0) {
-#pragma unroll
-    for (int c = 0; c < CW; ++c)
-#pragma unroll
-      for (int e = 0; e < EB; ++e) wg[c][e] = (active && e < E) ? Wg[static_cast<size_t>(j + c) * E + e] : 0.f;
+    for (int i = threadIdx.x; i < CW * EB * 256; i += blockDim.x) {
+      const int t = i % 256, ce = i / 256, c = ce / EB, e = ce % EB;
+      const int jj = (blockIdx.y * 256 + t) * CW + c;
+      swg[i] = (jj < H && e < E) ? Wg[static_cast<size_t>(jj) * E + e] : 0.f;
+    }
   }
   for (int tb = t0 + blockIdx.x * kOgTile; tb < t1; tb += gridDim.x * kOgTile) {
     const int nt = min(kOgTile, t1 - tb);
@@ -199,13 +203,17 @@ __global__ void __launch_bounds__(256)
       }
       if constexpr (EB > 0) {
 #pragma unroll
-        for (int u = 0; u < U; ++u)
+        for (int e = 0; e < EB; ++e) {
+          float d[U];
 #pragma unroll
-          for (int e = 0; e < EB; ++e) {
-            const float d = sdl[min(u0 + u, kOgTile - 1)][e];
+          for (int u = 0; u < U; ++u) d[u] = sdl[min(u0 + u, kOgTile - 1)][e];
 #pragma unroll
-            for (int c = 0; c < CW; ++c) acc[u][c] = fmaf(d, wg[c][e], acc[u][c]);
+          for (int c = 0; c < CW; ++c) {
+            const float wv = swg[(c * EB + e) * 256 + threadIdx.x];
+#pragma unroll
+            for (int u = 0; u < U; ++u) acc[u][c] = fmaf(d[u], wv, acc[u][c]);
           }
+        }
       } else if constexpr (EB < 0) {
         for (int e = 0; e < E; ++e) {
           float wc[CW];
