@@ -139,16 +139,18 @@ __global__ void __launch_bounds__(256)
   const int K = KT > 0 ? KT : Kr;
   __shared__ const __nv_bfloat16* src[kOgTile][KS];
   __shared__ float sw[kOgTile][KS];
-  __shared__ float sdl[kOgTile][DLW];
+  __shared__ __align__(16) float sdl[kOgTile][DLW];
   const int j = (blockIdx.y * blockDim.x + threadIdx.x) * CW;
   const bool active = j < H;
-  // gate-term form: this CTA's Wg columns in shared memory, [c][e][thread] so a warp's
-  // reads are conflict-free (in registers they cost 32 per thread and halved the resident
-  // CTAs, which left too few row loads in flight for HBM)
-  __shared__ float swg[EB > 0 ? CW * EB * 256 : 1];
+  // gate-term form: this CTA's Wg columns in shared memory, [e][thread][c] so each thread
+  // reads its CW columns of one expert as 16-byte vectors, conflict-free across the warp
+  // (in registers they cost 32 per thread and halved the resident CTAs, which left too
+  // few row loads in flight for HBM)
+  static_assert(EB <= 0 || CW % 4 == 0, "vector Wg reads need CW % 4 == 0");
+  __shared__ __align__(16) float swg[EB > 0 ? CW * EB * 256 : 4];
   if constexpr (EB > 0) {
     for (int i = threadIdx.x; i < CW * EB * 256; i += blockDim.x) {
-      const int t = i % 256, ce = i / 256, c = ce / EB, e = ce % EB;
+      const int c = i % CW, t = (i / CW) % 256, e = i / (CW * 256);
       const int jj = (blockIdx.y * 256 + t) * CW + c;
       swg[i] = (jj < H && e < E) ? Wg[static_cast<size_t>(jj) * E + e] : 0.f;
     }
@@ -202,16 +204,26 @@ __global__ void __launch_bounds__(256)
           if (s < K) acc_bf16<CW>(acc[u], v[u][s], sw[min(u0 + u, kOgTile - 1)][s]);
       }
       if constexpr (EB > 0) {
+        static_assert(EB % 4 == 0, "vector dL reads need EB % 4 == 0");
 #pragma unroll
-        for (int e = 0; e < EB; ++e) {
-          float d[U];
+        for (int e4 = 0; e4 < EB; e4 += 4) {
+          float4 d[U];
 #pragma unroll
-          for (int u = 0; u < U; ++u) d[u] = sdl[min(u0 + u, kOgTile - 1)][e];
+          for (int u = 0; u < U; ++u) d[u] = *reinterpret_cast<const float4*>(&sdl[min(u0 + u, kOgTile - 1)][e4]);
 #pragma unroll
-          for (int c = 0; c < CW; ++c) {
-            const float wv = swg[(c * EB + e) * 256 + threadIdx.x];
+          for (int ee = 0; ee < 4; ++ee) {
+            float wv[CW];
 #pragma unroll
-            for (int u = 0; u < U; ++u) acc[u][c] = fmaf(d[u], wv, acc[u][c]);
+            for (int c4 = 0; c4 < CW; c4 += 4)
+              *reinterpret_cast<float4*>(&wv[c4]) =
+                  *reinterpret_cast<const float4*>(&swg[((e4 + ee) * 256 + threadIdx.x) * CW + c4]);
+#pragma unroll
+            for (int c = 0; c < CW; ++c)
+#pragma unroll
+              for (int u = 0; u < U; ++u) {
+                const float dv = ee == 0 ? d[u].x : ee == 1 ? d[u].y : ee == 2 ? d[u].z : d[u].w;
+                acc[u][c] = fmaf(dv, wv[c], acc[u][c]);
+              }
           }
         }
       } else if constexpr (EB < 0) {
