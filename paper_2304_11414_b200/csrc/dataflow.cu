@@ -12,6 +12,8 @@
 //   gate_grads_kernel    dX = dx_acc + dL Wg^T and per-chunk X^T dL partials
 //                        (matmul backward of the gate projection, tensor.py:134-138).
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 
 #include "../../include/ppmoe_capi.h"
 #include "common.cuh"
@@ -258,6 +260,108 @@ __global__ void __launch_bounds__(256)
         s1 += v.y;
       }
       *reinterpret_cast<float2*>(part + static_cast<size_t>(b) * H + c) = make_float2(s0, s1);
+    }
+    __syncthreads();
+  }
+}
+
+// Column-slab form of bwd_dy_block_kernel (default): warp w owns the 256-column chunks
+// w, w+8, ... of all 32 rows of the block, so the dY column sums accumulate in registers
+// in the same row order (bit-identical partials) and phase 2's L2 re-read of dY is gone.
+// The per-row dot <dOut[t], Y[r]> (the dw of scale_rows' backward, tensor.py:184-196) is
+// summed per warp and then over the 8 warps in a fixed order through shared memory.
+// CPW = chunks per warp = ceil(H / 2048).
+template <int CPW>
+__global__ void __launch_bounds__(256, 8 / CPW)
+    bwd_dy_cols_kernel(const __nv_bfloat16* __restrict__ dOut, const __nv_bfloat16* __restrict__ Y,
+                       const int* __restrict__ seg, int El, int H, const int* __restrict__ tok_local,
+                       const float* __restrict__ w_local, int weight_scaling, float drop_p,
+                       unsigned long long seed, __nv_bfloat16* __restrict__ dY, float* __restrict__ dw,
+                       float* __restrict__ part) {
+  __shared__ float red[8][33];
+  const int rows = seg[El] - seg[0];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nblk = rows >> 5;
+  const int nchunk = H >> 8;
+  const float inv = drop_p > 0.f ? 1.f / (1.f - drop_p) : 1.f;
+  for (int b = blockIdx.x; b < nblk; b += gridDim.x) {
+    const int r0 = b << 5;
+    float cs[CPW][8];
+#pragma unroll
+    for (int q = 0; q < CPW; ++q)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) cs[q][i] = 0.f;
+#pragma unroll 2
+    for (int rr = 0; rr < 32; ++rr) {
+      const int r = r0 + rr;
+      const int tok = tok_local[r];
+      __nv_bfloat16* dy = dY + static_cast<size_t>(r) * H;
+      float acc = 0.f;
+      if (tok < 0) {
+#pragma unroll
+        for (int q = 0; q < CPW; ++q) {
+          const int ch = warp + 8 * q;
+          if (ch < nchunk) *reinterpret_cast<uint4*>(dy + ch * 256 + lane * 8) = make_uint4(0, 0, 0, 0);
+        }
+      } else {
+        const float sw = weight_scaling ? w_local[r] : 1.f;
+        const __nv_bfloat16* g = dOut + static_cast<size_t>(tok) * H;
+        const __nv_bfloat16* y = Y + static_cast<size_t>(r) * H;
+        uint4 gu[CPW], yu[CPW];
+#pragma unroll
+        for (int q = 0; q < CPW; ++q) {
+          const int ch = warp + 8 * q;
+          if (ch < nchunk) {
+            gu[q] = *reinterpret_cast<const uint4*>(g + ch * 256 + lane * 8);
+            yu[q] = *reinterpret_cast<const uint4*>(y + ch * 256 + lane * 8);
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < CPW; ++q) {
+          const int ch = warp + 8 * q;
+          if (ch >= nchunk) continue;
+          const int j = ch * 256 + lane * 8;
+          const __nv_bfloat162* gh = reinterpret_cast<const __nv_bfloat162*>(&gu[q]);
+          const __nv_bfloat162* yh = reinterpret_cast<const __nv_bfloat162*>(&yu[q]);
+          uint4 out;
+          uint32_t* o = reinterpret_cast<uint32_t*>(&out);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float2 gf = __bfloat1622float2(gh[i]);
+            const float2 yf = __bfloat1622float2(yh[i]);
+            acc = fmaf(gf.x, yf.x, acc);
+            acc = fmaf(gf.y, yf.y, acc);
+            float d0 = sw * gf.x, d1 = sw * gf.y;
+            if (drop_p > 0.f) {
+              d0 *= dropout_uniform(seed, r, j + 2 * i) >= drop_p ? inv : 0.f;
+              d1 *= dropout_uniform(seed, r, j + 2 * i + 1) >= drop_p ? inv : 0.f;
+            }
+            o[i] = pack_bf16x2(d0, d1);
+            const float2 v = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&o[i]));
+            cs[q][2 * i] += v.x;
+            cs[q][2 * i + 1] += v.y;
+          }
+          *reinterpret_cast<uint4*>(dy + j) = out;
+        }
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) red[warp][rr] = acc;
+    }
+#pragma unroll
+    for (int q = 0; q < CPW; ++q) {
+      const int ch = warp + 8 * q;
+      if (ch >= nchunk) continue;
+      float4* p = reinterpret_cast<float4*>(part + static_cast<size_t>(b) * H + ch * 256 + lane * 8);
+      p[0] = make_float4(cs[q][0], cs[q][1], cs[q][2], cs[q][3]);
+      p[1] = make_float4(cs[q][4], cs[q][5], cs[q][6], cs[q][7]);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      const int r = r0 + threadIdx.x;
+      float s = 0.f;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) s += red[w][threadIdx.x];
+      dw[r] = (weight_scaling && tok_local[r] >= 0) ? s : 0.f;
     }
     __syncthreads();
   }
@@ -971,6 +1075,26 @@ int ppmoe_bwd_dy(int dtype, const void* dOut, const void* Y, const int* seg, int
     PPMOE_REQUIRE(dtype == kBF16 && H % 256 == 0,
                   "dY column-sum partials need the bf16 path and hidden %% 256 == 0 (H=%d)", H);
     if (rows_cap == 0) return kOk;
+    const char* mode = std::getenv("PPMOE_BWD_DY");
+    const int cpw = (H + 2047) / 2048;
+    const bool cols = !(mode && std::strcmp(mode, "block") == 0) && cpw <= 4;
+    if (cols) {
+      const int grid = num_sms() * 8;
+      cudaStream_t s = static_cast<cudaStream_t>(stream);
+      auto* g = static_cast<const __nv_bfloat16*>(dOut);
+      auto* y = static_cast<const __nv_bfloat16*>(Y);
+      auto* d = static_cast<__nv_bfloat16*>(dY);
+      if (cpw == 1)
+        bwd_dy_cols_kernel<1><<<grid, 256, 0, s>>>(g, y, seg, El, H, tok_local, w_local, weight_scaling, dropout_p,
+                                                   seed, d, dw, dy_colsum_part);
+      else if (cpw == 2)
+        bwd_dy_cols_kernel<2><<<grid, 256, 0, s>>>(g, y, seg, El, H, tok_local, w_local, weight_scaling, dropout_p,
+                                                   seed, d, dw, dy_colsum_part);
+      else
+        bwd_dy_cols_kernel<4><<<grid, 256, 0, s>>>(g, y, seg, El, H, tok_local, w_local, weight_scaling, dropout_p,
+                                                   seed, d, dw, dy_colsum_part);
+      return check_launch("bwd_dy_cols_kernel");
+    }
     bwd_dy_block_kernel<<<num_sms() * 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(
         static_cast<const __nv_bfloat16*>(dOut), static_cast<const __nv_bfloat16*>(Y), seg, El, H, tok_local,
         w_local, weight_scaling, dropout_p, seed, static_cast<__nv_bfloat16*>(dY), dw, dy_colsum_part);

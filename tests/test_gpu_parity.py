@@ -506,6 +506,26 @@ def test_fused_bias_colsums_match_separate_pass(monkeypatch):
             assert np.array_equal(a["grads"][key], b["grads"][key]), key
 
 
+def test_bwd_dy_column_slab_matches_row_block(monkeypatch):
+    """The column-slab bwd_dy kernel (default) writes the same dY and dY column-sum
+    partials as the row-block form (PPMOE_BWD_DY=block): every expert gradient is
+    bit-identical; dw sums in a different fixed order, so the gate gradient and dX agree
+    to fp32 rounding."""
+    layer = oracle_rounded(O.init_layer(4096, 8, seed=23), torch.bfloat16)
+    hidden = torch.randn(700, 4096).bfloat16().double().numpy()
+    monkeypatch.setenv("PPMOE_BWD_DY", "block")
+    a = run_cuda_layer(hidden, device_weights(layer, torch.bfloat16), k=2)
+    monkeypatch.setenv("PPMOE_BWD_DY", "cols")
+    b = run_cuda_layer(hidden, device_weights(layer, torch.bfloat16), k=2)
+    assert np.array_equal(a["out"], b["out"])
+    for key in a["grads"]:
+        if key.startswith("expert"):
+            assert np.array_equal(a["grads"][key], b["grads"][key]), key
+        else:
+            assert scaled_err(b["grads"][key], a["grads"][key]) < 1e-4, key
+    assert scaled_err(b["grad_hidden"], a["grad_hidden"]) < 1e-2
+
+
 # ------------------------------------------------------------------ edge cases
 
 
