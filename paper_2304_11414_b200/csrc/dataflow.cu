@@ -28,7 +28,7 @@ __host__ __device__ inline size_t align_to(size_t v, size_t a) { return (v + a -
 constexpr int kGatherThreads = 128;
 constexpr int kGatherLag = 8;  // store groups allowed in flight before a slot is recycled
 
-template <typename T>
+template <typename T, int LAG>
 __global__ void __launch_bounds__(kGatherThreads)
     gather_bulk_kernel(const T* __restrict__ X, int H, const int* __restrict__ seg, int El,
                        const int* __restrict__ tok_sorted, const float* __restrict__ w_sorted, T* __restrict__ Xs,
@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(kGatherThreads)
     }
   };
   int issued = 0;
-  for (; issued < n && issued <= R - kGatherLag; ++issued) issue(issued);
+  for (; issued < n && issued <= R - LAG; ++issued) issue(issued);
   for (int i = 0; i < n; ++i) {
     const int slot = i % R;
     const int tok = stok[i];
@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(kGatherThreads)
                row_bytes);
     bulk_commit();
     if (issued < n) {
-      bulk_wait_read<kGatherLag - 1>();  // store of the row that last used this slot has left smem
+      bulk_wait_read<LAG - 1>();  // store of the row that last used this slot has left smem
       issue(issued++);
     }
   }
@@ -933,21 +933,26 @@ int ppmoe_gather(const void* X, int dtype, int N, int H, const int* seg, int El,
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const size_t esz = dtype == kBF16 ? 2 : 4;
   const size_t row_bytes = static_cast<size_t>(H) * esz;
-  const int grid = num_sms();
+  // PPMOE_GATHER_CTAS = CTAs per SM (1 or 2); with 2, each ring is half the size and the
+  // store lag 4 instead of 8, so the loads in flight per SM stay about the same.
+  const char* gc = std::getenv("PPMOE_GATHER_CTAS");
+  const int per_sm = (gc && std::atoi(gc) == 2) ? 2 : 1;
+  const int lag = per_sm == 2 ? 4 : kGatherLag;
+  const int grid = num_sms() * per_sm;
   const int per = (rows_cap + grid - 1) / grid;  // rows per CTA (upper bound)
   const size_t tok_bytes = align_to(static_cast<size_t>(per) * 4, 128);
-  const size_t budget = 200 * 1024;
+  const size_t budget = 200 * 1024 / per_sm;
   int R = static_cast<int>((budget - align_to(row_bytes, 128) - 512 - std::min(tok_bytes, budget / 2)) / row_bytes);
   if (R > 32) R = 32;
-  if (row_bytes % 16 == 0 && R >= kGatherLag + 2 && tok_bytes <= budget / 2) {
+  if (row_bytes % 16 == 0 && R >= lag + 2 && tok_bytes <= budget / 2) {
     const size_t smem = align_to(static_cast<size_t>(R) * 8, 128) + align_to(row_bytes, 128) + tok_bytes + R * row_bytes;
     if (dtype == kBF16) {
-      auto k = gather_bulk_kernel<__nv_bfloat16>;
+      auto k = per_sm == 2 ? gather_bulk_kernel<__nv_bfloat16, 4> : gather_bulk_kernel<__nv_bfloat16, kGatherLag>;
       PPMOE_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
       k<<<grid, kGatherThreads, smem, s>>>(static_cast<const __nv_bfloat16*>(X), H, seg, El, tok_sorted, w_sorted,
                                            static_cast<__nv_bfloat16*>(Xs), tok_local, w_local, R, per);
     } else {
-      auto k = gather_bulk_kernel<float>;
+      auto k = per_sm == 2 ? gather_bulk_kernel<float, 4> : gather_bulk_kernel<float, kGatherLag>;
       PPMOE_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
       k<<<grid, kGatherThreads, smem, s>>>(static_cast<const float*>(X), H, seg, El, tok_sorted, w_sorted,
                                            static_cast<float*>(Xs), tok_local, w_local, R, per);
