@@ -233,7 +233,9 @@ int ppmoe_ipc_free(void* ptr);
  * Barrier of T ranks on channel ch: writes `epoch` (release, system scope) into every
  * peer's signal pad (ppmoe_nvl_pad_bytes() each),
  * then waits until all T flags of this rank's pad reach `epoch`.  A spin longer than
- * timeout_cycles sets *err = 1 and returns instead of hanging.                       */
+ * timeout_cycles stores 1 to *err (plain store + system fence, so err may be pinned
+ * host memory mapped into the device: the host reads it without a sync) and returns
+ * instead of hanging; the caller must treat the exchange as failed.                  */
 size_t ppmoe_nvl_pad_bytes(void);
 int ppmoe_nvl_barrier(void* const* pads, int T, int rank, int ch, unsigned int epoch, int* err,
                       long long timeout_cycles, void* stream);

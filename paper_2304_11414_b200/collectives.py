@@ -145,16 +145,32 @@ class World:
             raise ValueError(f"rank {r} is not a member of {group.kind} group {group.members}")
         return group.members.index(r)
 
+    def register_groups(self, groups) -> None:
+        """Create the torch.distributed groups of ``groups`` collectively: every rank of the
+        job must call this with the same groups in the same order (dist.new_group is a
+        collective over the whole job), including ranks that are not members."""
+        if not self.distributed:
+            return
+        for group in groups:
+            if group.members == tuple(range(self.world_size)) or group.members in self._torch_groups:
+                continue
+            self._torch_groups[group.members] = dist.new_group(list(group.members))
+
     def torch_group(self, group: ProcessGroup):
-        """The torch.distributed (NCCL) group for ``group``; created collectively on first use."""
+        """The torch.distributed (NCCL) group for ``group``: WORLD for the whole job, else a
+        group created by ``register_groups`` / ``tp_groups`` (creating one lazily here would
+        call dist.new_group on the member ranks only, which hangs or mismatches groups when
+        the job has several tensor groups)."""
         if not self.distributed:
             return None
         if group.members == tuple(range(self.world_size)):
             return dist.group.WORLD
         g = self._torch_groups.get(group.members)
         if g is None:
-            g = dist.new_group(list(group.members))
-            self._torch_groups[group.members] = g
+            raise ConfigurationError(
+                f"{group.kind} group {group.members} has no torch.distributed group: create the job's groups "
+                f"collectively first (tp_groups(world, ...) or World.register_groups)"
+            )
         return g
 
     def all_reduce_(self, group: ProcessGroup, t: torch.Tensor, charge: bool = True, op_kind: str = "all_reduce"):
@@ -221,4 +237,5 @@ def tp_groups(world: World, tp: int, num_experts: int) -> GroupSet:
     tpg = tuple(ProcessGroup(TP, tuple(d * tp + t for t in range(tp))) for d in range(dp))
     dpg = tuple(ProcessGroup(DP, tuple(d * tp + t for d in range(dp))) for t in range(tp))
     epg = tuple(ProcessGroup(EP, g.members) for g in tpg)
+    world.register_groups(tpg + dpg)  # eagerly, in one fixed order on every rank
     return GroupSet(dp=dpg, tp=tpg, pp=(), ep=epg)

@@ -62,7 +62,10 @@ __global__ void nvl_barrier_kernel(const __grid_constant__ PeerSet<uint32_t> pad
     const long long t0 = clock64();
     while (static_cast<int>(ld_acquire_sys(mine) - epoch) < 0) {
       if (clock64() - t0 > timeout_cycles) {
-        atomicExch(err, 1);
+        // err is host-mapped pinned memory: a plain store + system fence reaches the host,
+        // which raises at its next check (nvlink.NvlArena.check_nonblocking)
+        *reinterpret_cast<volatile int*>(err) = 1;
+        __threadfence_system();
         break;
       }
     }
@@ -108,10 +111,14 @@ __device__ __forceinline__ void multimem_store(__nv_bfloat16* mc, const uint4& v
 __device__ __forceinline__ void multimem_store(__nv_bfloat16* mc, const uint2& v) {
   asm volatile("multimem.st.relaxed.sys.global.v2.f32 [%0], {%1, %2};" ::"l"(mc), "r"(v.x), "r"(v.y) : "memory");
 }
+__device__ __forceinline__ void multimem_store(__nv_bfloat16* mc, const uint32_t& v) {
+  asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(mc), "r"(v) : "memory");
+}
 
 template <int CW> struct OgVec;
 template <> struct OgVec<8> { using type = uint4; };
 template <> struct OgVec<4> { using type = uint2; };
+template <> struct OgVec<2> { using type = uint32_t; };
 
 template <int CW>
 __device__ __forceinline__ void acc_bf16(float (&acc)[CW], const typename OgVec<CW>::type& u, float s) {
@@ -146,8 +153,13 @@ __global__ void __launch_bounds__(256)
   // reads its CW columns of one expert as 16-byte vectors, conflict-free across the warp
   // (in registers they cost 32 per thread and halved the resident CTAs, which left too
   // few row loads in flight for HBM)
-  static_assert(EB <= 0 || CW % 4 == 0, "vector Wg reads need CW % 4 == 0");
-  __shared__ __align__(16) float swg[EB > 0 ? CW * EB * 256 : 4];
+  // E <= 8: 32 KB static; 8 < E <= 32: 64 KB of dynamic shared memory (E 16: 4 columns per
+  // thread, E 32: 2), staged once per CTA, so the gate term never re-reads Wg from L2
+  static_assert(EB <= 0 || CW % 2 == 0, "vector Wg reads need CW % 2 == 0");
+  constexpr bool kDynWg = EB > 8;
+  __shared__ __align__(16) float swg_s[(EB > 0 && !kDynWg) ? CW * EB * 256 : 4];
+  extern __shared__ __align__(16) float swg_d[];
+  float* swg = kDynWg ? swg_d : swg_s;
   if constexpr (EB > 0) {
     for (int i = threadIdx.x; i < CW * EB * 256; i += blockDim.x) {
       const int c = i % CW, t = (i / CW) % 256, e = i / (CW * 256);
@@ -213,10 +225,17 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
           for (int ee = 0; ee < 4; ++ee) {
             float wv[CW];
+            if constexpr (CW % 4 == 0) {
 #pragma unroll
-            for (int c4 = 0; c4 < CW; c4 += 4)
-              *reinterpret_cast<float4*>(&wv[c4]) =
-                  *reinterpret_cast<const float4*>(&swg[((e4 + ee) * 256 + threadIdx.x) * CW + c4]);
+              for (int c4 = 0; c4 < CW; c4 += 4)
+                *reinterpret_cast<float4*>(&wv[c4]) =
+                    *reinterpret_cast<const float4*>(&swg[((e4 + ee) * 256 + threadIdx.x) * CW + c4]);
+            } else {
+#pragma unroll
+              for (int c2 = 0; c2 < CW; c2 += 2)
+                *reinterpret_cast<float2*>(&wv[c2]) =
+                    *reinterpret_cast<const float2*>(&swg[((e4 + ee) * 256 + threadIdx.x) * CW + c2]);
+            }
 #pragma unroll
             for (int c = 0; c < CW; ++c)
 #pragma unroll
@@ -343,6 +362,10 @@ static int og_ctas_per_sm() {
   static int v = [] { const char* e = getenv("PPMOE_OG_CTAS"); return e ? atoi(e) : 5; }();
   return v;
 }
+static bool og_wide_e() {  // PPMOE_OG_WIDE_E=0: the any-E form (Wg from L2) for A/B runs
+  static bool v = [] { const char* e = getenv("PPMOE_OG_WIDE_E"); return !e || atoi(e) != 0; }();
+  return v;
+}
 static int og_fwd_cw() {
   static int v = [] { const char* e = getenv("PPMOE_OG_FWD_CW"); return e ? atoi(e) : 4; }();
   return v;
@@ -419,6 +442,16 @@ int ppmoe_nvl_owner_gather(const void* const* rows, const int* seg, int El, cons
     nvl_owner_gather_kernel<EB, U, KT, CW><<<dim3(max(1, min(tiles, num_sms() * og_ctas_per_sm() / gy_)), gy_), 256, 0, s>>>( \
         R, seg, El, idx, pair_pos, w, K, H, t0, t1, dl, Wg, E, O, OS, P, T, sym_mc);                       \
   } while (0)
+  // 8 < E <= 32: Wg columns in 64 KB of dynamic shared memory, 3 CTAs per SM
+#define PPMOE_OG_DYN(EB, U, KT, CW)                                                                        \
+  do {                                                                                                     \
+    auto kern_ = nvl_owner_gather_kernel<EB, U, KT, CW>;                                                   \
+    constexpr int smem_ = CW * EB * 256 * 4;                                                               \
+    PPMOE_CUDA(cudaFuncSetAttribute(kern_, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_));           \
+    const int gy_ = (H / CW + 255) / 256;                                                                  \
+    kern_<<<dim3(max(1, min(tiles, num_sms() * 3 / gy_)), gy_), 256, smem_, s>>>(                          \
+        R, seg, El, idx, pair_pos, w, K, H, t0, t1, dl, Wg, E, O, OS, P, T, sym_mc);                       \
+  } while (0)
   if (!dl) {
     if (K == 2 && og_fwd_cw() == 4) PPMOE_OG(0, 8, 2, 4);
     else if (K == 2) PPMOE_OG(0, 4, 2, 8);
@@ -428,11 +461,20 @@ int ppmoe_nvl_owner_gather(const void* const* rows, const int* seg, int El, cons
     if (K == 2) PPMOE_OG(8, 4, 2, 4);
     else if (K == 1) PPMOE_OG(8, 8, 1, 4);
     else PPMOE_OG(8, 1, 0, 4);
+  } else if (E <= 16 && og_wide_e()) {
+    if (K == 2) PPMOE_OG_DYN(16, 8, 2, 4);
+    else if (K == 1) PPMOE_OG_DYN(16, 8, 1, 4);
+    else PPMOE_OG_DYN(16, 1, 0, 4);
+  } else if (E <= 32 && og_wide_e()) {
+    if (K == 2) PPMOE_OG_DYN(32, 8, 2, 2);
+    else if (K == 1) PPMOE_OG_DYN(32, 8, 1, 2);
+    else PPMOE_OG_DYN(32, 2, 0, 2);
   } else {
     if (K == 2) PPMOE_OG(-1, 4, 2, 4);
     else PPMOE_OG(-1, 2, 0, 4);
   }
 #undef PPMOE_OG
+#undef PPMOE_OG_DYN
   return check_launch("nvl_owner_gather_kernel");
 }
 

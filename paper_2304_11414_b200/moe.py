@@ -29,6 +29,19 @@ from .rng import Rng
 # ---------------------------------------------------------------------- parameters
 
 
+def _draw_into(rng: Rng, dst: torch.Tensor, scale: float, chunk_elems: int = 1 << 24) -> None:
+    """dst <- rng.normal(dst.shape, scale) rounded to dst.dtype, drawn in row chunks."""
+    shape = tuple(dst.shape)
+    if len(shape) == 1:
+        dst.copy_(torch.from_numpy(rng.normal(shape, scale)))
+        return
+    cols = int(np.prod(shape[1:]))
+    step = max(1, chunk_elems // max(cols, 1))
+    for r0 in range(0, shape[0], step):
+        r1 = min(shape[0], r0 + step)
+        dst[r0:r1].copy_(torch.from_numpy(rng.normal((r1 - r0,) + shape[1:], scale)))
+
+
 def _as_param(a, dtype, device, requires_grad=True) -> torch.Tensor:
     t = torch.as_tensor(np.asarray(a), dtype=torch.float64).to(device=device, dtype=dtype).contiguous()
     return t.requires_grad_(requires_grad)
@@ -93,7 +106,7 @@ class ExpertFfn:
         bank = ExpertBank.stack([self])
         n = x.shape[0]
         gate = GateParams(torch.zeros((x.shape[1], 1), dtype=torch.float32, device=x.device))
-        world = World(1, 1)
+        world = World(1, 1, distributed=False)  # a private one-rank world, also inside a multi-GPU job
         out, _ = ppmoe_forward(world, ProcessGroup(EP, (0,)), x, gate, [bank], weight_scaling=False,
                                dropout_p=dropout_p, rng=rng,
                                route_override=torch.zeros(n, dtype=torch.int64, device=x.device))
@@ -188,25 +201,45 @@ class MoeLayerWeights:
 
     @classmethod
     def init(cls, hidden: int, num_experts: int, rng: Rng, bias: bool = True, dtype=torch.bfloat16, device="cuda",
-             ffn_mult: int = 4, experts: range | None = None) -> "MoeLayerWeights":
+             ffn_mult: int = 4, experts: range | None = None, threads: int | None = None) -> "MoeLayerWeights":
         """Bit-identical draws to the reference init (gate stream 1, expert e stream 10+e,
         moe.py:120-124), rounded to ``dtype``.  ``experts`` restricts the bank to a
-        block of expert ids (the local block of a tensor-parallel rank)."""
+        block of expert ids (the local block of a tensor-parallel rank).
+
+        Each expert's Philox stream is drawn in row chunks straight into the device bank
+        (a stream drawn in pieces equals the one-shot draw), one host thread per expert
+        (numpy releases the GIL), so BASELINE-size banks (C3: 17 GB of bf16) initialise in
+        seconds without a 69 GB fp64 host copy."""
+        from concurrent.futures import ThreadPoolExecutor
+
         gate = GateParams.init(hidden, num_experts, rng.spawn(1), device=device)
         ids = range(num_experts) if experts is None else experts
         scale = hidden ** -0.5
         inner = ffn_mult * hidden
-        ups, downs, bus, bds = [], [], [], []
-        for e in ids:
-            r = rng.spawn(10 + e)
-            ups.append(r.normal((hidden, inner), scale))
-            downs.append(r.normal((inner, hidden), scale))
+        el = len(ids)
+        up = torch.empty((el, hidden, inner), dtype=dtype, device=device)
+        down = torch.empty((el, inner, hidden), dtype=dtype, device=device)
+        bu = torch.empty((el, inner), dtype=dtype, device=device) if bias else None
+        bd = torch.empty((el, hidden), dtype=dtype, device=device) if bias else None
+
+        def fill(i):
+            r = rng.spawn(10 + ids[i])
+            _draw_into(r, up[i], scale)
+            _draw_into(r, down[i], scale)
             if bias:
-                bus.append(r.normal((inner,), scale))
-                bds.append(r.normal((hidden,), scale))
-        bank = ExpertBank(_as_param(np.stack(ups), dtype, device), _as_param(np.stack(downs), dtype, device),
-                          _as_param(np.stack(bus), dtype, device) if bias else None,
-                          _as_param(np.stack(bds), dtype, device) if bias else None, first=ids[0])
+                _draw_into(r, bu[i], scale)
+                _draw_into(r, bd[i], scale)
+
+        workers = max(1, min(el, threads or (os.cpu_count() or 1)))
+        if workers == 1:
+            for i in range(el):
+                fill(i)
+        else:
+            with ThreadPoolExecutor(workers) as ex:
+                list(ex.map(fill, range(el)))
+        if torch.device(device).type == "cuda":
+            torch.cuda.synchronize(device)
+        bank = ExpertBank(*(None if t is None else t.requires_grad_() for t in (up, down, bu, bd)), first=ids[0])
         return cls(gate, bank)
 
     @classmethod
@@ -355,6 +388,12 @@ def _override_tensor(route_override, n: int, k: int, num_experts: int, device) -
         raise ValueError(f"route override needs {k} expert ids per token, got {tuple(ov.shape)}")
     if ov.numel() and (int(ov.min()) < 0 or int(ov.max()) >= num_experts):
         raise ValueError("route override contains expert ids out of range")
+    if k > 1 and ov.numel():
+        srt = ov.sort(dim=1).values
+        if bool((srt[:, 1:] == srt[:, :-1]).any()):
+            # the router never picks an expert twice for a token, and the per-rank row bounds
+            # (_ops.local_rows_cap) rely on it
+            raise ValueError("route override repeats an expert id within a token's top-k")
     return ov.to(torch.int32).contiguous()
 
 
@@ -432,6 +471,7 @@ class _PPMoEFunction(torch.autograd.Function):
 
     @staticmethod
     def forward(ctx, hidden, wg, up, down, bias_up, bias_down, spec: _Spec):
+        nvlink.check_all()  # a barrier of an earlier exchange timed out: fail loudly
         n, h = hidden.shape
         e = wg.shape[1]
         if spec.sliced_router:
@@ -539,6 +579,7 @@ class _PPMoEFunction(torch.autograd.Function):
 
     @staticmethod
     def backward(ctx, g_out, g_aux):
+        nvlink.check_all()
         hidden, wg, up, down = ctx.saved_tensors
         rt, pl, st, has_bias, spec = ctx.state
         n, h = hidden.shape
@@ -731,6 +772,7 @@ def sync_gate_gradients(world: World, group: ProcessGroup, gate: GateParams) -> 
     if world.distributed and group.size > 1 and gate.wg.grad is not None:
         import torch.distributed as dist
 
+        nvlink.check_all()
         dist.all_reduce(gate.wg.grad, op=dist.ReduceOp.SUM, group=world.torch_group(group))
 
 
@@ -812,7 +854,7 @@ def global_batch_equivalence(weights: MoeLayerWeights, global_batch, dp: int, *,
         return term + l_aux if include_aux else term
 
     weights.zero_grad()
-    world_s = World(1, 1)
+    world_s = World(1, 1, distributed=False)  # single-process helper worlds, also under torchrun
     for x in global_batch:
         out, l_aux = dpmoe_forward(world_s, ProcessGroup(EP, (0,)), as_input(x), weights.gate,
                                    experts_by_rank=weights.shard(1), capacity_factor=math.inf,
@@ -821,7 +863,7 @@ def global_batch_equivalence(weights: MoeLayerWeights, global_batch, dp: int, *,
     spatial = snapshot()
 
     weights.zero_grad()
-    world_t = World(1, tp)
+    world_t = World(1, tp, distributed=False)
     group = ProcessGroup(EP, tuple(range(tp)))
     shards = weights.shard(tp)
     for x in global_batch:

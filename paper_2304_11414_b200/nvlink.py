@@ -29,8 +29,12 @@ from ._lib import ptr
 from ._ops import call  # event-timed under _ops.KernelProfile
 
 _ARENAS: dict = {}
-# ~2 s at 2 GHz: a barrier that waits longer reports an error instead of hanging the GPU
-_TIMEOUT_CYCLES = int(os.environ.get("PPMOE_NVL_TIMEOUT_CYCLES", str(4_000_000_000)))
+# ~2 minutes at 2 GHz: long enough for host-side skew between ranks (logging, checkpoints,
+# eval, first-step allocation), short enough that a dead peer ends in an error, not a hang.
+# A timed-out barrier sets the arena's host-mapped error flag; every layer call checks it
+# (check_all) and raises, and PPMOE_NVL_STRICT=1 synchronises and checks after each exchange.
+_TIMEOUT_CYCLES = int(os.environ.get("PPMOE_NVL_TIMEOUT_CYCLES", str(240_000_000_000)))
+_STRICT = os.environ.get("PPMOE_NVL_STRICT", "0") == "1"
 
 
 def ptr_set(ptrs):
@@ -98,7 +102,9 @@ class NvlArena:
         self.torch_group = world.torch_group(group)
         lib = _lib.load()
         self.pads = _PeerBuffer(self, lib.ppmoe_nvl_pad_bytes())
-        self.err = torch.zeros(1, dtype=torch.int32, device=self.device)
+        # barrier error flag in pinned host memory, mapped into the device address space
+        # (UVA): the barrier kernel stores 1 on a timeout and the host reads it without a sync
+        self.err = torch.zeros(1, dtype=torch.int32, pin_memory=True)
         self.epoch = [0] * 8
         self.bufs: dict = {}
         self.mc_bufs: dict = {}
@@ -177,10 +183,23 @@ class NvlArena:
         call("ppmoe_nvl_barrier", self.pads.table, self.tp, self.rank, ch, self.epoch[ch], ptr(self.err),
              _TIMEOUT_CYCLES, _lib.stream_ptr())
 
+    def check_nonblocking(self) -> None:
+        """Raise if a barrier of this arena that already ran timed out (no device sync)."""
+        if int(self.err[0]) != 0:
+            raise RuntimeError(f"NVLink barrier timed out on rank {self.rank} of tensor group {self.group.members}: "
+                               "a peer stopped responding; the exchanges since then read unfinished peer rows")
+
     def check(self) -> None:
-        """Raise if any barrier of this arena timed out (synchronises the device)."""
-        if int(self.err.item()) != 0:
-            raise RuntimeError("NVLink barrier timed out: a peer of the tensor group stopped responding")
+        """Raise if any barrier of this arena timed out (synchronises the device first)."""
+        torch.cuda.synchronize(self.device)
+        self.check_nonblocking()
+
+
+def check_all(sync: bool = False) -> None:
+    """Raise if a barrier of any arena of this process timed out (ppmoe_forward and its
+    backward call this on entry; sync=True waits for the queued work first)."""
+    for a in _ARENAS.values():
+        a.check() if sync else a.check_nonblocking()
 
 
 _UNAVAILABLE: set = set()
@@ -332,6 +351,8 @@ def exchange(ar: NvlArena, rows_name: str, seg, el: int, idx, pair_pos, w, n: in
     # copy engines by default: the all-gather then takes no SMs from the overlapped GEMMs
     pull = "ppmoe_nvl_pull_blocks" if os.environ.get("PPMOE_NVL_PULL", "ce") == "sm" else "ppmoe_nvl_pull_blocks_ce"
     call(pull, src, ar.tp, ar.rank, n, h, ptr(out), s)
+    if _STRICT:
+        ar.check()
     return out
 
 

@@ -124,8 +124,7 @@ class PipelineStack:
         self.tp_groups = [ProcessGroup(EP, tuple(s * tp + t for t in range(tp))) for s in range(stages)]
         self.pp_groups = [ProcessGroup(PP, tuple(s * tp + t for s in range(stages))) for t in range(tp)]
         if world.distributed:
-            for g in self.tp_groups + self.pp_groups:
-                world.torch_group(g)
+            world.register_groups(self.tp_groups + self.pp_groups)
         self.group = self.tp_groups[self.stage]
         self.pg = world.torch_group(self.group) if world.distributed and tp > 1 else None
         per = layers // stages

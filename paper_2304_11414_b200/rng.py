@@ -30,6 +30,18 @@ class Rng:
     def integers(self, low: int, high: int, count: int) -> np.ndarray:
         return self._gen.integers(low, high, size=count)
 
+    def normal_tensor(self, shape: Sequence[int], scale: float = 1.0, dtype=None, device="cuda"):
+        """``normal(shape, scale)`` rounded to ``dtype`` in a torch tensor on ``device``, drawn
+        in row chunks (the same values as one ``normal`` call, without the fp64 host copy):
+        BASELINE's hidden batch is ``Rng(1, 99).normal_tensor((N, h), dtype=torch.bfloat16)``."""
+        import torch
+
+        from .moe import _draw_into
+
+        out = torch.empty(tuple(shape), dtype=dtype or torch.float32, device=device)
+        _draw_into(self, out, scale)
+        return out
+
     def spawn(self, stream: int) -> "Rng":
         """Fresh generator on a sibling sub-stream of the same seed."""
         return Rng(self.seed, stream)

@@ -161,6 +161,21 @@ def _gloo_worker(rank, world_size, port, q):
         wg = torch.zeros(3, 2, requires_grad=True)
         wg.grad = torch.full((3, 2), float(rank + 1))
         P.sync_gate_gradients(world, g, P.GateParams(wg))
+        # single-process helper worlds stay usable inside the job (ExpertFfn.forward,
+        # global_batch_equivalence build World(1, 1, distributed=False))
+        assert not P.World(1, 1, distributed=False).distributed
+        with pytest.raises(P.ConfigurationError, match="does not match"):
+            P.World(1, 4)
+        # subgroups: torch_group never creates a group on a subset of ranks; tp_groups
+        # registers every group of the job on every rank in one fixed order
+        sub = P.ProcessGroup(P.TP, (rank,))
+        with pytest.raises(P.ConfigurationError, match="collectively"):
+            world.torch_group(sub)
+        gs = P.tp_groups(world, 1, 2)
+        mine = gs.group_of(P.TP, rank)
+        t = torch.full((2,), float(rank + 1))
+        dist.all_reduce(t, group=world.torch_group(mine))  # a group of one: unchanged
+        assert t.tolist() == [float(rank + 1)] * 2
         q.put((rank, part.tolist(), wg.grad.tolist(), world.ledger.count_for("EP", "gradient_sync")))
     finally:
         dist.destroy_process_group()

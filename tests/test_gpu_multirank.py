@@ -323,65 +323,146 @@ def test_pipeline_stack_matches_single_gpu(stages, tp, dtype):
             assert err(g, want) < (3e-2 if dtype == torch.bfloat16 else 1e-3), (key, err(g, want))
 
 
-def _full_worker(rank, world, port, q):
+def _full_worker(rank, world, port, q, cfg):
+    """One rank of a BASELINE-size layer on BASELINE's inputs (Rng(0) weights, this rank's
+    expert block only; Rng(1, 99) hidden).  The fp64 reference is the same TP decomposition
+    in fp64: this rank's experts give partial out / dX / dS, summed over the group by an
+    fp64 NCCL all-reduce, then the gate backward (ppmoe_testlib.fp64_*)."""
+    import json
+
     import torch.distributed as dist
 
     import paper_2304_11414_b200 as P
     from oracle import ppmoe_oracle as O
-    from ppmoe_testlib import per_token_oracle, scaled_err
+    from ppmoe_testlib import dev_scaled_err, fp64_expert_pass, fp64_gate_pass, routing_on_device
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(rank)
     dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
     try:
-        h, e, n, k = 4096, 8, 16384, 2
+        h, e, k, cf = {"C2": (4096, 8, 2, float("inf")), "C3": (8192, 16, 2, 1.25)}[cfg]
+        n = 16384
         el = e // world
-        full = P.MoeLayerWeights.random(h, e, seed=0, device="cuda")  # identical on every rank
-        gate = P.GateParams(full.gate.wg.detach().clone().requires_grad_())
-        bank = P.ExpertBank(*(t.detach()[rank * el:(rank + 1) * el].clone().requires_grad_()
-                              for t in (full.bank.up, full.bank.down, full.bank.bias_up, full.bank.bias_down)),
-                            first=rank * el)
-        x = torch.randn(n, h, device="cuda", generator=torch.Generator(device="cuda").manual_seed(1)).bfloat16()
-        x.requires_grad_()
+        ids = range(rank * el, (rank + 1) * el)
+        w = P.MoeLayerWeights.init(h, e, P.Rng(0), device="cuda", experts=ids,
+                                   threads=max(1, (os.cpu_count() or 1) // world))
+        x = P.Rng(1, 99).normal_tensor((n, h), dtype=torch.bfloat16).requires_grad_()
         wd = P.World(1, world)
         g = P.ProcessGroup(P.EP, tuple(range(world)))
-        out, l_aux = P.ppmoe_forward(wd, g, x, gate, [bank if r == rank else None for r in range(world)], top_k=k)
+        out, l_aux = P.ppmoe_forward(wd, g, x, w.gate, [w.bank if r == rank else None for r in range(world)],
+                                     top_k=k, capacity_factor=cf, check_replicas=True)
         torch.autograd.backward([out, l_aux], [torch.ones_like(out), torch.ones_like(l_aux)])
-        P.sync_gate_gradients(wd, g, gate)
+        P.sync_gate_gradients(wd, g, w.gate)
         torch.cuda.synchronize()
         x64 = x.detach().double().cpu().numpy()
-        wg64 = gate.wg.detach().double().cpu().numpy()
+        wg64 = w.gate.wg.detach().double().cpu().numpy()
         route = O.gate_topk(x64, wg64, k)
-        # every rank checks its own sample of tokens of the replicated out / dX
-        tokens = np.random.default_rng(rank).choice(n, size=24, replace=False)
-        ref_out, ref_dx = per_token_oracle(x64, wg64, full.bank, tokens, k, n, route)
-        sel = torch.as_tensor(tokens, device="cuda")
-        res = {"out": scaled_err(out.detach()[sel].double().cpu().numpy(), ref_out),
-               "dx": scaled_err(x.grad[sel].double().cpu().numpy(), ref_dx),
-               "l_aux": abs(float(l_aux.detach()) - route.l_aux),
-               "digest": float(out.detach().float().sum())}
+        _, kept, _ = O.dispatch_plan(route.indices, e, O.capacity_of(cf, n, k, e))
+        idx, wts, kept_d, scores, cnt = routing_on_device(route, kept)
+        errs = {}
+        ours = {"up": w.bank.up.grad, "down": w.bank.down.grad, "bias_up": w.bank.bias_up.grad,
+                "bias_down": w.bank.bias_down.grad}
+
+        def on_expert(ex, grads):
+            for nm, gr in grads.items():
+                errs[f"expert{ex}.{nm}"] = dev_scaled_err(ours[nm][ex - ids[0]], gr)
+
+        with torch.no_grad():
+            out_r, dx_r, ds = fp64_expert_pass(x, w.bank, list(ids), idx, wts, kept_d, e, on_expert=on_expert)
+            for t in (out_r, dx_r, ds):
+                dist.all_reduce(t)
+            errs["out"] = dev_scaled_err(out, out_r)
+            dwg_r, dxg = fp64_gate_pass(x, w.gate.wg, scores, cnt, ds)
+            errs["grad_hidden"] = dev_scaled_err(x.grad, dx_r + dxg)
+            errs["gate.wg"] = dev_scaled_err(w.gate.wg.grad, dwg_r)
+        print(json.dumps({"cfg": cfg, "tp": world, "rank": rank, "errors": errs}), flush=True)
+        res = {"errs": errs, "l_aux": abs(float(l_aux.detach()) - route.l_aux),
+               "digest": float(out.detach().float().sum()), "ndrop": int((~kept).sum())}
         q.put((rank, res))
     finally:
         dist.destroy_process_group()
 
 
-def test_tp_full_size_c2():
-    """BASELINE configs[1] at full size over the NVLink exchange (T = 4, or 2): each rank's
-    replicated out and dX on sampled tokens against the per-token closed form."""
-    world = 4 if torch.cuda.device_count() >= 4 else 2
+@pytest.mark.parametrize("cfg,world", [("C2", 2), ("C2", 4), ("C3", 2), ("C3", 4)])
+def test_tp_full_size_every_gradient(cfg, world):
+    """BASELINE configs[1] / configs[2] at full size over the NVLink exchange (T = 2, 4) on
+    BASELINE's inputs: the replicated out and dX, the synced dWg and every local expert
+    gradient over every element against the fp64 closed form, on every rank."""
     if torch.cuda.device_count() < world:
-        pytest.skip("needs >= 2 GPUs")
+        pytest.skip(f"needs {world} GPUs")
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 29600 + (os.getpid() + 7) % 500
-    procs = [ctx.Process(target=_full_worker, args=(r, world, port, q)) for r in range(world)]
+    port = 29600 + (os.getpid() + 7 * world + len(cfg)) % 500
+    procs = [ctx.Process(target=_full_worker, args=(r, world, port, q, cfg)) for r in range(world)]
     for p in procs:
         p.start()
-    got = _collect(q, procs, timeout=400)
+    got = _collect(q, procs, timeout=900)
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
+    e = {"C2": 8, "C3": 16}[cfg]
     for r in range(world):
-        assert got[r]["out"] < 2e-2 and got[r]["dx"] < 2e-2 and got[r]["l_aux"] < 1e-5, (r, got[r])
+        errs = got[r]["errs"]
+        bad = {key: v for key, v in errs.items() if not v < 2e-2}
+        assert not bad and got[r]["l_aux"] < 1e-5, (r, bad, got[r]["l_aux"])
+        assert len(errs) == 3 + 4 * (e // world)
     assert len({got[r]["digest"] for r in range(world)}) == 1  # identical replicas
+
+
+def _barrier_timeout_worker(rank, world, port, q):
+    """Rank 1 enters a barrier its peer never joins: the barrier times out, the arena's
+    host-mapped flag is set, and both the explicit check and the next layer call raise."""
+    os.environ["PPMOE_NVL_TIMEOUT_CYCLES"] = "200000000"  # ~0.1-0.15 s
+    import torch.distributed as dist
+
+    import paper_2304_11414_b200 as P
+    from paper_2304_11414_b200 import nvlink
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    try:
+        wd = P.World(1, world)
+        g = P.ProcessGroup(P.EP, tuple(range(world)))
+        assert nvlink.enabled(wd, g, torch.bfloat16, 256)
+        ar = nvlink.arena(wd, g)
+        res = {"raised_check": False, "raised_forward": False}
+        if rank == 1:
+            ar.barrier(3)  # rank 0 never arrives on channel 3
+            try:
+                ar.check()
+            except RuntimeError as exc:
+                res["raised_check"] = "timed out" in str(exc)
+            w = P.MoeLayerWeights.random(256, 4, seed=1, device="cuda", experts=range(2, 4))
+            x = torch.randn(64, 256, device="cuda").bfloat16()
+            try:
+                P.ppmoe_forward(wd, g, x, w.gate, [None, w.bank], top_k=2)
+            except RuntimeError as exc:
+                res["raised_forward"] = "timed out" in str(exc)
+        torch.cuda.synchronize()
+        q.put((rank, res))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nvl_barrier_timeout_raises():
+    """A peer that skips a barrier makes the exchange fail loudly: the timed-out
+    barrier's flag is read from pinned host memory and ppmoe_forward raises RuntimeError."""
+    world = 2
+    if torch.cuda.device_count() < world:
+        pytest.skip("needs 2 GPUs")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29600 + (os.getpid() + 13) % 500
+    procs = [ctx.Process(target=_barrier_timeout_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = _collect(q, procs, timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert got[1]["raised_check"] and got[1]["raised_forward"], got[1]
+    assert not got[0]["raised_check"] and not got[0]["raised_forward"]
