@@ -2,12 +2,13 @@
 """Benchmark of the B200 PPMoE MoE layer: tokens/s of one layer forward + backward.
 
 Workload (BASELINE.json configs[1], "C2"): hidden 4096, ffn 16384, 8 experts, top-2,
-16384 tokens, bf16 activations/expert weights, fp32 gate.  With --gpus N (under
-torchrun, one process per GPU) the N GPUs form one tensor-parallel group (TP=N):
-every rank routes the replicated tokens, runs its E/N experts and the group
-all-reduces the output (forward) and the input gradient (backward) over NCCL;
-the gate-weight gradient is all-reduced once per step (= one global batch).
-Total work is fixed as N grows ("scaling": "strong").
+16384 tokens, bf16 activations/expert weights, fp32 gate, BASELINE.md's Philox inputs.
+With --gpus N (one process per GPU; without a launcher the command re-runs itself under
+torch.distributed.run) the N GPUs form one tensor-parallel group (TP=N): every rank holds
+the replicated tokens, runs its E/N experts, and the group combines the output (forward)
+and the input gradient (backward) with the NVLink owner-gather exchange; the gate-weight
+gradient is all-reduced once per step (= one global batch).  Total work is fixed as N
+grows ("scaling": "strong").
 
 One step = route + dispatch plan + gather + expert fc1/fc2 (+combine) + all-reduce,
 then the full backward (all parameter and input gradients) + the dX all-reduce +
@@ -255,8 +256,28 @@ def run_reference(a):
 # ----------------------------------------------------------------------------- GPU path
 
 
+def relaunch_under_torchrun(a) -> int | None:
+    """`python bench.py --gpus N` without a launcher: re-run this command under
+    torch.distributed.run with N local ranks (one process per GPU, 127.0.0.1 rendezvous);
+    rank 0 prints the JSON line.  Returns the launcher's exit code, or None when this
+    process is already a rank (or N == 1)."""
+    if a.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve())] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     a = parse()
+    rc = relaunch_under_torchrun(a)
+    if rc is not None:
+        return rc
     if a.impl == "reference":
         return run_reference(a)
 
@@ -270,9 +291,7 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if world_size != a.gpus:
-        if world_size == 1 and a.gpus > 1:
-            print(f"--gpus {a.gpus} needs torchrun with {a.gpus} processes", file=sys.stderr)
-            return 2
+        raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={world_size}")
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     distributed = world_size > 1
@@ -288,12 +307,17 @@ def main():
     group = P.ProcessGroup(P.EP, tuple(range(tp)))
     el = E // tp
     block = range(rank * el, (rank + 1) * el)
-    w = P.MoeLayerWeights.random(h, E, seed=0, dtype=torch.bfloat16, device=dev, experts=block)
+    # BASELINE.md §3 inputs: MoeLayerWeights.init(h, E, Rng(0)) rounded to bf16 (this rank's
+    # expert block only; Philox streams per expert, so every block matches the full layer),
+    # hidden Rng(1, 99).normal((N, h)) rounded to bf16, identical on every rank
+    t_init = time.perf_counter()
+    w = P.MoeLayerWeights.init(h, E, P.Rng(0), dtype=torch.bfloat16, device=dev, experts=block,
+                               threads=max(1, (os.cpu_count() or 1) // world_size))
+    x = P.Rng(1, 99).normal_tensor((n, h), dtype=torch.bfloat16, device=dev).requires_grad_()
+    init_s = time.perf_counter() - t_init
     experts_by_rank = [w.bank if r == rank else None for r in range(tp)] if distributed else [w.bank]
     if not distributed:
         group = P.ProcessGroup(P.EP, (0,))
-    gen = torch.Generator(device=dev).manual_seed(1234)  # same hidden on every rank (replicated activation)
-    x = torch.randn(n, h, device=dev, generator=gen).to(torch.bfloat16).requires_grad_()
     # dOut: all ones gives constant-per-row dY (low tensor-core switching power, so ~3 % more
     # clock under the power cap than a random gradient); both are timed (upstream_alt)
     g_ones = torch.ones(n, h, device=dev, dtype=torch.bfloat16)
@@ -401,7 +425,7 @@ def main():
     # ---- end to end: host (pinned) input -> device -> fwd+bwd -> loss back to host
     e2e = None
     if not a.no_e2e:
-        x_host = torch.randn(n, h, generator=torch.Generator().manual_seed(1234)).to(torch.bfloat16).pin_memory()
+        x_host = x.detach().cpu().pin_memory()  # the same BASELINE batch, from pinned host memory
         loss_host = [torch.empty(1, dtype=torch.float32).pin_memory() for _ in range(2)]
         loss_ev = [torch.cuda.Event() for _ in range(2)]
         # each rank copies its 1/T row slice over PCIe, NCCL all_gather replicates it; the next
@@ -484,7 +508,9 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world_size, "steps": a.steps,
                 "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-                "vs_baseline": None, "dtype": "bf16", "data": f"synthetic (random-init weights of the {a.config.upper()} layer, N(0,1) tokens)",
+                "vs_baseline": None, "dtype": "bf16", "data": f"synthetic: BASELINE.md inputs of the {a.config.upper()} layer, weights "
+                                f"MoeLayerWeights.init(h, E, Rng(0)) and hidden Rng(1, 99).normal((N, h)), both "
+                                f"rounded to bf16 (Philox, bit-identical to the reference init; {init_s:.1f} s)",
                 "config": config_of(a, world_size), "roofline": roofline, "cpu_baseline": cb, "e2e": e2e,
                 "gpu_launches": int(launches), "clocks": clk.summary(), "a2a_comparator": a2a, "kernels": per_kernel,
                 "host_enqueue_ms_per_step": round(host_ms, 3), "upstream_alt": upstream_alt,

@@ -119,6 +119,22 @@ __global__ void scatter_rows_kernel(const T* __restrict__ src, int H, const int*
   }
 }
 
+// dst[map[o]] = src[o] for owner rows o < rows with map[o] >= 0: expert outputs / per-row
+// input gradients from the owner's expert-major layout back to receive order (a
+// permutation: plain 16-byte row copies, no atomics, no fp32 staging).
+__global__ void permute_rows_kernel(const uint4* __restrict__ src, int vec_per_row, int rows,
+                                    const int* __restrict__ map, uint4* __restrict__ dst) {
+  const int wpb = blockDim.x / 32;
+  const int lane = threadIdx.x & 31;
+  for (int o = blockIdx.x * wpb + (threadIdx.x >> 5); o < rows; o += gridDim.x * wpb) {
+    const int r = map[o];
+    if (r < 0) continue;
+    const uint4* a = src + static_cast<size_t>(o) * vec_per_row;
+    uint4* d = dst + static_cast<size_t>(r) * vec_per_row;
+    for (int j = lane; j < vec_per_row; j += 32) d[j] = a[j];
+  }
+}
+
 }  // namespace ppmoe
 
 using namespace ppmoe;
@@ -143,6 +159,17 @@ int ppmoe_a2a_owner_layout(const int* recv_counts, int T, int El, int rows_cap, 
   const size_t smem = (2 * static_cast<size_t>(T) * El + El + 1) * 4;
   a2a_owner_layout_kernel<<<1, 1024, smem, s>>>(recv_counts, T, El, rows_cap, seg_out, map);
   return check_launch("a2a_owner_layout_kernel");
+}
+
+int ppmoe_a2a_permute_rows(const void* src, int dtype, int H, int rows, const int* map, void* dst, void* stream) {
+  PPMOE_REQUIRE(dtype == kBF16 || dtype == kF32, "bad dtype");
+  const size_t row_bytes = static_cast<size_t>(H) * (dtype == kBF16 ? 2 : 4);
+  PPMOE_REQUIRE(H >= 1 && row_bytes % 16 == 0 && rows >= 0, "permute_rows needs 16-byte rows (H=%d)", H);
+  if (rows == 0) return kOk;
+  const int grid = num_sms() * 4;
+  permute_rows_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const uint4*>(src), static_cast<int>(row_bytes / 16), rows, map, static_cast<uint4*>(dst));
+  return check_launch("permute_rows_kernel");
 }
 
 int ppmoe_scatter_rows(const void* src, int dtype, int H, const int* nrows, const int* tok, const float* w, float* dst,
