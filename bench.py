@@ -350,17 +350,16 @@ def main():
     lib = _lib.load()
     launches0 = lib.ppmoe_kernel_launches()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with _ops.KernelProfile() as prof:
-        barrier()
-        clk.mark_start()
-        ev0.record()
-        h0 = time.perf_counter()
-        for _ in range(a.steps):
-            step(x)
-        host_ms = (time.perf_counter() - h0) * 1e3 / a.steps  # host enqueue time (the step never syncs)
-        ev1.record()
-        barrier()
-        clk.mark_end()
+    barrier()
+    clk.mark_start()
+    ev0.record()
+    h0 = time.perf_counter()
+    for _ in range(a.steps):
+        step(x)
+    host_ms = (time.perf_counter() - h0) * 1e3 / a.steps  # host enqueue time (the step never syncs)
+    ev1.record()
+    barrier()
+    clk.mark_end()
     clk.__exit__(None, None, None)
     launches = lib.ppmoe_kernel_launches() - launches0
     ms = ev0.elapsed_time(ev1) / a.steps
@@ -369,6 +368,13 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t)
     value = n / (ms / 1e3)
+    # per-entry-point CUDA-event times (roofline inputs) from a separate pass of the same
+    # steps, so the headline timed region carries no profiling events
+    with _ops.KernelProfile() as prof:
+        barrier()
+        for _ in range(a.steps):
+            step(x)
+        barrier()
     ksum = prof.summary()
 
     # ---- the same step with the other upstream gradient (untimed warm-up step first)
@@ -418,6 +424,7 @@ def main():
                 "algorithmic": f"12*P_r*h*f flop per step on this rank, P_r={local_pairs} of P={pairs} kept pairs; "
                                f"{gemm_ms:.3f} ms of GEMM per step",
                 "peak_source": peak_src, "gemm_share_of_step": gemm_ms / ms if ms else None,
+                "timing": "kernel times from a profiled pass of the same K steps after the timed region",
                 "frac_of_burst_peak": (achieved / peaks["bf16_tflops"]) if (achieved and "bf16_tflops" in peaks) else None,
                 "peak_note": "peak = cuBLAS bf16 8192^3 back-to-back for 4 s on this pool (power-capped, the regime a "
                              "long step runs in); frac_of_burst_peak uses the short-burst figure"}

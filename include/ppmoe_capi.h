@@ -214,6 +214,9 @@ int ppmoe_a2a_compact(const int* tok_sorted, const float* w_sorted, const int* s
  * (-1 padding).  recv_counts [T x El] rows per (source, local expert).             */
 int ppmoe_a2a_owner_layout(const int* recv_counts, int T, int El, int rows_cap, int* seg_out, int* map,
                            void* stream);
+/* dst[map[o]] = src[o] for o < rows with map[o] >= 0 (rows of H values in dtype, 16-byte
+ * multiples): the owner's expert-major rows back to all-to-all receive order.        */
+int ppmoe_a2a_permute_rows(const void* src, int dtype, int H, int rows, const int* map, void* dst, void* stream);
 /* dst[tok[r]] += w[r]*src[r] (fp32 dst, src in dtype) for r < nrows[0] (device scalar),
  * tok < 0 skipped, w NULL = 1 (index_assign back to token order, moe.py:461-467).   */
 int ppmoe_scatter_rows(const void* src, int dtype, int H, const int* nrows, const int* tok, const float* w, float* dst,

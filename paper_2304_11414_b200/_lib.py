@@ -39,6 +39,7 @@ _SIGNATURES = {
     "ppmoe_a2a_compact": (_I, [_P, _P, _P, _P, _I, _P, _P, _I, _P, _P, _P, _P, _P]),
     "ppmoe_a2a_owner_layout": (_I, [_P, _I, _I, _I, _P, _P, _P]),
     "ppmoe_scatter_rows": (_I, [_P, _I, _I, _P, _P, _P, _P, _P]),
+    "ppmoe_a2a_permute_rows": (_I, [_P, _I, _I, _I, _P, _P, _P]),
     "ppmoe_gather": (_I, [_P, _I, _I, _I, _P, _I, _P, _P, _I, _P, _P, _P, _P]),
     "ppmoe_chunk_rows": (_I, [_P, _P, _P, _I, _I, _I, _P, _P, _P]),
     "ppmoe_expert_fc1_fwd": (_I, [_I, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P]),

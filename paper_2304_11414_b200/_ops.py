@@ -411,6 +411,32 @@ def owner_layout(recv_counts: torch.Tensor, t: int, el: int, rows_cap: int):
     return seg, rmap
 
 
+def permute_rows(src: torch.Tensor, rows: int, rmap: torch.Tensor, dst: torch.Tensor) -> None:
+    """dst[rmap[o]] = src[o] for the first `rows` owner rows (rmap < 0: padding)."""
+    call("ppmoe_a2a_permute_rows", ptr(src), dtype_code(src.dtype), src.shape[1], int(rows), ptr(rmap), ptr(dst),
+         _stream())
+
+
+def compact_combine(rows: torch.Tensor, cstart: torch.Tensor, idx: torch.Tensor, pos_c: torch.Tensor,
+                    w: torch.Tensor | None, out: torch.Tensor, dl: torch.Tensor | None = None,
+                    wg: torch.Tensor | None = None) -> torch.Tensor:
+    """out[t] = sum over t's kept pairs (slot order) of w·rows[pos_c[t, s]] (+ dl[t]·wgᵀ), for
+    rows in the compact expert-major layout of the all-to-all comparator: the owner-gather
+    kernel with a group of one and every expert "local" (row = pos_c - cstart[0] = pos_c)."""
+    n, h = out.shape
+    k = pos_c.shape[1]
+    e_cols = wg.shape[1] if wg is not None else 0
+    num_experts = cstart.numel() - 1
+    if out.dtype != torch.bfloat16 or h % 8:  # fp32 reference-precision mode: the generic gather
+        call("ppmoe_combine", dtype_code(out.dtype), ptr(rows), ptr(cstart), num_experts, ptr(pos_c), ptr(w), n, k, h,
+             ptr(dl), ptr(wg), e_cols, ptr(out), _stream())
+        return out
+    rows_set = (ctypes.c_void_p * 1)(rows.data_ptr())
+    call("ppmoe_nvl_owner_gather", rows_set, ptr(cstart), num_experts, ptr(idx), ptr(pos_c), ptr(w), n, k, h, 1, 0,
+         ptr(dl), ptr(wg), e_cols, ptr(out), None, None, 0, _stream())
+    return out
+
+
 def scatter_rows(src: torch.Tensor, nrows: torch.Tensor, tok: torch.Tensor, w: torch.Tensor | None,
                  dst: torch.Tensor) -> None:
     call("ppmoe_scatter_rows", ptr(src), dtype_code(src.dtype), src.shape[1], ptr(nrows), ptr(tok), ptr(w), ptr(dst),

@@ -73,8 +73,7 @@ __global__ void a2a_owner_layout_kernel(const int* __restrict__ recv_counts, int
   }
   __syncthreads();
   for (int e = threadIdx.x; e <= El; e += blockDim.x) seg_out[e] = segs[e];
-  const int total = min(segs[El], rows_cap);
-  for (int r = threadIdx.x; r < total; r += blockDim.x) map[r] = -1;
+  for (int r = threadIdx.x; r < rows_cap; r += blockDim.x) map[r] = -1;  // incl. rows past seg[El]
   __syncthreads();
   for (int e = 0; e < El; ++e)
     for (int s = 0; s < T; ++s) {

@@ -887,12 +887,125 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Gate-weight gradient alone (dX not wanted): part[chunk] = X[chunk tokens]^T dL[chunk tokens]
+// over a slab of kDwgSlab columns (tensor.py:134-138, the matmul backward of X Wg).  X is
+// read once at HBM rate: a producer warp stages kDwgTok whole token slabs plus their dL rows
+// per ring stage with 1-D bulk copies (one mbarrier handshake per 16 tokens, not per token),
+// and the 8 consumer warps keep 4 columns x EB experts of partial sums in registers (FFMA2).
+constexpr int kDwgSlab = 1024;
+constexpr int kDwgTok = 16;
+constexpr int kDwgStages = 5;
+
+template <int EB>
+struct DwgGeom {
+  static constexpr int kX = kDwgTok * kDwgSlab * 2;  // bytes of the X slabs of one stage
+  static constexpr int kL = kDwgTok * EB * 4;        // bytes of the dL rows of one stage
+  static constexpr int kStage = kX + kL;
+  static constexpr size_t kSmem = static_cast<size_t>(kDwgStages) * kStage + 2 * kDwgStages * 8;
+};
+
+template <int EB>
+__global__ void __launch_bounds__(kIgConsumers + 32, 1)
+    dwg_bulk_kernel(const __nv_bfloat16* __restrict__ X, const float* __restrict__ dL, int N, int H, float* __restrict__ part) {
+  using G = DwgGeom<EB>;
+  extern __shared__ __align__(128) unsigned char sm[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + kDwgStages * G::kStage);
+  uint64_t* empty = full + kDwgStages;
+  const int c0 = blockIdx.x * kDwgSlab;
+  const int ncols = min(kDwgSlab, H - c0);
+  const uint32_t slab_bytes = static_cast<uint32_t>(ncols) * 2;
+  const int per = (N + gridDim.y - 1) / gridDim.y;
+  const int tb = blockIdx.y * per, te = min(N, tb + per);
+  const int nstage = te > tb ? (te - tb + kDwgTok - 1) / kDwgTok : 0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kDwgStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kIgConsumers / 32);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (threadIdx.x >= kIgConsumers) {  // ---------------- producer warp
+    const int lane = threadIdx.x & 31;
+    for (int i = 0; i < nstage; ++i) {
+      const int st = i % kDwgStages;
+      const int t0 = tb + i * kDwgTok;
+      const int nt = min(kDwgTok, te - t0);
+      unsigned char* stg = sm + static_cast<size_t>(st) * G::kStage;
+      if (lane == 0) {
+        if (i >= kDwgStages) mbar_wait(&empty[st], ((i / kDwgStages) - 1) & 1);
+        mbar_arrive_expect_tx(&full[st], nt * slab_bytes + nt * EB * 4);
+      }
+      __syncwarp();
+      if (lane < nt) bulk_load(stg + lane * kDwgSlab * 2, X + static_cast<size_t>(t0 + lane) * H + c0, slab_bytes, &full[st]);
+      if (lane == 31) bulk_load(stg + G::kX, dL + static_cast<size_t>(t0) * EB, nt * EB * 4, &full[st]);
+    }
+    return;
+  }
+  // ---------------------------------------------------- consumer warps
+  const int jl = threadIdx.x * 4;
+  const bool active = jl < ncols;
+  float2 pacc[4][EB / 2];
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int e = 0; e < EB / 2; ++e) pacc[q][e] = make_float2(0.f, 0.f);
+  for (int i = 0; i < nstage; ++i) {
+    const int st = i % kDwgStages;
+    const int nt = min(kDwgTok, te - tb - i * kDwgTok);
+    mbar_wait(&full[st], (i / kDwgStages) & 1);
+    const unsigned char* stg = sm + static_cast<size_t>(st) * G::kStage;
+    const float* dls = reinterpret_cast<const float*>(stg + G::kX);
+    if (active) {
+#pragma unroll 4
+      for (int u = 0; u < nt; ++u) {
+        const uint2 v = *reinterpret_cast<const uint2*>(stg + u * kDwgSlab * 2 + jl * 2);
+        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.x));
+        const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.y));
+        const float x[4] = {a.x, a.y, b.x, b.y};
+        float d[EB];
+#pragma unroll
+        for (int e = 0; e < EB; e += 4) {
+          const float4 f = *reinterpret_cast<const float4*>(dls + u * EB + e);
+          d[e] = f.x, d[e + 1] = f.y, d[e + 2] = f.z, d[e + 3] = f.w;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float2 xx = make_float2(x[q], x[q]);
+#pragma unroll
+          for (int e = 0; e < EB / 2; ++e) pacc[q][e] = __ffma2_rn(xx, make_float2(d[2 * e], d[2 * e + 1]), pacc[q][e]);
+        }
+      }
+    }
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[st]);
+  }
+  if (active) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float4* p = reinterpret_cast<float4*>(part + (static_cast<size_t>(blockIdx.y) * H + c0 + jl + q) * EB);
+#pragma unroll
+      for (int e = 0; e < EB / 2; e += 2) p[e / 2] = make_float4(pacc[q][e].x, pacc[q][e].y, pacc[q][e + 1].x, pacc[q][e + 1].y);
+    }
+  }
+}
+
+static int dwg_chunks(int N, int H) {
+  const int gx = (H + kDwgSlab - 1) / kDwgSlab;
+  return max(1, min((N + kDwgTok - 1) / kDwgTok, num_sms() / gx));
+}
+
 __global__ void dwg_reduce_kernel(const float* __restrict__ part, int C, int HE, float* __restrict__ dWg) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= HE) return;
   float s = 0.f;
   for (int c = 0; c < C; ++c) s += part[static_cast<size_t>(c) * HE + i];
   dWg[i] = s;
+}
+
+static bool dwg_bulk_ok(int dtype, int H, int E) {
+  const char* e = std::getenv("PPMOE_DWG");  // PPMOE_DWG=ring: the combined input-gradient kernel (A/B)
+  return !(e && std::strcmp(e, "ring") == 0) && dtype == kBF16 && H % 8 == 0 && (E == 4 || E == 8 || E == 16);
 }
 
 static int input_grads_chunks(int N, int H, int E) {
@@ -1011,7 +1124,7 @@ int ppmoe_combine(int dtype, const void* R, const int* seg, int El, const int* p
 
 size_t ppmoe_input_grads_workspace_bytes(int dtype, int N, int H, int E) {
   // fused-path partials for any k, or the gate_grads fallback's, whichever is larger
-  const size_t fused = static_cast<size_t>(input_grads_chunks(N, H, E)) * H * E * 4;
+  const size_t fused = static_cast<size_t>(std::max(input_grads_chunks(N, H, E), dwg_chunks(N, H))) * H * E * 4;
   return dtype == kBF16 ? std::max(fused, ppmoe_gate_grad_workspace_bytes(N, H, E))
                         : ppmoe_gate_grad_workspace_bytes(N, H, E);
 }
@@ -1031,6 +1144,22 @@ int ppmoe_input_grads(int dtype, const void* dXs, const int* seg, int El, const 
     return ppmoe_gate_grads(nullptr, X, dtype, dL, Wg, N, H, E, nullptr, dWg, ws, ws_bytes, stream);
   }
   if (!dX && !dWg) return kOk;
+  if (!dX && dwg_bulk_ok(dtype, H, E)) {  // gate-weight gradient alone: X read once at HBM rate
+    const int C = dwg_chunks(N, H);
+    dim3 grid((H + kDwgSlab - 1) / kDwgSlab, C);
+    float* part = static_cast<float*>(ws);
+    auto launch = [&](auto kern, size_t smem) {
+      PPMOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      kern<<<grid, kIgConsumers + 32, smem, s>>>(static_cast<const __nv_bfloat16*>(X), dL, N, H, part);
+      return check_launch("dwg_bulk_kernel");
+    };
+    int rc = E == 4 ? launch(dwg_bulk_kernel<4>, DwgGeom<4>::kSmem)
+             : E == 8 ? launch(dwg_bulk_kernel<8>, DwgGeom<8>::kSmem) : launch(dwg_bulk_kernel<16>, DwgGeom<16>::kSmem);
+    if (rc) return rc;
+    const int HE = H * E;
+    dwg_reduce_kernel<<<(HE + 255) / 256, 256, 0, s>>>(part, C, HE, static_cast<float*>(dWg));
+    return check_launch("dwg_reduce_kernel");
+  }
   const int C = input_grads_chunks(N, H, E);
   dim3 grid((H + kIgSlab - 1) / kIgSlab, C);
   float* part = dWg ? static_cast<float*>(ws) : nullptr;

@@ -52,7 +52,8 @@ def _a2a(world: World, group: ProcessGroup, out: torch.Tensor, inp: torch.Tensor
     moved = sum(n for i, n in enumerate(in_splits) if i != me) * row
     world.ledger.charge(group.kind, "all_to_all", moved)
     if not world.distributed or group.size == 1:
-        out.copy_(inp)
+        if out.data_ptr() != inp.data_ptr():
+            out.copy_(inp)
         return None
     return dist.all_to_all_single(out, inp, output_split_sizes=list(out_splits), input_split_sizes=list(in_splits),
                                   group=world.torch_group(group), async_op=async_op)
@@ -97,30 +98,32 @@ class _DPMoEFunction(torch.autograd.Function):
         _ops.call("ppmoe_gather", _ops.ptr(hidden), _ops.dtype_code(hidden.dtype), n, h, _ops.ptr(cstart), e,
                   _ops.ptr(tok_c), _ops.ptr(w_c), n_send, _ops.ptr(xsend), _ops.ptr(tmp_tok), _ops.ptr(tmp_w),
                   _ops._stream())
-        xrecv = torch.empty((max(n_recv, 1), h), dtype=hidden.dtype, device=dev)
+        # a group of one exchanges nothing: the receive buffers alias the send buffers
+        solo = t == 1
+        xrecv = xsend if solo else torch.empty((max(n_recv, 1), h), dtype=hidden.dtype, device=dev)
         _a2a(spec.world, spec.group, xrecv[:n_recv], xsend[:n_send], recv_rows, send_rows)
-        # owner: regroup per local expert (source order), expert FFNs, unscaled outputs per receive row
+        # owner: regroup per local expert (source order), expert FFNs; fc2 stores the unscaled
+        # bf16 outputs in the owner layout and a row permutation puts them in receive order
         rows_cap_o = n_recv + 128 * el
         seg_o, rmap = _ops.owner_layout(recv_counts, t, el, rows_cap_o)
-        yret = torch.zeros((max(n_recv, 1), h), dtype=torch.float32, device=dev)
-        st = _ops.expert_pipeline(xrecv, seg_o, el, rmap, None, rows_cap_o, up, down, bias_up, bias_down, False, yret,
+        st = _ops.expert_pipeline(xrecv, seg_o, el, rmap, None, rows_cap_o, up, down, bias_up, bias_down, False, None,
                                   spec.dropout_p, spec.seed)
-        yret_b = _ops.cast_out(yret, hidden.dtype)
-        del yret
-        yback = torch.empty((max(n_send, 1), h), dtype=hidden.dtype, device=dev)
-        _a2a(spec.world, spec.group, yback[:n_send], yret_b[:n_recv], send_rows, recv_rows)
-        # source: out[tok] += w * y
-        out_acc = torch.zeros((n, h), dtype=torch.float32, device=dev)
-        _ops.scatter_rows(yback, cstart[e:], tok_c, w_c if spec.weight_scaling else None, out_acc)
-        out = _ops.cast_out(out_acc, hidden.dtype)
+        yret = _ops._act((max(n_recv, 1), h), hidden.dtype, dev)
+        _ops.permute_rows(st.y, rows_cap_o, rmap, yret)
+        yback = yret if solo else torch.empty((max(n_send, 1), h), dtype=hidden.dtype, device=dev)
+        _a2a(spec.world, spec.group, yback[:n_send], yret[:n_recv], send_rows, recv_rows)
+        # source: out[t] = sum_s w * y (index_assign, moe.py:461-467) as a gather in slot order
+        out = _ops.compact_combine(yback, cstart, rt.idx, pos_c, rt.w if spec.weight_scaling else None,
+                                   torch.empty_like(hidden))
         ctx.save_for_backward(hidden, wg, up, down)
-        ctx.state = (rt, pl, cstart, tok_c, w_c, pos_c, send_rows, recv_rows, st, yback, bias_up is not None, spec)
+        ctx.state = (rt, pl, cstart, tok_c, w_c, pos_c, send_rows, recv_rows, st, rmap, yback, bias_up is not None,
+                     spec)
         return out, rt.l_aux[0].to(torch.float32)
 
     @staticmethod
     def backward(ctx, g_out, g_aux):
         hidden, wg, up, down = ctx.saved_tensors
-        rt, pl, cstart, tok_c, w_c, pos_c, send_rows, recv_rows, st, yback, has_bias, spec = ctx.state
+        rt, pl, cstart, tok_c, w_c, pos_c, send_rows, recv_rows, st, rmap, yback, has_bias, spec = ctx.state
         n, h = hidden.shape
         e = wg.shape[1]
         dev = hidden.device
@@ -134,28 +137,32 @@ class _DPMoEFunction(torch.autograd.Function):
         _ops.call("ppmoe_bwd_dy", _ops.dtype_code(hidden.dtype), _ops.ptr(g_out), _ops.ptr(yback), _ops.ptr(cstart), e,
                   h, max(n_send, 1), _ops.ptr(tok_c), _ops.ptr(w_c), int(spec.weight_scaling), 0.0, 0, _ops.ptr(dy_c),
                   _ops.ptr(dw_c), None, _ops._stream())
-        dy_recv = torch.empty((max(n_recv, 1), h), dtype=hidden.dtype, device=dev)
+        solo = spec.tp == 1
+        dy_recv = dy_c if solo else torch.empty((max(n_recv, 1), h), dtype=hidden.dtype, device=dev)
         _a2a(spec.world, spec.group, dy_recv[:n_recv], dy_c[:n_send], recv_rows, send_rows)
-        # owner: data gradients (dY gathered to owner rows by the receive map), dX rows per receive row
-        dx_recv = torch.zeros((max(n_recv, 1), h), dtype=torch.float32, device=dev)
-        dy, dh, _, parts = _ops.experts_backward_data(dy_recv, st, up, down, False, dx_recv, has_bias)
-        dx_recv_b = _ops.cast_out(dx_recv, hidden.dtype)
-        del dx_recv
-        dx_back = torch.empty((max(n_send, 1), h), dtype=hidden.dtype, device=dev)
-        work = _a2a(spec.world, spec.group, dx_back[:n_send], dx_recv_b[:n_recv], send_rows, recv_rows, async_op=True)
+        # owner: data gradients (dY gathered to owner rows by the receive map), per-row dX in the
+        # owner layout, permuted back to receive order (bf16, no fp32 scatter)
+        dxs = _ops._act((st.rows_cap, h), hidden.dtype, dev)
+        dy, dh, _, parts = _ops.experts_backward_data(dy_recv, st, up, down, False, None, has_bias, dxs)
+        dx_recv = _ops._act((max(n_recv, 1), h), hidden.dtype, dev)
+        _ops.permute_rows(dxs, st.rows_cap, rmap, dx_recv)
+        del dxs
+        dx_back = dx_recv if solo else torch.empty((max(n_send, 1), h), dtype=hidden.dtype, device=dev)
+        work = _a2a(spec.world, spec.group, dx_back[:n_send], dx_recv[:n_recv], send_rows, recv_rows, async_op=True)
         with _ops.sm_budget(_ops.overlap_sm_budget() if work is not None else 0):
             d_up, d_down, d_bu, d_bd = _ops.experts_backward_weights(st, dy, dh, up, down, has_bias, parts)
         if work is not None:
             work.wait()
-        # source: dX rows back to token order + the gate path
-        dx_acc = torch.zeros((n, h), dtype=torch.float32, device=dev)
-        _ops.scatter_rows(dx_back, cstart[e:], tok_c, None, dx_acc)
+        # source: dX[t] = sum_s dX rows (slot order) + dL Wg^T in one gather; dWg = X^T dL
         aux = None if g_aux is None else g_aux.detach().to(torch.float32).reshape(1).contiguous()
         dl = torch.empty((n, e), dtype=torch.float32, device=dev)
         _ops.call("ppmoe_gate_bwd", _ops.ptr(rt.scores), _ops.ptr(rt.idx), _ops.ptr(pos_c), _ops.ptr(dw_c),
                   _ops.ptr(cstart), e, _ops.ptr(rt.top1_counts), n, e, spec.k, _ops.ptr(aux), _ops.ptr(dl),
                   _ops._stream())
-        dx, dwg = _ops.gate_grads(dx_acc, hidden, dl, wg, ctx.needs_input_grad[0], ctx.needs_input_grad[1])
+        dx = None
+        if ctx.needs_input_grad[0]:
+            dx = _ops.compact_combine(dx_back, cstart, rt.idx, pos_c, None, torch.empty_like(hidden), dl, wg)
+        dwg = _ops.gate_weight_grad(hidden, dl, wg) if ctx.needs_input_grad[1] else None
         ctx.state = None
         return dx, dwg, d_up, d_down, d_bu, d_bd, None
 

@@ -138,7 +138,40 @@ def layer_case(name, case, sample_every=1):
     save(name, case, arrays, meta)
 
 
+def stack_case(name, case):
+    """A residual stack of (dense_tp_ffn_forward, ppmoe_forward) blocks (moe.py:316-335,
+    254-308) on one TP group: loss = sum(out) + sum of l_aux, tensor.backward.  Dense FFN of
+    block i: ExpertFfn.init(h, Rng(seed, 200 + i)) rounded to bf16; MoE of block i:
+    MoeLayerWeights.init(h, E, Rng(seed + 1 + i)) rounded like the layer goldens."""
+    h, e, n, tp, seed, nb = case["hidden"], case["experts"], case["tokens"], case["tp"], case["seed"], case["blocks"]
+    x0 = hidden_of(seed, n, h)
+    x = T.tensor(x0, requires_grad=True)
+    cur, aux, params = x, None, {}
+    for i in range(nb):
+        ffn = moe.ExpertFfn.init(h, T.Rng(seed, 200 + i))
+        ffn.up = T.tensor(bf16(ffn.up.data), requires_grad=True)
+        ffn.down = T.tensor(bf16(ffn.down.data), requires_grad=True)
+        ffn.bias_down = T.tensor(bf16(ffn.bias_down.data), requires_grad=True)
+        layer = rounded_layer(h, e, seed + 1 + i)
+        d = moe.dense_tp_ffn_forward(World(1, tp), ep(tp), cur, ffn)
+        x1 = T.add(cur, d)
+        out, l_aux = moe.ppmoe_forward(World(1, tp), ep(tp), x1, layer.gate, layer.shard(tp))
+        cur = T.add(x1, out)
+        aux = l_aux if aux is None else T.add(aux, l_aux)
+        params.update({f"{i}.dense.up": ffn.up, f"{i}.dense.down": ffn.down, f"{i}.dense.bias_down": ffn.bias_down})
+        params.update({f"{i}.moe.{k}": p for k, p in layer.named_parameters().items()})
+    T.backward(T.add(T.tsum(cur), aux))
+    arrays = {"out": cur.data, "grad_hidden": x.grad, "aux": np.array(aux.item())}
+    for k, p in params.items():
+        if p.grad is not None:
+            arrays[f"grad_{k}"] = p.grad
+    save(name, case, arrays)
+
+
 def main():
+    if sys.argv[1:] == ["stack"]:
+        stack_case("stack_2blocks_tp2", {"hidden": 32, "experts": 4, "tokens": 40, "tp": 2, "seed": 31, "blocks": 2})
+        return
     torch.set_num_threads(1)
     # gate_top1 on a random instance (test_moe.py:44-55 style) and the identity-gate goldens
     rng = T.Rng(50)
@@ -181,6 +214,7 @@ def main():
             arrays[f"grad_{k}"] = gr
         save(name, case, arrays, {"weights": weight_checksums(layer),
                                   "capacity": math.ceil(cf * 64 / 4)})
+    stack_case("stack_2blocks_tp2", {"hidden": 32, "experts": 4, "tokens": 40, "tp": 2, "seed": 31, "blocks": 2})
 
 
 if __name__ == "__main__":

@@ -623,3 +623,65 @@ def test_c3_full_size_sampled_tokens_vs_oracle():
     tol = TOL[torch.bfloat16]
     assert scaled_err(out.detach()[sel].double().cpu().numpy(), ref_out) < tol
     assert scaled_err(x.grad[sel].double().cpu().numpy(), ref_dx) < tol
+
+
+# ------------------------------------------------------------------ block stack vs oracle (configs[3])
+
+
+@pytest.mark.parametrize("layers,mbs", [(2, 1), (4, 3)])
+def test_pipeline_stack_vs_oracle(layers, mbs):
+    """The PPMoE block stack (pipeline.PipelineStack: dense FFN + PPMoE layer per residual
+    block, the reference's 1F1B op order) on one GPU in fp32, against the fp64 oracle
+    restatement oracle.block_stack (dense_tp_ffn_forward moe.py:316-335 + ppmoe_forward
+    moe.py:254-308, pinned to a moesim-generated stack golden in test_oracle.py): the op order
+    equals schedule_1f1b and every parameter gradient, accumulated over the micro-batches,
+    matches at the fp32 bar."""
+    from paper_2304_11414_b200.pipeline import PipelineStack, schedule_1f1b
+
+    h, e, k, n = 128, 8, 2, 192
+    stack = PipelineStack(P.World(1, 1, distributed=False), layers=layers, stages=1, tp=1, hidden=h, experts=e,
+                          top_k=k, seed=7, dtype=torch.float32)
+    gen = torch.Generator().manual_seed(11)
+    mb = [torch.randn(n, h, generator=gen).cuda() for _ in range(mbs)]
+    done = stack.train_step(mb)
+    torch.cuda.synchronize()
+    assert done == schedule_1f1b(1, mbs)[0]
+
+    def np64(t):
+        return t.detach().double().cpu().numpy()
+
+    blocks = []
+    for dense, moe in stack.blocks:
+        b = moe.bank
+        lay = O.OracleLayer(np64(moe.gate.wg), [np64(u) for u in b.up], [np64(d) for d in b.down],
+                            [np64(x) for x in b.bias_up], [np64(x) for x in b.bias_down])
+        blocks.append(O.StackBlock(np64(dense.up), np64(dense.down), np64(dense.bias_down), lay))
+    ref = None
+    gaps = []
+    for x in mb:
+        xx = np64(x)
+        # routing must not sit on a near-tie the fp32 stack could flip (check the block inputs)
+        cur = xx
+        for blk in blocks:
+            d, _, _ = O.dense_ffn(cur, blk.dense_up, blk.dense_down, blk.dense_bias_down)
+            cur = cur + d
+            r = O.gate_topk(cur, blk.moe.wg, k)
+            srt = -np.sort(-r.scores, axis=1)
+            gaps.append(float((srt[:, :k] - srt[:, 1:k + 1]).min()))
+            cur = cur + O.ppmoe_layer(cur, blk.moe, k=k, backward=False).out
+        _, _, grads, _ = O.block_stack(xx, blocks, k=k)
+        ref = grads if ref is None else [{nm: r0[nm] + g[nm] for nm in r0} for r0, g in zip(ref, grads)]
+    assert min(gaps) > 1e-5, f"routing near-tie {min(gaps)}: pick another seed"
+    errs = {}
+    for i, ((dense, moe), want) in enumerate(zip(stack.blocks, ref)):
+        got = {"dense.up": dense.up.grad, "dense.down": dense.down.grad, "dense.bias_down": dense.bias_down.grad,
+               "moe.gate.wg": moe.gate.wg.grad}
+        for ex in range(e):
+            for nm, t in (("up", moe.bank.up), ("down", moe.bank.down), ("bias_up", moe.bank.bias_up),
+                          ("bias_down", moe.bank.bias_down)):
+                got[f"moe.expert{ex}.{nm}"] = t.grad[ex]
+        for nm, g in want.items():
+            errs[f"{i}.{nm}"] = scaled_err(np64(got[nm]), g)
+    bad = {key: v for key, v in errs.items() if not v < TOL[torch.float32]}
+    assert not bad, bad
+    assert len(errs) == layers * (4 + 4 * e)
