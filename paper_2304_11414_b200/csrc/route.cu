@@ -311,6 +311,110 @@ __global__ void __launch_bounds__(kRouteThreads, EB == 8 ? 2 : 1) router_kernel(
   route_tail(lg, stat, t0, N, E, K, ovr, idx, w, scores, ssum, cnt_top1);
 }
 
+// One FP64 tensor-core MMA (DMMA 8x8x4, IEEE fp64): d += a (8x4, row) * b (4x8, col).
+// Fragments: lane l holds a = A[l/4][l%4], b = B[l%4][l/4], d = D[l/4][2(l%4) + {0,1}].
+__device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(d[0]), "+d"(d[1])
+      : "d"(a), "d"(b));
+}
+
+// Gate logits X*Wg on the FP64 tensor cores, then the shared softmax / top-k / aux tail.
+// bf16 activations and fp32 gate weights widen exactly to fp64, so every product is exact
+// and the only rounding is fp64 accumulation (as in the fp64 oracle, up to order).  A block
+// owns kRouteTB = 32 tokens (4 groups of 8 = the MMA's M) x EB experts (n-tiles of 8); its 8
+// warps split the hidden dimension and their partial logits are summed in a fixed order in
+// shared memory (deterministic).  MMA k-step j of a 32-column chunk maps k-index q to column
+// c0 + 8q + j, so a lane's A values for all 8 steps come from ONE 16-byte load of its token
+// row (x[t][c0+8q .. c0+8q+7]) and its B values are Wg[c0+8q+j][n] (L1-resident).
+// FP64 FMA work moves from 2 DFMA warp-instructions per 64 FMAs to one DMMA per 256.
+template <int EB>
+__global__ void __launch_bounds__(kRouteThreads) router_dmma_kernel(const __nv_bfloat16* __restrict__ X,
+                                                                    const float* __restrict__ Wg, int N, int H, int E,
+                                                                    int K, const int* __restrict__ ovr,
+                                                                    int* __restrict__ idx, float* __restrict__ w,
+                                                                    float* __restrict__ scores,
+                                                                    double* __restrict__ ssum,
+                                                                    int* __restrict__ cnt_top1) {
+  constexpr int NT = EB / 8;
+  constexpr int G = kRouteTB / 8;
+  constexpr int W = kRouteThreads / 32;
+  extern __shared__ __align__(16) unsigned char sm[];
+  double* part = reinterpret_cast<double*>(sm);  // [W][G][NT][32][2]
+  double* lg = part + W * G * NT * 64;           // [TB][E]
+  double* stat = lg + kRouteTB * E;              // [TB][2]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, q = lane & 3;
+  const int t0 = blockIdx.x * kRouteTB;
+  const int span = H / W;  // columns per warp (H % (32 W) == 0)
+  const int cw0 = warp * span;
+  const __nv_bfloat16* xr[G];
+  bool ok[G];
+#pragma unroll
+  for (int gi = 0; gi < G; ++gi) {
+    const int t = t0 + gi * 8 + g;
+    ok[gi] = t < N;
+    xr[gi] = X + static_cast<size_t>(ok[gi] ? t : 0) * H + 8 * q;
+  }
+  double acc[G][NT][2];
+#pragma unroll
+  for (int gi = 0; gi < G; ++gi)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) acc[gi][nt][0] = acc[gi][nt][1] = 0.0;
+  uint4 xa[G];
+#pragma unroll
+  for (int gi = 0; gi < G; ++gi) xa[gi] = ok[gi] ? ldg16(xr[gi] + cw0) : make_uint4(0, 0, 0, 0);
+  for (int c0 = cw0; c0 < cw0 + span; c0 += 32) {
+    uint4 xn[G];
+    const bool more = c0 + 32 < cw0 + span;
+#pragma unroll
+    for (int gi = 0; gi < G; ++gi) xn[gi] = (more && ok[gi]) ? ldg16(xr[gi] + c0 + 32) : make_uint4(0, 0, 0, 0);
+    double b[NT][8];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const int e = nt * 8 + g;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        b[nt][j] = e < E ? static_cast<double>(__ldg(Wg + static_cast<size_t>(c0 + 8 * q + j) * E + e)) : 0.0;
+    }
+#pragma unroll
+    for (int gi = 0; gi < G; ++gi) {
+      double a[8];
+      widen8<__nv_bfloat16>(&xa[gi], a);
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) dmma884(acc[gi][nt], a[j], b[nt][j]);
+    }
+#pragma unroll
+    for (int gi = 0; gi < G; ++gi) xa[gi] = xn[gi];
+  }
+#pragma unroll
+  for (int gi = 0; gi < G; ++gi)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      double* p = part + ((((warp * G + gi) * NT + nt) * 32) + lane) * 2;
+      p[0] = acc[gi][nt][0];
+      p[1] = acc[gi][nt][1];
+    }
+  __syncthreads();
+  for (int o = threadIdx.x; o < kRouteTB * E; o += kRouteThreads) {  // split-K sum, warp order
+    const int tl = o / E, e = o % E;
+    const int gi = tl >> 3, ln = (tl & 7) * 4 + ((e & 7) >> 1), nt = e >> 3, i = e & 1;
+    double v = 0.0;
+#pragma unroll
+    for (int ww = 0; ww < W; ++ww) v += part[((((ww * G + gi) * NT + nt) * 32) + ln) * 2 + i];
+    lg[tl * E + e] = v;
+  }
+  route_tail(lg, stat, t0, N, E, K, ovr, idx, w, scores, ssum, cnt_top1);
+}
+
+__host__ inline size_t route_dmma_smem_bytes(int E) {
+  const int NT = E <= 8 ? 1 : 2;
+  return static_cast<size_t>(kRouteThreads / 32) * (kRouteTB / 8) * NT * 64 * 8 + static_cast<size_t>(kRouteTB) * E * 8 +
+         2 * kRouteTB * 8;
+}
+
 // l_aux = E * sum_e frac_e * mean_t s[t,e]  with frac from the top-1 choice (moe.py:221-223)
 __global__ void __launch_bounds__(256) route_finalize_kernel(const double* __restrict__ ssum, int nblocks,
                                                              const int* __restrict__ cnt_top1, int N, int E,
@@ -553,6 +657,24 @@ static int launch_router(const void* X, const float* Wg, int N, int H, int E, in
   return check_launch("router_kernel");
 }
 
+static bool use_dmma_router(int dtype, int H, int E) {
+  const char* e = std::getenv("PPMOE_ROUTER");  // PPMOE_ROUTER=dfma: the CUDA-core fp64 kernel (A/B)
+  if (e && std::strcmp(e, "dfma") == 0) return false;
+  return dtype == kBF16 && H % (32 * (kRouteThreads / 32)) == 0 && E <= 16;
+}
+
+template <int EB>
+static int launch_router_dmma(const void* X, const float* Wg, int N, int H, int E, int K, const int* ovr, int* idx,
+                              float* w, float* scores, double* ssum, int* cnt, cudaStream_t s) {
+  const size_t smem = route_dmma_smem_bytes(E);
+  auto k = router_dmma_kernel<EB>;
+  PPMOE_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  const int nb = (N + kRouteTB - 1) / kRouteTB;
+  k<<<nb, kRouteThreads, smem, s>>>(static_cast<const __nv_bfloat16*>(X), Wg, N, H, E, K, ovr, idx, w, scores, ssum,
+                                     cnt);
+  return check_launch("router_dmma_kernel");
+}
+
 }  // namespace ppmoe
 
 using namespace ppmoe;
@@ -579,7 +701,10 @@ int ppmoe_route(const void* X, int dtype, const float* Wg, int N, int H, int E, 
   int* cnt = reinterpret_cast<int*>(static_cast<char*>(ws) + align_up(static_cast<size_t>(nb) * E * 8, 256));
   PPMOE_CUDA(cudaMemsetAsync(cnt, 0, static_cast<size_t>(E) * 4, s));
   int rc;
-  if (dtype == kBF16)
+  if (use_dmma_router(dtype, H, E))
+    rc = E <= 8 ? launch_router_dmma<8>(X, Wg, N, H, E, K, route_override, idx, w, scores, ssum, cnt, s)
+                : launch_router_dmma<16>(X, Wg, N, H, E, K, route_override, idx, w, scores, ssum, cnt, s);
+  else if (dtype == kBF16)
     rc = E <= 8 ? launch_router<__nv_bfloat16, 8>(X, Wg, N, H, E, K, route_override, idx, w, scores, ssum, cnt, s)
                 : launch_router<__nv_bfloat16, 16>(X, Wg, N, H, E, K, route_override, idx, w, scores, ssum, cnt, s);
   else

@@ -77,8 +77,11 @@ def run_ppmoe(case):
     x0 = hidden_of(seed, n, h)
     x = T.tensor(x0, requires_grad=True)
     override = case.get("override")
+    drop = case.get("dropout_p", 0.0)
+    rng = T.Rng(seed, 77) if drop > 0 else None
     out, l_aux = moe.ppmoe_forward(World(1, tp), ep(tp), x, layer.gate, layer.shard(tp),
-                                   weight_scaling=case.get("weight_scaling", True), route_override=override)
+                                   weight_scaling=case.get("weight_scaling", True), route_override=override,
+                                   dropout_p=drop, rng=rng)
     T.backward(T.add(T.tsum(out), l_aux))
     gate = moe.gate_top1(T.tensor(x0), layer.gate, route_override=override)
     plan = moe.build_dispatch_plan(gate.indices, e)
@@ -169,6 +172,10 @@ def stack_case(name, case):
 
 
 def main():
+    if sys.argv[1:] == ["dropout"]:
+        layer_case("ppmoe_dropout", {"hidden": 32, "experts": 4, "tokens": 64, "tp": 2, "seed": 15,
+                                     "dropout_p": 0.25})
+        return
     if sys.argv[1:] == ["stack"]:
         stack_case("stack_2blocks_tp2", {"hidden": 32, "experts": 4, "tokens": 40, "tp": 2, "seed": 31, "blocks": 2})
         return
@@ -198,6 +205,7 @@ def main():
                                         "bias": False, "weight_scaling": False})
     ov = T.Rng(14, 5).integers(0, 4, 48).tolist()
     layer_case("ppmoe_override", {"hidden": 64, "experts": 4, "tokens": 48, "tp": 2, "seed": 14, "override": ov})
+    layer_case("ppmoe_dropout", {"hidden": 32, "experts": 4, "tokens": 64, "tp": 2, "seed": 15, "dropout_p": 0.25})
     # C1 shape (BASELINE configs[0]): h=512, ffn=2048, E=8, top-1, 2048 tokens; rows sampled
     layer_case("ppmoe_c1", {"hidden": 512, "experts": 8, "tokens": 2048, "tp": 1, "seed": 0}, sample_every=16)
 

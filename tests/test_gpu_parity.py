@@ -666,12 +666,12 @@ def test_pipeline_stack_vs_oracle(layers, mbs):
             d, _, _ = O.dense_ffn(cur, blk.dense_up, blk.dense_down, blk.dense_bias_down)
             cur = cur + d
             r = O.gate_topk(cur, blk.moe.wg, k)
-            srt = -np.sort(-r.scores, axis=1)
-            gaps.append(float((srt[:, :k] - srt[:, 1:k + 1]).min()))
+            srt = -np.sort(-r.scores, axis=1)  # relative gaps: fp32 logits carry ~1e-6 relative error
+            gaps.append(float(((srt[:, :k] - srt[:, 1:k + 1]) / srt[:, :k]).min()))
             cur = cur + O.ppmoe_layer(cur, blk.moe, k=k, backward=False).out
         _, _, grads, _ = O.block_stack(xx, blocks, k=k)
         ref = grads if ref is None else [{nm: r0[nm] + g[nm] for nm in r0} for r0, g in zip(ref, grads)]
-    assert min(gaps) > 1e-5, f"routing near-tie {min(gaps)}: pick another seed"
+    assert min(gaps) > 1e-4, f"routing near-tie (relative gap {min(gaps)}): pick another seed"
     errs = {}
     for i, ((dense, moe), want) in enumerate(zip(stack.blocks, ref)):
         got = {"dense.up": dense.up.grad, "dense.down": dense.down.grad, "dense.bias_down": dense.bias_down.grad,
