@@ -123,13 +123,14 @@ int ppmoe_expert_fc1_fwd(int dtype, const void* Xs, const void* up, const void* 
 /* Expert FFN forward, second GEMM fused with the gate-weighted combine:
  * Y = Dropout(Act*down_g + bias_down) (stored, pre-scale), out_acc[tok] += w*Y
  * (moe.py:104-107, scale_rows tensor.py:184-196, index_assign 244-272, dropout
- * tensor.py:315-330 with a counter-based mask hash(seed, local row, column)).
+ * tensor.py:315-330 drawn from the reference's Philox stream: drop_stream = the
+ * descriptor of ppmoe_dropout_stream, required when dropout_p > 0, else may be NULL).
  * out_acc [N x H] fp32 must be zeroed by the caller; NULL = store Y only (for ppmoe_combine).
  * Y2 (optional) receives a second copy of Y (the peer-visible rows of ppmoe_nvl_owner_gather). */
 int ppmoe_expert_fc2_fwd(int dtype, const void* Act, const void* down, const void* bias_down, const int* seg,
                          int El, int H, int F, int rows_cap, const int* row_lo, const int* row_hi,
                          const int* tok_local, const float* w_local, int weight_scaling, float dropout_p,
-                         unsigned long long seed, void* Y, void* Y2, float* out_acc, void* stream);
+                         const unsigned long long* drop_stream, void* Y, void* Y2, float* out_acc, void* stream);
 
 /* Gather-combine over this rank's pairs, in slot order (deterministic):
  *   out[t] = sum_s w[t,s] * R[pair_pos[t,s] - seg[0]]  (+ dL[t,:] . Wg^T when dL != NULL)
@@ -155,6 +156,16 @@ int ppmoe_input_grads(int dtype, const void* dXs, const int* seg, int El, const 
  * after the TP all-reduce, collectives.py:135-153).                         */
 int ppmoe_cast_out(const float* acc, int n, void* out, int dtype, void* stream);
 
+/* Dropout stream descriptor (device, 3 + El uint64) of the reference's tensor.dropout draws
+ * (tensor.py:315-330, moesim Rng = numpy Philox4x64-10 keyed (key0, key1)): the experts
+ * draw one [kept rows x H] uniform block each in ascending id starting at draw first_draw
+ * of the stream; this rank's experts are [e0, e0+El); kept [E] device counts of every
+ * expert (kept pairs, i.e. rows).  threshold = ceil(p * 2^53): draw w is kept iff
+ * (w >> 11) >= threshold, i.e. its uniform (w >> 11) * 2^-53 >= p.                    */
+int ppmoe_dropout_stream(const int* kept, int E, int e0, int El, int H, unsigned long long key0,
+                         unsigned long long key1, unsigned long long threshold, unsigned long long first_draw,
+                         unsigned long long* desc, void* stream);
+
 /* Backward of scale_rows + index_assign + dropout (tensor.py:190-194, 264-270, 326-328):
  * dY[row] = w*dOut[tok] (times the forward's dropout mask / (1-p)),
  * dw[row] = <dOut[tok], Y[row]>; zero for padding.  dy_colsum_part (optional, bf16 and
@@ -162,7 +173,7 @@ int ppmoe_cast_out(const float* acc, int n, void* out, int dtype, void* stream);
  * ppmoe_expert_fc2_wgrad for the bias_down gradient.                        */
 int ppmoe_bwd_dy(int dtype, const void* dOut, const void* Y, const int* seg, int El, int H, int rows_cap,
                  const int* tok_local, const float* w_local, int weight_scaling, float dropout_p,
-                 unsigned long long seed, void* dY, float* dw, float* dy_colsum_part, void* stream);
+                 const unsigned long long* drop_stream, void* dY, float* dw, float* dy_colsum_part, void* stream);
 
 /* dH = (dY*down_g^T) .* GeluGrad   (matmul/gelu backward, tensor.py:134-138, 204-207).
  * dh_colsum_part (optional, bf16 path): [rows/32 x F] fp32 column sums of dH per 32-row
@@ -269,7 +280,7 @@ int ppmoe_nvl_sum_rows(const void* const* srcs, int T, int rank, int N, int C, f
  * slot from pair_pos [N x K], K <= 2), and ppmoe_nvl_sum_slots sums the valid slots.   */
 int ppmoe_expert_fc2_fwd_owner(int dtype, const void* Act, const void* down, const void* bias_down, const int* seg,
                                int El, int H, int F, int rows_cap, const int* tok_local, const float* w_local,
-                               int weight_scaling, float dropout_p, unsigned long long seed, void* Y,
+                               int weight_scaling, float dropout_p, const unsigned long long* drop_stream, void* Y,
                                float* const* owner_acc, void* const* owner_slots, const int* pair_pos, int K,
                                int owner_rows, void* stream);
 int ppmoe_nvl_cast_owned(float* acc, int rows, int H, void* out_rows, void* xch_rows, void* stream);

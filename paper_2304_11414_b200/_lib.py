@@ -43,7 +43,7 @@ _SIGNATURES = {
     "ppmoe_gather": (_I, [_P, _I, _I, _I, _P, _I, _P, _P, _I, _P, _P, _P, _P]),
     "ppmoe_chunk_rows": (_I, [_P, _P, _P, _I, _I, _I, _P, _P, _P]),
     "ppmoe_expert_fc1_fwd": (_I, [_I, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P]),
-    "ppmoe_expert_fc2_fwd": (_I, [_I, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _I, _F, _U, _P, _P, _P, _P]),
+    "ppmoe_expert_fc2_fwd": (_I, [_I, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _I, _F, _P, _P, _P, _P, _P]),
     "ppmoe_combine": (_I, [_I, _P, _P, _I, _P, _P, _I, _I, _I, _P, _P, _I, _P, _P]),
     "ppmoe_input_grads_workspace_bytes": (_S, [_I, _I, _I, _I]),
     "ppmoe_input_grads": (_I, [_I, _P, _P, _I, _P, _I, _I, _I, _P, _P, _P, _I, _P, _P, _P, _S, _P]),
@@ -60,11 +60,12 @@ _SIGNATURES = {
     "ppmoe_nvl_sum_rows": (_I, [_P, _I, _I, _I, _I, _P, _P]),
     "ppmoe_nvl_pull_blocks_ce": (_I, [_P, _I, _I, _I, _I, _P, _P]),
     "ppmoe_nvl_pull_range_ce": (_I, [_P, _I, _I, _I, _I, _I, _I, _P, _P]),
-    "ppmoe_expert_fc2_fwd_owner": (_I, [_I, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P, _I, _F, _U, _P, _P, _P, _P, _I, _I,
+    "ppmoe_expert_fc2_fwd_owner": (_I, [_I, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P, _I, _F, _P, _P, _P, _P, _P, _I, _I,
                                         _P]),
     "ppmoe_nvl_sum_slots": (_I, [_P, _I, _I, _I, _I, _P, _P, _P, _P]),
     "ppmoe_nvl_cast_owned": (_I, [_P, _I, _I, _P, _P, _P]),
-    "ppmoe_bwd_dy": (_I, [_I, _P, _P, _P, _I, _I, _I, _P, _P, _I, _F, _U, _P, _P, _P, _P]),
+    "ppmoe_bwd_dy": (_I, [_I, _P, _P, _P, _I, _I, _I, _P, _P, _I, _F, _P, _P, _P, _P, _P]),
+    "ppmoe_dropout_stream": (_I, [_P, _I, _I, _I, _I, _U, _U, _U, _U, _P, _P]),
     "ppmoe_expert_fc2_dgrad": (_I, [_I, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P]),
     "ppmoe_expert_fc2_wgrad": (_I, [_I, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P]),
     "ppmoe_expert_fc1_dgrad": (_I, [_I, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P]),

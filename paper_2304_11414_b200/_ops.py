@@ -240,6 +240,16 @@ def plan(idx: torch.Tensor, w: torch.Tensor | None, num_experts: int, capacity: 
     return Plan(counts, kept, seg, tok_sorted, w_sorted, pair_pos, capacity)
 
 
+def dropout_descriptor(kept: torch.Tensor, num_experts: int, e0: int, el: int, h: int, key0: int, key1: int,
+                       threshold: int, first_draw: int) -> torch.Tensor:
+    """Device descriptor of the reference's dropout stream for local experts [e0, e0+el)
+    (ppmoe_dropout_stream): [key0, key1, threshold, first draw of each local expert]."""
+    desc = torch.empty(3 + el, dtype=torch.int64, device=kept.device)
+    call("ppmoe_dropout_stream", ptr(kept), num_experts, e0, el, h, ctypes.c_ulonglong(key0), ctypes.c_ulonglong(key1),
+         ctypes.c_ulonglong(threshold), ctypes.c_ulonglong(first_draw), ptr(desc), _stream())
+    return desc
+
+
 def local_rows_cap(n: int, k: int, el: int, capacity: int) -> int:
     """Upper bound of the padded rows of `el` experts (no host sync on the true count)."""
     pairs = min(n * k, n * el)
@@ -264,12 +274,12 @@ class ExpertFwdState:
     act: torch.Tensor
     y: torch.Tensor
     drop_p: float = 0.0
-    seed: int = 0
+    drop: torch.Tensor | None = None  # dropout stream descriptor (moe.DropoutStream.descriptor)
 
 
 def experts_forward(hidden, pl: Plan, e0: int, el: int, up, down, bias_up, bias_down, k: int, weight_scaling: bool,
                     out_acc: torch.Tensor, chunks: int = 1, on_chunk=None, drop_p: float = 0.0,
-                    seed: int = 0, y_mirror: torch.Tensor | None = None, owner_table: torch.Tensor | None = None,
+                    drop: torch.Tensor | None = None, y_mirror: torch.Tensor | None = None, owner_table: torch.Tensor | None = None,
                     owner_rows: int = 0, owner_slots: torch.Tensor | None = None) -> ExpertFwdState:
     """index-slice gather -> fc1 (+bias, GeLU) -> fc2 (+bias, gate-scaled scatter-add combine)
     for experts [e0, e0+el) (moe.py:294-305).  out_acc None: fc2 only stores Y and the
@@ -298,11 +308,11 @@ def experts_forward(hidden, pl: Plan, e0: int, el: int, up, down, bias_up, bias_
         if owner_table is not None or owner_slots is not None:
             # combine fused into the epilogue: rows go to their owners (fp32 accumulators or bf16 slots)
             call("ppmoe_expert_fc2_fwd_owner", dt, ptr(act), ptr(down), ptr(bias_down), ptr(seg), el, h, f, rows_cap,
-                 ptr(tok_l), ptr(w_l), int(bool(weight_scaling)), float(drop_p), int(seed), ptr(y), ptr(owner_table),
+                 ptr(tok_l), ptr(w_l), int(bool(weight_scaling)), float(drop_p), ptr(drop), ptr(y), ptr(owner_table),
                  ptr(owner_slots), ptr(pl.pair_pos), k, int(owner_rows), s)
             return
         call("ppmoe_expert_fc2_fwd", dt, ptr(act), ptr(down), ptr(bias_down), ptr(seg), el, h, f, rows_cap, ptr(rlo),
-             ptr(rhi), ptr(tok_l), ptr(w_l), int(bool(weight_scaling)), float(drop_p), int(seed), ptr(y), ptr(y_mirror),
+             ptr(rhi), ptr(tok_l), ptr(w_l), int(bool(weight_scaling)), float(drop_p), ptr(drop), ptr(y), ptr(y_mirror),
              ptr(out_acc), s)
 
     if chunks <= 1:
@@ -322,12 +332,12 @@ def experts_forward(hidden, pl: Plan, e0: int, el: int, up, down, bias_up, bias_
         pad_lo, pad_hi = rlo[chunks * el:], rhi[chunks * el:]
         call("ppmoe_expert_fc1_fwd", dt, ptr(xs), ptr(up), ptr(bias_up), ptr(seg), el, h, f, rows_cap, ptr(pad_lo),
              ptr(pad_hi), ptr(gelu_grad), ptr(act), s)
-    return ExpertFwdState(e0, el, rows_cap, seg, xs, tok_l, w_l, gelu_grad, act, y, drop_p, seed)
+    return ExpertFwdState(e0, el, rows_cap, seg, xs, tok_l, w_l, gelu_grad, act, y, drop_p, drop)
 
 
 def expert_pipeline(xsrc: torch.Tensor, seg: torch.Tensor, el: int, tok_sorted: torch.Tensor,
                     w_sorted: torch.Tensor | None, rows_cap: int, up, down, bias_up, bias_down, weight_scaling: bool,
-                    out_acc: torch.Tensor, drop_p: float = 0.0, seed: int = 0) -> ExpertFwdState:
+                    out_acc: torch.Tensor, drop_p: float = 0.0, drop: torch.Tensor | None = None) -> ExpertFwdState:
     """gather(xsrc rows by tok_sorted) -> fc1 -> fc2 with the scatter-add into out_acc[tok],
     for an arbitrary padded-segment layout (used by the all-to-all comparator's owner side,
     where tok_sorted maps owner rows to receive-buffer rows)."""
@@ -347,8 +357,8 @@ def expert_pipeline(xsrc: torch.Tensor, seg: torch.Tensor, el: int, tok_sorted: 
     call("ppmoe_expert_fc1_fwd", dt, ptr(xs), ptr(up), ptr(bias_up), ptr(seg), el, h, f, rows_cap, None, None,
          ptr(gelu_grad), ptr(act), s)
     call("ppmoe_expert_fc2_fwd", dt, ptr(act), ptr(down), ptr(bias_down), ptr(seg), el, h, f, rows_cap, None, None,
-         ptr(tok_l), ptr(w_l), int(bool(weight_scaling)), float(drop_p), int(seed), ptr(y), None, ptr(out_acc), s)
-    return ExpertFwdState(0, el, rows_cap, seg, xs, tok_l, w_l, gelu_grad, act, y, drop_p, seed)
+         ptr(tok_l), ptr(w_l), int(bool(weight_scaling)), float(drop_p), ptr(drop), ptr(y), None, ptr(out_acc), s)
+    return ExpertFwdState(0, el, rows_cap, seg, xs, tok_l, w_l, gelu_grad, act, y, drop_p, drop)
 
 
 def combine_mode(dtype: torch.dtype, hidden: int) -> str:
@@ -466,7 +476,7 @@ def experts_backward_data(grad_out, st: ExpertFwdState, up, down, weight_scaling
     dy = _act((rows_cap, h), grad_out.dtype, dev)
     dw = _act(rows_cap, torch.float32, dev)
     call("ppmoe_bwd_dy", dt, ptr(grad_out), ptr(st.y), ptr(st.seg), el, h, rows_cap, ptr(st.tok_l), ptr(st.w_l),
-         int(bool(weight_scaling)), float(st.drop_p), int(st.seed), ptr(dy), ptr(dw), ptr(dy_part), s)
+         int(bool(weight_scaling)), float(st.drop_p), ptr(st.drop), ptr(dy), ptr(dw), ptr(dy_part), s)
     dh = _act((rows_cap, f), grad_out.dtype, dev)
     call("ppmoe_expert_fc2_dgrad", dt, ptr(dy), ptr(down), ptr(st.gelu_grad), ptr(st.seg), el, h, f, rows_cap, ptr(dh),
          ptr(dh_part), s)

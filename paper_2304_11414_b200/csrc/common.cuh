@@ -57,17 +57,68 @@ __device__ __forceinline__ void gelu_and_grad(float x, float& act, float& grad) 
   grad = fmaf(x * 0.39894228040143268f, e, cdf);
 }
 
-// Counter-based dropout keep mask: hash(seed, row, col) -> uniform in [0,1); keep if >= p.
-// The same (seed, local row, column) regenerates the mask in the backward.
-__host__ __device__ __forceinline__ float dropout_uniform(unsigned long long seed, int row, int col) {
-  unsigned long long z = seed ^ (static_cast<unsigned long long>(static_cast<unsigned>(row)) * 0x9E3779B97F4A7C15ull) ^
-                         (static_cast<unsigned long long>(static_cast<unsigned>(col)) * 0xC2B2AE3D27D4EB4Full);
-  z ^= z >> 30;
-  z *= 0xBF58476D1CE4E5B9ull;
-  z ^= z >> 27;
-  z *= 0x94D049BB133111EBull;
-  z ^= z >> 31;
-  return static_cast<float>(z >> 40) * (1.0f / 16777216.0f);
+// The reference's dropout stream (tensor.dropout with moesim's Rng, tensor.py:23-49 and
+// 315-330): numpy's Philox4x64-10 keyed (seed, stream).  Draw m of the stream is word m % 4 of
+// the block at counter m / 4 + 1, a uniform is (word >> 11) * 2^-53, and an element is kept
+// iff uniform >= p, i.e. (word >> 11) >= ceil(p * 2^53) -- an integer compare, exact for the
+// double p.  The experts draw one [rows, H] block each, in ascending expert id, so element
+// (r, c) of local expert g is draw desc[3 + g] + r * H + c.
+// desc (device, uint64) = [key0 (seed), key1 (stream), threshold, first draw of local expert
+// 0, 1, ...] (ppmoe_dropout_stream).
+__device__ __forceinline__ void philox4x64_10(unsigned long long ctr, unsigned long long k0, unsigned long long k1,
+                                              unsigned long long (&out)[4]) {
+  unsigned long long c0 = ctr, c1 = 0, c2 = 0, c3 = 0;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r) {
+      k0 += 0x9E3779B97F4A7C15ull;
+      k1 += 0xBB67AE8584CAA73Bull;
+    }
+    const unsigned long long hi0 = __umul64hi(0xD2E7470EE14C6C93ull, c0), lo0 = 0xD2E7470EE14C6C93ull * c0;
+    const unsigned long long hi1 = __umul64hi(0xCA5A826395121157ull, c2), lo1 = 0xCA5A826395121157ull * c2;
+    const unsigned long long n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0;
+    c1 = lo1;
+    c2 = n2;
+    c3 = lo0;
+  }
+  out[0] = c0;
+  out[1] = c1;
+  out[2] = c2;
+  out[3] = c3;
+}
+
+// Keep bits of W <= 32 consecutive draws m0 .. m0+W-1 (bit j: draw m0 + j kept).
+template <int W>
+__device__ __forceinline__ uint32_t drop_keep_bits(const unsigned long long* __restrict__ desc, unsigned long long m0) {
+  static_assert(W >= 1 && W <= 32, "at most 32 draws");
+  const unsigned long long k0 = desc[0], k1 = desc[1], thr = desc[2];
+  uint32_t bits = 0;
+  const unsigned long long b_end = (m0 + W - 1) >> 2;
+  for (unsigned long long b = m0 >> 2; b <= b_end; ++b) {
+    unsigned long long wd[4];
+    philox4x64_10(b + 1, k0, k1, wd);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const long long j = static_cast<long long>(4 * b + q - m0);
+      if (j >= 0 && j < W && (wd[q] >> 11) >= thr) bits |= 1u << j;
+    }
+  }
+  return bits;
+}
+
+// Local expert of local row r (rows relative to seg[0]) for the dropout draw index.
+__device__ __forceinline__ int segment_of(const int* __restrict__ seg, int El, int r) {
+  int g = 0;
+  const int base = seg[0];
+  while (g + 1 < El && r >= seg[g + 1] - base) ++g;
+  return g;
+}
+
+// First draw of local row r (local expert g) of the dropout stream.
+__device__ __forceinline__ unsigned long long drop_row_draw(const unsigned long long* __restrict__ desc,
+                                                            const int* __restrict__ seg, int g, int r, int H) {
+  return desc[3 + g] + static_cast<unsigned long long>(r - (seg[g] - seg[0])) * static_cast<unsigned long long>(H);
 }
 
 __device__ __forceinline__ float warp_sum(float v) {

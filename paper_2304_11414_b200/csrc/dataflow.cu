@@ -139,7 +139,8 @@ __global__ void cast_kernel(const float* __restrict__ src, size_t n, T* __restri
 template <typename T>
 __global__ void bwd_dy_kernel(const T* __restrict__ dOut, const T* __restrict__ Y, const int* __restrict__ seg, int El,
                               int H, const int* __restrict__ tok_local, const float* __restrict__ w_local,
-                              int weight_scaling, float drop_p, unsigned long long seed, T* __restrict__ dY,
+                              int weight_scaling, float drop_p, const unsigned long long* __restrict__ drop,
+                              T* __restrict__ dY,
                               float* __restrict__ dw) {
   const int rows = seg[El] - seg[0];
   const int lane = threadIdx.x & 31;
@@ -159,10 +160,11 @@ __global__ void bwd_dy_kernel(const T* __restrict__ dOut, const T* __restrict__ 
     float acc = 0.f;
     if (drop_p > 0.f) {  // Y is the dropped output; dY reaches the expert through the same mask
       const float inv = 1.f / (1.f - drop_p);
+      const unsigned long long rd = drop_row_draw(drop, seg, segment_of(seg, El, r), r, H);
       for (int j = lane; j < H; j += 32) {
         const float gv = to_f32(g[j]);
         acc = fmaf(gv, to_f32(y[j]), acc);
-        const float keep = dropout_uniform(seed, r, j) >= drop_p ? inv : 0.f;
+        const float keep = (drop_keep_bits<1>(drop, rd + j) & 1u) ? inv : 0.f;
         dy[j] = from_f32<T>(s * gv * keep);
       }
     } else if (vec && sizeof(T) == 2) {
@@ -202,7 +204,8 @@ __global__ void __launch_bounds__(256)
     bwd_dy_block_kernel(const __nv_bfloat16* __restrict__ dOut, const __nv_bfloat16* __restrict__ Y,
                         const int* __restrict__ seg, int El, int H, const int* __restrict__ tok_local,
                         const float* __restrict__ w_local, int weight_scaling, float drop_p,
-                        unsigned long long seed, __nv_bfloat16* __restrict__ dY, float* __restrict__ dw,
+                        const unsigned long long* __restrict__ drop, __nv_bfloat16* __restrict__ dY,
+                        float* __restrict__ dw,
                         float* __restrict__ part) {
   const int rows = seg[El] - seg[0];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -222,9 +225,11 @@ __global__ void __launch_bounds__(256)
       const float sw = weight_scaling ? w_local[r] : 1.f;
       const __nv_bfloat16* g = dOut + static_cast<size_t>(tok) * H;
       const __nv_bfloat16* y = Y + static_cast<size_t>(r) * H;
+      const unsigned long long rd = drop_p > 0.f ? drop_row_draw(drop, seg, segment_of(seg, El, r), r, H) : 0ull;
       float acc = 0.f;
 #pragma unroll 4
       for (int j = lane * 8; j < H; j += 256) {
+        const uint32_t kb = drop_p > 0.f ? drop_keep_bits<8>(drop, rd + j) : 0u;
         const uint4 gu = *reinterpret_cast<const uint4*>(g + j);
         const uint4 yu = *reinterpret_cast<const uint4*>(y + j);
         const __nv_bfloat162* gh = reinterpret_cast<const __nv_bfloat162*>(&gu);
@@ -239,8 +244,8 @@ __global__ void __launch_bounds__(256)
           acc = fmaf(gf.y, yf.y, acc);
           float d0 = sw * gf.x, d1 = sw * gf.y;
           if (drop_p > 0.f) {
-            d0 *= dropout_uniform(seed, r, j + 2 * i) >= drop_p ? inv : 0.f;
-            d1 *= dropout_uniform(seed, r, j + 2 * i + 1) >= drop_p ? inv : 0.f;
+            d0 *= ((kb >> (2 * i)) & 1u) ? inv : 0.f;
+            d1 *= ((kb >> (2 * i + 1)) & 1u) ? inv : 0.f;
           }
           o[i] = pack_bf16x2(d0, d1);
         }
@@ -276,7 +281,8 @@ __global__ void __launch_bounds__(256, 8 / CPW)
     bwd_dy_cols_kernel(const __nv_bfloat16* __restrict__ dOut, const __nv_bfloat16* __restrict__ Y,
                        const int* __restrict__ seg, int El, int H, const int* __restrict__ tok_local,
                        const float* __restrict__ w_local, int weight_scaling, float drop_p,
-                       unsigned long long seed, __nv_bfloat16* __restrict__ dY, float* __restrict__ dw,
+                       const unsigned long long* __restrict__ drop, __nv_bfloat16* __restrict__ dY,
+                       float* __restrict__ dw,
                        float* __restrict__ part) {
   __shared__ float red[8][33];
   const int rows = seg[El] - seg[0];
@@ -307,6 +313,7 @@ __global__ void __launch_bounds__(256, 8 / CPW)
         const float sw = weight_scaling ? w_local[r] : 1.f;
         const __nv_bfloat16* g = dOut + static_cast<size_t>(tok) * H;
         const __nv_bfloat16* y = Y + static_cast<size_t>(r) * H;
+        const unsigned long long rd = drop_p > 0.f ? drop_row_draw(drop, seg, segment_of(seg, El, r), r, H) : 0ull;
         uint4 gu[CPW], yu[CPW];
 #pragma unroll
         for (int q = 0; q < CPW; ++q) {
@@ -321,6 +328,7 @@ __global__ void __launch_bounds__(256, 8 / CPW)
           const int ch = warp + 8 * q;
           if (ch >= nchunk) continue;
           const int j = ch * 256 + lane * 8;
+          const uint32_t kb = drop_p > 0.f ? drop_keep_bits<8>(drop, rd + j) : 0u;
           const __nv_bfloat162* gh = reinterpret_cast<const __nv_bfloat162*>(&gu[q]);
           const __nv_bfloat162* yh = reinterpret_cast<const __nv_bfloat162*>(&yu[q]);
           uint4 out;
@@ -333,8 +341,8 @@ __global__ void __launch_bounds__(256, 8 / CPW)
             acc = fmaf(gf.y, yf.y, acc);
             float d0 = sw * gf.x, d1 = sw * gf.y;
             if (drop_p > 0.f) {
-              d0 *= dropout_uniform(seed, r, j + 2 * i) >= drop_p ? inv : 0.f;
-              d1 *= dropout_uniform(seed, r, j + 2 * i + 1) >= drop_p ? inv : 0.f;
+              d0 *= ((kb >> (2 * i)) & 1u) ? inv : 0.f;
+              d1 *= ((kb >> (2 * i + 1)) & 1u) ? inv : 0.f;
             }
             o[i] = pack_bf16x2(d0, d1);
             const float2 v = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&o[i]));
@@ -1031,6 +1039,23 @@ static int launch_input_grads(dim3 grid, cudaStream_t s, const void* dXs, const 
   return check_launch("input_grads_ring_kernel");
 }
 
+// desc = [key0, key1, threshold, first draw of local experts 0..El-1]: the experts before
+// e0 (on lower ranks, moe.py:294-301) consume kept[e] * H draws each, in ascending id.
+__global__ void dropout_stream_kernel(const int* __restrict__ kept, int e0, int El, int H, unsigned long long key0,
+                                      unsigned long long key1, unsigned long long threshold,
+                                      unsigned long long first_draw, unsigned long long* __restrict__ desc) {
+  if (threadIdx.x != 0) return;
+  desc[0] = key0;
+  desc[1] = key1;
+  desc[2] = threshold;
+  unsigned long long m = first_draw;
+  for (int e = 0; e < e0; ++e) m += static_cast<unsigned long long>(kept[e]) * H;
+  for (int g = 0; g < El; ++g) {
+    desc[3 + g] = m;
+    m += static_cast<unsigned long long>(kept[e0 + g]) * H;
+  }
+}
+
 }  // namespace ppmoe
 
 using namespace ppmoe;
@@ -1122,6 +1147,16 @@ int ppmoe_combine(int dtype, const void* R, const int* seg, int El, const int* p
   return check_launch("combine_rows_kernel");
 }
 
+int ppmoe_dropout_stream(const int* kept, int E, int e0, int El, int H, unsigned long long key0,
+                         unsigned long long key1, unsigned long long threshold, unsigned long long first_draw,
+                         unsigned long long* desc, void* stream) {
+  PPMOE_REQUIRE(E >= 1 && El >= 1 && e0 >= 0 && e0 + El <= E && H >= 1, "bad dropout stream E=%d e0=%d El=%d", E, e0,
+                El);
+  dropout_stream_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(kept, e0, El, H, key0, key1, threshold,
+                                                                         first_draw, desc);
+  return check_launch("dropout_stream_kernel");
+}
+
 size_t ppmoe_input_grads_workspace_bytes(int dtype, int N, int H, int E) {
   // fused-path partials for any k, or the gate_grads fallback's, whichever is larger
   const size_t fused = static_cast<size_t>(std::max(input_grads_chunks(N, H, E), dwg_chunks(N, H))) * H * E * 4;
@@ -1203,8 +1238,9 @@ int ppmoe_cast_out(const float* acc, int n, void* out, int dtype, void* stream) 
 
 int ppmoe_bwd_dy(int dtype, const void* dOut, const void* Y, const int* seg, int El, int H, int rows_cap,
                  const int* tok_local, const float* w_local, int weight_scaling, float dropout_p,
-                 unsigned long long seed, void* dY, float* dw, float* dy_colsum_part, void* stream) {
+                 const unsigned long long* drop_stream, void* dY, float* dw, float* dy_colsum_part, void* stream) {
   PPMOE_REQUIRE(dropout_p >= 0.f && dropout_p < 1.f, "dropout probability must be in [0, 1), got %g", dropout_p);
+  PPMOE_REQUIRE(dropout_p == 0.f || drop_stream, "dropout needs its stream descriptor (ppmoe_dropout_stream)");
   if (dy_colsum_part) {
     PPMOE_REQUIRE(dtype == kBF16 && H % 256 == 0,
                   "dY column-sum partials need the bf16 path and hidden %% 256 == 0 (H=%d)", H);
@@ -1220,18 +1256,18 @@ int ppmoe_bwd_dy(int dtype, const void* dOut, const void* Y, const int* seg, int
       auto* d = static_cast<__nv_bfloat16*>(dY);
       if (cpw == 1)
         bwd_dy_cols_kernel<1><<<grid, 256, 0, s>>>(g, y, seg, El, H, tok_local, w_local, weight_scaling, dropout_p,
-                                                   seed, d, dw, dy_colsum_part);
+                                                   drop_stream, d, dw, dy_colsum_part);
       else if (cpw == 2)
         bwd_dy_cols_kernel<2><<<grid, 256, 0, s>>>(g, y, seg, El, H, tok_local, w_local, weight_scaling, dropout_p,
-                                                   seed, d, dw, dy_colsum_part);
+                                                   drop_stream, d, dw, dy_colsum_part);
       else
         bwd_dy_cols_kernel<4><<<grid, 256, 0, s>>>(g, y, seg, El, H, tok_local, w_local, weight_scaling, dropout_p,
-                                                   seed, d, dw, dy_colsum_part);
+                                                   drop_stream, d, dw, dy_colsum_part);
       return check_launch("bwd_dy_cols_kernel");
     }
     bwd_dy_block_kernel<<<num_sms() * 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(
         static_cast<const __nv_bfloat16*>(dOut), static_cast<const __nv_bfloat16*>(Y), seg, El, H, tok_local,
-        w_local, weight_scaling, dropout_p, seed, static_cast<__nv_bfloat16*>(dY), dw, dy_colsum_part);
+        w_local, weight_scaling, dropout_p, drop_stream, static_cast<__nv_bfloat16*>(dY), dw, dy_colsum_part);
     return check_launch("bwd_dy_block_kernel");
   }
   PPMOE_REQUIRE(dtype == kBF16 || dtype == kF32, "bad dtype");
@@ -1241,11 +1277,11 @@ int ppmoe_bwd_dy(int dtype, const void* dOut, const void* Y, const int* seg, int
   if (dtype == kBF16)
     bwd_dy_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(dOut),
                                                       static_cast<const __nv_bfloat16*>(Y), seg, El, H, tok_local,
-                                                      w_local, weight_scaling, dropout_p, seed,
+                                                      w_local, weight_scaling, dropout_p, drop_stream,
                                                       static_cast<__nv_bfloat16*>(dY), dw);
   else
     bwd_dy_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(dOut), static_cast<const float*>(Y), seg, El, H,
-                                              tok_local, w_local, weight_scaling, dropout_p, seed,
+                                              tok_local, w_local, weight_scaling, dropout_p, drop_stream,
                                               static_cast<float*>(dY), dw);
   return check_launch("bwd_dy_kernel");
 }

@@ -190,7 +190,7 @@ struct EpiFc2Fwd {
   float* out_acc;  // [N*H] fp32, zero-initialised
   int cs;
   float drop_p;             // inverted dropout on the expert output (tensor.py:315-330)
-  unsigned long long seed;
+  const unsigned long long* drop;  // the reference's Philox dropout stream (common.cuh), or null
   // Owner mode (NVLink exchange): the weighted row goes straight into the fp32 accumulator
   // of the rank owning the token (owner_acc = device table of T peer pointers, each
   // [owner_rows x H]), over NVLink, tile by tile while the GEMM runs.
@@ -215,8 +215,9 @@ struct EpiFc2Fwd {
     for (int j = 0; j < 32; ++j) x[j] = v[j] + b[j];
     if (drop_p > 0.f) {
       const float inv = 1.f / (1.f - drop_p);
+      const uint32_t kb = drop_keep_bits<32>(drop, drop_row_draw(drop, seg, g, row, H) + n0);
 #pragma unroll
-      for (int j = 0; j < 32; ++j) x[j] = dropout_uniform(seed, row, n0 + j) >= drop_p ? x[j] * inv : 0.f;
+      for (int j = 0; j < 32; ++j) x[j] = ((kb >> j) & 1u) ? x[j] * inv : 0.f;
     }
   }
   __device__ __forceinline__ T* stage_dst(int g, int m, int row, int n0, int which) const {
@@ -236,9 +237,11 @@ struct EpiFc2Fwd {
 #pragma unroll
     for (int j = 0; j < W; ++j) x[j] = v[j] + b[j];
     if (drop_p > 0.f) {
+      static_assert(W <= 32, "dropout keep bits cover at most 32 columns");
       const float inv = 1.f / (1.f - drop_p);
+      const uint32_t kb = drop_keep_bits<W>(drop, drop_row_draw(drop, seg, g, row, H) + n0);
 #pragma unroll
-      for (int j = 0; j < W; ++j) x[j] = dropout_uniform(seed, row, n0 + j) >= drop_p ? x[j] * inv : 0.f;
+      for (int j = 0; j < W; ++j) x[j] = ((kb >> j) & 1u) ? x[j] * inv : 0.f;
     }
     store_row<T, W>(y + static_cast<size_t>(row) * H + n0, x, valid, cs);
     if (y2) store_row<T, W>(y2 + static_cast<size_t>(row) * H + n0, x, valid, 0);

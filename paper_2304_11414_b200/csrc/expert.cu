@@ -256,12 +256,13 @@ static GroupGeom geom(int G, int N, int M_fixed, int K_fixed, const int* seg, in
 
 static int fc2_fwd_impl(int dtype, const void* Act, const void* down, const void* bias_down, const int* seg, int El,
                         int H, int F, int rows_cap, const int* row_lo, const int* row_hi, const int* tok_local,
-                        const float* w_local, int weight_scaling, float dropout_p, unsigned long long seed, void* Y,
-                        void* Y2, float* out_acc, float* const* owner_acc, int owner_rows, void* const* owner_slots,
+                        const float* w_local, int weight_scaling, float dropout_p, const unsigned long long* drop,
+                        void* Y, void* Y2, float* out_acc, float* const* owner_acc, int owner_rows, void* const* owner_slots,
                         const int* pair_pos, int K, void* stream) {
   if (int rc = check_common(dtype, El, H, F, rows_cap)) return rc;
   PPMOE_REQUIRE((row_lo == nullptr) == (row_hi == nullptr), "row_lo and row_hi must both be given or both be NULL");
   PPMOE_REQUIRE(dropout_p >= 0.f && dropout_p < 1.f, "dropout probability must be in [0, 1), got %g", dropout_p);
+  PPMOE_REQUIRE(dropout_p == 0.f || drop, "dropout needs its stream descriptor (ppmoe_dropout_stream)");
   PPMOE_REQUIRE(!(out_acc && owner_acc), "give at most one of out_acc / owner_acc");
   PPMOE_REQUIRE(!owner_acc || owner_rows >= 1, "owner_acc needs owner_rows >= 1");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -276,13 +277,13 @@ static int fc2_fwd_impl(int dtype, const void* Act, const void* down, const void
     if (int rc = tmap_kmajor(&ta, Act, F, rows_cap, kBM)) return rc;
     if (int rc = tmap_mnmajor(&tb, down, H, static_cast<uint64_t>(El) * F)) return rc;
     EpiFc2Fwd<bf16> epi{static_cast<bf16*>(Y), static_cast<bf16*>(Y2), static_cast<const bf16*>(bias_down), H, seg,
-                        tok_local, w_local, weight_scaling, out_acc, stream_stores(), dropout_p, seed, owner_acc,
+                        tok_local, w_local, weight_scaling, out_acc, stream_stores(), dropout_p, drop, owner_acc,
                         owner_rows, reinterpret_cast<bf16* const*>(owner_slots), pair_pos, K};
     return launch_tc<false, true>(ta, tb, geo, epi, s);
   }
   PPMOE_REQUIRE(!owner_slots, "owner slots are a bf16 path");
   EpiFc2Fwd<float> epi{static_cast<float*>(Y), static_cast<float*>(Y2), static_cast<const float*>(bias_down), H, seg,
-                       tok_local, w_local, weight_scaling, out_acc, 0, dropout_p, seed, owner_acc, owner_rows,
+                       tok_local, w_local, weight_scaling, out_acc, 0, dropout_p, drop, owner_acc, owner_rows,
                        nullptr, nullptr, 0};
   return launch_simt<float, false, true>(static_cast<const float*>(Act), F, static_cast<const float*>(down), H, geo,
                                          rows_cap, epi, s);
@@ -325,21 +326,21 @@ int ppmoe_expert_fc1_fwd(int dtype, const void* Xs, const void* up, const void* 
 
 int ppmoe_expert_fc2_fwd(int dtype, const void* Act, const void* down, const void* bias_down, const int* seg, int El,
                          int H, int F, int rows_cap, const int* row_lo, const int* row_hi, const int* tok_local,
-                         const float* w_local, int weight_scaling, float dropout_p, unsigned long long seed,
+                         const float* w_local, int weight_scaling, float dropout_p, const unsigned long long* drop_stream,
                          void* Y, void* Y2, float* out_acc, void* stream) {
   return fc2_fwd_impl(dtype, Act, down, bias_down, seg, El, H, F, rows_cap, row_lo, row_hi, tok_local, w_local,
-                      weight_scaling, dropout_p, seed, Y, Y2, out_acc, nullptr, 0, nullptr, nullptr, 0, stream);
+                      weight_scaling, dropout_p, drop_stream, Y, Y2, out_acc, nullptr, 0, nullptr, nullptr, 0, stream);
 }
 
 int ppmoe_expert_fc2_fwd_owner(int dtype, const void* Act, const void* down, const void* bias_down, const int* seg,
                                int El, int H, int F, int rows_cap, const int* tok_local, const float* w_local,
-                               int weight_scaling, float dropout_p, unsigned long long seed, void* Y,
+                               int weight_scaling, float dropout_p, const unsigned long long* drop_stream, void* Y,
                                float* const* owner_acc, void* const* owner_slots, const int* pair_pos, int K,
                                int owner_rows, void* stream) {
   PPMOE_REQUIRE((owner_acc != nullptr) != (owner_slots != nullptr), "give exactly one of owner_acc / owner_slots");
   PPMOE_REQUIRE(!owner_slots || (pair_pos && K >= 1 && K <= 2), "owner slots need pair_pos and k <= 2");
   return fc2_fwd_impl(dtype, Act, down, bias_down, seg, El, H, F, rows_cap, nullptr, nullptr, tok_local, w_local,
-                      weight_scaling, dropout_p, seed, Y, nullptr, nullptr, owner_acc, owner_rows, owner_slots,
+                      weight_scaling, dropout_p, drop_stream, Y, nullptr, nullptr, owner_acc, owner_rows, owner_slots,
                       pair_pos, K, stream);
 }
 

@@ -141,7 +141,7 @@ __device__ __forceinline__ void route_tail(double* lg, double* stat, int t0, int
     stat[2 * tid + 1] = s;
   }
   __syncthreads();
-  for (int i = tid; i < kRouteTB * E; i += kRouteThreads) {
+  for (int i = tid; i < kRouteTB * E; i += blockDim.x) {
     const int tl = i / E, e = i % E;
     const double sc = exp(lg[i] - stat[2 * tl]) / stat[2 * tl + 1];
     lg[i] = sc;
@@ -171,7 +171,7 @@ __device__ __forceinline__ void route_tail(double* lg, double* stat, int t0, int
     }
   }
   // per-block expert score sums in token order (deterministic aux-loss reduction)
-  for (int e = tid; e < E; e += kRouteThreads) {
+  for (int e = tid; e < E; e += blockDim.x) {
     double s = 0.0;
     for (int r = 0; r < kRouteTB && t0 + r < N; ++r) s += lg[r * E + e];
     ssum[static_cast<size_t>(blockIdx.x) * E + e] = s;
@@ -328,17 +328,32 @@ __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
 // c0 + 8q + j, so a lane's A values for all 8 steps come from ONE 16-byte load of its token
 // row (x[t][c0+8q .. c0+8q+7]) and its B values are Wg[c0+8q+j][n] (L1-resident).
 // FP64 FMA work moves from 2 DFMA warp-instructions per 64 FMAs to one DMMA per 256.
-template <int EB>
-__global__ void __launch_bounds__(kRouteThreads) router_dmma_kernel(const __nv_bfloat16* __restrict__ X,
-                                                                    const float* __restrict__ Wg, int N, int H, int E,
-                                                                    int K, const int* __restrict__ ovr,
-                                                                    int* __restrict__ idx, float* __restrict__ w,
-                                                                    float* __restrict__ scores,
-                                                                    double* __restrict__ ssum,
-                                                                    int* __restrict__ cnt_top1) {
+// Exact bf16 -> fp64 of the 16-bit pattern b (normal numbers and zero; the caller routes
+// subnormal / inf / nan groups through the F2F path).
+__device__ __forceinline__ double bf16_fast_f64(uint32_t b) {
+  const uint32_t m = b & 0x7FFFu;
+  const uint32_t mag = m ? (m << 13) + 0x38000000u : 0u;
+  return __hiloint2double(static_cast<int>(((b & 0x8000u) << 16) | mag), 0);
+}
+__device__ __forceinline__ bool bf16x8_special(const uint4& u) {
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+  uint32_t sp = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t lo = w[i] & 0x7FFFu, hi = (w[i] >> 16) & 0x7FFFu;
+    sp |= (lo - 1u < 0x7Fu) | (lo >= 0x7F80u) | (hi - 1u < 0x7Fu) | (hi >= 0x7F80u);
+  }
+  return sp != 0;
+}
+
+template <int EB, int W, int MINB>
+__global__ void __launch_bounds__(32 * W, MINB) router_dmma_kernel(const __nv_bfloat16* __restrict__ X,
+                                                             const float* __restrict__ Wg, int N, int H, int E, int K,
+                                                             const int* __restrict__ ovr, int* __restrict__ idx,
+                                                             float* __restrict__ w, float* __restrict__ scores,
+                                                             double* __restrict__ ssum, int* __restrict__ cnt_top1) {
   constexpr int NT = EB / 8;
   constexpr int G = kRouteTB / 8;
-  constexpr int W = kRouteThreads / 32;
   extern __shared__ __align__(16) unsigned char sm[];
   double* part = reinterpret_cast<double*>(sm);  // [W][G][NT][32][2]
   double* lg = part + W * G * NT * 64;           // [TB][E]
@@ -348,27 +363,27 @@ __global__ void __launch_bounds__(kRouteThreads) router_dmma_kernel(const __nv_b
   const int t0 = blockIdx.x * kRouteTB;
   const int span = H / W;  // columns per warp (H % (32 W) == 0)
   const int cw0 = warp * span;
-  const __nv_bfloat16* xr[G];
-  bool ok[G];
-#pragma unroll
-  for (int gi = 0; gi < G; ++gi) {
-    const int t = t0 + gi * 8 + g;
-    ok[gi] = t < N;
-    xr[gi] = X + static_cast<size_t>(ok[gi] ? t : 0) * H + 8 * q;
-  }
   double acc[G][NT][2];
 #pragma unroll
   for (int gi = 0; gi < G; ++gi)
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) acc[gi][nt][0] = acc[gi][nt][1] = 0.0;
+  const size_t xoff = static_cast<size_t>(8 * q);
+  auto row_ptr = [&](int gi) {
+    const int t = t0 + gi * 8 + g;
+    return X + static_cast<size_t>(t < N ? t : 0) * H + xoff;
+  };
+  auto load_x = [&](int gi, int c) {
+    return t0 + gi * 8 + g < N ? ldg16(row_ptr(gi) + c) : make_uint4(0, 0, 0, 0);
+  };
   uint4 xa[G];
 #pragma unroll
-  for (int gi = 0; gi < G; ++gi) xa[gi] = ok[gi] ? ldg16(xr[gi] + cw0) : make_uint4(0, 0, 0, 0);
+  for (int gi = 0; gi < G; ++gi) xa[gi] = load_x(gi, cw0);
   for (int c0 = cw0; c0 < cw0 + span; c0 += 32) {
     uint4 xn[G];
     const bool more = c0 + 32 < cw0 + span;
 #pragma unroll
-    for (int gi = 0; gi < G; ++gi) xn[gi] = (more && ok[gi]) ? ldg16(xr[gi] + c0 + 32) : make_uint4(0, 0, 0, 0);
+    for (int gi = 0; gi < G; ++gi) xn[gi] = more ? load_x(gi, c0 + 32) : make_uint4(0, 0, 0, 0);
     double b[NT][8];
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
@@ -377,14 +392,22 @@ __global__ void __launch_bounds__(kRouteThreads) router_dmma_kernel(const __nv_b
       for (int j = 0; j < 8; ++j)
         b[nt][j] = e < E ? static_cast<double>(__ldg(Wg + static_cast<size_t>(c0 + 8 * q + j) * E + e)) : 0.0;
     }
+    bool sp = false;
 #pragma unroll
-    for (int gi = 0; gi < G; ++gi) {
-      double a[8];
-      widen8<__nv_bfloat16>(&xa[gi], a);
+    for (int gi = 0; gi < G; ++gi) sp |= bf16x8_special(xa[gi]);
+    const bool slow = __any_sync(0xffffffffu, sp);  // warp-uniform: subnormal/inf/nan take F2F
+    // k-step j outermost: the G*NT accumulator chains are independent, so consecutive DMMAs
+    // never wait on each other's result
 #pragma unroll
-      for (int j = 0; j < 8; ++j)
+    for (int j = 0; j < 8; ++j) {
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) dmma884(acc[gi][nt], a[j], b[nt][j]);
+      for (int gi = 0; gi < G; ++gi) {
+        const uint32_t word = j < 2 ? xa[gi].x : j < 4 ? xa[gi].y : j < 6 ? xa[gi].z : xa[gi].w;
+        const uint32_t bits = (j & 1) ? (word >> 16) : (word & 0xFFFFu);
+        const double a = slow ? static_cast<double>(__uint_as_float(bits << 16)) : bf16_fast_f64(bits);
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) dmma884(acc[gi][nt], a, b[nt][j]);
+      }
     }
 #pragma unroll
     for (int gi = 0; gi < G; ++gi) xa[gi] = xn[gi];
@@ -398,7 +421,7 @@ __global__ void __launch_bounds__(kRouteThreads) router_dmma_kernel(const __nv_b
       p[1] = acc[gi][nt][1];
     }
   __syncthreads();
-  for (int o = threadIdx.x; o < kRouteTB * E; o += kRouteThreads) {  // split-K sum, warp order
+  for (int o = threadIdx.x; o < kRouteTB * E; o += blockDim.x) {  // split-K sum, warp order
     const int tl = o / E, e = o % E;
     const int gi = tl >> 3, ln = (tl & 7) * 4 + ((e & 7) >> 1), nt = e >> 3, i = e & 1;
     double v = 0.0;
@@ -409,9 +432,11 @@ __global__ void __launch_bounds__(kRouteThreads) router_dmma_kernel(const __nv_b
   route_tail(lg, stat, t0, N, E, K, ovr, idx, w, scores, ssum, cnt_top1);
 }
 
-__host__ inline size_t route_dmma_smem_bytes(int E) {
+constexpr int kRouteDmmaMaxWarps = 8;  // warps per 32-token block (hidden-dimension split)
+
+__host__ inline size_t route_dmma_smem_bytes(int E, int W) {
   const int NT = E <= 8 ? 1 : 2;
-  return static_cast<size_t>(kRouteThreads / 32) * (kRouteTB / 8) * NT * 64 * 8 + static_cast<size_t>(kRouteTB) * E * 8 +
+  return static_cast<size_t>(W) * (kRouteTB / 8) * NT * 64 * 8 + static_cast<size_t>(kRouteTB) * E * 8 +
          2 * kRouteTB * 8;
 }
 
@@ -660,19 +685,35 @@ static int launch_router(const void* X, const float* Wg, int N, int H, int E, in
 static bool use_dmma_router(int dtype, int H, int E) {
   const char* e = std::getenv("PPMOE_ROUTER");  // PPMOE_ROUTER=dfma: the CUDA-core fp64 kernel (A/B)
   if (e && std::strcmp(e, "dfma") == 0) return false;
-  return dtype == kBF16 && H % (32 * (kRouteThreads / 32)) == 0 && E <= 16;
+  return dtype == kBF16 && H % (32 * kRouteDmmaMaxWarps) == 0 && E <= 16;
+}
+
+// (warps per block, min blocks per SM) of the DMMA router; PPMOE_ROUTER_CFG=0..3 for A/B runs
+static int router_cfg() {
+  const char* e = std::getenv("PPMOE_ROUTER_CFG");
+  return e ? std::atoi(e) : 0;
+}
+
+template <int EB, int W, int MINB>
+static int launch_router_dmma_cfg(const void* X, const float* Wg, int N, int H, int E, int K, const int* ovr, int* idx,
+                                  float* w, float* scores, double* ssum, int* cnt, cudaStream_t s) {
+  const size_t smem = route_dmma_smem_bytes(E, W);
+  auto k = router_dmma_kernel<EB, W, MINB>;
+  PPMOE_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  const int nb = (N + kRouteTB - 1) / kRouteTB;
+  k<<<nb, 32 * W, smem, s>>>(static_cast<const __nv_bfloat16*>(X), Wg, N, H, E, K, ovr, idx, w, scores, ssum, cnt);
+  return check_launch("router_dmma_kernel");
 }
 
 template <int EB>
 static int launch_router_dmma(const void* X, const float* Wg, int N, int H, int E, int K, const int* ovr, int* idx,
                               float* w, float* scores, double* ssum, int* cnt, cudaStream_t s) {
-  const size_t smem = route_dmma_smem_bytes(E);
-  auto k = router_dmma_kernel<EB>;
-  PPMOE_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  const int nb = (N + kRouteTB - 1) / kRouteTB;
-  k<<<nb, kRouteThreads, smem, s>>>(static_cast<const __nv_bfloat16*>(X), Wg, N, H, E, K, ovr, idx, w, scores, ssum,
-                                     cnt);
-  return check_launch("router_dmma_kernel");
+  switch (router_cfg()) {
+    case 1: return launch_router_dmma_cfg<EB, 8, 3>(X, Wg, N, H, E, K, ovr, idx, w, scores, ssum, cnt, s);
+    case 2: return launch_router_dmma_cfg<EB, 4, 4>(X, Wg, N, H, E, K, ovr, idx, w, scores, ssum, cnt, s);
+    case 3: return launch_router_dmma_cfg<EB, 4, 6>(X, Wg, N, H, E, K, ovr, idx, w, scores, ssum, cnt, s);
+    default: return launch_router_dmma_cfg<EB, 8, 2>(X, Wg, N, H, E, K, ovr, idx, w, scores, ssum, cnt, s);
+  }
 }
 
 }  // namespace ppmoe

@@ -40,7 +40,7 @@ class _A2ASpec:
     weight_scaling: bool
     override: torch.Tensor | None
     dropout_p: float = 0.0
-    seed: int = 0
+    drop: object = None  # moe.DropoutStream
 
 
 def _a2a(world: World, group: ProcessGroup, out: torch.Tensor, inp: torch.Tensor, out_splits, in_splits,
@@ -106,8 +106,17 @@ class _DPMoEFunction(torch.autograd.Function):
         # bf16 outputs in the owner layout and a row permutation puts them in receive order
         rows_cap_o = n_recv + 128 * el
         seg_o, rmap = _ops.owner_layout(recv_counts, t, el, rows_cap_o)
+        desc = None
+        if spec.drop is not None:
+            # the reference draws each expert's [rows received from all sources, h] block in
+            # ascending expert id (moe.py:443-448): offsets from the global per-expert counts
+            kept_all = pl.kept.clone()
+            if t > 1:
+                dist.all_reduce(kept_all, group=spec.world.torch_group(spec.group))
+            desc = spec.drop.descriptor(kept_all, e, spec.me * el, el, h)
+            spec.drop.advance(h * int(kept_all.sum()))
         st = _ops.expert_pipeline(xrecv, seg_o, el, rmap, None, rows_cap_o, up, down, bias_up, bias_down, False, None,
-                                  spec.dropout_p, spec.seed)
+                                  spec.dropout_p, desc)
         yret = _ops._act((max(n_recv, 1), h), hidden.dtype, dev)
         _ops.permute_rows(st.y, rows_cap_o, rmap, yret)
         yback = yret if solo else torch.empty((max(n_send, 1), h), dtype=hidden.dtype, device=dev)
@@ -176,7 +185,7 @@ def dpmoe_forward(world: World, ep_group: ProcessGroup, hidden_per_rank, gate, *
     list whose own entry is used); returns (out, l_aux) of this rank.  A single-rank world
     runs the same path without communication.
     """
-    from .moe import ExpertBank, _bank_of, _dropout_seed, _override_tensor
+    from .moe import ExpertBank, _bank_of, DropoutStream, _override_tensor
 
     dp = ep_group.size
     if world.distributed:
@@ -194,7 +203,7 @@ def dpmoe_forward(world: World, ep_group: ProcessGroup, hidden_per_rank, gate, *
         hidden = hidden_per_rank
     if len(experts_by_rank) != dp:
         raise ValueError(f"need hidden and experts for each of {dp} ranks")
-    seed = _dropout_seed(dropout_p, rng)
+    drop = DropoutStream.of(dropout_p, rng)
     local: ExpertBank = _bank_of(experts_by_rank[me])
     num_experts = gate.num_experts
     if local.count * dp != num_experts:
@@ -205,7 +214,7 @@ def dpmoe_forward(world: World, ep_group: ProcessGroup, hidden_per_rank, gate, *
                               len(route_overrides) == dp else route_overrides,
                               hidden.shape[0], top_k, num_experts, hidden.device)
     spec = _A2ASpec(world, ep_group, me, dp, local.count, top_k, float(capacity_factor), bool(weight_scaling), ov,
-                    float(dropout_p), seed)
+                    float(dropout_p), drop)
     wg = gate.wg if gate.wg.dtype == torch.float32 else gate.wg.float()
     return _DPMoEFunction.apply(hidden.contiguous(), wg, local.up.contiguous(), local.down.contiguous(),
                                 None if local.bias_up is None else local.bias_up.contiguous(),

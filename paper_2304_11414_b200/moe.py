@@ -460,8 +460,9 @@ class _Spec:
     aux_here: bool
     fwd_chunks: int = 1
     dropout_p: float = 0.0
-    seed: int = 0
+    drop: "DropoutStream | None" = None
     sliced_router: bool = False
+    route: object = None  # the forward's routing (for check_replicas)
 
 
 class _PPMoEFunction(torch.autograd.Function):
@@ -478,8 +479,14 @@ class _PPMoEFunction(torch.autograd.Function):
             rt = _ops.route_sliced(spec.world, spec.group, hidden, wg, spec.k, spec.override)
         else:
             rt = _ops.route(hidden, wg, spec.k, spec.override)
+        spec.route = (rt, None)
         cap = _ops.capacity_for(spec.capacity_factor, n, spec.k, e)
         pl = _ops.plan(rt.idx, rt.w, e, cap)
+        spec.route = (rt, pl)
+        desc = None
+        if spec.drop is not None:  # the reference's per-expert dropout draws (moe.py:301, tensor.py:315-330)
+            desc = spec.drop.descriptor(pl.kept, e, spec.e0, spec.el, h)
+            spec.drop.advance(h * int(pl.kept.sum()))
         if spec.fwd_chunks > 1:
             out_acc = torch.zeros((n, h), dtype=torch.float32, device=hidden.device)
             # combine all-reduce pipelined by token chunk: chunk c goes on the wire while the
@@ -496,7 +503,7 @@ class _PPMoEFunction(torch.autograd.Function):
 
             st = _ops.experts_forward(hidden, pl, spec.e0, spec.el, up, down, bias_up, bias_down, spec.k,
                                       spec.weight_scaling, out_acc, spec.fwd_chunks, on_chunk, spec.dropout_p,
-                                      spec.seed)
+                                      desc)
             spec.world.charge_all_reduce(spec.group, out.numel())
             for wk in works:
                 if wk is not None:
@@ -513,7 +520,7 @@ class _PPMoEFunction(torch.autograd.Function):
                 # (plain P2P stores, tile by tile during the GEMM); owners sum, then all-gather
                 table, rows = nvlink.owner_slots(ar, n, spec.k, h)
                 st = _ops.experts_forward(hidden, pl, spec.e0, spec.el, up, down, bias_up, bias_down, spec.k,
-                                          spec.weight_scaling, None, drop_p=spec.dropout_p, seed=spec.seed,
+                                          spec.weight_scaling, None, drop_p=spec.dropout_p, drop=desc,
                                           owner_slots=table, owner_rows=rows)
                 out = nvlink.finish_slots_forward(ar, n, spec.k, h, pl.pair_pos, torch.empty_like(hidden))
             elif mode == "fused":
@@ -521,7 +528,7 @@ class _PPMoEFunction(torch.autograd.Function):
                 # over NVLink, tile by tile during the GEMM; owners cast, then all-gather
                 table, rows = nvlink.owner_accumulator(ar, n, h)
                 st = _ops.experts_forward(hidden, pl, spec.e0, spec.el, up, down, bias_up, bias_down, spec.k,
-                                          spec.weight_scaling, None, drop_p=spec.dropout_p, seed=spec.seed,
+                                          spec.weight_scaling, None, drop_p=spec.dropout_p, drop=desc,
                                           owner_table=table, owner_rows=rows)
                 out = nvlink.finish_fused_forward(ar, n, h, torch.empty_like(hidden))
             elif nvlink.forward_chunks(ar, n) > 1:
@@ -541,13 +548,13 @@ class _PPMoEFunction(torch.autograd.Function):
                                               out)
 
                 st = _ops.experts_forward(hidden, pl, spec.e0, spec.el, up, down, bias_up, bias_down, spec.k,
-                                          spec.weight_scaling, None, chunks, on_chunk, spec.dropout_p, spec.seed,
+                                          spec.weight_scaling, None, chunks, on_chunk, spec.dropout_p, desc,
                                           y_mirror=ym)
                 main.wait_stream(side)
             else:
                 ym = ar.tensor("y", (_ops.local_rows_cap(n, spec.k, spec.el, cap), h), hidden.dtype)
                 st = _ops.experts_forward(hidden, pl, spec.e0, spec.el, up, down, bias_up, bias_down, spec.k,
-                                          spec.weight_scaling, None, drop_p=spec.dropout_p, seed=spec.seed,
+                                          spec.weight_scaling, None, drop_p=spec.dropout_p, drop=desc,
                                           y_mirror=ym)
                 out = nvlink.exchange(ar, "y", pl.seg, spec.el, rt.idx, pl.pair_pos,
                                       rt.w if spec.weight_scaling else None, n, h, torch.empty_like(hidden))
@@ -555,20 +562,20 @@ class _PPMoEFunction(torch.autograd.Function):
         elif spec.el == e and _ops.combine_mode(hidden.dtype, h) == "owner":
             # all experts local: fc2 stores Y, the owner-gather kernel sums every token's rows
             st = _ops.experts_forward(hidden, pl, spec.e0, spec.el, up, down, bias_up, bias_down, spec.k,
-                                      spec.weight_scaling, None, drop_p=spec.dropout_p, seed=spec.seed)
+                                      spec.weight_scaling, None, drop_p=spec.dropout_p, drop=desc)
             out = _ops.local_combine(st.y, st, pl, rt.idx, rt.w if spec.weight_scaling else None,
                                      torch.empty_like(hidden))
             spec.world.all_reduce_(spec.group, out)  # a group of one: ledger only (moe.py:307)
         elif _ops.combine_mode(hidden.dtype, h) != "scatter":
             # fc2 stores Y; the combine gathers each token's local pairs (no fp32 accumulator)
             st = _ops.experts_forward(hidden, pl, spec.e0, spec.el, up, down, bias_up, bias_down, spec.k,
-                                      spec.weight_scaling, None, drop_p=spec.dropout_p, seed=spec.seed)
+                                      spec.weight_scaling, None, drop_p=spec.dropout_p, drop=desc)
             out = _ops.combine(st.y, st, pl, rt.w if spec.weight_scaling else None, torch.empty_like(hidden))
             spec.world.all_reduce_(spec.group, out)  # reduce_from_tensor_parallel_region (moe.py:307)
         else:
             out_acc = torch.zeros((n, h), dtype=torch.float32, device=hidden.device)
             st = _ops.experts_forward(hidden, pl, spec.e0, spec.el, up, down, bias_up, bias_down, spec.k,
-                                      spec.weight_scaling, out_acc, drop_p=spec.dropout_p, seed=spec.seed)
+                                      spec.weight_scaling, out_acc, drop_p=spec.dropout_p, drop=desc)
             out = _ops.cast_out(out_acc, hidden.dtype)
             del out_acc
             spec.world.all_reduce_(spec.group, out)  # reduce_from_tensor_parallel_region (moe.py:307)
@@ -661,16 +668,44 @@ class _PPMoEFunction(torch.autograd.Function):
         return dx, dwg, d_up, d_down, d_bu, d_bd, None
 
 
-def _dropout_seed(dropout_p: float, rng) -> int:
-    """Validate dropout arguments like tensor.dropout (tensor.py:315-322) and draw the mask
-    seed from the caller's Rng (every rank of a TP group draws the same value)."""
-    if not 0.0 <= dropout_p < 1.0:
-        raise ValueError(f"dropout probability must be in [0, 1), got {dropout_p}")
-    if dropout_p == 0.0:
-        return 0
-    if rng is None:
-        raise ValueError("dropout with p > 0 requires an rng")
-    return int(rng.integers(0, 2**62, 1)[0])
+class DropoutStream:
+    """The reference's expert dropout draws (tensor.dropout, tensor.py:315-330, called in
+    ExpertFfn.forward for every expert with rows, ascending id, moe.py:294-301): expert e
+    consumes one uniform [rows_e, h] block of the caller's Rng (numpy Philox4x64-10), and an
+    element survives iff its uniform >= p.  The device regenerates exactly those draws
+    (csrc/common.cuh) from the stream's key and position, so masks equal the reference's
+    and the caller's Rng ends where the reference leaves it.  Every rank of a TP group holds
+    the same Rng state and routing, so its experts' draws are the simulated reference's."""
+
+    def __init__(self, p: float, rng):
+        from .rng import stream_position
+
+        gen = getattr(rng, "_gen", None)
+        if not isinstance(gen, np.random.Generator):
+            raise ValueError("dropout with p > 0 needs a Philox-backed Rng (moesim's Rng)")
+        self.p, self.gen = float(p), gen
+        self.key0, self.key1, self.first = stream_position(gen)
+        self.threshold = int(math.ceil(self.p * 2.0 ** 53))  # (word >> 11) >= ceil(p 2^53) <=> uniform >= p
+
+    @classmethod
+    def of(cls, dropout_p: float, rng) -> "DropoutStream | None":
+        """Validate like tensor.dropout (tensor.py:315-322); None when p == 0."""
+        if not 0.0 <= dropout_p < 1.0:
+            raise ValueError(f"dropout probability must be in [0, 1), got {dropout_p}")
+        if dropout_p == 0.0:
+            return None
+        if rng is None:
+            raise ValueError("dropout with p > 0 requires an rng")
+        return cls(dropout_p, rng)
+
+    def descriptor(self, kept: torch.Tensor, num_experts: int, e0: int, el: int, h: int) -> torch.Tensor:
+        return _ops.dropout_descriptor(kept, num_experts, e0, el, h, self.key0, self.key1, self.threshold, self.first)
+
+    def advance(self, draws: int) -> None:
+        """The caller's Rng moves past the layer's draws (host-visible kept counts: one sync)."""
+        from .rng import set_stream_position
+
+        set_stream_position(self.gen, self.first + draws)
 
 
 def _as_single(value, what: str):
@@ -707,7 +742,7 @@ def ppmoe_forward(world: World, group: ProcessGroup, hidden, gate, experts_by_ra
     tp = group.size
     if len(experts_by_rank) != tp:
         raise ValueError(f"need one expert list per rank: {len(experts_by_rank)} for group of {tp}")
-    seed = _dropout_seed(dropout_p, rng)
+    drop = DropoutStream.of(dropout_p, rng)
     num_experts = gate.num_experts
     if not 1 <= top_k <= num_experts:
         raise ValueError(f"top_k must be in [1, {num_experts}], got {top_k}")
@@ -743,27 +778,45 @@ def ppmoe_forward(world: World, group: ProcessGroup, hidden, gate, experts_by_ra
     sliced = (world.distributed and tp > 1 and hidden.shape[0] % tp == 0
               and os.environ.get("PPMOE_SLICED_ROUTER", "1") != "0")
     spec = _Spec(world, group, top_k, float(capacity_factor), bool(weight_scaling), ov, e0, el, aux_here, chunks,
-                 float(dropout_p), seed, sliced)
+                 float(dropout_p), drop, sliced)
     wg = gate.wg if gate.wg.dtype == torch.float32 else gate.wg.float()
     out, l_aux = _PPMoEFunction.apply(hidden.contiguous(), wg, local.up.contiguous(), local.down.contiguous(),
                                       None if local.bias_up is None else local.bias_up.contiguous(),
                                       None if local.bias_down is None else local.bias_down.contiguous(), spec)
     if check_replicas and world.distributed and tp > 1:
-        _check_dispatch_agreement(world, group, hidden)
+        _check_dispatch_agreement(world, group, hidden, *spec.route)
     return out, l_aux
 
 
-def _check_dispatch_agreement(world: World, group: ProcessGroup, hidden: torch.Tensor) -> None:
-    """Debug-mode replacement of the reference's replica comparison (moe.py:289-291)."""
+def _check_dispatch_agreement(world: World, group: ProcessGroup, hidden: torch.Tensor, route=None,
+                              plan=None) -> None:
+    """Debug-mode replacement of the reference's replica checks (moe.py:289-291): every rank
+    of the group must hold the same hidden activation AND the same dispatch (routing indices,
+    per-expert kept counts): an int64 position-weighted hash of the indices plus the counts
+    are compared across ranks with MIN/MAX all-reduces."""
     import torch.distributed as dist
 
+    pg = world.torch_group(group)
     sig = torch.stack([hidden.float().sum(), (hidden.float() * torch.arange(1, hidden.shape[1] + 1,
                                                                              device=hidden.device)).sum()])
     lo, hi = sig.clone(), sig.clone()
-    dist.all_reduce(lo, op=dist.ReduceOp.MIN, group=world.torch_group(group))
-    dist.all_reduce(hi, op=dist.ReduceOp.MAX, group=world.torch_group(group))
+    dist.all_reduce(lo, op=dist.ReduceOp.MIN, group=pg)
+    dist.all_reduce(hi, op=dist.ReduceOp.MAX, group=pg)
     if not torch.equal(lo, hi):
         raise ValueError("TP replica divergence: hidden activation differs across ranks")
+    if route is None:
+        return
+    idx = route.idx.long().reshape(-1)
+    pos = torch.arange(1, idx.numel() + 1, device=idx.device, dtype=torch.int64)
+    parts = [(idx * pos).sum().reshape(1), (idx * idx * (pos % 1009)).sum().reshape(1)]
+    if plan is not None:
+        parts.append(plan.kept.long())
+    dig = torch.cat(parts)
+    lo, hi = dig.clone(), dig.clone()
+    dist.all_reduce(lo, op=dist.ReduceOp.MIN, group=pg)
+    dist.all_reduce(hi, op=dist.ReduceOp.MAX, group=pg)
+    if not torch.equal(lo, hi):
+        raise ValueError("TP replica divergence: dispatch order differs across ranks")
 
 
 def sync_gate_gradients(world: World, group: ProcessGroup, gate: GateParams) -> None:
@@ -798,6 +851,7 @@ class PPMoELayer(torch.nn.Module):
                 weights = MoeLayerWeights.init(cfg.hidden, cfg.experts, Rng(cfg.seed), dtype=dtype, device=device,
                                                experts=block)
         self.weights = weights
+        self.rng = Rng(cfg.seed, 5)  # the dropout stream the reference's CLI uses (cli.py:137)
         for name, p in zip(("wg", "up", "down", "bias_up", "bias_down"),
                            (weights.gate.wg, weights.bank.up, weights.bank.down, weights.bank.bias_up,
                             weights.bank.bias_down)):
@@ -818,6 +872,7 @@ class PPMoELayer(torch.nn.Module):
     def forward(self, hidden: torch.Tensor, route_override=None):
         return ppmoe_forward(self.world, self.group, hidden, self.weights.gate, self.experts_by_rank(),
                              weight_scaling=self.cfg.weight_scaling, dropout_p=self.cfg.dropout_p,
+                             rng=self.rng if self.cfg.dropout_p > 0 else None,
                              route_override=route_override, top_k=self.cfg.top_k,
                              capacity_factor=self.cfg.capacity_factor)
 

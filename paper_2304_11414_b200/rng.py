@@ -45,3 +45,54 @@ class Rng:
     def spawn(self, stream: int) -> "Rng":
         """Fresh generator on a sibling sub-stream of the same seed."""
         return Rng(self.seed, stream)
+
+
+_M64 = (1 << 64) - 1
+
+
+def philox4x64_block(counter: int, key0: int, key1: int) -> list:
+    """One block of numpy's Philox4x64-10 (the bit generator behind Rng): the four 64-bit
+    words at `counter` (< 2^64) under key (key0, key1).  Used to rebuild a generator's buffer
+    after the device consumed draws (DropoutStream.advance); the device twin is
+    csrc/common.cuh philox4x64_10."""
+    c = [counter & _M64, 0, 0, 0]
+    k0, k1 = key0 & _M64, key1 & _M64
+    for r in range(10):
+        if r:
+            k0 = (k0 + 0x9E3779B97F4A7C15) & _M64
+            k1 = (k1 + 0xBB67AE8584CAA73B) & _M64
+        p0 = 0xD2E7470EE14C6C93 * c[0]
+        p1 = 0xCA5A826395121157 * c[2]
+        c = [(p1 >> 64) ^ c[1] ^ k0, p1 & _M64, (p0 >> 64) ^ c[3] ^ k1, p0 & _M64]
+    return c
+
+
+def stream_position(gen: np.random.Generator) -> tuple:
+    """(key0, key1, draws consumed) of a Philox generator: draw m of the stream is word m % 4
+    of the block at counter m // 4 + 1."""
+    st = gen.bit_generator.state
+    if st.get("bit_generator") != "Philox":
+        raise ValueError("dropout needs a Philox-backed Rng (moesim's Rng)")
+    ctr = [int(v) for v in st["state"]["counter"]]
+    if any(ctr[1:]):
+        raise ValueError("Philox counter beyond 2^64 blocks is not supported")
+    key = [int(v) for v in st["state"]["key"]]
+    return key[0], key[1], 4 * ctr[0] + int(st["buffer_pos"]) - 4
+
+
+def set_stream_position(gen: np.random.Generator, draws: int) -> None:
+    """Move a Philox generator to `draws` consumed draws of its stream (as if drawn)."""
+    st = gen.bit_generator.state
+    key0, key1 = (int(v) for v in st["state"]["key"])
+    if draws == 0:
+        ctr, pos, buf = 0, 4, [0, 0, 0, 0]
+    else:
+        ctr = (draws + 3) // 4
+        pos = draws - 4 * (ctr - 1)
+        buf = philox4x64_block(ctr, key0, key1)
+    st["state"]["counter"] = np.array([ctr, 0, 0, 0], dtype=np.uint64)
+    st["buffer"] = np.array(buf, dtype=np.uint64)
+    st["buffer_pos"] = pos
+    st["has_uint32"] = 0
+    st["uinteger"] = 0
+    gen.bit_generator.state = st

@@ -34,12 +34,14 @@ def device_weights(layer: O.OracleLayer, dtype=torch.bfloat16, device="cuda") ->
 
 
 def run_cuda_layer(hidden: np.ndarray, w: P.MoeLayerWeights, *, tp=1, k=1, capacity_factor=math.inf,
-                   weight_scaling=True, route_override=None, dtype=torch.bfloat16, grad_out=None):
+                   weight_scaling=True, route_override=None, dtype=torch.bfloat16, grad_out=None, dropout_p=0.0,
+                   rng=None):
     x = torch.as_tensor(hidden, dtype=torch.float64).to("cuda", dtype).requires_grad_()
     world = P.World(1, tp)
     group = P.ProcessGroup(P.EP, tuple(range(tp)))
     out, l_aux = P.ppmoe_forward(world, group, x, w.gate, w.shard(tp), weight_scaling=weight_scaling,
-                                 route_override=route_override, top_k=k, capacity_factor=capacity_factor)
+                                 route_override=route_override, top_k=k, capacity_factor=capacity_factor,
+                                 dropout_p=dropout_p, rng=rng)
     if grad_out is None:
         loss = out.float().sum() + l_aux
     else:

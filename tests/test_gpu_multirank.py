@@ -59,7 +59,9 @@ def _worker(rank, world, port, q, k, cf, env=None, e=8):
         wd = P.World(1, world)
         g = P.ProcessGroup(P.EP, tuple(range(world)))
         ebr = [local.bank if r == rank else None for r in range(world)]
-        out, l_aux = P.ppmoe_forward(wd, g, x, local.gate, ebr, top_k=k, capacity_factor=cf, check_replicas=True)
+        drop = float(os.environ.get("_TEST_DROPOUT", "0"))
+        out, l_aux = P.ppmoe_forward(wd, g, x, local.gate, ebr, top_k=k, capacity_factor=cf, check_replicas=True,
+                                     dropout_p=drop, rng=P.Rng(41, 2) if drop else None)
         (out.float().sum() + l_aux).backward()
         P.sync_gate_gradients(wd, g, local.gate)
         torch.cuda.synchronize()
@@ -84,6 +86,7 @@ def test_tp_one_expert_per_rank(world, k, cf, env, e):
     (2, 2, 1.25, {"PPMOE_NVL_FWD": "fused"}), (2, 2, float("inf"), {"PPMOE_NVL_FWD": "slots"}),
     (2, 2, float("inf"), {"PPMOE_TP_COMM": "nccl"}), (2, 2, float("inf"), {"PPMOE_NVL_PUSH": "1", "PPMOE_NVL_PULL": "sm"}),
     (2, 2, float("inf"), {"PPMOE_NVL_MC": "1"}), (2, 2, 1.25, {"PPMOE_NVL_CHUNKS": "2"}),
+    (2, 2, 1.25, {"_TEST_DROPOUT": "0.2"}), (4, 1, float("inf"), {"_TEST_DROPOUT": "0.1"}),
     (4, 2, float("inf"), {"PPMOE_NVL_CHUNKS": "2"}),
 ])
 def test_tp_nccl_matches_simulated(world, k, cf, env, e=8):
@@ -106,8 +109,10 @@ def test_tp_nccl_matches_simulated(world, k, cf, env, e=8):
     full = P.MoeLayerWeights.random(h, e, seed=11, device="cuda")
     x = torch.randn(n, h, device="cuda", generator=torch.Generator(device="cuda").manual_seed(5)).bfloat16()
     x.requires_grad_()
+    drop = float((env or {}).get("_TEST_DROPOUT", "0"))
     out, l_aux = P.ppmoe_forward(P.World(1, world), P.ProcessGroup(P.EP, tuple(range(world))), x, full.gate,
-                                 full.shard(world), top_k=k, capacity_factor=cf)
+                                 full.shard(world), top_k=k, capacity_factor=cf, dropout_p=drop,
+                                 rng=P.Rng(41, 2) if drop else None)
     (out.float().sum() + l_aux).backward()
     ref_out = out.detach().float().cpu().numpy()
 
@@ -466,3 +471,56 @@ def test_nvl_barrier_timeout_raises():
         assert p.exitcode == 0
     assert got[1]["raised_check"] and got[1]["raised_forward"], got[1]
     assert not got[0]["raised_check"] and not got[0]["raised_forward"]
+
+
+def _divergence_worker(rank, world, port, q):
+    """Identical hidden, different route overrides per rank (full routing on every rank, no
+    sliced router): check_replicas must report the dispatch divergence (moe.py:289-291)."""
+    os.environ["PPMOE_SLICED_ROUTER"] = "0"
+    import torch.distributed as dist
+
+    import paper_2304_11414_b200 as P
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    try:
+        w = P.MoeLayerWeights.random(256, 4, seed=3, device="cuda", experts=range(2 * rank, 2 * rank + 2))
+        x = torch.randn(64, 256, device="cuda", generator=torch.Generator(device="cuda").manual_seed(4)).bfloat16()
+        wd, g = P.World(1, world), P.ProcessGroup(P.EP, (0, 1))
+        ebr = [w.bank if r == rank else None for r in range(world)]
+        ok_same = True
+        try:  # same routing everywhere: no error
+            P.ppmoe_forward(wd, g, x, w.gate, ebr, top_k=1, check_replicas=True)
+        except ValueError:
+            ok_same = False
+        ov = torch.full((64,), rank, dtype=torch.int64, device="cuda")  # rank 0 -> expert 0, rank 1 -> 1
+        msg = ""
+        try:
+            P.ppmoe_forward(wd, g, x, w.gate, ebr, top_k=1, route_override=ov, check_replicas=True)
+        except ValueError as exc:
+            msg = str(exc)
+        torch.cuda.synchronize()
+        q.put((rank, {"ok_same": ok_same, "msg": msg}))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_check_replicas_detects_dispatch_divergence():
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29600 + (os.getpid() + 17) % 500
+    procs = [ctx.Process(target=_divergence_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = _collect(q, procs, timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for r in range(2):
+        assert got[r]["ok_same"], got[r]
+        assert "dispatch order differs" in got[r]["msg"], got[r]

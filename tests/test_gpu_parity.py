@@ -406,6 +406,59 @@ def test_dropout_gradient_directional_finite_difference():
     assert abs(analytic - numeric) <= 2e-3 * max(1.0, abs(numeric)), (analytic, numeric)
 
 
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_dropout_vs_reference_golden(dtype):
+    """Dropout masks identical to the reference's: the reference golden (ppmoe_forward with
+    dropout_p 0.25 and Rng(15, 77), T = 2, tensor.backward) is reproduced by the device, which
+    regenerates moesim's Philox draws per expert (csrc/common.cuh); the caller's Rng ends where
+    the reference's does (N*h draws)."""
+    from paper_2304_11414_b200.rng import stream_position
+
+    meta, a = load("ppmoe_dropout")
+    case = meta["case"]
+    hidden, layer = golden_inputs(case)
+    rng = P.Rng(case["seed"], 77)
+    res = run_cuda_layer(hidden, device_weights(layer, dtype), tp=case["tp"], dtype=dtype,
+                         dropout_p=case["dropout_p"], rng=rng)
+    grads = {k[5:]: v for k, v in a.items() if k.startswith("grad_") and k != "grad_hidden"}
+    _compare(res, a["out"], a["grad_hidden"], grads, dtype, rows=a["rows"], name="ppmoe_dropout")
+    # the dropped elements are the reference's: exact zeros in the same places
+    ref_zero = a["out"] == 0
+    assert ref_zero.mean() > 0.1 and np.array_equal(res["out"][a["rows"]] == 0, ref_zero)
+    assert stream_position(rng._gen)[2] == case["tokens"] * case["hidden"]
+
+
+@pytest.mark.parametrize("k,cf,tp", [(2, 1.25, 2), (1, math.inf, 1)])
+def test_dropout_vs_oracle_bf16_tensor_core_path(k, cf, tp):
+    """Dropout on the tcgen05 path (fc2 epilogue keep bits for 32 columns, column-slab bwd_dy)
+    against the oracle drawing the same Philox stream (top-k and capacity generalise the
+    reference's per-expert draw: each expert's kept rows, ascending id)."""
+    h, e, n, p = 256, 8, 700, 0.3
+    layer = oracle_rounded(O.init_layer(h, e, seed=91), torch.bfloat16)
+    hidden = torch.randn(n, h, generator=torch.Generator().manual_seed(92)).bfloat16().double().numpy()
+    ref = O.ppmoe_layer(hidden, layer, k=k, capacity_factor=cf, dropout_p=p, rng=O.OracleRng(93, 4))
+    res = run_cuda_layer(hidden, device_weights(layer, torch.bfloat16), tp=tp, k=k, capacity_factor=cf,
+                         dropout_p=p, rng=P.Rng(93, 4))
+    _compare(res, ref.out, ref.grad_hidden, ref.grads, torch.bfloat16, name=f"dropout k{k}")
+
+
+def test_dpmoe_single_rank_dropout_matches_ppmoe():
+    """One all-to-all rank draws its experts' dropout blocks in the reference's dpmoe order
+    (moe.py:443-448), which for a single rank is the PPMoE order: same masks, same results."""
+    layer = oracle_rounded(O.init_layer(256, 4, seed=95), torch.bfloat16)
+    hidden = torch.randn(300, 256, generator=torch.Generator().manual_seed(96)).bfloat16().double().numpy()
+    pp = run_cuda_layer(hidden, device_weights(layer, torch.bfloat16), k=2, dropout_p=0.2, rng=P.Rng(97, 1))
+    w = device_weights(layer, torch.bfloat16)
+    x = torch.as_tensor(hidden).to("cuda", torch.bfloat16).requires_grad_()
+    out, l_aux = P.dpmoe_forward(P.World(1, 1), P.ProcessGroup(P.EP, (0,)), x, w.gate, experts_by_rank=w.shard(1),
+                                 top_k=2, dropout_p=0.2, rng=P.Rng(97, 1))
+    (out.float().sum() + l_aux).backward()
+    assert np.array_equal(out.detach().double().cpu().numpy() == 0, pp["out"] == 0)
+    assert scaled_err(out.detach().double().cpu().numpy(), pp["out"]) < 1e-2
+    for key, g in w.named_grads().items():
+        assert scaled_err(g.double().cpu().numpy(), pp["grads"][key]) < 2e-2, key
+
+
 # ------------------------------------------------------------------ spatial vs temporal spans (moe.py:475-533)
 
 

@@ -17,8 +17,9 @@ for name, h, e, k in (("C2", 4096, 8, 2), ("C3", 8192, 16, 2)):
     res = {}
     outs = {}
     for rep in range(6):
-        for mode in ("dfma", "dmma"):
-            os.environ["PPMOE_ROUTER"] = mode
+        for mode in ("dfma", "dmma0", "dmma1", "dmma2", "dmma3"):
+            os.environ["PPMOE_ROUTER"] = mode[:4]
+            os.environ["PPMOE_ROUTER_CFG"] = mode[4:] or "0"
             torch.cuda.synchronize()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
@@ -30,8 +31,9 @@ for name, h, e, k in (("C2", 4096, 8, 2), ("C3", 8192, 16, 2)):
                 res.setdefault(mode, []).append(a.elapsed_time(b) / 20)
             outs[mode] = rt
     med = {m: sorted(v)[len(v) // 2] * 1e3 for m, v in res.items()}
-    same = all(torch.equal(getattr(outs["dfma"], f), getattr(outs["dmma"], f)) for f in ("idx", "top1_counts"))
-    wdiff = float((outs["dfma"].w - outs["dmma"].w).abs().max())
+    same = all(torch.equal(getattr(outs["dfma"], f), getattr(outs[m], f)) for f in ("idx", "top1_counts")
+               for m in outs)
+    wdiff = max(float((outs["dfma"].w - outs[m].w).abs().max()) for m in outs)
     bytes_ = n * h * 2 + h * e * 4 + n * k * 8
     print(f"{name}: router us/call {med}  HBM frac (6528.7 GB/s): "
           f"{ {m: round(bytes_ / (v * 1e-6) / 6528.7e9, 3) for m, v in med.items()} }  idx equal {same}  max|dw| {wdiff:.2e}")
