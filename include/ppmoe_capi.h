@@ -10,9 +10,14 @@
  *
  * Conventions
  *  - All pointers are DEVICE pointers owned by the caller (PyTorch caching
- *    allocator).  The library never allocates or frees device memory, keeps no
- *    global state, and never synchronises the host: every call only enqueues
- *    kernels on `stream` (a cudaStream_t passed as void*).
+ *    allocator).  The library never allocates or frees device memory (except the
+ *    explicit ppmoe_ipc_* helpers) and never synchronises the host: every call only
+ *    enqueues kernels / async copies on `stream` (a cudaStream_t passed as void*).
+ *    Its only state: the thread-local GEMM SM budget (ppmoe_set_gemm_sm_budget) and
+ *    GEMM mode, the thread-local error string, and one 4-byte module-scope device
+ *    word per device (the grouped GEMM's wave-synchronisation counter, reset on the
+ *    launch stream before each long-K GEMM; PPMOE_KSYNC=0 disables it).  Long-K
+ *    GEMMs of one device must therefore be stream-ordered (they are, in this path).
  *  - Return value 0 = success; negative = error, message via ppmoe_last_error()
  *    (thread-local).  -1/-3 map to ValueError, -2/-4 to RuntimeError.
  *  - dtype: 0 = bf16 (activations/expert weights bf16, fp32 accumulation),

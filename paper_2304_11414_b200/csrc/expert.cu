@@ -63,20 +63,20 @@ static bool use_wide() {
   return atoi(e) != 0;
 }
 
+// The soft wave synchronisation's counter: module-scope device storage (one word per device
+// context, created with the module image, never cudaMalloc'd), reset on the launch stream
+// before every synchronised GEMM.  Synchronised GEMMs of one device are stream-ordered.
+__device__ unsigned int g_ksync_counter;
+
 template <bool A_MN, bool B_MN, class Epi>
 static int launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const GroupGeom& geo_in, const Epi& epi,
                      cudaStream_t s) {
   GroupGeom geo = geo_in;
   if (geo.ksync > 0 && geo.K_fixed > 0) {  // soft wave synchronisation (see GroupGeom::ksync)
-    // one counter per device, reset on the launch stream before every synchronised GEMM
-    constexpr int kMaxDevices = 64;
-    static unsigned int* ctr[kMaxDevices] = {};
-    int dev = 0;
-    PPMOE_CUDA(cudaGetDevice(&dev));
-    if (dev < 0 || dev >= kMaxDevices) return set_error(kErrUnsupported, "device ordinal %d out of range", dev);
-    if (!ctr[dev]) PPMOE_CUDA(cudaMalloc(&ctr[dev], sizeof(unsigned int)));
-    PPMOE_CUDA(cudaMemsetAsync(ctr[dev], 0, sizeof(unsigned int), s));
-    geo.ksync_ctr = ctr[dev];
+    void* ctr = nullptr;
+    PPMOE_CUDA(cudaGetSymbolAddress(&ctr, g_ksync_counter));
+    PPMOE_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned int), s));
+    geo.ksync_ctr = static_cast<unsigned int*>(ctr);
   } else {
     geo.ksync = 0;
   }

@@ -57,4 +57,5 @@ for _ in range(10):
 pr.disable()
 if rank == 0:
     pstats.Stats(pr).sort_stats("tottime").print_stats(30)
+    pstats.Stats(pr).sort_stats("cumulative").print_stats(45)
 dist.destroy_process_group()
