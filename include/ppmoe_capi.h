@@ -97,6 +97,11 @@ int ppmoe_route(const void* X, int dtype, const float* Wg, int N, int H, int E, 
  *   pair_pos    [N x K] out: sorted row of every pair, -1 if dropped
  *   rows_cap_global >= N*K + 128*E
  */
+/* Sliced routing (T ranks each routed N/T tokens with ppmoe_route, score_sums + counts_top1
+ * written into their record of stats): stats [T x 4E] int32 words per rank = E fp64 score
+ * sums, E int32 top-1 counts, E words of padding (16-byte records), all-gathered.  Sums the records in rank order and writes
+ * l_aux [2] (value, sum of fractions) and the global counts_top1 [E] (moe.py:211-223).   */
+int ppmoe_route_combine_stats(const int* stats, int T, int N, int E, double* l_aux, int* counts_top1, void* stream);
 size_t ppmoe_dispatch_workspace_bytes(int N, int E, int K);
 int ppmoe_dispatch_plan(const int* idx, const float* w, int N, int E, int K, int capacity, const int* rank_offset,
                         int* counts, int* kept, int* seg, int* tok_sorted, float* w_sorted, int* pair_pos,

@@ -172,10 +172,11 @@ def route(hidden: torch.Tensor, wg: torch.Tensor, k: int, override: torch.Tensor
 def route_sliced(world, group, hidden: torch.Tensor, wg: torch.Tensor, k: int,
                  override: torch.Tensor | None = None) -> Route:
     """Routing of a replicated activation split across the TP group: each rank routes its
-    N/T-token slice and one all-gather assembles the identical full routing on every rank
-    (the reference gates every replica identically, moe.py:288-291; the logits are computed
-    once instead of T times).  l_aux is recombined from per-slice score sums and top-1
-    counts in rank order (deterministic, identical on all ranks)."""
+    N/T-token slice straight into its rows of the full routing tensors, and in-place NCCL
+    all-gathers complete them identically on every rank (the reference gates every replica
+    identically, moe.py:288-291; the logits are computed once instead of T times).  l_aux is
+    recombined on the device from the per-slice score sums and top-1 counts in rank order
+    (ppmoe_route_combine_stats: deterministic, identical on all ranks)."""
     import torch.distributed as dist
 
     n, h = hidden.shape
@@ -184,32 +185,26 @@ def route_sliced(world, group, hidden: torch.Tensor, wg: torch.Tensor, k: int,
     me = world.rank_in(group)
     nr = n // t
     dev = hidden.device
-    sums = torch.empty(e, dtype=torch.float64, device=dev)
     sl = slice(me * nr, (me + 1) * nr)
-    rt = route(hidden[sl], wg, k, None if override is None else override[sl].contiguous(), sums)
-    # one packed all-gather: idx | w | scores | score_sums (as 2 int32) | top-1 counts
-    parts = [rt.idx.reshape(-1), rt.w.reshape(-1).view(torch.int32), rt.scores.reshape(-1).view(torch.int32),
-             sums.view(torch.int32), rt.top1_counts]
-    sizes = [p.numel() for p in parts]
-    packed = torch.cat(parts)
-    gathered = torch.empty((t, packed.numel()), dtype=torch.int32, device=dev)
-    dist.all_gather_into_tensor(gathered, packed, group=world.torch_group(group))
-    offs = [0]
-    for sz in sizes:
-        offs.append(offs[-1] + sz)
-    col = lambda i: gathered[:, offs[i]:offs[i + 1]]  # noqa: E731
-    idx = col(0).reshape(n, k).contiguous()
-    w = col(1).contiguous().view(torch.float32).reshape(n, k)
-    scores = col(2).contiguous().view(torch.float32).reshape(n, e)
-    s_all = col(3).contiguous().view(torch.float64).reshape(t, e)
-    c_all = col(4).reshape(t, e)
-    s_tot = s_all[0].clone()
-    for r in range(1, t):  # rank order: deterministic
-        s_tot += s_all[r]
-    cnt = c_all.sum(0).to(torch.int32)
-    frac = cnt.to(torch.float64) / n
-    l_aux = torch.stack([(s_tot * frac).sum() * (e / n), frac.sum()])
-    return Route(idx, w, scores, l_aux, cnt.contiguous())
+    idx = torch.empty((n, k), dtype=torch.int32, device=dev)
+    w = torch.empty((n, k), dtype=torch.float32, device=dev)
+    scores = torch.empty((n, e), dtype=torch.float32, device=dev)
+    stats = torch.zeros((t, 4 * e), dtype=torch.int32, device=dev)  # per rank: E fp64 sums | E counts | pad
+    mine = stats[me]
+    l_aux_slice = torch.empty(2, dtype=torch.float64, device=dev)
+    lib = _lib.load()
+    ws = _ws(lib.ppmoe_route_workspace_bytes(nr, e, k), dev)
+    ov = None if override is None else override[sl].contiguous()
+    call("ppmoe_route", ptr(hidden[sl]), dtype_code(hidden.dtype), ptr(wg), nr, h, e, k, ptr(ov), ptr(idx[sl]),
+         ptr(w[sl]), ptr(scores[sl]), ptr(l_aux_slice), ptr(mine[2 * e:3 * e]), ptr(mine[:2 * e]), ptr(ws), ws.numel(),
+         _stream())
+    pg = world.torch_group(group)
+    for full in (idx, w, scores, stats):
+        dist.all_gather_into_tensor(full, full[me * full.shape[0] // t:(me + 1) * full.shape[0] // t], group=pg)
+    l_aux = torch.empty(2, dtype=torch.float64, device=dev)
+    cnt = torch.empty(e, dtype=torch.int32, device=dev)
+    call("ppmoe_route_combine_stats", ptr(stats), t, n, e, ptr(l_aux), ptr(cnt), _stream())
+    return Route(idx, w, scores, l_aux, cnt)
 
 
 def capacity_for(capacity_factor: float, tokens: int, k: int, num_experts: int) -> int:

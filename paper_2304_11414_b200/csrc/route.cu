@@ -473,6 +473,30 @@ __global__ void __launch_bounds__(256) route_finalize_kernel(const double* __res
   }
 }
 
+// Sliced routing: every rank routed N/T tokens and the T per-rank [score sums (E fp64) |
+// top-1 counts (E int32) | E pad] records were all-gathered (stats [T][4E] int32 words).  Sum them
+// in rank order (deterministic, identical on every rank) and form l_aux (moe.py:211-223).
+__global__ void route_combine_stats_kernel(const int* __restrict__ stats, int T, int N, int E,
+                                           double* __restrict__ l_aux, int* __restrict__ counts_top1) {
+  if (threadIdx.x != 0) return;
+  double tot = 0.0, fr = 0.0;
+  for (int e = 0; e < E; ++e) {
+    double s = 0.0;
+    int c = 0;
+    for (int r = 0; r < T; ++r) {
+      const int* rec = stats + static_cast<size_t>(r) * 4 * E;  // 16-byte aligned records
+      s += reinterpret_cast<const double*>(rec)[e];
+      c += rec[2 * E + e];
+    }
+    const double frac = static_cast<double>(c) / N;
+    tot += s * frac;
+    fr += frac;
+    counts_top1[e] = c;
+  }
+  l_aux[0] = tot * (static_cast<double>(E) / N);
+  l_aux[1] = fr;
+}
+
 // ------------------------------------------------------------------ dispatch plan
 
 struct PlanWs {
@@ -688,11 +712,6 @@ static bool use_dmma_router(int dtype, int H, int E) {
   return dtype == kBF16 && H % (32 * kRouteDmmaMaxWarps) == 0 && E <= 16;
 }
 
-// (warps per block, min blocks per SM) of the DMMA router; PPMOE_ROUTER_CFG=0..3 for A/B runs
-static int router_cfg() {
-  const char* e = std::getenv("PPMOE_ROUTER_CFG");
-  return e ? std::atoi(e) : 0;
-}
 
 template <int EB, int W, int MINB>
 static int launch_router_dmma_cfg(const void* X, const float* Wg, int N, int H, int E, int K, const int* ovr, int* idx,
@@ -705,15 +724,13 @@ static int launch_router_dmma_cfg(const void* X, const float* Wg, int N, int H, 
   return check_launch("router_dmma_kernel");
 }
 
+// 8 warps per 32-token block, 2 blocks per SM.  Measured alternatives (tools/ab_router.py,
+// profiles/r02_router_ab.txt): 4 warps x 4-6 blocks per SM, 3 blocks per SM (register
+// spills), and a TMA shared-memory ring for X and Wg: equal or slower.
 template <int EB>
 static int launch_router_dmma(const void* X, const float* Wg, int N, int H, int E, int K, const int* ovr, int* idx,
                               float* w, float* scores, double* ssum, int* cnt, cudaStream_t s) {
-  switch (router_cfg()) {
-    case 1: return launch_router_dmma_cfg<EB, 8, 3>(X, Wg, N, H, E, K, ovr, idx, w, scores, ssum, cnt, s);
-    case 2: return launch_router_dmma_cfg<EB, 4, 4>(X, Wg, N, H, E, K, ovr, idx, w, scores, ssum, cnt, s);
-    case 3: return launch_router_dmma_cfg<EB, 4, 6>(X, Wg, N, H, E, K, ovr, idx, w, scores, ssum, cnt, s);
-    default: return launch_router_dmma_cfg<EB, 8, 2>(X, Wg, N, H, E, K, ovr, idx, w, scores, ssum, cnt, s);
-  }
+  return launch_router_dmma_cfg<EB, 8, 2>(X, Wg, N, H, E, K, ovr, idx, w, scores, ssum, cnt, s);
 }
 
 }  // namespace ppmoe
@@ -756,6 +773,12 @@ int ppmoe_route(const void* X, int dtype, const float* Wg, int N, int H, int E, 
   if (int rc2 = check_launch("route_finalize_kernel")) return rc2;
   if (counts_top1) PPMOE_CUDA(cudaMemcpyAsync(counts_top1, cnt, static_cast<size_t>(E) * 4, cudaMemcpyDeviceToDevice, s));
   return kOk;
+}
+
+int ppmoe_route_combine_stats(const int* stats, int T, int N, int E, double* l_aux, int* counts_top1, void* stream) {
+  PPMOE_REQUIRE(T >= 1 && N >= 1 && E >= 1 && E <= kMaxE, "bad route stats T=%d N=%d E=%d", T, N, E);
+  route_combine_stats_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(stats, T, N, E, l_aux, counts_top1);
+  return check_launch("route_combine_stats_kernel");
 }
 
 size_t ppmoe_dispatch_workspace_bytes(int N, int E, int K) { return plan_ws_layout(N, E, K, nullptr, nullptr); }

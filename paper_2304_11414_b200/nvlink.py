@@ -105,6 +105,8 @@ class NvlArena:
         # barrier error flag in pinned host memory, mapped into the device address space
         # (UVA): the barrier kernel stores 1 on a timeout and the host reads it without a sync
         self.err = torch.zeros(1, dtype=torch.int32, pin_memory=True)
+        self._err_view = self.err.numpy()  # host view of the same pinned word (cheap reads)
+        self._views: dict = {}  # (name, shape, dtype) -> tensor view of a peer buffer
         self.epoch = [0] * 8
         self.bufs: dict = {}
         self.mc_bufs: dict = {}
@@ -120,16 +122,23 @@ class NvlArena:
                 torch.cuda.synchronize()
                 dist.barrier(group=self.torch_group)  # no peer still reads the old buffer
                 b.release()
+                self._views = {k: v for k, v in self._views.items() if k[0] != name}
             b = _PeerBuffer(self, nbytes)
             self.bufs[name] = b
         return b
 
     def tensor(self, name: str, shape, dtype: torch.dtype) -> torch.Tensor:
+        key = (name, tuple(shape), dtype)
+        t = self._views.get(key)
+        if t is not None:
+            return t
         n = 1
         for s in shape:
             n *= s
         nbytes = max(n * torch.empty((), dtype=dtype).element_size(), 16)
-        return _wrap(self.buffer(name, nbytes).local, shape, dtype, self.device)
+        t = _wrap(self.buffer(name, nbytes).local, shape, dtype, self.device)
+        self._views[key] = t
+        return t
 
     def table(self, name: str):
         return self.bufs[name].table
@@ -185,7 +194,7 @@ class NvlArena:
 
     def check_nonblocking(self) -> None:
         """Raise if a barrier of this arena that already ran timed out (no device sync)."""
-        if int(self.err[0]) != 0:
+        if self._err_view[0] != 0:
             raise RuntimeError(f"NVLink barrier timed out on rank {self.rank} of tensor group {self.group.members}: "
                                "a peer stopped responding; the exchanges since then read unfinished peer rows")
 

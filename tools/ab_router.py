@@ -17,9 +17,8 @@ for name, h, e, k in (("C2", 4096, 8, 2), ("C3", 8192, 16, 2)):
     res = {}
     outs = {}
     for rep in range(6):
-        for mode in ("dfma", "dmma0", "dmma1", "dmma2", "dmma3"):
-            os.environ["PPMOE_ROUTER"] = mode[:4]
-            os.environ["PPMOE_ROUTER_CFG"] = mode[4:] or "0"
+        for mode in ("dfma", "dmma"):
+            os.environ["PPMOE_ROUTER"] = mode
             torch.cuda.synchronize()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
