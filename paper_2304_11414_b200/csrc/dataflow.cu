@@ -200,6 +200,7 @@ __global__ void bwd_dy_kernel(const T* __restrict__ dOut, const T* __restrict__ 
 // CTA per 32-row block: phase 1 is bwd_dy_kernel's warp-per-row pass (8 warps x 4 rows);
 // phase 2 re-reads the block's freshly written dY rows (L2-hot) column-wise and writes the
 // block's column sums (the bias_down gradient partials) -- no DRAM pass over dY.
+template <bool DROP>
 __global__ void __launch_bounds__(256)
     bwd_dy_block_kernel(const __nv_bfloat16* __restrict__ dOut, const __nv_bfloat16* __restrict__ Y,
                         const int* __restrict__ seg, int El, int H, const int* __restrict__ tok_local,
@@ -225,11 +226,11 @@ __global__ void __launch_bounds__(256)
       const float sw = weight_scaling ? w_local[r] : 1.f;
       const __nv_bfloat16* g = dOut + static_cast<size_t>(tok) * H;
       const __nv_bfloat16* y = Y + static_cast<size_t>(r) * H;
-      const unsigned long long rd = drop_p > 0.f ? drop_row_draw(drop, seg, segment_of(seg, El, r), r, H) : 0ull;
+      const unsigned long long rd = DROP ? drop_row_draw(drop, seg, segment_of(seg, El, r), r, H) : 0ull;
       float acc = 0.f;
 #pragma unroll 4
       for (int j = lane * 8; j < H; j += 256) {
-        const uint32_t kb = drop_p > 0.f ? drop_keep_bits<8>(drop, rd + j) : 0u;
+        const uint32_t kb = DROP ? drop_keep_bits<8>(drop, rd + j) : 0u;
         const uint4 gu = *reinterpret_cast<const uint4*>(g + j);
         const uint4 yu = *reinterpret_cast<const uint4*>(y + j);
         const __nv_bfloat162* gh = reinterpret_cast<const __nv_bfloat162*>(&gu);
@@ -243,7 +244,7 @@ __global__ void __launch_bounds__(256)
           acc = fmaf(gf.x, yf.x, acc);
           acc = fmaf(gf.y, yf.y, acc);
           float d0 = sw * gf.x, d1 = sw * gf.y;
-          if (drop_p > 0.f) {
+          if (DROP) {
             d0 *= ((kb >> (2 * i)) & 1u) ? inv : 0.f;
             d1 *= ((kb >> (2 * i + 1)) & 1u) ? inv : 0.f;
           }
@@ -276,7 +277,8 @@ __global__ void __launch_bounds__(256)
 // The per-row dot <dOut[t], Y[r]> (the dw of scale_rows' backward, tensor.py:184-196) is
 // summed per warp and then over the 8 warps in a fixed order through shared memory.
 // CPW = chunks per warp = ceil(H / 2048).
-template <int CPW>
+template <int CPW, bool DROP>  // DROP: dropout mask regenerated (a separate instantiation keeps
+                                // the Philox code out of the register budget of the p = 0 path)
 __global__ void __launch_bounds__(256, 8 / CPW)
     bwd_dy_cols_kernel(const __nv_bfloat16* __restrict__ dOut, const __nv_bfloat16* __restrict__ Y,
                        const int* __restrict__ seg, int El, int H, const int* __restrict__ tok_local,
@@ -313,7 +315,7 @@ __global__ void __launch_bounds__(256, 8 / CPW)
         const float sw = weight_scaling ? w_local[r] : 1.f;
         const __nv_bfloat16* g = dOut + static_cast<size_t>(tok) * H;
         const __nv_bfloat16* y = Y + static_cast<size_t>(r) * H;
-        const unsigned long long rd = drop_p > 0.f ? drop_row_draw(drop, seg, segment_of(seg, El, r), r, H) : 0ull;
+        const unsigned long long rd = DROP ? drop_row_draw(drop, seg, segment_of(seg, El, r), r, H) : 0ull;
         uint4 gu[CPW], yu[CPW];
 #pragma unroll
         for (int q = 0; q < CPW; ++q) {
@@ -328,7 +330,7 @@ __global__ void __launch_bounds__(256, 8 / CPW)
           const int ch = warp + 8 * q;
           if (ch >= nchunk) continue;
           const int j = ch * 256 + lane * 8;
-          const uint32_t kb = drop_p > 0.f ? drop_keep_bits<8>(drop, rd + j) : 0u;
+          const uint32_t kb = DROP ? drop_keep_bits<8>(drop, rd + j) : 0u;
           const __nv_bfloat162* gh = reinterpret_cast<const __nv_bfloat162*>(&gu[q]);
           const __nv_bfloat162* yh = reinterpret_cast<const __nv_bfloat162*>(&yu[q]);
           uint4 out;
@@ -340,7 +342,7 @@ __global__ void __launch_bounds__(256, 8 / CPW)
             acc = fmaf(gf.x, yf.x, acc);
             acc = fmaf(gf.y, yf.y, acc);
             float d0 = sw * gf.x, d1 = sw * gf.y;
-            if (drop_p > 0.f) {
+            if (DROP) {
               d0 *= ((kb >> (2 * i)) & 1u) ? inv : 0.f;
               d1 *= ((kb >> (2 * i + 1)) & 1u) ? inv : 0.f;
             }
@@ -1254,18 +1256,22 @@ int ppmoe_bwd_dy(int dtype, const void* dOut, const void* Y, const int* seg, int
       auto* g = static_cast<const __nv_bfloat16*>(dOut);
       auto* y = static_cast<const __nv_bfloat16*>(Y);
       auto* d = static_cast<__nv_bfloat16*>(dY);
-      if (cpw == 1)
-        bwd_dy_cols_kernel<1><<<grid, 256, 0, s>>>(g, y, seg, El, H, tok_local, w_local, weight_scaling, dropout_p,
-                                                   drop_stream, d, dw, dy_colsum_part);
-      else if (cpw == 2)
-        bwd_dy_cols_kernel<2><<<grid, 256, 0, s>>>(g, y, seg, El, H, tok_local, w_local, weight_scaling, dropout_p,
-                                                   drop_stream, d, dw, dy_colsum_part);
-      else
-        bwd_dy_cols_kernel<4><<<grid, 256, 0, s>>>(g, y, seg, El, H, tok_local, w_local, weight_scaling, dropout_p,
-                                                   drop_stream, d, dw, dy_colsum_part);
+      const bool drop = dropout_p > 0.f;
+#define PPMOE_DY_COLS(C, D) \
+  bwd_dy_cols_kernel<C, D><<<grid, 256, 0, s>>>(g, y, seg, El, H, tok_local, w_local, weight_scaling, dropout_p, \
+                                                drop_stream, d, dw, dy_colsum_part)
+      if (cpw == 1) {
+        if (drop) PPMOE_DY_COLS(1, true); else PPMOE_DY_COLS(1, false);
+      } else if (cpw == 2) {
+        if (drop) PPMOE_DY_COLS(2, true); else PPMOE_DY_COLS(2, false);
+      } else {
+        if (drop) PPMOE_DY_COLS(4, true); else PPMOE_DY_COLS(4, false);
+      }
+#undef PPMOE_DY_COLS
       return check_launch("bwd_dy_cols_kernel");
     }
-    bwd_dy_block_kernel<<<num_sms() * 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+    auto blk = dropout_p > 0.f ? bwd_dy_block_kernel<true> : bwd_dy_block_kernel<false>;
+    blk<<<num_sms() * 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(
         static_cast<const __nv_bfloat16*>(dOut), static_cast<const __nv_bfloat16*>(Y), seg, El, H, tok_local,
         w_local, weight_scaling, dropout_p, drop_stream, static_cast<__nv_bfloat16*>(dY), dw, dy_colsum_part);
     return check_launch("bwd_dy_block_kernel");

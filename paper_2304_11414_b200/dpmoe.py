@@ -82,6 +82,8 @@ class _DPMoEFunction(torch.autograd.Function):
                 off = allc[: spec.me].sum(0) + torch.cumsum(tot, 0) - tot
                 offset = off.to(torch.int32).contiguous()
         pl = _ops.plan(rt.idx, rt.w, e, cap, offset)
+        if t == 1 and _ops.combine_mode(hidden.dtype, h) == "owner":
+            return _DPMoEFunction._forward_solo(ctx, hidden, wg, up, down, bias_up, bias_down, spec, rt, pl)
         cstart, tok_c, w_c, pos_c = _ops.a2a_compact(pl, rt.idx, e)
         # counts exchange: kept rows per destination (owner, local expert)
         recv_counts = torch.empty(t * el, dtype=torch.int32, device=dev)
@@ -130,7 +132,53 @@ class _DPMoEFunction(torch.autograd.Function):
         return out, rt.l_aux[0].to(torch.float32)
 
     @staticmethod
+    def _forward_solo(ctx, hidden, wg, up, down, bias_up, bias_down, spec, rt, pl):
+        """A group of one exchanges nothing: the conventional layer is then local dispatch
+        (gather into expert-major padded segments), the expert FFNs and the local combine --
+        the same kernels as the PPMoE layer at T = 1, so the comparator measures only what
+        the all-to-all adds at T > 1.  The ledger still records the reference's five
+        (empty) all-to-alls per step (moe.py:363-469)."""
+        n, h = hidden.shape
+        e = wg.shape[1]
+        desc = None
+        if spec.drop is not None:
+            desc = spec.drop.descriptor(pl.kept, e, 0, e, h)
+            spec.drop.advance(h * int(pl.kept.sum()))
+        st = _ops.experts_forward(hidden, pl, 0, e, up, down, bias_up, bias_down, spec.k, spec.weight_scaling, None,
+                                  drop_p=spec.dropout_p, drop=desc)
+        out = _ops.local_combine(st.y, st, pl, rt.idx, rt.w if spec.weight_scaling else None, torch.empty_like(hidden))
+        for _ in range(3):  # counts exchange, dispatch, return
+            spec.world.ledger.charge(spec.group.kind, "all_to_all", 0.0)
+        ctx.save_for_backward(hidden, wg, up, down)
+        ctx.state = ("solo", rt, pl, st, bias_up is not None, spec)
+        return out, rt.l_aux[0].to(torch.float32)
+
+    @staticmethod
+    def _backward_solo(ctx, g_out, g_aux):
+        hidden, wg, up, down = ctx.saved_tensors
+        _, rt, pl, st, has_bias, spec = ctx.state
+        n, h = hidden.shape
+        if g_out is None:
+            g_out = torch.zeros_like(hidden)
+        g_out = g_out.to(hidden.dtype).contiguous()
+        aux = None if g_aux is None else g_aux.detach().to(torch.float32).reshape(1).contiguous()
+        dxs = _ops._act((st.rows_cap, h), hidden.dtype, hidden.device)
+        dy, dh, dw, parts = _ops.experts_backward_data(g_out, st, up, down, spec.weight_scaling, None, has_bias, dxs)
+        dl = _ops.gate_backward(rt, pl, st, dw, aux)
+        dx = _ops.local_combine(dxs, st, pl, rt.idx, None, torch.empty_like(hidden), dl, wg) \
+            if ctx.needs_input_grad[0] else None
+        dwg = _ops.gate_weight_grad(hidden, dl, wg) if ctx.needs_input_grad[1] else None
+        del dxs
+        d_up, d_down, d_bu, d_bd = _ops.experts_backward_weights(st, dy, dh, up, down, has_bias, parts)
+        for _ in range(2):  # dY dispatch and dX return
+            spec.world.ledger.charge(spec.group.kind, "all_to_all", 0.0)
+        ctx.state = None
+        return dx, dwg, d_up, d_down, d_bu, d_bd, None
+
+    @staticmethod
     def backward(ctx, g_out, g_aux):
+        if ctx.state[0] == "solo":
+            return _DPMoEFunction._backward_solo(ctx, g_out, g_aux)
         hidden, wg, up, down = ctx.saved_tensors
         rt, pl, cstart, tok_c, w_c, pos_c, send_rows, recv_rows, st, rmap, yback, has_bias, spec = ctx.state
         n, h = hidden.shape
