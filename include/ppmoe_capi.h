@@ -305,11 +305,15 @@ int ppmoe_nvl_pull_range_ce(const void* const* srcs, int T, int rank, int N, int
                             void* stream);
 
 /* Self-test entry: plain grouped GEMM D_g = A_g * B_g through the tcgen05 path
- * (use_tc=1 default, 2 1-CTA, 3 CTA pair 256x256, 4 CTA pair 256x512) or the
+ * (use_tc=1 default, 2 1-CTA, 3 CTA pair 256x256, 4 CTA pair 256x512, 5 CTA pair 256x128) or the
  * CUDA-core path (use_tc=0).  mode 0: A [rows x K] K-major
  * per segment, B [G*K x N] MN-major, D [rows x N]; mode 1: K from segments,
  * A [rows x M] MN-major, B [rows x N] MN-major, D [G x M x N];
  * mode 2: A K-major segments, B [G*N x K] K-major, D [rows x N].           */
+/* Thread-local tile choice of the long-K token GEMMs (fc2 fwd, fc1 dgrad): 1 = the narrow
+ * 256 x 128 CTA-pair tile (twice the tiles: a fuller last wave when few expert rows sit on
+ * a GPU), 0 = the 256 x 256 tile, -1 = PPMOE_NARROW / default (256 x 256).             */
+int ppmoe_set_gemm_narrow(int narrow);
 int ppmoe_gemm_selftest(int mode, int use_tc, int dtype, const void* A, const void* B, const int* seg, int G, int M,
                         int N, int K, int rows_cap, void* D, void* stream);
 

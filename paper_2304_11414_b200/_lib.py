@@ -32,6 +32,7 @@ _SIGNATURES = {
     "ppmoe_kernel_launches": (ctypes.c_ulonglong, []),
     "ppmoe_set_gemm_sm_budget": (_I, [_I]),
     "ppmoe_set_gemm_mode": (_I, [_I]),
+    "ppmoe_set_gemm_narrow": (_I, [_I]),
     "ppmoe_route_workspace_bytes": (_S, [_I, _I, _I]),
     "ppmoe_route": (_I, [_P, _I, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _S, _P]),
     "ppmoe_route_combine_stats": (_I, [_P, _I, _I, _I, _P, _P, _P]),

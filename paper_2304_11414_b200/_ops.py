@@ -29,13 +29,44 @@ def dtype_code(dt: torch.dtype) -> int:
         raise ValueError(f"PPMoE kernels support bf16 and fp32 activations, got {dt}") from None
 
 
+_GUARDS: list = []  # (guard view, expected bytes) of PPMOE_GUARD=1 buffers
+_GUARD_ROWS = 64
+
+
 def _act(shape, dtype, device) -> torch.Tensor:
     """Activation/scratch buffer.  PPMOE_POISON=1 fills it with NaN (ints: -7) so that any
-    read of a row a kernel should have written shows up in the parity tests."""
-    if os.environ.get("PPMOE_POISON") == "1":
+    read of a row a kernel should have written shows up in the parity tests.
+    PPMOE_GUARD=1 (test mode; compute-sanitizer is not available on the pool) allocates 64
+    extra rows after the buffer, filled with a random byte pattern that ``check_guards``
+    verifies: a kernel writing past the rows it was given corrupts them."""
+    poison = os.environ.get("PPMOE_POISON") == "1"
+    if os.environ.get("PPMOE_GUARD") == "1":
+        shape = tuple(shape) if isinstance(shape, (tuple, list)) else (int(shape),)
+        full = torch.empty((shape[0] + _GUARD_ROWS,) + shape[1:], dtype=dtype, device=device)
+        main, guard = full[: shape[0]], full[shape[0]:]
+        pattern = torch.randint(0, 256, (guard.numel() * guard.element_size(),), dtype=torch.uint8, device=device)
+        guard.view(torch.uint8).view(-1).copy_(pattern)
+        _GUARDS.append((guard, pattern))
+        if poison:
+            main.fill_(float("nan") if dtype.is_floating_point else -7)
+        return main
+    if poison:
         shape = tuple(shape) if isinstance(shape, (tuple, list)) else (int(shape),)
         return torch.full(shape, float("nan") if dtype.is_floating_point else -7, dtype=dtype, device=device)
     return torch.empty(shape, dtype=dtype, device=device)
+
+
+def check_guards(clear: bool = True) -> int:
+    """Verify every PPMOE_GUARD guard region (synchronises); raises on a corrupted one.
+    Returns the number of guards checked."""
+    torch.cuda.synchronize()
+    n = len(_GUARDS)
+    bad = [i for i, (g, pat) in enumerate(_GUARDS) if not torch.equal(g.view(torch.uint8).reshape(-1), pat)]
+    if clear:
+        _GUARDS.clear()
+    if bad:
+        raise RuntimeError(f"out-of-bounds write: {len(bad)} of {n} guard regions past PPMoE buffers were modified")
+    return n
 
 
 def _ws(nbytes: int, device) -> torch.Tensor:

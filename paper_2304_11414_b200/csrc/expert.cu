@@ -39,8 +39,21 @@ struct LongKScope {  // marks a token-segment GEMM with a long reduction dimensi
   ~LongKScope() { g_long_k = 0; }
 };
 
-// Rows of a K-major B box: the pair kernel stages half of each 256-wide MMA per CTA.
-static uint32_t b_box_rows() { return use_pair() ? kBN / 2 : kBN; }
+// Narrow 256 x 128 pair tile for the long-K token GEMMs (fc2 fwd, fc1 dgrad: N = H).  With
+// few expert rows per GPU (T >= 4) their 256-wide tile count leaves a ragged last wave
+// (C2 T = 4: 544 tiles on 74 CTA pairs = 7.35 waves); the narrow tile doubles the tile count.
+// PPMOE_NARROW: 0 never (default), 1 the long-K token GEMMs; ppmoe_set_gemm_narrow(1)
+// selects it for the calling thread's next launches (the layer decides from its shape).
+static thread_local int g_force_narrow = -1;
+static bool use_narrow() {
+  if (!g_long_k) return false;
+  if (g_force_narrow >= 0) return g_force_narrow != 0;
+  const char* e = getenv("PPMOE_NARROW");
+  return e && atoi(e) != 0;
+}
+
+// Rows of a K-major B box: the pair kernel stages half of each MMA's B columns per CTA.
+static uint32_t b_box_rows() { return use_pair() ? (use_narrow() ? kBN / 4 : kBN / 2) : kBN; }
 
 // Pair-kernel tile width: 256 x 512 ("wide", two MMAs per k-step, 25 % fewer L2 -> SM
 // bytes, epilogue not overlapped) or 256 x 256 (double-buffered TMEM).  PPMOE_WIDE:
@@ -82,6 +95,13 @@ static int launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const GroupGe
   }
   if (use_pair()) {
     geo.stage = staged_stores(use_wide());
+    if (use_narrow() && !use_wide()) {
+      auto kern = grouped_gemm_sm100_pair<kBN / 2, A_MN, B_MN, Epi>;
+      constexpr int smem = PairSmem<kBN / 2>::kTotal;
+      PPMOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      kern<<<gemm_ctas() / 2 * 2, kPairThreads, smem, s>>>(ta, tb, geo, epi);
+      return check_launch("grouped_gemm_sm100_pair");
+    }
     if (use_wide()) {
       auto kern = grouped_gemm_sm100_pair<2 * kBN, A_MN, B_MN, Epi>;
       constexpr int smem = PairSmem<2 * kBN>::kTotal;
@@ -295,6 +315,12 @@ using namespace ppmoe;
 
 extern "C" {
 
+int ppmoe_set_gemm_narrow(int narrow) {
+  PPMOE_REQUIRE(narrow >= -1 && narrow <= 1, "gemm narrow: -1 env/default, 0 off, 1 long-K token GEMMs");
+  g_force_narrow = narrow;
+  return kOk;
+}
+
 int ppmoe_set_gemm_mode(int mode) {
   PPMOE_REQUIRE(mode >= 0 && mode <= 2, "gemm mode: 0 auto/env, 1 single-CTA, 2 CTA pair");
   g_force_mode = mode;
@@ -440,18 +466,24 @@ int ppmoe_gemm_selftest(int mode, int use_tc, int dtype, const void* A, const vo
                         int N, int K, int rows_cap, void* D, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   PPMOE_REQUIRE(mode >= 0 && mode <= 2, "mode must be 0..2");
-  PPMOE_REQUIRE(use_tc >= 0 && use_tc <= 4,
-                "use_tc: 0 CUDA cores, 1 default tcgen05, 2 1-CTA, 3 CTA pair 256x256, 4 CTA pair 256x512");
+  PPMOE_REQUIRE(use_tc >= 0 && use_tc <= 5,
+                "use_tc: 0 CUDA cores, 1 default tcgen05, 2 1-CTA, 3 CTA pair 256x256, 4 CTA pair 256x512, "
+                "5 CTA pair 256x128");
   struct ForceGuard {
-    explicit ForceGuard(int m, int w) {
+    explicit ForceGuard(int m, int w, int nr) {
       g_force_mode = m;
       g_force_wide = w;
+      g_force_narrow = nr;
+      if (nr == 1) g_long_k = 1;
     }
     ~ForceGuard() {
       g_force_mode = 0;
       g_force_wide = -1;
+      g_force_narrow = -1;
+      g_long_k = 0;
     }
-  } guard(use_tc >= 2 ? (use_tc >= 3 ? 2 : 1) : 0, use_tc == 4 ? 1 : (use_tc == 3 ? 0 : -1));
+  } guard(use_tc >= 2 ? (use_tc >= 3 ? 2 : 1) : 0, use_tc == 4 ? 1 : (use_tc == 3 || use_tc == 5 ? 0 : -1),
+          use_tc == 5 ? 1 : 0);
   PPMOE_REQUIRE(G >= 1 && G <= kMaxGroups, "bad group count %d", G);
   PPMOE_REQUIRE(!use_tc || dtype == kBF16, "tcgen05 path is bf16 only");
   if (mode == 0) {  // D[seg rows x N] = A[seg rows x K] * B_g[K x N] (B MN-major)

@@ -133,7 +133,7 @@ __device__ __forceinline__ void acc_bf16(float (&acc)[CW], const typename OgVec<
 
 // One CTA per tile of kOgTile owned tokens x (256*CW) columns.  CW columns per thread.
 template <int EB, int U, int KT, int CW>  // KT = k (1, 2) or 0: any k <= 8 read at run time
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, EB > 8 ? 3 : 1)
     nvl_owner_gather_kernel(const __grid_constant__ PeerSet<const __nv_bfloat16> rows, const int* __restrict__ seg,
                             int El, const int* __restrict__ idx, const int* __restrict__ pair_pos,
                             const float* __restrict__ w, int Kr, int H, int t0, int t1,
@@ -237,11 +237,14 @@ __global__ void __launch_bounds__(256)
                     *reinterpret_cast<const float2*>(&swg[((e4 + ee) * 256 + threadIdx.x) * CW + c2]);
             }
 #pragma unroll
-            for (int c = 0; c < CW; ++c)
+            for (int c = 0; c < CW; c += 2)  // paired columns: FFMA2, half the FMA issue slots
 #pragma unroll
               for (int u = 0; u < U; ++u) {
                 const float dv = ee == 0 ? d[u].x : ee == 1 ? d[u].y : ee == 2 ? d[u].z : d[u].w;
-                acc[u][c] = fmaf(dv, wv[c], acc[u][c]);
+                const float2 r = __ffma2_rn(make_float2(dv, dv), make_float2(wv[c], wv[c + 1]),
+                                            make_float2(acc[u][c], acc[u][c + 1]));
+                acc[u][c] = r.x;
+                acc[u][c + 1] = r.y;
               }
           }
         }
@@ -362,6 +365,10 @@ static int og_ctas_per_sm() {
   static int v = [] { const char* e = getenv("PPMOE_OG_CTAS"); return e ? atoi(e) : 5; }();
   return v;
 }
+static int og16_u() {  // tokens per thread of the 8 < E <= 16 gate-term form (PPMOE_OG16_U: 4 or 8)
+  static int v = [] { const char* e = getenv("PPMOE_OG16_U"); return e ? atoi(e) : 8; }();
+  return v;
+}
 static bool og_wide_e() {  // PPMOE_OG_WIDE_E=0: the any-E form (Wg from L2) for A/B runs
   static bool v = [] { const char* e = getenv("PPMOE_OG_WIDE_E"); return !e || atoi(e) != 0; }();
   return v;
@@ -462,7 +469,8 @@ int ppmoe_nvl_owner_gather(const void* const* rows, const int* seg, int El, cons
     else if (K == 1) PPMOE_OG(8, 8, 1, 4);
     else PPMOE_OG(8, 1, 0, 4);
   } else if (E <= 16 && og_wide_e()) {
-    if (K == 2) PPMOE_OG_DYN(16, 8, 2, 4);
+    if (K == 2 && og16_u() == 4) PPMOE_OG_DYN(16, 4, 2, 4);
+    else if (K == 2) PPMOE_OG_DYN(16, 8, 2, 4);
     else if (K == 1) PPMOE_OG_DYN(16, 8, 1, 4);
     else PPMOE_OG_DYN(16, 1, 0, 4);
   } else if (E <= 32 && og_wide_e()) {

@@ -36,7 +36,7 @@ def _segments(counts):
     return seg
 
 
-@pytest.mark.parametrize("use_tc", [4, 3, 2, 0])
+@pytest.mark.parametrize("use_tc", [5, 4, 3, 2, 0])
 @pytest.mark.parametrize("mode,counts,M,N,K", [
     (0, [128], 0, 256, 64), (0, [100, 300, 0, 5], 0, 512, 256), (0, [700, 64], 0, 768, 448),
     (2, [128], 0, 256, 64), (2, [200, 33], 0, 512, 320),
@@ -738,3 +738,34 @@ def test_pipeline_stack_vs_oracle(layers, mbs):
     bad = {key: v for key, v in errs.items() if not v < TOL[torch.float32]}
     assert not bad, bad
     assert len(errs) == layers * (4 + 4 * e)
+
+
+# ------------------------------------------------------------------ out-of-bounds guard (sanitizer substitute)
+
+
+@pytest.mark.parametrize("n,h,e,k,tp,cf,drop,dtype", [
+    (700, 256, 8, 2, 1, math.inf, 0.0, torch.bfloat16), (700, 256, 8, 2, 2, 1.25, 0.1, torch.bfloat16),
+    (513, 128, 16, 3, 4, 0.5, 0.0, torch.bfloat16), (300, 264, 6, 2, 3, math.inf, 0.2, torch.bfloat16),
+    (257, 64, 4, 1, 2, 1.0, 0.0, torch.float32), (5, 64, 4, 4, 2, math.inf, 0.0, torch.bfloat16),
+])
+def test_no_out_of_bounds_writes(monkeypatch, n, h, e, k, tp, cf, drop, dtype):
+    """compute-sanitizer is closed on this pool (profiles/r02_compute_sanitizer_closed.log), so
+    every scratch / activation buffer of a layer step gets 64 guard rows of random bytes
+    (PPMOE_GUARD=1): fwd + bwd through the C-ABI, then every guard must be intact.  Covers
+    the gather, the six GEMM epilogues, bwd_dy, the owner gathers, capacity drops, dropout,
+    odd expert counts and k = E; the all-to-all comparator too."""
+    from paper_2304_11414_b200 import _ops
+
+    monkeypatch.setenv("PPMOE_GUARD", "1")
+    _ops._GUARDS.clear()
+    layer = oracle_rounded(O.init_layer(h, e, seed=n + h), dtype)
+    hidden = torch.randn(n, h, generator=torch.Generator().manual_seed(n)).to(dtype).double().numpy()
+    run_cuda_layer(hidden, device_weights(layer, dtype), tp=tp, k=k, capacity_factor=cf, dtype=dtype,
+                   dropout_p=drop, rng=P.Rng(3, 3) if drop else None)
+    assert _ops.check_guards() > 10
+    w = device_weights(layer, dtype)
+    x = torch.as_tensor(hidden).to("cuda", dtype).requires_grad_()
+    out, l_aux = P.dpmoe_forward(P.World(1, 1), P.ProcessGroup(P.EP, (0,)), x, w.gate, experts_by_rank=w.shard(1),
+                                 top_k=k, capacity_factor=cf)
+    (out.float().sum() + l_aux).backward()
+    assert _ops.check_guards() > 5
