@@ -366,7 +366,7 @@ static int og_ctas_per_sm() {
   return v;
 }
 static int og16_u() {  // tokens per thread of the 8 < E <= 16 gate-term form (PPMOE_OG16_U: 4 or 8)
-  static int v = [] { const char* e = getenv("PPMOE_OG16_U"); return e ? atoi(e) : 8; }();
+  static int v = [] { const char* e = getenv("PPMOE_OG16_U"); return e ? atoi(e) : 4; }();
   return v;
 }
 static bool og_wide_e() {  // PPMOE_OG_WIDE_E=0: the any-E form (Wg from L2) for A/B runs
