@@ -358,7 +358,11 @@ def exchange(ar: NvlArena, rows_name: str, seg, el: int, idx, pair_pos, w, n: in
     # push: every block already sits in the local exchange buffer; pull: read the owners'
     src = ar.local_table("xch") if push else ar.table("xch")
     # copy engines by default: the all-gather then takes no SMs from the overlapped GEMMs
-    pull = "ppmoe_nvl_pull_blocks" if os.environ.get("PPMOE_NVL_PULL", "ce") == "sm" else "ppmoe_nvl_pull_blocks_ce"
+    # (backward); PPMOE_NVL_PULL_FWD picks the forward's separately (nothing to overlap there)
+    mode = os.environ.get("PPMOE_NVL_PULL", "ce")
+    if rows_name == "y":
+        mode = os.environ.get("PPMOE_NVL_PULL_FWD", mode)
+    pull = "ppmoe_nvl_pull_blocks" if mode == "sm" else "ppmoe_nvl_pull_blocks_ce"
     call(pull, src, ar.tp, ar.rank, n, h, ptr(out), s)
     if _STRICT:
         ar.check()
