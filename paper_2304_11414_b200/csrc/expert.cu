@@ -199,6 +199,14 @@ static int banded_order() {
   const char* e = getenv("PPMOE_ORDER");
   return (e && strcmp(e, "band") == 0) ? 1 : 0;
 }
+// Tile order of the long-K token GEMMs (fc2 fwd, fc1 dgrad) alone: PPMOE_ORDER_LONG=band puts
+// them in square-ish 8-tile bands (a wave reads ~8 A + ~9 B panels instead of ~5 A + all 16 B
+// panels of an expert), with the wave sync keeping the bands' k-slices L2-resident.
+static int banded_order_long() {
+  const char* e = getenv("PPMOE_ORDER_LONG");
+  if (!e) return banded_order();
+  return strcmp(e, "band") == 0 ? 1 : 0;
+}
 // k-blocks between the soft wave barriers of the GEMMs that use them (PPMOE_KSYNC, 0 = off).
 // Enabled for fc2 fwd, fc2 dgrad and fc1 dgrad: halves their DRAM traffic, which under the
 // power cap buys clock; fc1 fwd measured slower with it.
@@ -291,6 +299,7 @@ static int fc2_fwd_impl(int dtype, const void* Act, const void* down, const void
   geo.rlo = row_lo;
   geo.rhi = row_hi;
   geo.ksync = ksync_interval();
+  geo.banded = banded_order_long();
   if (rows_cap == 0) return kOk;
   if (dtype == kBF16) {
     CUtensorMap ta, tb;
@@ -399,6 +408,7 @@ int ppmoe_expert_fc1_dgrad(int dtype, const void* dH, const void* up, const int*
   LongKScope long_k(F);
   GroupGeom geo = geom(El, H, 0, F, seg, 1, 0, 0, H);
   geo.ksync = ksync_interval();
+  geo.banded = banded_order_long();
   if (rows_cap == 0) return kOk;
   if (dtype == kBF16) {
     CUtensorMap ta, tb;
