@@ -227,6 +227,25 @@ def test_single_expert_reduces_to_dense_ffn():
     assert scaled_err(got, ref) < 1e-5
 
 
+def test_expert_forward_dropout_matches_reference_formula():
+    """ExpertFfn.forward(x, p, rng) == Dropout(GeLU(x up + b_up) down + b_down) with the mask
+    of tensor.dropout (moe.py:100-107, tensor.py:315-330): uniform draws of rng over the
+    [n, h] output, kept iff >= p, scaled 1/(1-p); rng advanced by n*h draws."""
+    from paper_2304_11414_b200.rng import stream_position
+
+    layer = oracle_rounded(O.init_layer(128, 1, seed=54), torch.float32)
+    hidden = np.asarray(torch.randn(80, 128).double())
+    w = device_weights(layer, torch.float32)
+    rng = P.Rng(7, 3)
+    got = w.experts[0].forward(torch.tensor(hidden, dtype=torch.float32, device="cuda"), 0.3, rng)
+    got = got.detach().double().cpu().numpy()
+    keep = (O.OracleRng(7, 3).uniform((80, 128)) >= 0.3) / 0.7
+    ref = (O.gelu(hidden @ layer.up[0] + layer.bias_up[0]) @ layer.down[0] + layer.bias_down[0]) * keep
+    assert np.array_equal(got == 0, ref == 0)
+    assert scaled_err(got, ref) < 1e-5
+    assert stream_position(rng._gen)[2] == 80 * 128
+
+
 def test_replica_divergence_detected():
     layer = oracle_rounded(O.init_layer(64, 2, seed=61), torch.bfloat16)
     w = device_weights(layer, torch.bfloat16)
