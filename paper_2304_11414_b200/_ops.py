@@ -111,7 +111,7 @@ def overlap_sm_budget() -> int:
     v = os.environ.get("PPMOE_OVERLAP_SMS")
     if v is not None:
         return int(v)
-    n = _lib.load().ppmoe_num_sms()
+    n = _lib.query("ppmoe_num_sms")
     return max(2, n - 16)
 
 
@@ -193,8 +193,7 @@ def route(hidden: torch.Tensor, wg: torch.Tensor, k: int, override: torch.Tensor
     scores = torch.empty((n, e), dtype=torch.float32, device=dev)
     l_aux = torch.empty(2, dtype=torch.float64, device=dev)
     cnt1 = torch.empty(e, dtype=torch.int32, device=dev)
-    lib = _lib.load()
-    ws = _ws(lib.ppmoe_route_workspace_bytes(n, e, k), dev)
+    ws = _ws(_lib.query("ppmoe_route_workspace_bytes", n, e, k), dev)
     call("ppmoe_route", ptr(hidden), dtype_code(hidden.dtype), ptr(wg), n, h, e, k, ptr(override), ptr(idx), ptr(w),
          ptr(scores), ptr(l_aux), ptr(cnt1), ptr(score_sums), ptr(ws), ws.numel(), _stream())
     return Route(idx, w, scores, l_aux, cnt1)
@@ -223,8 +222,7 @@ def route_sliced(world, group, hidden: torch.Tensor, wg: torch.Tensor, k: int,
     stats = torch.zeros((t, 4 * e), dtype=torch.int32, device=dev)  # per rank: E fp64 sums | E counts | pad
     mine = stats[me]
     l_aux_slice = torch.empty(2, dtype=torch.float64, device=dev)
-    lib = _lib.load()
-    ws = _ws(lib.ppmoe_route_workspace_bytes(nr, e, k), dev)
+    ws = _ws(_lib.query("ppmoe_route_workspace_bytes", nr, e, k), dev)
     ov = None if override is None else override[sl].contiguous()
     call("ppmoe_route", ptr(hidden[sl]), dtype_code(hidden.dtype), ptr(wg), nr, h, e, k, ptr(ov), ptr(idx[sl]),
          ptr(w[sl]), ptr(scores[sl]), ptr(l_aux_slice), ptr(mine[2 * e:3 * e]), ptr(mine[:2 * e]), ptr(ws), ws.numel(),
@@ -258,8 +256,7 @@ def plan(idx: torch.Tensor, w: torch.Tensor | None, num_experts: int, capacity: 
     tok_sorted = torch.empty(rows_cap, dtype=torch.int32, device=dev)
     w_sorted = torch.empty(rows_cap, dtype=torch.float32, device=dev)
     pair_pos = torch.empty((n, k), dtype=torch.int32, device=dev)
-    lib = _lib.load()
-    ws = _ws(lib.ppmoe_dispatch_workspace_bytes(n, e, k), dev)
+    ws = _ws(_lib.query("ppmoe_dispatch_workspace_bytes", n, e, k), dev)
     call("ppmoe_dispatch_plan", ptr(idx), ptr(w), n, e, k, int(capacity), ptr(rank_offset), ptr(counts), ptr(kept),
          ptr(seg),
          ptr(tok_sorted), ptr(w_sorted), ptr(pair_pos), rows_cap, ptr(ws), ws.numel(), _stream())
@@ -557,8 +554,7 @@ def input_grads(dxs, st: ExpertFwdState, pl: Plan, hidden, dl, wg, want_dx: bool
     dev = hidden.device
     dx = torch.empty_like(hidden) if want_dx else None
     dwg = torch.empty((h, e), dtype=torch.float32, device=dev) if want_dwg else None
-    lib = _lib.load()
-    ws = _ws(lib.ppmoe_input_grads_workspace_bytes(dt, n, h, e) if want_dwg else 0, dev)
+    ws = _ws(_lib.query("ppmoe_input_grads_workspace_bytes", dt, n, h, e) if want_dwg else 0, dev)
     call("ppmoe_input_grads", dt, ptr(dxs), ptr(st.seg), st.el, ptr(pl.pair_pos), n, k, h, ptr(hidden), ptr(dl),
          ptr(wg), e, ptr(dx), ptr(dwg), ptr(ws), ws.numel(), _stream())
     return dx, dwg
@@ -573,8 +569,7 @@ def gate_weight_grad(hidden_rows: torch.Tensor, dl_rows: torch.Tensor, wg: torch
     dwg = out if out is not None else torch.empty((h, e), dtype=torch.float32, device=hidden_rows.device)
     if n == 0:
         return dwg.zero_()
-    lib = _lib.load()
-    ws = _ws(lib.ppmoe_input_grads_workspace_bytes(dt, n, h, e), hidden_rows.device)
+    ws = _ws(_lib.query("ppmoe_input_grads_workspace_bytes", dt, n, h, e), hidden_rows.device)
     call("ppmoe_input_grads", dt, None, None, 1, None, n, 1, h, ptr(hidden_rows), ptr(dl_rows), ptr(wg), e, None,
          ptr(dwg), ptr(ws), ws.numel(), _stream())
     return dwg
@@ -587,8 +582,7 @@ def gate_grads(dx_acc, hidden, dl, wg, want_dx: bool, want_dwg: bool):
     dev = hidden.device
     dx = torch.empty_like(hidden) if want_dx else None
     dwg = torch.empty((h, e), dtype=torch.float32, device=dev) if want_dwg else None
-    lib = _lib.load()
-    ws = _ws(lib.ppmoe_gate_grad_workspace_bytes(n, h, e) if want_dwg else 0, dev)
+    ws = _ws(_lib.query("ppmoe_gate_grad_workspace_bytes", n, h, e) if want_dwg else 0, dev)
     call("ppmoe_gate_grads", ptr(dx_acc), ptr(hidden), dtype_code(hidden.dtype), ptr(dl), ptr(wg), n, h, e, ptr(dx),
          ptr(dwg), ptr(ws), ws.numel(), _stream())
     return dx, dwg

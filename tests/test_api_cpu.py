@@ -259,3 +259,25 @@ def test_bench_reference_arm_contract():
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
+
+
+def test_fastcall_bindings_generated_and_complete():
+    """csrc/fastcall.c is what tools/gen_fastcall.py generates from _lib._SIGNATURES, and the
+    built module exposes every int/size-returning entry point with the same status behaviour
+    (an invalid call raises ValueError through _lib.call without a GPU)."""
+    import importlib.util
+
+    from paper_2304_11414_b200 import _lib
+
+    spec = importlib.util.spec_from_file_location("gen_fastcall", ROOT / "tools" / "gen_fastcall.py")
+    gen = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(gen)
+    assert gen.TARGET.read_text() == gen.generate(), "run python tools/gen_fastcall.py"
+    fast = _lib._load_fast()
+    assert fast, "lib/_fastcall extension not built (make -j)"
+    import ctypes
+    want = [n for n, (res, _) in _lib._SIGNATURES.items() if res in (ctypes.c_int, ctypes.c_size_t, ctypes.c_ulonglong)]
+    assert all(hasattr(fast, n) for n in want)
+    assert _lib.query("ppmoe_route_workspace_bytes", 100, 8, 2) == _lib.load().ppmoe_route_workspace_bytes(100, 8, 2)
+    with pytest.raises(ValueError, match="zero tokens"):
+        _lib.call("ppmoe_route", None, 0, None, 0, 0, 0, 0, None, None, None, None, None, None, None, None, 0, None)
