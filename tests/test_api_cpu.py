@@ -281,3 +281,12 @@ def test_fastcall_bindings_generated_and_complete():
     assert _lib.query("ppmoe_route_workspace_bytes", 100, 8, 2) == _lib.load().ppmoe_route_workspace_bytes(100, 8, 2)
     with pytest.raises(ValueError, match="zero tokens"):
         _lib.call("ppmoe_route", None, 0, None, 0, 0, 0, 0, None, None, None, None, None, None, None, None, 0, None)
+    # pointer arguments mean what they mean to ctypes
+    v = ctypes.c_void_p()
+    arr = (ctypes.c_void_p * 3)(1, 2, 3)
+    sbuf = ctypes.create_string_buffer(64)
+    assert fast._address(None) == 0 and fast._address(12345) == 12345
+    assert fast._address(ctypes.byref(v)) == ctypes.addressof(v)
+    assert fast._address(ctypes.c_void_p(777)) == 777
+    assert fast._address(arr) == ctypes.addressof(arr)
+    assert fast._address(sbuf) == ctypes.addressof(sbuf)
