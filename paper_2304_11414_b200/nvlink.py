@@ -235,6 +235,8 @@ def _probe(world, group) -> bool:
     try:
         arena(world, group)
     except Exception as exc:  # no P2P / IPC on this box: fall back to NCCL, loudly
+        if os.environ.get("PPMOE_NVL_REQUIRE") == "1":  # tests: the exchange must come up
+            raise
         import warnings
         warnings.warn(f"NVLink exchange unavailable, using NCCL all-reduces: {exc}")
         ok = 0

@@ -8,6 +8,8 @@ ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "tests"))
 os.environ.setdefault("PYTHONDONTWRITEBYTECODE", "1")
+# multi-GPU tests must run the NVLink exchange, not silently fall back to NCCL all-reduces
+os.environ.setdefault("PPMOE_NVL_REQUIRE", "1")
 
 
 def pytest_configure(config):
