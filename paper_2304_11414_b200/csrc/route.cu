@@ -363,11 +363,11 @@ __global__ void __launch_bounds__(32 * W, MINB) router_dmma_kernel(const __nv_bf
   const int t0 = blockIdx.x * kRouteTB;
   const int span = H / W;  // columns per warp (H % (32 W) == 0)
   const int cw0 = warp * span;
-  double acc[G][NT][2], acc2[G][NT][2];  // even / odd k-steps: twice the independent DMMA chains
+  double acc[G][NT][2];
 #pragma unroll
   for (int gi = 0; gi < G; ++gi)
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) acc[gi][nt][0] = acc[gi][nt][1] = acc2[gi][nt][0] = acc2[gi][nt][1] = 0.0;
+    for (int nt = 0; nt < NT; ++nt) acc[gi][nt][0] = acc[gi][nt][1] = 0.0;
   const size_t xoff = static_cast<size_t>(8 * q);
   auto row_ptr = [&](int gi) {
     const int t = t0 + gi * 8 + g;
@@ -406,7 +406,7 @@ __global__ void __launch_bounds__(32 * W, MINB) router_dmma_kernel(const __nv_bf
         const uint32_t bits = (j & 1) ? (word >> 16) : (word & 0xFFFFu);
         const double a = slow ? static_cast<double>(__uint_as_float(bits << 16)) : bf16_fast_f64(bits);
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) dmma884((NT == 1 && (j & 1)) ? acc2[gi][nt] : acc[gi][nt], a, b[nt][j]);
+        for (int nt = 0; nt < NT; ++nt) dmma884(acc[gi][nt], a, b[nt][j]);
       }
     }
 #pragma unroll
@@ -417,8 +417,8 @@ __global__ void __launch_bounds__(32 * W, MINB) router_dmma_kernel(const __nv_bf
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
       double* p = part + ((((warp * G + gi) * NT + nt) * 32) + lane) * 2;
-      p[0] = acc[gi][nt][0] + acc2[gi][nt][0];
-      p[1] = acc[gi][nt][1] + acc2[gi][nt][1];
+      p[0] = acc[gi][nt][0];
+      p[1] = acc[gi][nt][1];
     }
   __syncthreads();
   for (int o = threadIdx.x; o < kRouteTB * E; o += blockDim.x) {  // split-K sum, warp order
