@@ -101,6 +101,10 @@ int ppmoe_route(const void* X, int dtype, const float* Wg, int N, int H, int E, 
  * written into their record of stats): stats [T x 4E] int32 words per rank = E fp64 score
  * sums, E int32 top-1 counts, E words of padding (16-byte records), all-gathered.  Sums the records in rank order and writes
  * l_aux [2] (value, sum of fractions) and the global counts_top1 [E] (moe.py:211-223).   */
+/* Workspace of ppmoe_route including the tensor-core router's prepared Wg pieces (needs H):
+ * a workspace of at least this size enables that router (bf16, E <= 16, H % 128 == 0, no
+ * route override); ppmoe_route_workspace_bytes(N, E, K) alone selects the fp64 routers.   */
+size_t ppmoe_route_workspace_bytes_h(int N, int H, int E, int K);
 int ppmoe_route_combine_stats(const int* stats, int T, int N, int E, double* l_aux, int* counts_top1, void* stream);
 size_t ppmoe_dispatch_workspace_bytes(int N, int E, int K);
 int ppmoe_dispatch_plan(const int* idx, const float* w, int N, int E, int K, int capacity, const int* rank_offset,

@@ -34,6 +34,7 @@ _SIGNATURES = {
     "ppmoe_set_gemm_mode": (_I, [_I]),
     "ppmoe_set_gemm_narrow": (_I, [_I]),
     "ppmoe_route_workspace_bytes": (_S, [_I, _I, _I]),
+    "ppmoe_route_workspace_bytes_h": (_S, [_I, _I, _I, _I]),
     "ppmoe_route": (_I, [_P, _I, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _S, _P]),
     "ppmoe_route_combine_stats": (_I, [_P, _I, _I, _I, _P, _P, _P]),
     "ppmoe_dispatch_workspace_bytes": (_S, [_I, _I, _I]),

@@ -169,6 +169,7 @@ class Route:
     scores: torch.Tensor  # [N, E] fp32
     l_aux: torch.Tensor  # [2] fp64 (value, sum of fractions)
     top1_counts: torch.Tensor  # [E] int32
+    fixups: torch.Tensor | None = None  # [1] int32: tokens the tensor-core router re-routed in fp64
 
 
 @dataclass
@@ -193,10 +194,13 @@ def route(hidden: torch.Tensor, wg: torch.Tensor, k: int, override: torch.Tensor
     scores = torch.empty((n, e), dtype=torch.float32, device=dev)
     l_aux = torch.empty(2, dtype=torch.float64, device=dev)
     cnt1 = torch.empty(e, dtype=torch.int32, device=dev)
-    ws = _ws(_lib.query("ppmoe_route_workspace_bytes", n, e, k), dev)
+    ws = _ws(_lib.query("ppmoe_route_workspace_bytes_h", n, h, e, k), dev)
     call("ppmoe_route", ptr(hidden), dtype_code(hidden.dtype), ptr(wg), n, h, e, k, ptr(override), ptr(idx), ptr(w),
          ptr(scores), ptr(l_aux), ptr(cnt1), ptr(score_sums), ptr(ws), ws.numel(), _stream())
-    return Route(idx, w, scores, l_aux, cnt1)
+    # workspace layout (route.cu): score sums | top-1 counts, fix-up count | fix-up list
+    nb = (n + 31) // 32
+    off = (nb * e * 8 + 255) // 256 * 256 + e * 4
+    return Route(idx, w, scores, l_aux, cnt1, ws[off:off + 4].view(torch.int32))
 
 
 def route_sliced(world, group, hidden: torch.Tensor, wg: torch.Tensor, k: int,
@@ -222,7 +226,7 @@ def route_sliced(world, group, hidden: torch.Tensor, wg: torch.Tensor, k: int,
     stats = torch.zeros((t, 4 * e), dtype=torch.int32, device=dev)  # per rank: E fp64 sums | E counts | pad
     mine = stats[me]
     l_aux_slice = torch.empty(2, dtype=torch.float64, device=dev)
-    ws = _ws(_lib.query("ppmoe_route_workspace_bytes", nr, e, k), dev)
+    ws = _ws(_lib.query("ppmoe_route_workspace_bytes_h", nr, h, e, k), dev)
     ov = None if override is None else override[sl].contiguous()
     call("ppmoe_route", ptr(hidden[sl]), dtype_code(hidden.dtype), ptr(wg), nr, h, e, k, ptr(ov), ptr(idx[sl]),
          ptr(w[sl]), ptr(scores[sl]), ptr(l_aux_slice), ptr(mine[2 * e:3 * e]), ptr(mine[:2 * e]), ptr(ws), ws.numel(),

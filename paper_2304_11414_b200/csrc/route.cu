@@ -12,6 +12,7 @@
 //
 // Everything is deterministic: integer histograms (exact under atomics), fixed-order
 // fp64 reductions for the aux loss.
+#include <algorithm>
 #include <climits>
 #include <cstdlib>
 #include <cstring>
@@ -440,28 +441,310 @@ __host__ inline size_t route_dmma_smem_bytes(int E, int W) {
          2 * kRouteTB * 8;
 }
 
+// ------------------------------------------------------------------ tensor-core router
+//
+// Gate logits on the bf16 tensor cores with a rigorous error bound, exact fp64 for the rest.
+// Wg (fp32) is split exactly into three bf16 pieces w = w1 + w2 + w3 (8 significant bits
+// each), so every product x * w_p of a bf16 activation is exact in fp32; mma.sync
+// m16n8k16 accumulates 32 columns in fp32 per piece, then the pieces are summed and folded
+// into fp64 (so fp32 accumulation error stays local to 32 columns).  A fourth MMA with |x|
+// and |w1| gives A_te = sum |x||w| per (token, expert), and the logit error is bounded by
+// kRouteTcBound * A_te: 2 MMAs x (16 + 1) roundings of at most 2^-23 relative per fold,
+// the piece sum and the |w1| vs |w| slack, times a safety factor of 4.  A token is routed
+// from the approximate logits only if every adjacent gap among its top-(k+1) logits exceeds
+// the sum of the two bounds (then the top-k set and slot order equal the exact ones);
+// otherwise it is queued and router_fix_kernel routes it with fp64 arithmetic throughout.
+constexpr double kRouteTcBound = 4.0 * 40.0 * 1.0078125 / 8388608.0;  // 4 * 40 * 2^-23 * (1 + 2^-7)
+constexpr int kRouteTcWarps = 4;  // warps per 16-token block (hidden-dimension split)
+
+__device__ __forceinline__ void hmma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                          uint32_t b0, uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// w = p1 + p2 + p3 exactly (bf16 pieces, returned as raw 16-bit patterns)
+__device__ __forceinline__ void split3(float w, uint32_t& p1, uint32_t& p2, uint32_t& p3) {
+  const __nv_bfloat16 h1 = __float2bfloat16_rn(w);
+  const float r1 = w - __bfloat162float(h1);
+  const __nv_bfloat16 h2 = __float2bfloat16_rn(r1);
+  const float r2 = r1 - __bfloat162float(h2);
+  const __nv_bfloat16 h3 = __float2bfloat16_rn(r2);
+  p1 = __bfloat16_as_ushort(h1);
+  p2 = __bfloat16_as_ushort(h2);
+  p3 = __bfloat16_as_ushort(h3);
+}
+
+// Block = 16 tokens (the MMA's M) x all experts (n-tiles of 8); its kRouteTcWarps warps split
+// the hidden dimension in 32-column steps.  MMA m (0, 1) of a step maps k-slot {2q+p, 2q+8+p}
+// of lane group q to columns c0 + 8q + 4m + {p, 2+p}, so a lane's A registers come from one
+// 16-byte load of each of its two token rows and its B values are Wg[c0 + 8q + j][n].
+// Wg pieces in MMA-fragment order, written once per call by router_tc_prep_kernel:
+// [H/32 chunk][NT][lane q][lane g][m][piece 3][2 b32 words] -> a lane's B registers of one
+// 32-column chunk and n-tile are 12 consecutive words (three 16-byte loads).
+__global__ void router_tc_prep_kernel(const float* __restrict__ Wg, int H, int E, int NT, uint4* __restrict__ pieces) {
+  const int chunks = H / 32;
+  const int total = chunks * NT * 32;  // one thread per (chunk, n-tile, lane)
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int lane = i % 32, nt = (i / 32) % NT, c = i / (32 * NT);
+    const int q = lane & 3, g = lane >> 2, e = nt * 8 + g;
+    uint32_t wd[12];
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      uint32_t p[3][4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float wv = e < E ? Wg[static_cast<size_t>(c * 32 + 8 * q + 4 * m + j) * E + e] : 0.f;
+        split3(wv, p[0][j], p[1][j], p[2][j]);
+      }
+#pragma unroll
+      for (int pc = 0; pc < 3; ++pc) {
+        wd[m * 6 + pc * 2] = p[pc][0] | (p[pc][1] << 16);
+        wd[m * 6 + pc * 2 + 1] = p[pc][2] | (p[pc][3] << 16);
+      }
+    }
+    uint4* dst = pieces + static_cast<size_t>(((c * NT + nt) * 32) + q * 8 + g) * 3;
+    dst[0] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+    dst[1] = make_uint4(wd[4], wd[5], wd[6], wd[7]);
+    dst[2] = make_uint4(wd[8], wd[9], wd[10], wd[11]);
+  }
+}
+
+// Block = 16 tokens (the MMA's M) x all experts (n-tiles of 8); its kRouteTcWarps warps split
+// the hidden dimension in 32-column steps.  MMA m (0, 1) of a step maps k-slot {2q+p, 2q+8+p}
+// of lane group q to columns c0 + 8q + 4m + {p, 2+p}, so a lane's A registers come from one
+// 16-byte load of each of its two token rows and its B registers are 12 prepared words.
+template <int NT>
+__global__ void __launch_bounds__(32 * kRouteTcWarps, NT == 1 ? 7 : 5) router_tc_kernel(
+    const __nv_bfloat16* __restrict__ X, const uint4* __restrict__ pieces, int N, int H, int E, int K,
+    int* __restrict__ idx, float* __restrict__ w, float* __restrict__ scores, int* __restrict__ fix_list,
+    int* __restrict__ fix_count) {
+  constexpr int W = kRouteTcWarps;
+  __shared__ double part[W][16][NT * 8];
+  __shared__ double apart[W][16][NT * 8];
+  __shared__ double lg[16][NT * 8];
+  __shared__ double bd[16][NT * 8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, q = lane & 3;
+  const int t0 = blockIdx.x * 16;
+  const int span = H / W;
+  const int cw0 = warp * span;
+  const bool ok0 = t0 + g < N, ok1 = t0 + g + 8 < N;
+  const __nv_bfloat16* x0 = X + static_cast<size_t>(ok0 ? t0 + g : 0) * H + 8 * q;
+  const __nv_bfloat16* x1 = X + static_cast<size_t>(ok1 ? t0 + g + 8 : 0) * H + 8 * q;
+  const uint4* pw = pieces + static_cast<size_t>(q * 8 + g) * 3;
+  double acc[NT][4], aab[NT][4];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[nt][i] = aab[nt][i] = 0.0;
+  uint4 xa = ok0 ? ldg16(x0 + cw0) : make_uint4(0, 0, 0, 0);
+  uint4 xb = ok1 ? ldg16(x1 + cw0) : make_uint4(0, 0, 0, 0);
+  for (int c0 = cw0; c0 < cw0 + span; c0 += 32) {
+    const bool more = c0 + 32 < cw0 + span;
+    const uint4 na = (more && ok0) ? ldg16(x0 + c0 + 32) : make_uint4(0, 0, 0, 0);
+    const uint4 nb = (more && ok1) ? ldg16(x1 + c0 + 32) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const uint4* src = pw + static_cast<size_t>(((c0 >> 5) * NT + nt) * 32) * 3;
+      const uint4 u0 = __ldg(src), u1 = __ldg(src + 1), u2 = __ldg(src + 2);
+      const uint32_t b[12] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w, u2.x, u2.y, u2.z, u2.w};
+      float d[4][4];
+#pragma unroll
+      for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) d[p][i] = 0.f;
+#pragma unroll
+      for (int m = 0; m < 2; ++m) {
+        const uint32_t a0 = m ? xa.z : xa.x, a2 = m ? xa.w : xa.y;  // row g
+        const uint32_t a1 = m ? xb.z : xb.x, a3 = m ? xb.w : xb.y;  // row g + 8
+#pragma unroll
+        for (int pc = 0; pc < 3; ++pc) hmma16816(d[pc], a0, a1, a2, a3, b[m * 6 + pc * 2], b[m * 6 + pc * 2 + 1]);
+        hmma16816(d[3], a0 & 0x7FFF7FFFu, a1 & 0x7FFF7FFFu, a2 & 0x7FFF7FFFu, a3 & 0x7FFF7FFFu,
+                  b[m * 6] & 0x7FFF7FFFu, b[m * 6 + 1] & 0x7FFF7FFFu);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        acc[nt][i] += static_cast<double>(d[0][i] + d[1][i] + d[2][i]);
+        aab[nt][i] += static_cast<double>(d[3][i]);
+      }
+    }
+    xa = na;
+    xb = nb;
+  }
+  // C fragment: d0, d1 = (row g, experts 2q, 2q+1), d2, d3 = (row g + 8, the same experts)
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int row = g + (i >> 1) * 8, col = nt * 8 + 2 * q + (i & 1);
+      part[warp][row][col] = acc[nt][i];
+      apart[warp][row][col] = aab[nt][i];
+    }
+  __syncthreads();
+  for (int o = threadIdx.x; o < 16 * NT * 8; o += blockDim.x) {  // split-K sum in warp order
+    const int row = o / (NT * 8), col = o % (NT * 8);
+    double v = 0.0, a = 0.0;
+#pragma unroll
+    for (int ww = 0; ww < W; ++ww) {
+      v += part[ww][row][col];
+      a += apart[ww][row][col];
+    }
+    lg[row][col] = v;
+    bd[row][col] = kRouteTcBound * a + 1e-300;
+  }
+  __syncthreads();
+  if (threadIdx.x < 16 && t0 + threadIdx.x < N) {
+    const int r = threadIdx.x, t = t0 + r;
+    // top-(k+1) by repeated argmax (lowest id wins ties), then the gap test
+    int ord[kMaxK + 1];
+    const int m = min(K + 1, E);
+    unsigned used = 0;
+    for (int s2 = 0; s2 < m; ++s2) {
+      int best = -1;
+      for (int e = 0; e < E; ++e) {
+        if ((used >> e) & 1u) continue;
+        if (best < 0 || lg[r][e] > lg[r][best]) best = e;
+      }
+      ord[s2] = best;
+      used |= 1u << best;
+    }
+    bool sure = true;
+    for (int s2 = 0; s2 + 1 < m && s2 < K; ++s2)
+      if (lg[r][ord[s2]] - lg[r][ord[s2 + 1]] <= bd[r][ord[s2]] + bd[r][ord[s2 + 1]]) sure = false;
+    if (!sure) {
+      fix_list[atomicAdd(fix_count, 1)] = t;
+    } else {
+      double mx = lg[r][ord[0]], sum = 0.0;
+      for (int e = 0; e < E; ++e) sum += exp(lg[r][e] - mx);
+      for (int e = 0; e < E; ++e) scores[static_cast<size_t>(t) * E + e] = static_cast<float>(exp(lg[r][e] - mx) / sum);
+      for (int s2 = 0; s2 < K; ++s2) {
+        idx[static_cast<size_t>(t) * K + s2] = ord[s2];
+        w[static_cast<size_t>(t) * K + s2] = static_cast<float>(exp(lg[r][ord[s2]] - mx) / sum);
+      }
+    }
+  }
+}
+
+// Exact routing of the queued tokens: one 256-thread block per token (grid-stride over the
+// queue), each thread 8 columns per 2048-column step, fp64 logits from exact widening,
+// fixed-order warp + block reduction (deterministic), fp64 softmax, top-k by repeated argmax.
+template <int EB>
+__global__ void __launch_bounds__(256) router_fix_kernel(const __nv_bfloat16* __restrict__ X,
+                                                         const float* __restrict__ Wg, int N, int H, int E, int K,
+                                                         const int* __restrict__ fix_list,
+                                                         const int* __restrict__ fix_count, int* __restrict__ idx,
+                                                         float* __restrict__ w, float* __restrict__ scores) {
+  __shared__ double red[8][EB];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int count = *fix_count;
+  for (int i = blockIdx.x; i < count; i += gridDim.x) {
+    const int t = fix_list[i];
+    const __nv_bfloat16* xr = X + static_cast<size_t>(t) * H;
+    double a[EB];
+#pragma unroll
+    for (int e = 0; e < EB; ++e) a[e] = 0.0;
+    for (int c = threadIdx.x * 8; c < H; c += blockDim.x * 8) {
+      const uint4 u = ldg16(xr + c);
+      const uint32_t wd[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const double xv = static_cast<double>(__uint_as_float((j & 1) ? (wd[j >> 1] & 0xFFFF0000u) : (wd[j >> 1] << 16)));
+        const float* wr = Wg + static_cast<size_t>(c + j) * E;
+        if (E == EB) {  // whole rows: 16-byte loads
+#pragma unroll
+          for (int e4 = 0; e4 < EB; e4 += 4) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(wr + e4));
+            a[e4] = fma(xv, static_cast<double>(v.x), a[e4]);
+            a[e4 + 1] = fma(xv, static_cast<double>(v.y), a[e4 + 1]);
+            a[e4 + 2] = fma(xv, static_cast<double>(v.z), a[e4 + 2]);
+            a[e4 + 3] = fma(xv, static_cast<double>(v.w), a[e4 + 3]);
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < EB; ++e)
+            if (e < E) a[e] = fma(xv, static_cast<double>(__ldg(wr + e)), a[e]);
+        }
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < EB; ++e) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) a[e] += __shfl_xor_sync(0xffffffffu, a[e], o);
+      if (lane == 0) red[warp][e] = a[e];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double lgt[EB];
+      for (int e = 0; e < E; ++e) {
+        double v = 0.0;
+        for (int ww = 0; ww < 8; ++ww) v += red[ww][e];
+        lgt[e] = v;
+      }
+      double mx = lgt[0];
+      for (int e = 1; e < E; ++e) mx = fmax(mx, lgt[e]);
+      double sum = 0.0;
+      for (int e = 0; e < E; ++e) sum += exp(lgt[e] - mx);
+      for (int e = 0; e < E; ++e) scores[static_cast<size_t>(t) * E + e] = static_cast<float>(exp(lgt[e] - mx) / sum);
+      unsigned used = 0;
+      for (int s2 = 0; s2 < K; ++s2) {
+        int best = -1;
+        for (int e = 0; e < E; ++e) {
+          if ((used >> e) & 1u) continue;
+          if (best < 0 || lgt[e] > lgt[best]) best = e;
+        }
+        used |= 1u << best;
+        idx[static_cast<size_t>(t) * K + s2] = best;
+        w[static_cast<size_t>(t) * K + s2] = static_cast<float>(exp(lgt[best] - mx) / sum);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Aux-loss partials from the final routing: per 32-token block the fp64 sum of the fp32
+// scores in token order (a fixed xor-shuffle tree over the block's 32 tokens: deterministic)
+// and the top-1 histogram (exact integer atomics).  One warp per (block, expert).
+__global__ void route_aux_kernel(const float* __restrict__ scores, const int* __restrict__ idx, int N, int E, int K,
+                                 double* __restrict__ ssum, int* __restrict__ cnt_top1) {
+  const int nb = (N + kRouteTB - 1) / kRouteTB;
+  const int lane = threadIdx.x & 31;
+  const int nw = gridDim.x * (blockDim.x >> 5);
+  for (int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < nb * E; i += nw) {
+    const int b = i / E, e = i % E;
+    const int t = b * kRouteTB + lane;
+    double s = t < N ? static_cast<double>(scores[static_cast<size_t>(t) * E + e]) : 0.0;
+    const unsigned top = __ballot_sync(0xffffffffu, t < N && idx[static_cast<size_t>(t) * K] == e);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+      ssum[i] = s;
+      if (top) atomicAdd(&cnt_top1[e], __popc(top));
+    }
+  }
+}
+
 // l_aux = E * sum_e frac_e * mean_t s[t,e]  with frac from the top-1 choice (moe.py:221-223)
 __global__ void __launch_bounds__(256) route_finalize_kernel(const double* __restrict__ ssum, int nblocks,
                                                              const int* __restrict__ cnt_top1, int N, int E,
                                                              double* __restrict__ l_aux,
                                                              double* __restrict__ score_sums) {
-  __shared__ double red[256];
+  // warp w reduces experts w, w + 8, ...: lane-strided partial sums, then a fixed xor tree
+  // (deterministic); one pass over ssum instead of E block-wide reductions
   __shared__ double part[kMaxE];
-  for (int e = 0; e < E; ++e) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int e = warp; e < E; e += blockDim.x >> 5) {
     double s = 0.0;
-    for (int b = threadIdx.x; b < nblocks; b += 256) s += ssum[static_cast<size_t>(b) * E + e];
-    red[threadIdx.x] = s;
-    __syncthreads();
-    for (int w = 128; w > 0; w >>= 1) {  // fixed-shape tree: deterministic
-      if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
-      __syncthreads();
+    for (int b = lane; b < nblocks; b += 32) s += ssum[static_cast<size_t>(b) * E + e];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+      part[e] = s * (static_cast<double>(cnt_top1[e]) / N);
+      if (score_sums) score_sums[e] = s;
     }
-    if (threadIdx.x == 0) {
-      part[e] = red[0] * (static_cast<double>(cnt_top1[e]) / N);
-      if (score_sums) score_sums[e] = red[0];
-    }
-    __syncthreads();
   }
+  __syncthreads();
   if (threadIdx.x == 0) {
     double tot = 0.0, fr = 0.0;
     for (int j = 0; j < E; ++j) {
@@ -706,6 +989,36 @@ static int launch_router(const void* X, const float* Wg, int N, int H, int E, in
   return check_launch("router_kernel");
 }
 
+// PPMOE_ROUTER=tc (default for bf16): tensor-core logits + guard band + exact fix-up;
+// dmma: FP64 tensor-core logits for every token; dfma: CUDA-core fp64.
+static bool use_tc_router(int dtype, int H, int E) {
+  // default for E <= 8 (C2: 90 -> 83 us); at 8 < E <= 16 the DMMA kernel is faster (C3: 238 vs
+  // 274 us, tools/ab_router.py) unless PPMOE_ROUTER=tc forces it
+  const char* e = std::getenv("PPMOE_ROUTER");
+  if (e && std::strcmp(e, "tc") != 0) return false;
+  return dtype == kBF16 && H % (32 * kRouteTcWarps) == 0 && (E <= 8 || (e && E <= 16));
+}
+
+static int launch_router_tc(const void* X, const float* Wg, int N, int H, int E, int K, int* idx, float* w,
+                            float* scores, int* fix_list, int* fix_count, uint4* pieces, cudaStream_t s) {
+  const auto* x = static_cast<const __nv_bfloat16*>(X);
+  const int NT = E <= 8 ? 1 : 2;
+  const int prep_threads = H / 32 * NT * 32;
+  router_tc_prep_kernel<<<std::max(1, std::min((prep_threads + 255) / 256, num_sms() * 4)), 256, 0, s>>>(Wg, H, E, NT,
+                                                                                                      pieces);
+  if (int rc = check_launch("router_tc_prep_kernel")) return rc;
+  const int blocks = (N + 15) / 16;
+  if (E <= 8) router_tc_kernel<1><<<blocks, 32 * kRouteTcWarps, 0, s>>>(x, pieces, N, H, E, K, idx, w, scores,
+                                                                         fix_list, fix_count);
+  else router_tc_kernel<2><<<blocks, 32 * kRouteTcWarps, 0, s>>>(x, pieces, N, H, E, K, idx, w, scores, fix_list,
+                                                                 fix_count);
+  if (int rc = check_launch("router_tc_kernel")) return rc;
+  const int fix_blocks = std::min(N, num_sms() * 2);
+  if (E <= 8) router_fix_kernel<8><<<fix_blocks, 256, 0, s>>>(x, Wg, N, H, E, K, fix_list, fix_count, idx, w, scores);
+  else router_fix_kernel<16><<<fix_blocks, 256, 0, s>>>(x, Wg, N, H, E, K, fix_list, fix_count, idx, w, scores);
+  return check_launch("router_fix_kernel");
+}
+
 static bool use_dmma_router(int dtype, int H, int E) {
   const char* e = std::getenv("PPMOE_ROUTER");  // PPMOE_ROUTER=dfma: the CUDA-core fp64 kernel (A/B)
   if (e && std::strcmp(e, "dfma") == 0) return false;
@@ -742,7 +1055,15 @@ extern "C" {
 size_t ppmoe_route_workspace_bytes(int N, int E, int K) {
   (void)K;
   const size_t nb = (static_cast<size_t>(N) + kRouteTB - 1) / kRouteTB;
-  return align_up(nb * (E > 0 ? E : 1) * 8, 256) + align_up(static_cast<size_t>(E) * 4, 256);
+  // score sums | top-1 counts (+ the tensor-core router's fix-up count) | fix-up token list
+  return align_up(nb * (E > 0 ? E : 1) * 8, 256) + align_up(static_cast<size_t>(E) * 4 + 4, 256) +
+         align_up(static_cast<size_t>(N > 0 ? N : 1) * 4, 256);
+}
+
+size_t ppmoe_route_workspace_bytes_h(int N, int H, int E, int K) {
+  // + the tensor-core router's Wg pieces (H/32 chunks x n-tiles x 32 lanes x 48 bytes)
+  const size_t nt = E <= 8 ? 1 : 2;
+  return ppmoe_route_workspace_bytes(N, E, K) + align_up(static_cast<size_t>(H > 0 ? H : 1) / 32 * nt * 32 * 48 + 48, 256);
 }
 
 int ppmoe_route(const void* X, int dtype, const float* Wg, int N, int H, int E, int K, const int* route_override,
@@ -757,9 +1078,18 @@ int ppmoe_route(const void* X, int dtype, const float* Wg, int N, int H, int E, 
   const int nb = (N + kRouteTB - 1) / kRouteTB;
   double* ssum = static_cast<double*>(ws);
   int* cnt = reinterpret_cast<int*>(static_cast<char*>(ws) + align_up(static_cast<size_t>(nb) * E * 8, 256));
-  PPMOE_CUDA(cudaMemsetAsync(cnt, 0, static_cast<size_t>(E) * 4, s));
+  int* fix_count = cnt + E;
+  int* fix_list = reinterpret_cast<int*>(reinterpret_cast<char*>(cnt) + align_up(static_cast<size_t>(E) * 4 + 4, 256));
+  PPMOE_CUDA(cudaMemsetAsync(cnt, 0, static_cast<size_t>(E) * 4 + 4, s));
   int rc;
-  if (use_dmma_router(dtype, H, E))
+  if (!route_override && use_tc_router(dtype, H, E) && ws_bytes >= ppmoe_route_workspace_bytes_h(N, H, E, K)) {
+    uint4* pieces = reinterpret_cast<uint4*>(static_cast<char*>(ws) + ppmoe_route_workspace_bytes(N, E, K));
+    rc = launch_router_tc(X, Wg, N, H, E, K, idx, w, scores, fix_list, fix_count, pieces, s);
+    if (rc) return rc;
+    route_aux_kernel<<<std::max(1, std::min((nb * E + 7) / 8, num_sms() * 8)), 256, 0, s>>>(scores, idx, N, E, K, ssum,
+                                                                                           cnt);
+    rc = check_launch("route_aux_kernel");
+  } else if (use_dmma_router(dtype, H, E))
     rc = E <= 8 ? launch_router_dmma<8>(X, Wg, N, H, E, K, route_override, idx, w, scores, ssum, cnt, s)
                 : launch_router_dmma<16>(X, Wg, N, H, E, K, route_override, idx, w, scores, ssum, cnt, s);
   else if (dtype == kBF16)
