@@ -788,3 +788,33 @@ def test_no_out_of_bounds_writes(monkeypatch, n, h, e, k, tp, cf, drop, dtype):
                                  top_k=k, capacity_factor=cf)
     (out.float().sum() + l_aux).backward()
     assert _ops.check_guards() >= 5
+
+
+@pytest.mark.parametrize("case", ["near_tie", "all_tie", "random"])
+def test_tensor_core_router_guard_band(case):
+    """The default bf16 router (tensor-core logits + error bound + fp64 fix-up) stays bit-exact
+    against the fp64 oracle when logits nearly tie (two gate columns 1e-7 apart: most tokens
+    must be re-routed in fp64) and when they tie exactly (zero gate: every token re-routed,
+    lowest expert id wins), and re-routes only a small fraction of random tokens."""
+    from paper_2304_11414_b200 import _ops
+
+    n, h, e, k = 4096, 1024, 8, 2
+    g = torch.Generator(device="cuda").manual_seed(77)
+    x = torch.randn(n, h, device="cuda", generator=g).bfloat16()
+    wg = (torch.randn(h, e, device="cuda", generator=g) * h ** -0.5).float()
+    if case == "near_tie":
+        wg[:, 1] = wg[:, 0] + 1e-7 * torch.randn(h, device="cuda", generator=g)
+    elif case == "all_tie":
+        wg.zero_()
+    rt = _ops.route(x, wg, k)
+    ref = O.gate_topk(x.double().cpu().numpy(), wg.double().cpu().numpy(), k)
+    assert np.array_equal(rt.idx.cpu().numpy(), ref.indices)
+    assert np.abs(rt.w.cpu().numpy() - ref.weights).max() < 1e-6
+    assert abs(float(rt.l_aux[0]) - ref.l_aux) < 1e-5
+    fix = int(rt.fixups[0])
+    if case == "all_tie":
+        assert fix == n
+    elif case == "near_tie":
+        assert fix > n // 4
+    else:
+        assert fix < n // 20
