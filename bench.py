@@ -525,7 +525,7 @@ def main():
                 "router": {"kernel": "tensor-core logits + guard band + fp64 fix-up" if E <= 8 else
                            "FP64 tensor-core (DMMA) logits",
                            "fixup_tokens": router_fixups if E <= 8 else None,
-                           "fixup_scope": "tokens of this rank's routing slice re-routed in fp64 "
+                           "fixup_scope": "tokens of the full N-token batch re-routed in fp64 by one routing call "
                                           "(adjacent top-(k+1) logit gap within the error bound)"},
                 "gemm_launches_per_step": gemm_launches}
         print(json.dumps(line), flush=True)
