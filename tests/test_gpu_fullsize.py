@@ -81,11 +81,11 @@ def test_baseline_inputs_routing_bit_exact(cfg, k, cf, drops):
                       "top1_counts": ref.top1_counts.tolist()}))
 
 
-def _full_layer_check(cfg, k, cf, tol=TOL[torch.bfloat16]):
+def _full_layer_check(cfg, k, cf, tol=TOL[torch.bfloat16], dtype=torch.bfloat16):
     h, e = {"C2": (4096, 8), "C3": (8192, 16)}[cfg]
     n = 16384
-    w = P.MoeLayerWeights.init(h, e, P.Rng(0), device="cuda")
-    x = baseline_hidden(n, h).requires_grad_()
+    w = P.MoeLayerWeights.init(h, e, P.Rng(0), device="cuda", dtype=dtype)
+    x = P.Rng(1, 99).normal_tensor((n, h), dtype=dtype, device="cuda").requires_grad_()
     out, l_aux = P.ppmoe_forward(P.World(1, 1), P.ProcessGroup(P.EP, (0,)), x, w.gate, [w.bank], top_k=k,
                                  capacity_factor=cf)
     torch.autograd.backward([out, l_aux], [torch.ones_like(out), torch.ones_like(l_aux)])
@@ -127,6 +127,13 @@ def test_c2_full_size_every_gradient(k, cf):
     parameter gradients over every element, against the fp64 closed form.  Top-2 is the
     BASELINE config; top-1 with cf 1.0 is the reference's own routing with 143 dropped tokens."""
     _full_layer_check("C2", k, cf)
+
+
+def test_c2_fp32_full_size_every_gradient():
+    """The reference-precision mode (fp32 activations and experts, CUDA-core grouped GEMM) at the
+    full C2 shape with the reference's own routing (top-1): every output and gradient element
+    against the fp64 closed form at the north_star's fp32 bar, rtol 1e-4."""
+    _full_layer_check("C2", 1, math.inf, tol=TOL[torch.float32], dtype=torch.float32)
 
 
 def test_c3_full_size_every_gradient():
