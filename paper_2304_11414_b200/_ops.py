@@ -197,9 +197,8 @@ def route(hidden: torch.Tensor, wg: torch.Tensor, k: int, override: torch.Tensor
     ws = _ws(_lib.query("ppmoe_route_workspace_bytes_h", n, h, e, k), dev)
     call("ppmoe_route", ptr(hidden), dtype_code(hidden.dtype), ptr(wg), n, h, e, k, ptr(override), ptr(idx), ptr(w),
          ptr(scores), ptr(l_aux), ptr(cnt1), ptr(score_sums), ptr(ws), ws.numel(), _stream())
-    # workspace layout (route.cu): score sums | top-1 counts, fix-up count | fix-up list
-    nb = (n + 31) // 32
-    off = (nb * e * 8 + 255) // 256 * 256 + e * 4
+    # workspace layout (route.cu): score-sum records (one per 16 tokens) | top-1 counts, fix-up count | queue
+    off = ((n + 15) // 16 * e * 8 + 255) // 256 * 256 + e * 4
     return Route(idx, w, scores, l_aux, cnt1, ws[off:off + 4].view(torch.int32))
 
 

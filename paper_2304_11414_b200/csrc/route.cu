@@ -455,6 +455,7 @@ __host__ inline size_t route_dmma_smem_bytes(int E, int W) {
 // the sum of the two bounds (then the top-k set and slot order equal the exact ones);
 // otherwise it is queued and router_fix_kernel routes it with fp64 arithmetic throughout.
 constexpr double kRouteTcBound = 4.0 * 40.0 * 1.0078125 / 8388608.0;  // 4 * 40 * 2^-23 * (1 + 2^-7)
+constexpr int kFinalizeThreads = 512;
 constexpr int kRouteTcWarps = 4;  // warps per 16-token block (hidden-dimension split)
 
 __device__ __forceinline__ void hmma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
@@ -476,6 +477,140 @@ __device__ __forceinline__ void split3(float w, uint32_t& p1, uint32_t& p2, uint
   p3 = __bfloat16_as_ushort(h3);
 }
 
+// Exact routing of the queued tokens (the tensor-core router wrote its best guess and counted
+// its top-1; both are corrected here, and the last fixer of a 16-token block rewrites the
+// block's aux partial from the final scores): one kFixThreads block per token (grid-stride over
+// the queue).  Thread i takes columns i, i + kFixThreads, ... four at a time with every load of
+// the four issued up front (one memory round trip per four columns), fp64 logits from exact
+// widening, fixed-order warp + block reduction (deterministic), fp64 softmax, top-k by argmax.
+constexpr int kFixThreads = 512;
+template <int EB>
+__global__ void __launch_bounds__(kFixThreads) router_fix_kernel(const __nv_bfloat16* __restrict__ X,
+                                                                 const float* __restrict__ Wg, int N, int H, int E,
+                                                                 int K, const int* __restrict__ fix_list,
+                                                                 const int* __restrict__ fix_count,
+                                                                 int* __restrict__ idx, float* __restrict__ w,
+                                                                 float* __restrict__ scores, int* __restrict__ cnt_top1,
+                                                                 int* __restrict__ pending, double* __restrict__ ssum) {
+  constexpr int U = 4;
+  constexpr int NW = kFixThreads / 32;
+  __shared__ double red[NW][EB];
+  __shared__ double lgt[EB], ex[EB];
+  __shared__ float tile[16][EB];
+  __shared__ int last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int count = *fix_count;
+  const unsigned short* xs = reinterpret_cast<const unsigned short*>(X);
+  for (int i = blockIdx.x; i < count; i += gridDim.x) {
+    const int t = fix_list[i];
+    const unsigned short* xr = xs + static_cast<size_t>(t) * H;
+    double a[EB];
+#pragma unroll
+    for (int e = 0; e < EB; ++e) a[e] = 0.0;
+    for (int c0 = threadIdx.x; c0 < H; c0 += kFixThreads * U) {
+      float xv[U];
+      float4 wv[U][EB / 4];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int c = c0 + u * kFixThreads;
+        const bool ok = c < H;
+        xv[u] = ok ? __uint_as_float(static_cast<uint32_t>(__ldg(xr + c)) << 16) : 0.f;
+        const float* wr = Wg + static_cast<size_t>(ok ? c : 0) * E;
+#pragma unroll
+        for (int e4 = 0; e4 < EB / 4; ++e4) {
+          if (E == EB) {  // whole rows: 16-byte loads
+            wv[u][e4] = __ldg(reinterpret_cast<const float4*>(wr) + e4);
+          } else {
+            const int e = 4 * e4;
+            wv[u][e4] = make_float4(e < E ? __ldg(wr + e) : 0.f, e + 1 < E ? __ldg(wr + e + 1) : 0.f,
+                                    e + 2 < E ? __ldg(wr + e + 2) : 0.f, e + 3 < E ? __ldg(wr + e + 3) : 0.f);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const double x = static_cast<double>(xv[u]);
+#pragma unroll
+        for (int e4 = 0; e4 < EB / 4; ++e4) {
+          a[4 * e4] = fma(x, static_cast<double>(wv[u][e4].x), a[4 * e4]);
+          a[4 * e4 + 1] = fma(x, static_cast<double>(wv[u][e4].y), a[4 * e4 + 1]);
+          a[4 * e4 + 2] = fma(x, static_cast<double>(wv[u][e4].z), a[4 * e4 + 2]);
+          a[4 * e4 + 3] = fma(x, static_cast<double>(wv[u][e4].w), a[4 * e4 + 3]);
+        }
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < EB; ++e) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) a[e] += __shfl_xor_sync(0xffffffffu, a[e], o);
+      if (lane == 0) red[warp][e] = a[e];
+    }
+    __syncthreads();
+    if (threadIdx.x < E) {  // fixed-order block sum; then exps and divisions one expert per thread
+      double v = 0.0;
+      for (int ww = 0; ww < NW; ++ww) v += red[ww][threadIdx.x];
+      lgt[threadIdx.x] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double mx = lgt[0];
+      for (int e = 1; e < E; ++e) mx = fmax(mx, lgt[e]);
+      red[0][0] = mx;
+    }
+    __syncthreads();
+    if (threadIdx.x < E) ex[threadIdx.x] = exp(lgt[threadIdx.x] - red[0][0]);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double sum = 0.0;
+      for (int e = 0; e < E; ++e) sum += ex[e];
+      red[0][1] = sum;
+    }
+    __syncthreads();
+    if (threadIdx.x < E) {
+      const float sc = static_cast<float>(ex[threadIdx.x] / red[0][1]);
+      scores[static_cast<size_t>(t) * E + threadIdx.x] = sc;
+      ex[threadIdx.x] = sc;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned used = 0;
+      for (int s2 = 0; s2 < K; ++s2) {
+        int best = -1;
+        for (int e = 0; e < E; ++e) {
+          if ((used >> e) & 1u) continue;
+          if (best < 0 || lgt[e] > lgt[best]) best = e;
+        }
+        used |= 1u << best;
+        if (s2 == 0 && idx[static_cast<size_t>(t) * K] != best) {  // the queued top-1 guess was wrong
+          atomicSub(&cnt_top1[idx[static_cast<size_t>(t) * K]], 1);
+          atomicAdd(&cnt_top1[best], 1);
+        }
+        idx[static_cast<size_t>(t) * K + s2] = best;
+        w[static_cast<size_t>(t) * K + s2] = static_cast<float>(ex[best]);
+      }
+    }
+    __threadfence();  // this token's scores before the block's queued count drops
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicSub(&pending[t / 16], 1) == 1;
+    __syncthreads();
+    if (last) {  // every queued token of this 16-token block is final: rewrite its aux partial
+      __threadfence();
+      const int b = t / 16;
+      if (threadIdx.x < 16 * E) {
+        const int r = threadIdx.x / E, e = threadIdx.x % E;
+        tile[r][e] = b * 16 + r < N ? __ldcg(&scores[static_cast<size_t>(b) * 16 * E + threadIdx.x]) : 0.f;
+      }
+      __syncthreads();
+      if (threadIdx.x < E) {
+        double v = 0.0;
+        for (int r = 0; r < 16; ++r) v += tile[r][threadIdx.x];
+        ssum[static_cast<size_t>(b) * E + threadIdx.x] = v;
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // Block = 16 tokens (the MMA's M) x all experts (n-tiles of 8); its kRouteTcWarps warps split
 // the hidden dimension in 32-column steps.  MMA m (0, 1) of a step maps k-slot {2q+p, 2q+8+p}
 // of lane group q to columns c0 + 8q + 4m + {p, 2+p}, so a lane's A registers come from one
@@ -483,7 +618,9 @@ __device__ __forceinline__ void split3(float w, uint32_t& p1, uint32_t& p2, uint
 // Wg pieces in MMA-fragment order, written once per call by router_tc_prep_kernel:
 // [H/32 chunk][NT][lane q][lane g][m][piece 3][2 b32 words] -> a lane's B registers of one
 // 32-column chunk and n-tile are 12 consecutive words (three 16-byte loads).
-__global__ void router_tc_prep_kernel(const float* __restrict__ Wg, int H, int E, int NT, uint4* __restrict__ pieces) {
+__global__ void router_tc_prep_kernel(const float* __restrict__ Wg, int H, int E, int NT, uint4* __restrict__ pieces,
+                                      int* __restrict__ zero) {
+  if (blockIdx.x == 0 && threadIdx.x <= E) zero[threadIdx.x] = 0;  // top-1 counts + fix-up count
   const int chunks = H / 32;
   const int total = chunks * NT * 32;  // one thread per (chunk, n-tile, lane)
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
@@ -504,51 +641,86 @@ __global__ void router_tc_prep_kernel(const float* __restrict__ Wg, int H, int E
         wd[m * 6 + pc * 2 + 1] = p[pc][2] | (p[pc][3] << 16);
       }
     }
-    uint4* dst = pieces + static_cast<size_t>(((c * NT + nt) * 32) + q * 8 + g) * 3;
+    uint4* dst = pieces + static_cast<size_t>(c * NT + nt) * 96 + lane;  // [chunk][n-tile][3][lane]
     dst[0] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
-    dst[1] = make_uint4(wd[4], wd[5], wd[6], wd[7]);
-    dst[2] = make_uint4(wd[8], wd[9], wd[10], wd[11]);
+    dst[32] = make_uint4(wd[4], wd[5], wd[6], wd[7]);
+    dst[64] = make_uint4(wd[8], wd[9], wd[10], wd[11]);
   }
 }
 
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+
 // Block = 16 tokens (the MMA's M) x all experts (n-tiles of 8); its kRouteTcWarps warps split
 // the hidden dimension in 32-column steps.  MMA m (0, 1) of a step maps k-slot {2q+p, 2q+8+p}
-// of lane group q to columns c0 + 8q + 4m + {p, 2+p}, so a lane's A registers come from one
-// 16-byte load of each of its two token rows and its B registers are 12 prepared words.
-template <int NT>
-__global__ void __launch_bounds__(32 * kRouteTcWarps, NT == 1 ? 7 : 5) router_tc_kernel(
-    const __nv_bfloat16* __restrict__ X, const uint4* __restrict__ pieces, int N, int H, int E, int K,
-    int* __restrict__ idx, float* __restrict__ w, float* __restrict__ scores, int* __restrict__ fix_list,
-    int* __restrict__ fix_count) {
+// of lane group q to columns c0 + 8q + 4m + {p, 2+p}, so a lane's A registers are one 16-byte
+// chunk of each of its two token rows, and its B registers are 12 prepared words.  Each lane
+// streams its own chunks through a private cp.async ring in shared memory (S steps
+// deep: the bytes in flight do not cost registers); tokens past N are zero-filled.
+// Tokens whose routing the error bound cannot certify get the block's best guess and are queued
+// for router_fix_kernel.  The block then writes its aux-loss partial (fp64 sums of its 16 tokens'
+// stored fp32 scores, in token order) and adds its top-1 counts; route_finalize_kernel recomputes
+// the partials of blocks with queued tokens once those are fixed.
+template <int NT, int S>
+__global__ void __launch_bounds__(32 * kRouteTcWarps, NT == 1 ? (S == 2 ? 7 : 6) : 5) router_tc_kernel(
+    const __nv_bfloat16* __restrict__ X, const float* __restrict__ Wg, const uint4* __restrict__ pieces, int N, int H,
+    int E, int K, int* __restrict__ idx, float* __restrict__ w, float* __restrict__ scores, double* __restrict__ ssum,
+    int* __restrict__ cnt_top1, int* __restrict__ fix_list, int* __restrict__ fix_count, int* __restrict__ pending) {
   constexpr int W = kRouteTcWarps;
-  __shared__ double part[W][16][NT * 8];
-  __shared__ double apart[W][16][NT * 8];
-  __shared__ double lg[16][NT * 8];
-  __shared__ double bd[16][NT * 8];
+  constexpr int EB = NT * 8;
+  // the cp.async ring and the split-K partials share one buffer (ring dead once the loop ends)
+  constexpr int R = 2 + 3 * NT;  // 16-byte chunks per lane and step: x rows g, g + 8, the pieces
+  constexpr int kRingBytes = W * S * R * 32 * 16, kPartBytes = 2 * W * 16 * EB * 8;
+  __shared__ __align__(16) unsigned char sbuf[kRingBytes > kPartBytes ? kRingBytes : kPartBytes];
+  auto ring = reinterpret_cast<uint4(*)[S][R][32]>(sbuf);
+  auto part = reinterpret_cast<double(*)[16][EB]>(sbuf);
+  auto apart = reinterpret_cast<double(*)[16][EB]>(sbuf + kPartBytes / 2);
+  __shared__ double lg[16][EB];
+  __shared__ double bd[16][EB];
+  __shared__ int flagged[16], top1[16];
+  __shared__ int nflag;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, q = lane & 3;
   const int t0 = blockIdx.x * 16;
   const int span = H / W;
   const int cw0 = warp * span;
+  const int nsteps = span / 32;
   const bool ok0 = t0 + g < N, ok1 = t0 + g + 8 < N;
-  const __nv_bfloat16* x0 = X + static_cast<size_t>(ok0 ? t0 + g : 0) * H + 8 * q;
-  const __nv_bfloat16* x1 = X + static_cast<size_t>(ok1 ? t0 + g + 8 : 0) * H + 8 * q;
-  const uint4* pw = pieces + static_cast<size_t>(q * 8 + g) * 3;
+  const __nv_bfloat16* x0 = X + static_cast<size_t>(ok0 ? t0 + g : 0) * H + 8 * q + cw0;
+  const __nv_bfloat16* x1 = X + static_cast<size_t>(ok1 ? t0 + g + 8 : 0) * H + 8 * q + cw0;
+  const uint4* pw = pieces + static_cast<size_t>(cw0 >> 5) * NT * 96 + lane;
+  if (threadIdx.x == 0) nflag = 0;
   double acc[NT][4], aab[NT][4];
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
     for (int i = 0; i < 4; ++i) acc[nt][i] = aab[nt][i] = 0.0;
-  uint4 xa = ok0 ? ldg16(x0 + cw0) : make_uint4(0, 0, 0, 0);
-  uint4 xb = ok1 ? ldg16(x1 + cw0) : make_uint4(0, 0, 0, 0);
-  for (int c0 = cw0; c0 < cw0 + span; c0 += 32) {
-    const bool more = c0 + 32 < cw0 + span;
-    const uint4 na = (more && ok0) ? ldg16(x0 + c0 + 32) : make_uint4(0, 0, 0, 0);
-    const uint4 nb = (more && ok1) ? ldg16(x1 + c0 + 32) : make_uint4(0, 0, 0, 0);
+  auto issue = [&](int step) {
+    if (step < nsteps) {
+      uint4(*slot)[32] = ring[warp][step % S];
+      cp_async16(smem_u32(&slot[0][lane]), x0 + step * 32, ok0);
+      cp_async16(smem_u32(&slot[1][lane]), x1 + step * 32, ok1);
+#pragma unroll
+      for (int u = 0; u < 3 * NT; ++u) cp_async16(smem_u32(&slot[2 + u][lane]), pw + (step * NT * 3 + u) * 32, true);
+    }
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int st = 0; st < S - 1; ++st) issue(st);
+  for (int step = 0; step < nsteps; ++step) {
+    issue(step + S - 1);
+    cp_async_wait<S - 1>();
+    const uint4(*slot)[32] = ring[warp][step % S];
+    const uint4 xa = slot[0][lane];
+    const uint4 xb = slot[1][lane];
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
-      const uint4* src = pw + static_cast<size_t>(((c0 >> 5) * NT + nt) * 32) * 3;
-      const uint4 u0 = __ldg(src), u1 = __ldg(src + 1), u2 = __ldg(src + 2);
+      const uint4 u0 = slot[2 + 3 * nt][lane], u1 = slot[3 + 3 * nt][lane], u2 = slot[4 + 3 * nt][lane];
       const uint32_t b[12] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w, u2.x, u2.y, u2.z, u2.w};
       float d[4][4];
 #pragma unroll
@@ -570,9 +742,9 @@ __global__ void __launch_bounds__(32 * kRouteTcWarps, NT == 1 ? 7 : 5) router_tc
         aab[nt][i] += static_cast<double>(d[3][i]);
       }
     }
-    xa = na;
-    xb = nb;
   }
+  cp_async_wait<0>();
+  __syncthreads();  // every warp is done with its ring before the partials overwrite it
   // C fragment: d0, d1 = (row g, experts 2q, 2q+1), d2, d3 = (row g + 8, the same experts)
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt)
@@ -583,8 +755,8 @@ __global__ void __launch_bounds__(32 * kRouteTcWarps, NT == 1 ? 7 : 5) router_tc
       apart[warp][row][col] = aab[nt][i];
     }
   __syncthreads();
-  for (int o = threadIdx.x; o < 16 * NT * 8; o += blockDim.x) {  // split-K sum in warp order
-    const int row = o / (NT * 8), col = o % (NT * 8);
+  for (int o = threadIdx.x; o < 16 * EB; o += blockDim.x) {  // split-K sum in warp order
+    const int row = o / EB, col = o % EB;
     double v = 0.0, a = 0.0;
 #pragma unroll
     for (int ww = 0; ww < W; ++ww) {
@@ -596,7 +768,7 @@ __global__ void __launch_bounds__(32 * kRouteTcWarps, NT == 1 ? 7 : 5) router_tc
   }
   __syncthreads();
   if (threadIdx.x < 16 && t0 + threadIdx.x < N) {
-    const int r = threadIdx.x, t = t0 + r;
+    const int r = threadIdx.x;
     // top-(k+1) by repeated argmax (lowest id wins ties), then the gap test
     int ord[kMaxK + 1];
     const int m = min(K + 1, E);
@@ -613,145 +785,109 @@ __global__ void __launch_bounds__(32 * kRouteTcWarps, NT == 1 ? 7 : 5) router_tc
     bool sure = true;
     for (int s2 = 0; s2 + 1 < m && s2 < K; ++s2)
       if (lg[r][ord[s2]] - lg[r][ord[s2 + 1]] <= bd[r][ord[s2]] + bd[r][ord[s2 + 1]]) sure = false;
-    if (!sure) {
-      fix_list[atomicAdd(fix_count, 1)] = t;
-    } else {
-      double mx = lg[r][ord[0]], sum = 0.0;
-      for (int e = 0; e < E; ++e) sum += exp(lg[r][e] - mx);
-      for (int e = 0; e < E; ++e) scores[static_cast<size_t>(t) * E + e] = static_cast<float>(exp(lg[r][e] - mx) / sum);
-      for (int s2 = 0; s2 < K; ++s2) {
-        idx[static_cast<size_t>(t) * K + s2] = ord[s2];
-        w[static_cast<size_t>(t) * K + s2] = static_cast<float>(exp(lg[r][ord[s2]] - mx) / sum);
-      }
-    }
-  }
-}
-
-// Exact routing of the queued tokens: one 256-thread block per token (grid-stride over the
-// queue), each thread 8 columns per 2048-column step, fp64 logits from exact widening,
-// fixed-order warp + block reduction (deterministic), fp64 softmax, top-k by repeated argmax.
-template <int EB>
-__global__ void __launch_bounds__(256) router_fix_kernel(const __nv_bfloat16* __restrict__ X,
-                                                         const float* __restrict__ Wg, int N, int H, int E, int K,
-                                                         const int* __restrict__ fix_list,
-                                                         const int* __restrict__ fix_count, int* __restrict__ idx,
-                                                         float* __restrict__ w, float* __restrict__ scores) {
-  __shared__ double red[8][EB];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int count = *fix_count;
-  for (int i = blockIdx.x; i < count; i += gridDim.x) {
-    const int t = fix_list[i];
-    const __nv_bfloat16* xr = X + static_cast<size_t>(t) * H;
-    double a[EB];
-#pragma unroll
-    for (int e = 0; e < EB; ++e) a[e] = 0.0;
-    for (int c = threadIdx.x * 8; c < H; c += blockDim.x * 8) {
-      const uint4 u = ldg16(xr + c);
-      const uint32_t wd[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const double xv = static_cast<double>(__uint_as_float((j & 1) ? (wd[j >> 1] & 0xFFFF0000u) : (wd[j >> 1] << 16)));
-        const float* wr = Wg + static_cast<size_t>(c + j) * E;
-        if (E == EB) {  // whole rows: 16-byte loads
-#pragma unroll
-          for (int e4 = 0; e4 < EB; e4 += 4) {
-            const float4 v = __ldg(reinterpret_cast<const float4*>(wr + e4));
-            a[e4] = fma(xv, static_cast<double>(v.x), a[e4]);
-            a[e4 + 1] = fma(xv, static_cast<double>(v.y), a[e4 + 1]);
-            a[e4 + 2] = fma(xv, static_cast<double>(v.z), a[e4 + 2]);
-            a[e4 + 3] = fma(xv, static_cast<double>(v.w), a[e4 + 3]);
-          }
-        } else {
-#pragma unroll
-          for (int e = 0; e < EB; ++e)
-            if (e < E) a[e] = fma(xv, static_cast<double>(__ldg(wr + e)), a[e]);
-        }
-      }
-    }
-#pragma unroll
-    for (int e = 0; e < EB; ++e) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) a[e] += __shfl_xor_sync(0xffffffffu, a[e], o);
-      if (lane == 0) red[warp][e] = a[e];
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double lgt[EB];
-      for (int e = 0; e < E; ++e) {
-        double v = 0.0;
-        for (int ww = 0; ww < 8; ++ww) v += red[ww][e];
-        lgt[e] = v;
-      }
-      double mx = lgt[0];
-      for (int e = 1; e < E; ++e) mx = fmax(mx, lgt[e]);
-      double sum = 0.0;
-      for (int e = 0; e < E; ++e) sum += exp(lgt[e] - mx);
-      for (int e = 0; e < E; ++e) scores[static_cast<size_t>(t) * E + e] = static_cast<float>(exp(lgt[e] - mx) / sum);
-      unsigned used = 0;
-      for (int s2 = 0; s2 < K; ++s2) {
-        int best = -1;
-        for (int e = 0; e < E; ++e) {
-          if ((used >> e) & 1u) continue;
-          if (best < 0 || lgt[e] > lgt[best]) best = e;
-        }
-        used |= 1u << best;
-        idx[static_cast<size_t>(t) * K + s2] = best;
-        w[static_cast<size_t>(t) * K + s2] = static_cast<float>(exp(lgt[best] - mx) / sum);
-      }
-    }
-    __syncthreads();
-  }
-}
-
-// Aux-loss partials from the final routing: per 32-token block the fp64 sum of the fp32
-// scores in token order (a fixed xor-shuffle tree over the block's 32 tokens: deterministic)
-// and the top-1 histogram (exact integer atomics).  One warp per (block, expert).
-__global__ void route_aux_kernel(const float* __restrict__ scores, const int* __restrict__ idx, int N, int E, int K,
-                                 double* __restrict__ ssum, int* __restrict__ cnt_top1) {
-  const int nb = (N + kRouteTB - 1) / kRouteTB;
-  const int lane = threadIdx.x & 31;
-  const int nw = gridDim.x * (blockDim.x >> 5);
-  for (int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < nb * E; i += nw) {
-    const int b = i / E, e = i % E;
-    const int t = b * kRouteTB + lane;
-    double s = t < N ? static_cast<double>(scores[static_cast<size_t>(t) * E + e]) : 0.0;
-    const unsigned top = __ballot_sync(0xffffffffu, t < N && idx[static_cast<size_t>(t) * K] == e);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) {
-      ssum[i] = s;
-      if (top) atomicAdd(&cnt_top1[e], __popc(top));
-    }
-  }
-}
-
-// l_aux = E * sum_e frac_e * mean_t s[t,e]  with frac from the top-1 choice (moe.py:221-223)
-__global__ void __launch_bounds__(256) route_finalize_kernel(const double* __restrict__ ssum, int nblocks,
-                                                             const int* __restrict__ cnt_top1, int N, int E,
-                                                             double* __restrict__ l_aux,
-                                                             double* __restrict__ score_sums) {
-  // warp w reduces experts w, w + 8, ...: lane-strided partial sums, then a fixed xor tree
-  // (deterministic); one pass over ssum instead of E block-wide reductions
-  __shared__ double part[kMaxE];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int e = warp; e < E; e += blockDim.x >> 5) {
-    double s = 0.0;
-    for (int b = lane; b < nblocks; b += 32) s += ssum[static_cast<size_t>(b) * E + e];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) {
-      part[e] = s * (static_cast<double>(cnt_top1[e]) / N);
-      if (score_sums) score_sums[e] = s;
-    }
+    if (!sure) flagged[atomicAdd(&nflag, 1)] = r;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    double tot = 0.0, fr = 0.0;
-    for (int j = 0; j < E; ++j) {
-      tot += part[j];
-      fr += static_cast<double>(cnt_top1[j]) / N;
+    pending[blockIdx.x] = nflag;
+    if (nflag) {
+      const int base = atomicAdd(fix_count, nflag);
+      for (int f = 0; f < nflag; ++f) fix_list[base + f] = t0 + flagged[f];
     }
-    l_aux[0] = tot * (static_cast<double>(E) / N);
+  }
+  // softmax, top-k and outputs of the 16 tokens (fp64 from the certified logits): the exps and
+  // divisions one (token, expert) per thread, the max / sum / top-k per token in expert order
+  __shared__ double rmx[16], rsum[16];
+  if (threadIdx.x < 16) {
+    const int r = threadIdx.x;
+    double mx = lg[r][0];
+    for (int e = 1; e < E; ++e) mx = fmax(mx, lg[r][e]);
+    rmx[r] = mx;
+  }
+  __syncthreads();
+  for (int o = threadIdx.x; o < 16 * EB; o += blockDim.x) {
+    const int r = o / EB, e = o % EB;
+    if (e < E) bd[r][e] = exp(lg[r][e] - rmx[r]);
+  }
+  __syncthreads();
+  if (threadIdx.x < 16) {
+    const int r = threadIdx.x;
+    double sum = 0.0;
+    for (int e = 0; e < E; ++e) sum += bd[r][e];
+    rsum[r] = sum;
+  }
+  __syncthreads();
+  for (int o = threadIdx.x; o < 16 * E; o += blockDim.x) {  // coalesced score rows
+    const int r = o / E, e = o % E;
+    const float sc = static_cast<float>(bd[r][e] / rsum[r]);
+    bd[r][e] = sc;  // reused: the token's stored scores, for w and the aux sums
+    if (t0 + r < N) scores[static_cast<size_t>(t0) * E + o] = sc;
+  }
+  __syncthreads();
+  if (threadIdx.x < 16 && t0 + threadIdx.x < N) {
+    const int r = threadIdx.x, t = t0 + r;
+    unsigned used = 0;
+    for (int s2 = 0; s2 < K; ++s2) {
+      int best = -1;
+      for (int e = 0; e < E; ++e) {
+        if ((used >> e) & 1u) continue;
+        if (best < 0 || lg[r][e] > lg[r][best]) best = e;
+      }
+      used |= 1u << best;
+      idx[static_cast<size_t>(t) * K + s2] = best;
+      w[static_cast<size_t>(t) * K + s2] = static_cast<float>(bd[r][best]);
+      if (s2 == 0) top1[r] = best;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < E) {  // aux partials of the block's tokens, in token order
+    const int e = threadIdx.x;
+    double ssc = 0.0;
+    int c = 0;
+    for (int r = 0; r < 16 && t0 + r < N; ++r) {
+      ssc += bd[r][e];
+      c += top1[r] == e;
+    }
+    ssum[static_cast<size_t>(blockIdx.x) * E + e] = ssc;
+    if (c) atomicAdd(&cnt_top1[e], c);
+  }
+}
+
+// l_aux = E * sum_e frac_e * mean_t s[t,e]  with frac from the top-1 choice (moe.py:221-223).
+// Thread (j, e) sums partials j, j + J, ... of expert e (J = blockDim / E; independent loads in
+// flight), then thread e adds its J sums in j order: deterministic, one memory round trip deep.
+__global__ void __launch_bounds__(kFinalizeThreads) route_finalize_kernel(const double* __restrict__ ssum,
+                                                                          int nblocks,
+                                                                          const int* __restrict__ cnt_top1, int N,
+                                                                          int E, double* __restrict__ l_aux,
+                                                                          double* __restrict__ score_sums,
+                                                                          int* __restrict__ counts_top1) {
+  __shared__ double part[kFinalizeThreads];
+  __shared__ double tot[kMaxE];
+  const int J = blockDim.x / E;
+  const int j = threadIdx.x / E, e = threadIdx.x % E;
+  if (j < J) {
+    double v = 0.0;
+#pragma unroll 8
+    for (int b = j; b < nblocks; b += J) v += ssum[static_cast<size_t>(b) * E + e];
+    part[threadIdx.x] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < E) {
+    double v = 0.0;
+    for (int jj = 0; jj < J; ++jj) v += part[jj * E + threadIdx.x];
+    tot[threadIdx.x] = v;
+    if (score_sums) score_sums[threadIdx.x] = v;
+    if (counts_top1) counts_top1[threadIdx.x] = cnt_top1[threadIdx.x];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double acc = 0.0, fr = 0.0;
+    for (int k = 0; k < E; ++k) {
+      acc += tot[k] * (static_cast<double>(cnt_top1[k]) / N);
+      fr += static_cast<double>(cnt_top1[k]) / N;
+    }
+    l_aux[0] = acc * (static_cast<double>(E) / N);
     l_aux[1] = fr;
   }
 }
@@ -992,30 +1128,39 @@ static int launch_router(const void* X, const float* Wg, int N, int H, int E, in
 // PPMOE_ROUTER=tc (default for bf16): tensor-core logits + guard band + exact fix-up;
 // dmma: FP64 tensor-core logits for every token; dfma: CUDA-core fp64.
 static bool use_tc_router(int dtype, int H, int E) {
-  // default for E <= 8 (C2: 90 -> 83 us); at 8 < E <= 16 the DMMA kernel is faster (C3: 238 vs
-  // 274 us, tools/ab_router.py) unless PPMOE_ROUTER=tc forces it
+  // default for bf16 and E <= 16 (tools/ab_router.py, C2 / C3: 64 / 189 us against the DMMA
+  // router's 89 / 237); PPMOE_ROUTER=dmma|dfma selects the fp64 routers
   const char* e = std::getenv("PPMOE_ROUTER");
   if (e && std::strcmp(e, "tc") != 0) return false;
-  return dtype == kBF16 && H % (32 * kRouteTcWarps) == 0 && (E <= 8 || (e && E <= 16));
+  return dtype == kBF16 && H % (32 * kRouteTcWarps) == 0 && E <= 16;
 }
 
 static int launch_router_tc(const void* X, const float* Wg, int N, int H, int E, int K, int* idx, float* w,
-                            float* scores, int* fix_list, int* fix_count, uint4* pieces, cudaStream_t s) {
+                            float* scores, double* ssum, int* cnt, int* fix_list, int* fix_count, int* pending,
+                            uint4* pieces, cudaStream_t s) {
   const auto* x = static_cast<const __nv_bfloat16*>(X);
   const int NT = E <= 8 ? 1 : 2;
   const int prep_threads = H / 32 * NT * 32;
   router_tc_prep_kernel<<<std::max(1, std::min((prep_threads + 255) / 256, num_sms() * 4)), 256, 0, s>>>(Wg, H, E, NT,
-                                                                                                      pieces);
+                                                                                                      pieces, cnt);
   if (int rc = check_launch("router_tc_prep_kernel")) return rc;
   const int blocks = (N + 15) / 16;
-  if (E <= 8) router_tc_kernel<1><<<blocks, 32 * kRouteTcWarps, 0, s>>>(x, pieces, N, H, E, K, idx, w, scores,
-                                                                         fix_list, fix_count);
-  else router_tc_kernel<2><<<blocks, 32 * kRouteTcWarps, 0, s>>>(x, pieces, N, H, E, K, idx, w, scores, fix_list,
-                                                                 fix_count);
+  static const int stages = getenv("PPMOE_TC_STAGES") ? atoi(getenv("PPMOE_TC_STAGES")) : 2;
+  if (E <= 8 && stages == 3)
+    router_tc_kernel<1, 3><<<blocks, 32 * kRouteTcWarps, 0, s>>>(x, Wg, pieces, N, H, E, K, idx, w, scores, ssum, cnt,
+                                                                 fix_list, fix_count, pending);
+  else if (E <= 8)
+    router_tc_kernel<1, 2><<<blocks, 32 * kRouteTcWarps, 0, s>>>(x, Wg, pieces, N, H, E, K, idx, w, scores, ssum, cnt,
+                                                                 fix_list, fix_count, pending);
+  else
+    router_tc_kernel<2, 2><<<blocks, 32 * kRouteTcWarps, 0, s>>>(x, Wg, pieces, N, H, E, K, idx, w, scores, ssum, cnt,
+                                                                 fix_list, fix_count, pending);
   if (int rc = check_launch("router_tc_kernel")) return rc;
   const int fix_blocks = std::min(N, num_sms() * 2);
-  if (E <= 8) router_fix_kernel<8><<<fix_blocks, 256, 0, s>>>(x, Wg, N, H, E, K, fix_list, fix_count, idx, w, scores);
-  else router_fix_kernel<16><<<fix_blocks, 256, 0, s>>>(x, Wg, N, H, E, K, fix_list, fix_count, idx, w, scores);
+  if (E <= 8) router_fix_kernel<8><<<fix_blocks, kFixThreads, 0, s>>>(x, Wg, N, H, E, K, fix_list, fix_count, idx, w, scores, cnt,
+                                                              pending, ssum);
+  else router_fix_kernel<16><<<fix_blocks, kFixThreads, 0, s>>>(x, Wg, N, H, E, K, fix_list, fix_count, idx, w, scores, cnt,
+                                                               pending, ssum);
   return check_launch("router_fix_kernel");
 }
 
@@ -1052,12 +1197,17 @@ using namespace ppmoe;
 
 extern "C" {
 
+// ppmoe_route workspace: aux score-sum records (one per 16 tokens; the fp64 routers use one per
+// 32) | top-1 counts + the tensor-core router's fix-up count | fix-up queue, per-16-token-block
+// queued counts | (with H) the Wg pieces.
+static size_t route_ssum_bytes(int N, int E) {
+  return align_up((static_cast<size_t>(N) + 15) / 16 * (E > 0 ? E : 1) * 8, 256);
+}
+
 size_t ppmoe_route_workspace_bytes(int N, int E, int K) {
   (void)K;
-  const size_t nb = (static_cast<size_t>(N) + kRouteTB - 1) / kRouteTB;
-  // score sums | top-1 counts (+ the tensor-core router's fix-up count) | fix-up token list
-  return align_up(nb * (E > 0 ? E : 1) * 8, 256) + align_up(static_cast<size_t>(E) * 4 + 4, 256) +
-         align_up(static_cast<size_t>(N > 0 ? N : 1) * 4, 256);
+  return route_ssum_bytes(N, E) + align_up(static_cast<size_t>(E) * 4 + 4, 256) +
+         align_up(align_up(static_cast<size_t>(N > 0 ? N : 1), 64) * 4 + (static_cast<size_t>(N) + 15) / 16 * 4, 256);
 }
 
 size_t ppmoe_route_workspace_bytes_h(int N, int H, int E, int K) {
@@ -1077,18 +1227,18 @@ int ppmoe_route(const void* X, int dtype, const float* Wg, int N, int H, int E, 
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int nb = (N + kRouteTB - 1) / kRouteTB;
   double* ssum = static_cast<double*>(ws);
-  int* cnt = reinterpret_cast<int*>(static_cast<char*>(ws) + align_up(static_cast<size_t>(nb) * E * 8, 256));
+  int* cnt = reinterpret_cast<int*>(static_cast<char*>(ws) + route_ssum_bytes(N, E));
   int* fix_count = cnt + E;
   int* fix_list = reinterpret_cast<int*>(reinterpret_cast<char*>(cnt) + align_up(static_cast<size_t>(E) * 4 + 4, 256));
-  PPMOE_CUDA(cudaMemsetAsync(cnt, 0, static_cast<size_t>(E) * 4 + 4, s));
   int rc;
-  if (!route_override && use_tc_router(dtype, H, E) && ws_bytes >= ppmoe_route_workspace_bytes_h(N, H, E, K)) {
+  int nparts = nb;  // aux partial records: 32-token blocks, or 16-token blocks of the tensor-core router
+  const bool tc = !route_override && use_tc_router(dtype, H, E) && ws_bytes >= ppmoe_route_workspace_bytes_h(N, H, E, K);
+  if (!tc) PPMOE_CUDA(cudaMemsetAsync(cnt, 0, static_cast<size_t>(E) * 4 + 4, s));  // the tc prep kernel zeroes them
+  if (tc) {
     uint4* pieces = reinterpret_cast<uint4*>(static_cast<char*>(ws) + ppmoe_route_workspace_bytes(N, E, K));
-    rc = launch_router_tc(X, Wg, N, H, E, K, idx, w, scores, fix_list, fix_count, pieces, s);
-    if (rc) return rc;
-    route_aux_kernel<<<std::max(1, std::min((nb * E + 7) / 8, num_sms() * 8)), 256, 0, s>>>(scores, idx, N, E, K, ssum,
-                                                                                           cnt);
-    rc = check_launch("route_aux_kernel");
+    int* pending = fix_list + align_up(static_cast<size_t>(N), 64);
+    rc = launch_router_tc(X, Wg, N, H, E, K, idx, w, scores, ssum, cnt, fix_list, fix_count, pending, pieces, s);
+    nparts = (N + 15) / 16;
   } else if (use_dmma_router(dtype, H, E))
     rc = E <= 8 ? launch_router_dmma<8>(X, Wg, N, H, E, K, route_override, idx, w, scores, ssum, cnt, s)
                 : launch_router_dmma<16>(X, Wg, N, H, E, K, route_override, idx, w, scores, ssum, cnt, s);
@@ -1099,10 +1249,8 @@ int ppmoe_route(const void* X, int dtype, const float* Wg, int N, int H, int E, 
     rc = E <= 8 ? launch_router<float, 8>(X, Wg, N, H, E, K, route_override, idx, w, scores, ssum, cnt, s)
                 : launch_router<float, 16>(X, Wg, N, H, E, K, route_override, idx, w, scores, ssum, cnt, s);
   if (rc) return rc;
-  route_finalize_kernel<<<1, 256, 0, s>>>(ssum, nb, cnt, N, E, l_aux, score_sums);
-  if (int rc2 = check_launch("route_finalize_kernel")) return rc2;
-  if (counts_top1) PPMOE_CUDA(cudaMemcpyAsync(counts_top1, cnt, static_cast<size_t>(E) * 4, cudaMemcpyDeviceToDevice, s));
-  return kOk;
+  route_finalize_kernel<<<1, kFinalizeThreads, 0, s>>>(ssum, nparts, cnt, N, E, l_aux, score_sums, counts_top1);
+  return check_launch("route_finalize_kernel");
 }
 
 int ppmoe_route_combine_stats(const int* stats, int T, int N, int E, double* l_aux, int* counts_top1, void* stream) {

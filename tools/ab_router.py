@@ -33,8 +33,9 @@ for name, h, e, k in (("C2", 4096, 8, 2), ("C3", 8192, 16, 2)):
     same = all(torch.equal(getattr(outs["dfma"], f), getattr(outs[m], f)) for f in ("idx", "top1_counts")
                for m in outs)
     wdiff = max(float((outs["dfma"].w - outs[m].w).abs().max()) for m in outs)
+    ldiff = max(float((outs["dfma"].l_aux - outs[m].l_aux).abs().max()) for m in outs)
     bytes_ = n * h * 2 + h * e * 4 + n * k * 8
     fix = int(outs["tc"].fixups[0]) if outs["tc"].fixups is not None else -1
     print(f"{name}: tensor-core router re-routed {fix} of {n} tokens in fp64")
     print(f"{name}: router us/call {med}  HBM frac (6528.7 GB/s): "
-          f"{ {m: round(bytes_ / (v * 1e-6) / 6528.7e9, 3) for m, v in med.items()} }  idx equal {same}  max|dw| {wdiff:.2e}")
+          f"{ {m: round(bytes_ / (v * 1e-6) / 6528.7e9, 3) for m, v in med.items()} }  idx equal {same}  max|dw| {wdiff:.2e}  max|dl_aux| {ldiff:.2e}")

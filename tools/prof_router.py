@@ -1,5 +1,7 @@
-"""Dev tool: one C2 (or C3 with argv[1] == 'c3') router call for ncu (-k regex:router)."""
+"""Dev tool: C2 (or C3 with argv[1] == 'c3') router calls for ncu (-k regex:route); prints the
+host enqueue time of one route() call so a host-bound loop is visible."""
 import sys
+import time
 
 sys.path.insert(0, ".")
 import torch
@@ -15,3 +17,15 @@ wg = P.GateParams.init(h, e, P.Rng(0).spawn(1), device=dev).wg.detach()
 for _ in range(3):
     _ops.route(x, wg, k)
 torch.cuda.synchronize()
+t0 = time.perf_counter()
+for _ in range(20):
+    _ops.route(x, wg, k)
+t1 = time.perf_counter()
+torch.cuda.synchronize()
+a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+a.record()
+for _ in range(20):
+    _ops.route(x, wg, k)
+b.record()
+torch.cuda.synchronize()
+print(f"route() host enqueue {(t1 - t0) / 20 * 1e6:.1f} us/call, device {a.elapsed_time(b) / 20 * 1e3:.1f} us/call")
