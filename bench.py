@@ -402,7 +402,7 @@ def main():
     # algorithmic work: kept (token, expert) pairs of this rank's experts (capacity may drop some)
     rt_ = _ops.route(x.detach(), w.gate.wg.detach(), k)
     pl_ = _ops.plan(rt_.idx, rt_.w, E, _ops.capacity_for(a.capacity_factor, n, k, E))
-    router_fixups = int(rt_.fixups[0]) if (rt_.fixups is not None and E <= 8) else 0
+    router_fixups = int(rt_.fixups[0]) if (rt_.fixups is not None and E <= 16) else 0
     kept_all = pl_.kept.cpu()
     pairs = int(kept_all.sum())
     local_pairs = int(kept_all[rank * el:(rank + 1) * el].sum())
@@ -522,9 +522,9 @@ def main():
                 "config": config_of(a, world_size), "roofline": roofline, "cpu_baseline": cb, "e2e": e2e,
                 "gpu_launches": int(launches), "clocks": clk.summary(), "a2a_comparator": a2a, "kernels": per_kernel,
                 "host_enqueue_ms_per_step": round(host_ms, 3), "upstream_alt": upstream_alt,
-                "router": {"kernel": "tensor-core logits + guard band + fp64 fix-up" if E <= 8 else
+                "router": {"kernel": "tensor-core logits + guard band + fp64 fix-up" if E <= 16 else
                            "FP64 tensor-core (DMMA) logits",
-                           "fixup_tokens": router_fixups if E <= 8 else None,
+                           "fixup_tokens": router_fixups if E <= 16 else None,
                            "fixup_scope": "tokens of the full N-token batch re-routed in fp64 by one routing call "
                                           "(adjacent top-(k+1) logit gap within the error bound)"},
                 "gemm_launches_per_step": gemm_launches}
