@@ -258,7 +258,7 @@ int ppmoe_ipc_close(void* ptr);
 int ppmoe_ipc_free(void* ptr);
 /* Pointer sets (pads, rows, push, srcs) are HOST arrays of T device pointers (passed to
  * the kernels by value; T <= 8), entry q = rank q's buffer as mapped in this process.
- * Barrier of T ranks on channel ch: writes `epoch` (release, system scope) into every
+ * Barrier of T ranks on channel ch (0 <= ch < 16): writes `epoch` (release, system scope) into every
  * peer's signal pad (ppmoe_nvl_pad_bytes() each),
  * then waits until all T flags of this rank's pad reach `epoch`.  A spin longer than
  * timeout_cycles stores 1 to *err (plain store + system fence, so err may be pinned
@@ -283,6 +283,10 @@ int ppmoe_nvl_owner_gather(const void* const* rows, const int* seg, int El, cons
 /* out [t1-t0 x C] = sum over q (rank order) of srcs[q] rows [t0, t1) (fp32 [N x C]): the
  * owned rows of the ranks' partial gate-logit gradients.                               */
 int ppmoe_nvl_sum_rows(const void* const* srcs, int T, int rank, int N, int C, float* out, void* stream);
+/* out [count] = sum over q (rank order) of srcs[q][0, count) (fp32): the all-reduce of the
+ * gate-weight gradient over the tensor group (replaces collectives.py:135-153 all_reduce_sum
+ * in sync_gate_gradients, moe.py:311-313), called after a barrier that published srcs.    */
+int ppmoe_nvl_sum_all(const void* const* srcs, int T, int count, float* out, void* stream);
 /* Fused forward variant: ppmoe_expert_fc2_fwd_owner's epilogue scatter-adds w*Y of every
  * row straight into the fp32 accumulator of the rank that owns the row's token (owner_acc
  * = DEVICE array of T peer pointers, each [owner_rows x H], token t owned by t / owner_rows,

@@ -27,7 +27,7 @@
 namespace ppmoe {
 
 constexpr int kNvlMaxRanks = 8;
-constexpr int kNvlChannels = 8;
+constexpr int kNvlChannels = 16;
 
 // The group's peer pointers travel by value in the kernel parameters (no device tables).
 template <typename T>
@@ -484,6 +484,15 @@ int ppmoe_nvl_owner_gather(const void* const* rows, const int* seg, int El, cons
 #undef PPMOE_OG
 #undef PPMOE_OG_DYN
   return check_launch("nvl_owner_gather_kernel");
+}
+
+int ppmoe_nvl_sum_all(const void* const* srcs, int T, int count, float* out, void* stream) {
+  PPMOE_REQUIRE(T >= 1 && T <= kNvlMaxRanks && count >= 0, "bad sum_all arguments");
+  if (count == 0) return kOk;
+  const int grid = std::min((count + 255) / 256, num_sms() * 4);
+  nvl_sum_rows_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(peer_set<const float>(srcs, T), T, count, 0,
+                                                                            1, out);
+  return check_launch("nvl_sum_rows_kernel");
 }
 
 int ppmoe_nvl_sum_rows(const void* const* srcs, int T, int rank, int N, int C, float* out, void* stream) {

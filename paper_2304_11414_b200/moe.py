@@ -826,7 +826,12 @@ def sync_gate_gradients(world: World, group: ProcessGroup, gate: GateParams) -> 
         import torch.distributed as dist
 
         nvlink.check_all()
-        dist.all_reduce(gate.wg.grad, op=dist.ReduceOp.SUM, group=world.torch_group(group))
+        g = gate.wg.grad
+        if (g.is_cuda and g.dtype == torch.float32 and g.is_contiguous()
+                and nvlink.enabled(world, group, torch.bfloat16, 8)):
+            nvlink.all_reduce_grad(nvlink.arena(world, group), g)  # peer memory, one barrier
+        else:
+            dist.all_reduce(g, op=dist.ReduceOp.SUM, group=world.torch_group(group))
 
 
 class PPMoELayer(torch.nn.Module):

@@ -107,7 +107,7 @@ class NvlArena:
         self.err = torch.zeros(1, dtype=torch.int32, pin_memory=True)
         self._err_view = self.err.numpy()  # host view of the same pinned word (cheap reads)
         self._views: dict = {}  # (name, shape, dtype) -> tensor view of a peer buffer
-        self.epoch = [0] * 8
+        self.epoch = [0] * 16  # kNvlChannels
         self.bufs: dict = {}
         self.mc_bufs: dict = {}
         self.mc_disabled = False
@@ -270,6 +270,22 @@ def sum_owned_rows(ar: NvlArena, name: str, n: int, c: int) -> torch.Tensor:
     out = torch.empty((t1 - t0, c), dtype=torch.float32, device=ar.device)
     call("ppmoe_nvl_sum_rows", ar.table(name), ar.tp, ar.rank, n, c, ptr(out), _lib.stream_ptr())
     return out
+
+
+_CH_GSYNC = 8  # barrier channel of the gate-gradient sync (0-7: exchange, feed, chunks)
+
+
+def all_reduce_grad(ar: NvlArena, grad: torch.Tensor) -> None:
+    """In-place sum over the group (rank order, identical on every rank) of an fp32 tensor
+    through the arena: publish into a peer-visible buffer, one barrier, every rank sums the
+    T copies.  Two buffers alternate, so a rank that runs ahead cannot overwrite a buffer a
+    peer still reads (it would have to pass the next sync's barrier first)."""
+    ar.gsync = getattr(ar, "gsync", 0) ^ 1
+    name = f"gsync{ar.gsync}"
+    buf = ar.tensor(name, (grad.numel(),), torch.float32)
+    buf.copy_(grad.reshape(-1))
+    ar.barrier(_CH_GSYNC)
+    call("ppmoe_nvl_sum_all", ar.table(name), ar.tp, grad.numel(), ptr(grad), _lib.stream_ptr())
 
 
 def fused_forward_mode(ar: NvlArena, n: int, k: int) -> str:

@@ -42,9 +42,9 @@ for _ in range(5):
 torch.cuda.synchronize()
 if ws > 1:
     dist.barrier()
-steps = 3
-with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) as prof:
-    for _ in range(steps):
+steps, skip = 3, 4  # the first steps after the sync wait on the host: summarise the last 3
+with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA], acc_events=True) as prof:
+    for _ in range(skip + steps):
         step()
     torch.cuda.synchronize()
 if rank == 0:
@@ -53,6 +53,17 @@ if rank == 0:
     prof.export_chrome_trace(path)
     ev = [e for e in json.load(open(path))["traceEvents"] if e.get("cat") == "kernel"]
     ev.sort(key=lambda e: e["ts"])
+    starts = [i for i, e in enumerate(ev) if "router_tc_prep" in e["name"] or "router_dmma" in e["name"]]
+    ev = ev[starts[skip]:] if len(starts) > skip else ev
+    gaps = []
+    end, prev = ev[0]["ts"], ev[0]
+    for e in ev:
+        if e["ts"] - end > 5:
+            gaps.append((e["ts"] - end, prev["name"].split("(")[0][-40:], e["name"].split("(")[0][-40:]))
+        if e["ts"] + e["dur"] > end:
+            end, prev = e["ts"] + e["dur"], e
+    for g in sorted(gaps, reverse=True)[:12]:
+        print(f"  gap {g[0]:8.1f} us  {g[1]} -> {g[2]}")
     t0, t1 = ev[0]["ts"], max(e["ts"] + e["dur"] for e in ev)
     # intervals covered by GEMMs; everything else is exposed
     gem = [(e["ts"], e["ts"] + e["dur"]) for e in ev if "grouped_gemm" in e["name"]]
