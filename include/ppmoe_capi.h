@@ -287,6 +287,13 @@ int ppmoe_nvl_sum_rows(const void* const* srcs, int T, int rank, int N, int C, f
  * gate-weight gradient over the tensor group (replaces collectives.py:135-153 all_reduce_sum
  * in sync_gate_gradients, moe.py:311-313), called after a barrier that published srcs.    */
 int ppmoe_nvl_sum_all(const void* const* srcs, int T, int count, float* out, void* stream);
+/* Sliced routing over peer memory (the all-gather of moe.py:288-291's replicated gate
+ * outputs): recs = the T ranks' records of their nr-token slices, 32-bit words
+ * [stats 4E (ppmoe_route's score_sums fp64 | counts_top1 | pad) | idx nr*K | w nr*K |
+ * scores nr*E]; writes the full idx [T*nr x K], w, scores [T*nr x E] and stats [T x 4E]
+ * (the input of ppmoe_route_combine_stats).  Call after a barrier that published recs. */
+int ppmoe_nvl_route_gather(const void* const* recs, int T, int nr, int K, int E, int* idx, float* w, float* scores,
+                           int* stats, void* stream);
 /* Fused forward variant: ppmoe_expert_fc2_fwd_owner's epilogue scatter-adds w*Y of every
  * row straight into the fp32 accumulator of the rank that owns the row's token (owner_acc
  * = DEVICE array of T peer pointers, each [owner_rows x H], token t owned by t / owner_rows,

@@ -62,6 +62,7 @@ _SIGNATURES = {
     "ppmoe_nvl_pull_blocks": (_I, [_P, _I, _I, _I, _I, _P, _P]),
     "ppmoe_nvl_sum_rows": (_I, [_P, _I, _I, _I, _I, _P, _P]),
     "ppmoe_nvl_sum_all": (_I, [_P, _I, _I, _P, _P]),
+    "ppmoe_nvl_route_gather": (_I, [_P, _I, _I, _I, _I, _P, _P, _P, _P, _P]),
     "ppmoe_nvl_pull_blocks_ce": (_I, [_P, _I, _I, _I, _I, _P, _P]),
     "ppmoe_nvl_pull_range_ce": (_I, [_P, _I, _I, _I, _I, _I, _I, _P, _P]),
     "ppmoe_expert_fc2_fwd_owner": (_I, [_I, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P, _I, _F, _P, _P, _P, _P, _P, _I, _I,

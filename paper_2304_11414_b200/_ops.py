@@ -205,13 +205,12 @@ def route(hidden: torch.Tensor, wg: torch.Tensor, k: int, override: torch.Tensor
 def route_sliced(world, group, hidden: torch.Tensor, wg: torch.Tensor, k: int,
                  override: torch.Tensor | None = None) -> Route:
     """Routing of a replicated activation split across the TP group: each rank routes its
-    N/T-token slice straight into its rows of the full routing tensors, and in-place NCCL
-    all-gathers complete them identically on every rank (the reference gates every replica
-    identically, moe.py:288-291; the logits are computed once instead of T times).  l_aux is
+    N/T-token slice, and the slices are gathered identically on every rank -- over NVLink
+    peer memory (one barrier + ppmoe_nvl_route_gather), or in-place NCCL all-gathers without
+    the arena (the reference gates every replica identically, moe.py:288-291; the logits are
+    computed once instead of T times).  l_aux is
     recombined on the device from the per-slice score sums and top-1 counts in rank order
     (ppmoe_route_combine_stats: deterministic, identical on all ranks)."""
-    import torch.distributed as dist
-
     n, h = hidden.shape
     e = wg.shape[1]
     t = group.size
@@ -227,16 +226,50 @@ def route_sliced(world, group, hidden: torch.Tensor, wg: torch.Tensor, k: int,
     l_aux_slice = torch.empty(2, dtype=torch.float64, device=dev)
     ws = _ws(_lib.query("ppmoe_route_workspace_bytes_h", nr, h, e, k), dev)
     ov = None if override is None else override[sl].contiguous()
+    from . import nvlink
+
+    if nvlink.enabled(world, group, torch.bfloat16, 8):
+        # peer memory instead of four NCCL all-gathers: route into this rank's record of a
+        # peer-visible buffer, one barrier, every rank copies the T records (one kernel).
+        # Two records alternate, so a rank that runs ahead cannot overwrite one a peer still
+        # reads (it would have to pass the next call's barrier first).
+        ar = nvlink.arena(world, group)
+        ar.route_parity = getattr(ar, "route_parity", 0) ^ 1
+        name = f"route{ar.route_parity}"
+        rec = ar.tensor(name, (4 * e + nr * (2 * k + e),), torch.int32)
+        r_idx = rec[4 * e:4 * e + nr * k]
+        r_w = rec[4 * e + nr * k:4 * e + 2 * nr * k].view(torch.float32)
+        r_sc = rec[4 * e + 2 * nr * k:].view(torch.float32)
+        call("ppmoe_route", ptr(hidden[sl]), dtype_code(hidden.dtype), ptr(wg), nr, h, e, k, ptr(ov), ptr(r_idx),
+             ptr(r_w), ptr(r_sc), ptr(l_aux_slice), ptr(rec[2 * e:3 * e]), ptr(rec[:2 * e]), ptr(ws), ws.numel(),
+             _stream())
+        ar.barrier(nvlink.CH_ROUTE)
+        call("ppmoe_nvl_route_gather", ar.table(name), t, nr, k, e, ptr(idx), ptr(w), ptr(scores), ptr(stats),
+             _stream())
+    else:
+        _route_slice_nccl(world, group, hidden, wg, k, sl, ov, idx, w, scores, stats, mine, l_aux_slice, ws)
+    l_aux = torch.empty(2, dtype=torch.float64, device=dev)
+    cnt = torch.empty(e, dtype=torch.int32, device=dev)
+    call("ppmoe_route_combine_stats", ptr(stats), t, n, e, ptr(l_aux), ptr(cnt), _stream())
+    return Route(idx, w, scores, l_aux, cnt)
+
+
+def _route_slice_nccl(world, group, hidden, wg, k, sl, ov, idx, w, scores, stats, mine, l_aux_slice, ws):
+    """route_sliced without the NVLink arena: route the slice in place, then in-place NCCL
+    all-gathers of the four routing tensors."""
+    import torch.distributed as dist
+
+    n, h = hidden.shape
+    e = wg.shape[1]
+    t = group.size
+    me = world.rank_in(group)
+    nr = n // t
     call("ppmoe_route", ptr(hidden[sl]), dtype_code(hidden.dtype), ptr(wg), nr, h, e, k, ptr(ov), ptr(idx[sl]),
          ptr(w[sl]), ptr(scores[sl]), ptr(l_aux_slice), ptr(mine[2 * e:3 * e]), ptr(mine[:2 * e]), ptr(ws), ws.numel(),
          _stream())
     pg = world.torch_group(group)
     for full in (idx, w, scores, stats):
         dist.all_gather_into_tensor(full, full[me * full.shape[0] // t:(me + 1) * full.shape[0] // t], group=pg)
-    l_aux = torch.empty(2, dtype=torch.float64, device=dev)
-    cnt = torch.empty(e, dtype=torch.int32, device=dev)
-    call("ppmoe_route_combine_stats", ptr(stats), t, n, e, ptr(l_aux), ptr(cnt), _stream())
-    return Route(idx, w, scores, l_aux, cnt)
 
 
 def capacity_for(capacity_factor: float, tokens: int, k: int, num_experts: int) -> int:

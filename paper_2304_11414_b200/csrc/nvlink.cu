@@ -486,6 +486,42 @@ int ppmoe_nvl_owner_gather(const void* const* rows, const int* seg, int El, cons
   return check_launch("nvl_owner_gather_kernel");
 }
 
+// Sliced routing over peer memory: rank q's record (its N/T tokens) is [stats 4E | idx nr*K |
+// w nr*K | scores nr*E] 32-bit words; every rank copies all T records into its full routing
+// tensors (rows q*nr ..) and the per-rank stats table.
+__global__ void nvl_route_gather_kernel(const __grid_constant__ PeerSet<const uint32_t> recs, int T, int nr, int K,
+                                        int E, uint32_t* __restrict__ idx, uint32_t* __restrict__ w,
+                                        uint32_t* __restrict__ scores, uint32_t* __restrict__ stats) {
+  const size_t ns = 4 * static_cast<size_t>(E), ni = static_cast<size_t>(nr) * K, nsc = static_cast<size_t>(nr) * E;
+  const size_t rec = ns + 2 * ni + nsc;
+  for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < T * rec;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int q = static_cast<int>(i / rec);
+    size_t o = i - q * rec;
+    const uint32_t v = recs.p[q][o];
+    if (o < ns) {
+      stats[q * ns + o] = v;
+    } else if ((o -= ns) < ni) {
+      idx[q * ni + o] = v;
+    } else if ((o -= ni) < ni) {
+      w[q * ni + o] = v;
+    } else {
+      scores[q * nsc + (o - ni)] = v;
+    }
+  }
+}
+
+int ppmoe_nvl_route_gather(const void* const* recs, int T, int nr, int K, int E, int* idx, float* w, float* scores,
+                           int* stats, void* stream) {
+  PPMOE_REQUIRE(T >= 1 && T <= kNvlMaxRanks && nr >= 0 && K >= 1 && E >= 1, "bad route_gather arguments");
+  const size_t words = static_cast<size_t>(T) * (4 * static_cast<size_t>(E) + static_cast<size_t>(nr) * (2 * K + E));
+  const int grid = static_cast<int>(std::min<size_t>((words + 255) / 256, static_cast<size_t>(num_sms()) * 4));
+  nvl_route_gather_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      peer_set<const uint32_t>(recs, T), T, nr, K, E, reinterpret_cast<uint32_t*>(idx), reinterpret_cast<uint32_t*>(w),
+      reinterpret_cast<uint32_t*>(scores), reinterpret_cast<uint32_t*>(stats));
+  return check_launch("nvl_route_gather_kernel");
+}
+
 int ppmoe_nvl_sum_all(const void* const* srcs, int T, int count, float* out, void* stream) {
   PPMOE_REQUIRE(T >= 1 && T <= kNvlMaxRanks && count >= 0, "bad sum_all arguments");
   if (count == 0) return kOk;

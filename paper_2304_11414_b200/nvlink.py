@@ -273,6 +273,7 @@ def sum_owned_rows(ar: NvlArena, name: str, n: int, c: int) -> torch.Tensor:
 
 
 _CH_GSYNC = 8  # barrier channel of the gate-gradient sync (0-7: exchange, feed, chunks)
+CH_ROUTE = 9  # barrier channel of the sliced routing (_ops.route_sliced)
 
 
 def all_reduce_grad(ar: NvlArena, grad: torch.Tensor) -> None:
