@@ -281,7 +281,8 @@ def _pp_worker(rank, world, port, q, stages, tp, dtype):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("stages,tp,dtype", [(2, 1, torch.bfloat16), (2, 2, torch.float32)])
+@pytest.mark.parametrize("stages,tp,dtype", [(2, 1, torch.bfloat16), (2, 2, torch.float32),
+                                             (2, 4, torch.float32)])  # 2 x 4: BASELINE configs[3] on 8 GPUs
 def test_pipeline_stack_matches_single_gpu(stages, tp, dtype):
     """1F1B over P stages x T tensor ranks (NCCL p2p, TP dense FFN, PPMoE exchange) gives the
     gradients of the same 4-block stack run on one GPU (BASELINE configs[3] structure).
