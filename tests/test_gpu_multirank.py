@@ -46,7 +46,7 @@ def _worker(rank, world, port, q, k, cf, env=None, e=8):
     torch.cuda.set_device(rank)
     dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
     try:
-        h, n = 512, 1024
+        h, n = 512, int(os.environ.get("_TEST_N", "1024"))
         el = e // world
         full = P.MoeLayerWeights.random(h, e, seed=11, device="cuda")  # identical on every rank
         local = P.MoeLayerWeights(P.GateParams(full.gate.wg.detach().clone().requires_grad_()),
@@ -88,6 +88,7 @@ def test_tp_one_expert_per_rank(world, k, cf, env, e):
     (2, 2, float("inf"), {"PPMOE_NVL_MC": "1"}), (2, 2, 1.25, {"PPMOE_NVL_CHUNKS": "2"}),
     (2, 2, 1.25, {"_TEST_DROPOUT": "0.2"}), (4, 1, float("inf"), {"_TEST_DROPOUT": "0.1"}),
     (4, 2, float("inf"), {"PPMOE_NVL_CHUNKS": "2"}),
+    (4, 2, 1.25, {"_TEST_N": "1022"}),  # N % T != 0: every rank routes the whole batch, uneven owner blocks
 ])
 def test_tp_nccl_matches_simulated(world, k, cf, env, e=8):
     if torch.cuda.device_count() < world:
@@ -105,7 +106,7 @@ def test_tp_nccl_matches_simulated(world, k, cf, env, e=8):
         p.join(timeout=120)
         assert p.exitcode == 0
     # single-process reference: simulated TP world on GPU 0
-    h, n = 512, 1024
+    h, n = 512, int((env or {}).get("_TEST_N", "1024"))
     full = P.MoeLayerWeights.random(h, e, seed=11, device="cuda")
     x = torch.randn(n, h, device="cuda", generator=torch.Generator(device="cuda").manual_seed(5)).bfloat16()
     x.requires_grad_()
