@@ -132,8 +132,15 @@ __device__ __forceinline__ void acc_bf16(float (&acc)[CW], const typename OgVec<
 }
 
 // One CTA per tile of kOgTile owned tokens x (256*CW) columns.  CW columns per thread.
+// Register budgets: 4 CTAs per SM where the accumulators fit in 64 registers (more row loads
+// in flight per SM: C2 backward with the gate term 128 -> 92 us, forward 79 -> 73 us), else 3;
+// the grid is sized to the resident CTAs (occupancy API), so the grid-stride tile loop has
+// no second partial wave.
 template <int EB, int U, int KT, int CW>  // KT = k (1, 2) or 0: any k <= 8 read at run time
-__global__ void __launch_bounds__(256, EB > 8 ? 3 : 1)
+__global__ void __launch_bounds__(256, EB > 8 ? 3
+                                           : EB == 8 ? (U * CW <= 16 ? 4 : 3)
+                                           : EB == 0 ? (U * CW <= 32 ? 4 : 3)
+                                                     : 1)
     nvl_owner_gather_kernel(const __grid_constant__ PeerSet<const __nv_bfloat16> rows, const int* __restrict__ seg,
                             int El, const int* __restrict__ idx, const int* __restrict__ pair_pos,
                             const float* __restrict__ w, int Kr, int H, int t0, int t1,
@@ -361,12 +368,16 @@ __global__ void __launch_bounds__(256)
 
 // Owner-gather CTAs per SM (PPMOE_OG_CTAS).  5 = full residency of the 48-register forms
 // (ncu, C2: forward 65 -> 60 us, gate-term backward 97 -> 89 us against 4; 6 overshoots).
-static int og_ctas_per_sm() {
-  static int v = [] { const char* e = getenv("PPMOE_OG_CTAS"); return e ? atoi(e) : 5; }();
+static int og_ctas_per_sm() {  // PPMOE_OG_CTAS overrides the grid's CTAs per SM (A/B runs)
+  static int v = [] { const char* e = getenv("PPMOE_OG_CTAS"); return e ? atoi(e) : 0; }();
   return v;
 }
 static int og16_u() {  // tokens per thread of the 8 < E <= 16 gate-term form (PPMOE_OG16_U: 4 or 8)
   static int v = [] { const char* e = getenv("PPMOE_OG16_U"); return e ? atoi(e) : 4; }();
+  return v;
+}
+static int og8_u() {  // tokens per thread of the E <= 8 gate-term form (PPMOE_OG8_U: 4 or 8)
+  static int v = [] { const char* e = getenv("PPMOE_OG8_U"); return e ? atoi(e) : 4; }();
   return v;
 }
 static bool og_wide_e() {  // PPMOE_OG_WIDE_E=0: the any-E form (Wg from L2) for A/B runs
@@ -446,7 +457,13 @@ int ppmoe_nvl_owner_gather(const void* const* rows, const int* seg, int El, cons
 #define PPMOE_OG(EB, U, KT, CW)                                                                            \
   do {                                                                                                     \
     const int gy_ = (H / CW + 255) / 256;                                                                  \
-    nvl_owner_gather_kernel<EB, U, KT, CW><<<dim3(max(1, min(tiles, num_sms() * og_ctas_per_sm() / gy_)), gy_), 256, 0, s>>>( \
+    static const int occ_ = [] {                                                                           \
+      int b = 0;                                                                                           \
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, nvl_owner_gather_kernel<EB, U, KT, CW>, 256, 0);   \
+      return b > 0 ? b : 1;                                                                                \
+    }();                                                                                                   \
+    const int per_sm_ = og_ctas_per_sm() > 0 ? og_ctas_per_sm() : occ_;                                    \
+    nvl_owner_gather_kernel<EB, U, KT, CW><<<dim3(max(1, min(tiles, num_sms() * per_sm_ / gy_)), gy_), 256, 0, s>>>( \
         R, seg, El, idx, pair_pos, w, K, H, t0, t1, dl, Wg, E, O, OS, P, T, sym_mc);                       \
   } while (0)
   // 8 < E <= 32: Wg columns in 64 KB of dynamic shared memory, 3 CTAs per SM
@@ -456,7 +473,12 @@ int ppmoe_nvl_owner_gather(const void* const* rows, const int* seg, int El, cons
     constexpr int smem_ = CW * EB * 256 * 4;                                                               \
     PPMOE_CUDA(cudaFuncSetAttribute(kern_, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_));           \
     const int gy_ = (H / CW + 255) / 256;                                                                  \
-    kern_<<<dim3(max(1, min(tiles, num_sms() * 3 / gy_)), gy_), 256, smem_, s>>>(                          \
+    static const int occ_ = [&] {                                                                          \
+      int b = 0;                                                                                           \
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern_, 256, smem_);                                \
+      return b > 0 ? b : 1;                                                                                \
+    }();                                                                                                   \
+    kern_<<<dim3(max(1, min(tiles, num_sms() * occ_ / gy_)), gy_), 256, smem_, s>>>(                       \
         R, seg, El, idx, pair_pos, w, K, H, t0, t1, dl, Wg, E, O, OS, P, T, sym_mc);                       \
   } while (0)
   if (!dl) {
@@ -465,11 +487,12 @@ int ppmoe_nvl_owner_gather(const void* const* rows, const int* seg, int El, cons
     else if (K == 1) PPMOE_OG(0, 8, 1, 8);
     else PPMOE_OG(0, 1, 0, 8);
   } else if (E <= 8) {
-    if (K == 2) PPMOE_OG(8, 4, 2, 4);
+    if (K == 2 && og8_u() == 8) PPMOE_OG(8, 8, 2, 4);
+    else if (K == 2) PPMOE_OG(8, 4, 2, 4);
     else if (K == 1) PPMOE_OG(8, 8, 1, 4);
     else PPMOE_OG(8, 1, 0, 4);
   } else if (E <= 16 && og_wide_e()) {
-    if (K == 2 && og16_u() == 4) PPMOE_OG_DYN(16, 4, 2, 4);
+    if (K == 2 && og16_u() == 4) PPMOE_OG_DYN(16, 4, 2, 4);  // (8 tokens x 2 columns: 425 vs 230 us at C3)
     else if (K == 2) PPMOE_OG_DYN(16, 8, 2, 4);
     else if (K == 1) PPMOE_OG_DYN(16, 8, 1, 4);
     else PPMOE_OG_DYN(16, 1, 0, 4);

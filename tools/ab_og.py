@@ -1,6 +1,6 @@
 """Dev tool: owner-gather combine timings (forward form, backward form with the gate term)
 at a given shape on one GPU, through the public layer call (the two launches of a step).
-usage: python tools/ab_og.py H E [k] (env knobs apply: PPMOE_OG16_U, ...)"""
+usage: python tools/ab_og.py H E [k] (env knobs apply: PPMOE_OG16_U, PPMOE_OG8_U, PPMOE_OG8_CTAS, PPMOE_OG_CTAS)"""
 import sys
 
 sys.path.insert(0, ".")
