@@ -34,6 +34,12 @@ def _collect(q, procs, timeout=240):
     return got
 
 
+def _test_override(n, k, e):
+    """A fixed routing with k distinct experts per token (route_override, moe.py:273-285)."""
+    g = torch.Generator().manual_seed(123)
+    return torch.stack([torch.randperm(e, generator=g)[:k] for _ in range(n)]).to("cuda")
+
+
 def _worker(rank, world, port, q, k, cf, env=None, e=8):
     import torch.distributed as dist
 
@@ -60,8 +66,9 @@ def _worker(rank, world, port, q, k, cf, env=None, e=8):
         g = P.ProcessGroup(P.EP, tuple(range(world)))
         ebr = [local.bank if r == rank else None for r in range(world)]
         drop = float(os.environ.get("_TEST_DROPOUT", "0"))
+        ov = _test_override(n, k, e) if os.environ.get("_TEST_OVERRIDE") else None
         out, l_aux = P.ppmoe_forward(wd, g, x, local.gate, ebr, top_k=k, capacity_factor=cf, check_replicas=True,
-                                     dropout_p=drop, rng=P.Rng(41, 2) if drop else None)
+                                     dropout_p=drop, rng=P.Rng(41, 2) if drop else None, route_override=ov)
         (out.float().sum() + l_aux).backward()
         P.sync_gate_gradients(wd, g, local.gate)
         torch.cuda.synchronize()
@@ -89,6 +96,7 @@ def test_tp_one_expert_per_rank(world, k, cf, env, e):
     (2, 2, 1.25, {"_TEST_DROPOUT": "0.2"}), (4, 1, float("inf"), {"_TEST_DROPOUT": "0.1"}),
     (4, 2, float("inf"), {"PPMOE_NVL_CHUNKS": "2"}),
     (4, 2, 1.25, {"_TEST_N": "1022"}),  # N % T != 0: every rank routes the whole batch, uneven owner blocks
+    (2, 2, 1.25, {"_TEST_OVERRIDE": "1"}),  # route override through the sliced routing records
 ])
 def test_tp_nccl_matches_simulated(world, k, cf, env, e=8):
     if torch.cuda.device_count() < world:
@@ -111,9 +119,10 @@ def test_tp_nccl_matches_simulated(world, k, cf, env, e=8):
     x = torch.randn(n, h, device="cuda", generator=torch.Generator(device="cuda").manual_seed(5)).bfloat16()
     x.requires_grad_()
     drop = float((env or {}).get("_TEST_DROPOUT", "0"))
+    ov = _test_override(n, k, e) if (env or {}).get("_TEST_OVERRIDE") else None
     out, l_aux = P.ppmoe_forward(P.World(1, world), P.ProcessGroup(P.EP, tuple(range(world))), x, full.gate,
                                  full.shard(world), top_k=k, capacity_factor=cf, dropout_p=drop,
-                                 rng=P.Rng(41, 2) if drop else None)
+                                 rng=P.Rng(41, 2) if drop else None, route_override=ov)
     (out.float().sum() + l_aux).backward()
     ref_out = out.detach().float().cpu().numpy()
 
