@@ -81,6 +81,11 @@ static bool use_wide() {
 // before every synchronised GEMM.  Synchronised GEMMs of one device are stream-ordered.
 __device__ unsigned int g_ksync_counter;
 
+// M = 128 tail tiles of the token GEMMs (PPMOE_TAIL128=0 turns them off for A/B runs)
+static bool tail128_on() {
+  const char* e = getenv("PPMOE_TAIL128");  // read per launch: tools/ab_env.py switches it in-process
+  return !e || atoi(e) != 0;
+}
 template <bool A_MN, bool B_MN, class Epi>
 static int launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const GroupGeom& geo_in, const Epi& epi,
                      cudaStream_t s) {
@@ -95,6 +100,7 @@ static int launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const GroupGe
   }
   if (use_pair()) {
     geo.stage = staged_stores(use_wide());
+    geo.tail128 = !A_MN && !use_wide() && !use_narrow() && tail128_on();
     if (use_narrow() && !use_wide()) {
       auto kern = grouped_gemm_sm100_pair<kBN / 2, A_MN, B_MN, Epi>;
       constexpr int smem = PairSmem<kBN / 2>::kTotal;
@@ -269,6 +275,7 @@ static GroupGeom geom(int G, int N, int M_fixed, int K_fixed, const int* seg, in
   g.ksync_ctr = nullptr;
   g.ksync = 0;
   g.stage = 0;
+  g.tail128 = 0;
   g.hint = load_hint();
   g.G = G;
   g.N = N;

@@ -50,6 +50,7 @@ struct GroupGeom {
   unsigned int* ksync_ctr;
   int ksync;
   int stage;      // pair kernel: warp-cooperative staged row stores for stageable epilogues
+  int tail128;    // pair kernel: a group's last tile with 128 rows runs M = 128 MMAs (half the work)
 };
 
 // Epilogues that can hand their bf16 rows to the staged (coalesced) store path.
@@ -119,6 +120,12 @@ __device__ __forceinline__ void tile_coords(const SchedTables& t, int g, int loc
     nt = b * kBand + r % bw;
     mt = r / bw;
   }
+}
+
+// The group's last m-tile holds 128 rows (M = padded segment rows, a multiple of 128): the
+// CTA pair runs it with M = 128 MMAs (64 rows per CTA) instead of 256 rows half padding.
+__device__ __forceinline__ bool pair_tail(const GroupGeom& geo, const SchedTables& t, int g, int mt) {
+  return geo.tail128 && t.m_rows[g] - mt * 256 <= 128;
 }
 
 __device__ __forceinline__ void sched_locate(const SchedTables& t, int G, int tile, int& g, int& local) {
@@ -450,7 +457,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         int mt, nt;
         tile_coords(tab, g, local, n_tiles, mt, nt, geo.banded);
         const int kb_n = tab.k_blocks[g];
-        const int arow = mt * kPairBM + static_cast<int>(rank) * 128;
+        // tail tile (128 rows left in the group): each CTA's A half is 64 rows (the box still
+        // loads 128; the M = 128 MMA reads the first 64 of each CTA)
+        const bool tail = BN == 256 && pair_tail(geo, tab, g, mt);
+        const int arow = mt * kPairBM + static_cast<int>(rank) * (tail ? 64 : 128);
         const int bcol = nt * BN + static_cast<int>(rank) * (kMmaN / 2);  // + kMmaN j for MMA j
         const int abase = tab.a_base[g];
         const int bbase = tab.b_base[g];
@@ -515,7 +525,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     // issue stream must keep up with the tensor pipe while two epilogue warps share this
     // SM sub-partition.
     if (leader) {
-      constexpr uint32_t idesc = make_idesc_bf16(kPairBM, kMmaN, A_MN, B_MN);
+      constexpr uint32_t idesc256 = make_idesc_bf16(kPairBM, kMmaN, A_MN, B_MN);
+      constexpr uint32_t idesc128 = make_idesc_bf16(kPairBM / 2, kMmaN, A_MN, B_MN);
       constexpr uint32_t a_lbo = A_MN ? (64 * kBK * 2) : 16;
       constexpr uint32_t b_lbo = B_MN ? (64 * kBK * 2) : 16;
       constexpr uint32_t k_step_a = A_MN ? (kUMMAK * 128) : (kUMMAK * 2);
@@ -531,6 +542,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         int g, local;
         sched_locate(tab, G, tile, g, local);
         const int kb_n = tab.k_blocks[g];
+        int mt_, nt_;
+        tile_coords(tab, g, local, n_tiles, mt_, nt_, geo.banded);
+        const uint32_t idesc = BN == 256 && pair_tail(geo, tab, g, mt_) ? idesc128 : idesc256;
         const int acc = iter % kAcc;
         const uint32_t acc_phase = (iter / kAcc) & 1;
 #ifdef PPMOE_GEMM_STATS
@@ -588,7 +602,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     const int q = warp & 3;
     const int half = (warp - 2) >> 2;
     constexpr int kChunksPerWarp = BN / 32 / (kPairEpiWarps / 4);
-    const int row_in_tile = static_cast<int>(rank) * 128 + q * 32 + lane;
+    const int row_full = static_cast<int>(rank) * 128 + q * 32 + lane;
+    // M = 128 pair MMA (tail tile): each CTA's 64 rows x N land folded in its TMEM -- lanes
+    // 0-63 hold columns [0, N/2), lanes 64-127 the same rows' columns [N/2, N) (measured,
+    // tools/tail_probe.py) -- so lane quarter q holds rows (q & 1) * 32 + lane of this CTA's
+    // half and output columns (q >> 1) * N/2 + TMEM column
+    const int row_tail = static_cast<int>(rank) * 64 + (q & 1) * 32 + lane;
     const uint32_t empty_leader = mapa_shared(&tmem_empty[0], 0);
     constexpr bool kCanStage = StageTrait<Epi>::value && L::kHasStageBuf;
     uint8_t* stage_buf = smem + L::kStageBufOffset + (warp - 2) * 32 * kStageStride;
@@ -606,10 +625,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       mbar_wait_sleep(&tmem_full[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
-      const int m = mt * kPairBM + row_in_tile;
-      static_assert(kChunksPerWarp % 2 == 0, "64-column TMEM loads");
+      const bool tail = BN == 256 && pair_tail(geo, tab, g, mt);
+      const int m = mt * kPairBM + (tail ? row_tail : row_full);
+      // TMEM column chunks of this warp, and the output column of TMEM column 0
+      const int cpw = tail ? kChunksPerWarp / 2 : kChunksPerWarp;
+      const int col0 = nt * BN + (tail ? (q >> 1) * (BN / 2) : 0);
+      static_assert(BN != 256 || kChunksPerWarp % 4 == 0, "64-column TMEM loads, also for the folded tail");
 #pragma unroll 1
-      for (int c = half * kChunksPerWarp; c < (half + 1) * kChunksPerWarp; c += 2) {
+      for (int c = half * cpw; c < (half + 1) * cpw; c += 2) {
         float v[64];
         tmem_ld64(taddr + c * 32, v);
         if (!has_k) {
@@ -617,7 +640,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           for (int j = 0; j < 64; ++j) v[j] = 0.f;
         }
         const bool row_ok = m < tab.m_rows[g];
-        const int n0 = nt * BN + c * 32;
+        const int n0 = col0 + c * 32;
         if constexpr (kCanStage) {
           if (staged) {  // warp-uniform
             const int row = tab.row_base[g] + m;
