@@ -428,7 +428,9 @@ def main():
                 "timing": "kernel times from a profiled pass of the same K steps after the timed region",
                 "frac_of_burst_peak": (achieved / peaks["bf16_tflops"]) if (achieved and "bf16_tflops" in peaks) else None,
                 "peak_note": "peak = cuBLAS bf16 8192^3 back-to-back for 4 s on this pool (power-capped, the regime a "
-                             "long step runs in); frac_of_burst_peak uses the short-burst figure"}
+                             "long step runs in); frac_of_burst_peak uses the short-burst figure. The power-capped "
+                             "clock differs from box to box (see clocks), so frac can exceed 1 on a box that holds "
+                             "a higher clock than the one the sustained figure was measured on"}
 
     # ---- end to end: host (pinned) input -> device -> fwd+bwd -> loss back to host
     e2e = None
