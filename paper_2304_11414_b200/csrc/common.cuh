@@ -57,6 +57,39 @@ __device__ __forceinline__ void gelu_and_grad(float x, float& act, float& grad) 
   grad = fmaf(x * 0.39894228040143268f, e, cdf);
 }
 
+// The same for two elements with the paired fp32 pipe (FFMA2 / FMUL2 / FADD2: one issue slot
+// per pair; the MUFU ops stay per element), operation for operation the scalar form above.
+// The epilogue's GeLU arithmetic was what held the fc1 GEMM's tensor pipe at 87 % (98 %
+// with it stubbed out), through issue slots shared with the MMA warp's sub-partition.
+__device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
+__device__ __forceinline__ float rcp_approx(float x) {  // MUFU.RCP, as __fdividef(1, x)
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float ex2_approx(float x) {  // MUFU.EX2, as __expf after its log2(e) scale
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ void gelu_and_grad2(float2 x, float2& act, float2& grad) {
+  const float2 z = __fmul2_rn(make_float2(fabsf(x.x), fabsf(x.y)), f2(0.70710678118654752f));
+  const float2 den = __ffma2_rn(f2(0.3275911f), z, f2(1.0f));
+  const float2 t = make_float2(rcp_approx(den.x), rcp_approx(den.y));
+  float2 p = __ffma2_rn(t, f2(1.061405429f), f2(-1.453152027f));
+  p = __ffma2_rn(t, p, f2(1.421413741f));
+  p = __ffma2_rn(t, p, f2(-0.284496736f));
+  p = __ffma2_rn(t, p, f2(0.254829592f));
+  const float2 poly = __fmul2_rn(t, p);
+  const float2 m = __fmul2_rn(__fmul2_rn(__fmul2_rn(f2(-0.5f), x), x), f2(1.4426950408889634f));
+  const float2 e = make_float2(ex2_approx(m.x), ex2_approx(m.y));
+  const float2 q = __fmul2_rn(__fmul2_rn(f2(0.5f), poly), e);  // erfc(|x|/sqrt2) / 2
+  const float2 omq = __fadd2_rn(f2(1.0f), make_float2(-q.x, -q.y));
+  const float2 cdf = make_float2(x.x >= 0.f ? omq.x : q.x, x.y >= 0.f ? omq.y : q.y);
+  act = __fmul2_rn(x, cdf);
+  grad = __ffma2_rn(__fmul2_rn(x, f2(0.39894228040143268f)), e, cdf);
+}
+
 // The reference's dropout stream (tensor.dropout with moesim's Rng, tensor.py:23-49 and
 // 315-330): numpy's Philox4x64-10 keyed (seed, stream).  Draw m of the stream is word m % 4 of
 // the block at counter m / 4 + 1, a uniform is (word >> 11) * 2^-53, and an element is kept

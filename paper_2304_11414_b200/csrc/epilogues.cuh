@@ -164,9 +164,15 @@ struct EpiFc1Fwd {
 #pragma unroll
       for (int j = 0; j < W; ++j) b[j] = 0.f;
     float d[W], a[W];
+    static_assert(W % 2 == 0, "paired GeLU");
 #pragma unroll
-    for (int j = 0; j < W; ++j) {
-      gelu_and_grad(v[j] + b[j], a[j], d[j]);
+    for (int j = 0; j < W; j += 2) {
+      float2 aa, dd;
+      gelu_and_grad2(__fadd2_rn(make_float2(v[j], v[j + 1]), make_float2(b[j], b[j + 1])), aa, dd);
+      a[j] = aa.x;
+      a[j + 1] = aa.y;
+      d[j] = dd.x;
+      d[j + 1] = dd.y;
     }
     const size_t off = static_cast<size_t>(row) * F + n0;
     store_row<T, W>(gelu_grad + off, d, valid, cs);
