@@ -167,11 +167,20 @@ __device__ __forceinline__ float warp_column_sums32(float (&v)[32]) {
 #pragma unroll
   for (int o = 16, n = 32; o >= 1; o >>= 1, n >>= 1) {
     const bool upper = (lane & o) != 0;
+    if (n >= 4) {  // the adds of two slots at a time on the paired fp32 pipe
 #pragma unroll
-    for (int i = 0; i < n / 2; ++i) {
-      const float send = upper ? v[i] : v[i + n / 2];
-      const float keep = upper ? v[i + n / 2] : v[i];
-      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      for (int i = 0; i < n / 2; i += 2) {
+        const float s0 = upper ? v[i] : v[i + n / 2], s1 = upper ? v[i + 1] : v[i + 1 + n / 2];
+        const float k0 = upper ? v[i + n / 2] : v[i], k1 = upper ? v[i + 1 + n / 2] : v[i + 1];
+        const float2 r = __fadd2_rn(make_float2(k0, k1), make_float2(__shfl_xor_sync(0xffffffffu, s0, o),
+                                                                     __shfl_xor_sync(0xffffffffu, s1, o)));
+        v[i] = r.x;
+        v[i + 1] = r.y;
+      }
+    } else {
+      const float send = upper ? v[0] : v[1];
+      const float keep = upper ? v[1] : v[0];
+      v[0] = keep + __shfl_xor_sync(0xffffffffu, send, o);
     }
   }
   return v[0];

@@ -295,8 +295,17 @@ struct EpiFc2Dgrad {
     float gd[W];
     load_row<T, W>(gelu_grad + off, gd, valid);
     float x[W];
+    if constexpr (W % 2 == 0) {
 #pragma unroll
-    for (int j = 0; j < W; ++j) x[j] = v[j] * gd[j];
+      for (int j = 0; j < W; j += 2) {  // paired fp32 multiplies
+        const float2 r = __fmul2_rn(make_float2(v[j], v[j + 1]), make_float2(gd[j], gd[j + 1]));
+        x[j] = r.x;
+        x[j + 1] = r.y;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < W; ++j) x[j] = v[j] * gd[j];
+    }
     store_row<T, W>(dh + off, x, valid, cs);
     if constexpr (W == 32) {
       if (colsum_part) {
