@@ -165,6 +165,10 @@ struct EpiFc1Fwd {
       for (int j = 0; j < W; ++j) b[j] = 0.f;
     float d[W], a[W];
     static_assert(W % 2 == 0, "paired GeLU");
+#ifdef PPMOE_GELU_SCALAR  // dev A/B: the one-element-at-a-time form
+#pragma unroll
+    for (int j = 0; j < W; ++j) gelu_and_grad(v[j] + b[j], a[j], d[j]);
+#else
 #pragma unroll
     for (int j = 0; j < W; j += 2) {
       float2 aa, dd;
@@ -174,6 +178,7 @@ struct EpiFc1Fwd {
       d[j] = dd.x;
       d[j + 1] = dd.y;
     }
+#endif
     const size_t off = static_cast<size_t>(row) * F + n0;
     store_row<T, W>(gelu_grad + off, d, valid, cs);
     store_row<T, W>(act + off, a, valid, cs);
