@@ -43,8 +43,8 @@ __device__ __forceinline__ float gelu_grad_f(float x) {
 // Phi(x) = erfc(-x/sqrt2)/2 from the Abramowitz-Stegun 7.1.26 rational form
 // erfc(z) = t(a1 + t(a2 + t(a3 + t(a4 + t a5)))) e^{-z^2}, t = 1/(1 + p z), z >= 0
 // (|error| <= 1.5e-7, no cancellation for x << 0), sharing e^{-x^2/2} with phi(x):
-// one MUFU.RCP + one MUFU.EX2 + 12 FMA per element instead of erff's branchy polynomial
-// plus a separate exp -- the fc1 epilogue was the limiter of that GEMM.
+// one MUFU.RCP + one MUFU.EX2 + ~12 fp32 ops per element instead of erff's branchy
+// polynomial plus a separate exp.  The fc1 epilogue uses the paired form below.
 __device__ __forceinline__ void gelu_and_grad(float x, float& act, float& grad) {
   const float z = fabsf(x) * 0.70710678118654752f;
   const float t = __fdividef(1.0f, fmaf(0.3275911f, z, 1.0f));
