@@ -656,8 +656,8 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 
-// Block = 16 tokens (the MMA's M) x all experts (n-tiles of 8); its kRouteTcWarps warps split
-// the hidden dimension in 32-column steps.  MMA m (0, 1) of a step maps k-slot {2q+p, 2q+8+p}
+// Block = 16 tokens (the MMA's M) x all experts (n-tiles of 8); its W warps (4, or 8 for small
+// N) split the hidden dimension in 32-column steps.  MMA m (0, 1) of a step maps k-slot {2q+p, 2q+8+p}
 // of lane group q to columns c0 + 8q + 4m + {p, 2+p}, so a lane's A registers are one 16-byte
 // chunk of each of its two token rows, and its B registers are 12 prepared words.  Each lane
 // streams its own chunks through a private cp.async ring in shared memory (S steps
@@ -666,12 +666,11 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // for router_fix_kernel.  The block then writes its aux-loss partial (fp64 sums of its 16 tokens'
 // stored fp32 scores, in token order) and adds its top-1 counts; route_finalize_kernel recomputes
 // the partials of blocks with queued tokens once those are fixed.
-template <int NT, int S>
-__global__ void __launch_bounds__(32 * kRouteTcWarps, NT == 1 ? 7 : 5) router_tc_kernel(
+template <int NT, int S, int W>
+__global__ void __launch_bounds__(32 * W, NT == 1 ? (W == 4 ? 7 : 3) : 5) router_tc_kernel(
     const __nv_bfloat16* __restrict__ X, const float* __restrict__ Wg, const uint4* __restrict__ pieces, int N, int H,
     int E, int K, int* __restrict__ idx, float* __restrict__ w, float* __restrict__ scores, double* __restrict__ ssum,
     int* __restrict__ cnt_top1, int* __restrict__ fix_list, int* __restrict__ fix_count, int* __restrict__ pending) {
-  constexpr int W = kRouteTcWarps;
   constexpr int EB = NT * 8;
   // the cp.async rings and the split-K partials share one buffer (rings dead once the loop
   // ends): x chunks S steps deep, Wg pieces (L2-resident, shorter latency) two steps deep
@@ -1158,13 +1157,21 @@ static int launch_router_tc(const void* X, const float* Wg, int N, int H, int E,
                                                                                                       pieces, cnt);
   if (int rc = check_launch("router_tc_prep_kernel")) return rc;
   const int blocks = (N + 15) / 16;
-  // x two steps deep (a three-deep x ring measured 37.7 vs 35.5 us at C2, 164 vs 166 at C3)
-  if (E <= 8)
-    router_tc_kernel<1, 2><<<blocks, 32 * kRouteTcWarps, 0, s>>>(x, Wg, pieces, N, H, E, K, idx, w, scores, ssum, cnt,
-                                                                 fix_list, fix_count, pending);
+  // x two steps deep (a three-deep x ring measured 37.7 vs 35.5 us at C2, 164 vs 166 at C3).
+  // Few blocks (a TP rank's N/T-token slice, <= 2 per SM) fill the SMs better with 8 warps per
+  // block instead of 4, each splitting the hidden dimension further (ncu, C2 shape: 4096 tokens
+  // 17.3 -> 15.5 us; 8192 tokens 23.6 -> 29 us, so only below that); PPMOE_TC_W=4|8 forces one.
+  const char* we = getenv("PPMOE_TC_W");
+  const int wsel = we ? atoi(we) : (blocks <= num_sms() * 2 ? 8 : 4);
+  if (E <= 8 && wsel == 8 && H % 256 == 0)
+    router_tc_kernel<1, 2, 8><<<blocks, 256, 0, s>>>(x, Wg, pieces, N, H, E, K, idx, w, scores, ssum, cnt, fix_list,
+                                                     fix_count, pending);
+  else if (E <= 8)
+    router_tc_kernel<1, 2, kRouteTcWarps><<<blocks, 32 * kRouteTcWarps, 0, s>>>(
+        x, Wg, pieces, N, H, E, K, idx, w, scores, ssum, cnt, fix_list, fix_count, pending);
   else
-    router_tc_kernel<2, 2><<<blocks, 32 * kRouteTcWarps, 0, s>>>(x, Wg, pieces, N, H, E, K, idx, w, scores, ssum, cnt,
-                                                                 fix_list, fix_count, pending);
+    router_tc_kernel<2, 2, kRouteTcWarps><<<blocks, 32 * kRouteTcWarps, 0, s>>>(
+        x, Wg, pieces, N, H, E, K, idx, w, scores, ssum, cnt, fix_list, fix_count, pending);
   if (int rc = check_launch("router_tc_kernel")) return rc;
   const int fix_blocks = std::min(N, num_sms() * 2);
   if (E <= 8) router_fix_kernel<8><<<fix_blocks, kFixThreads, 0, s>>>(x, Wg, N, H, E, K, fix_list, fix_count, idx, w, scores, cnt,

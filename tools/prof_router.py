@@ -11,6 +11,8 @@ from paper_2304_11414_b200 import _ops
 
 c3 = len(sys.argv) > 1 and sys.argv[1] == "c3"
 h, e, k, n = (8192, 16, 2, 16384) if c3 else (4096, 8, 2, 16384)
+if len(sys.argv) > 2:
+    n = int(sys.argv[2])  # a TP rank's routing slice: N / T tokens
 dev = torch.device("cuda", 0)
 x = P.Rng(1, 99).normal_tensor((n, h), dtype=torch.bfloat16, device=dev)
 wg = P.GateParams.init(h, e, P.Rng(0).spawn(1), device=dev).wg.detach()
