@@ -245,8 +245,17 @@ struct EpiFc2Fwd {
 #pragma unroll
       for (int j = 0; j < W; ++j) b[j] = 0.f;
     float x[W];
+    if constexpr (W % 2 == 0) {
 #pragma unroll
-    for (int j = 0; j < W; ++j) x[j] = v[j] + b[j];
+      for (int j = 0; j < W; j += 2) {  // paired fp32 adds
+        const float2 r = __fadd2_rn(make_float2(v[j], v[j + 1]), make_float2(b[j], b[j + 1]));
+        x[j] = r.x;
+        x[j + 1] = r.y;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < W; ++j) x[j] = v[j] + b[j];
+    }
     if (drop_p > 0.f) {
       static_assert(W <= 32, "dropout keep bits cover at most 32 columns");
       const float inv = 1.f / (1.f - drop_p);
