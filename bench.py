@@ -97,7 +97,7 @@ class ClockSampler:
               "clocks_event_reasons.sw_power_cap")
     NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
-    def __init__(self, indices, period_ms: int = 50, active: bool = True):
+    def __init__(self, indices, period_ms: int = 20, active: bool = True):
         vis = os.environ.get("CUDA_VISIBLE_DEVICES")
         if vis:  # local ordinals -> the ids nvidia-smi knows (ints or UUIDs)
             ids = [v.strip() for v in vis.split(",") if v.strip()]
@@ -160,6 +160,7 @@ class ClockSampler:
 
     def summary(self):
         recs = list(self.samples)
+        whole = set().union(*(r[3] for r in recs)) if recs else set()
         if self.t0 is not None and self.t1 is not None:
             inside = [r for r in recs if self.t0 <= r[0] <= self.t1]
             if not inside:  # region shorter than the period: the samples bracketing it
@@ -172,7 +173,10 @@ class ClockSampler:
         sm = [r[1] for r in recs]
         reasons = set().union(*(r[3] for r in recs))
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(r[2] for r in recs), "reasons": sorted(reasons),
-                "samples": len(sm), "sm_mhz_min": min(sm), "gpus": len(self.indices)}
+                "samples": len(sm), "sm_mhz_min": min(sm), "gpus": len(self.indices),
+                # throttle reasons seen anywhere from the warm-up to the end of the timed region
+                # (the power-cap bit toggles; a short region can miss it in its few samples)
+                "reasons_around": sorted(whole)}
 
 
 # ----------------------------------------------------------------------------- CPU baseline
