@@ -478,9 +478,10 @@ def main():
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": n / (float(te) / 1e3), "unit": UNIT, "h2d_bytes_per_step": feed.h2d_bytes,
                "d2h_bytes_per_step": 4, "ms_per_step": float(te),
-               "h2d_scope": "per rank: its 1/T row slice of the pinned [N,H] bf16 batch, replicated over "
-                            + ("NVLink peer memory (copy-engine pulls)" if feed.arena is not None else
-                               ("an NCCL all_gather" if world_size > 1 else "nothing (one rank)"))
+               "h2d_scope": ("per rank: its 1/T row slice of the pinned [N,H] bf16 batch, replicated over "
+                             + ("NVLink peer memory (copy-engine pulls)" if feed.arena is not None else
+                                "an NCCL all_gather") if world_size > 1 else
+                             "the whole pinned [N,H] bf16 batch (one rank)")
                             + "; the next batch's copy overlaps this batch's compute",
                "path": "paper_2304_11414_b200.ReplicatedFeed + ppmoe_forward + backward (C-ABI) from pinned host"}
 
