@@ -228,6 +228,22 @@ def run_reference(a):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
+    # torch.distributed.run sets OMP_NUM_THREADS=1 for its ranks; the reference arm runs on rank 0
+    # alone and gets every host core back (the BLAS pools are resized at run time)
+    try:
+        import numpy  # noqa: F401 -- load the BLAS first: threadpoolctl only sees loaded pools
+        from threadpoolctl import threadpool_limits
+        limits = threadpool_limits(limits=os.cpu_count() or 1)
+    except Exception:  # pragma: no cover
+        limits = None
+    try:
+        return _run_reference(a)
+    finally:
+        if limits is not None:
+            limits.restore_original_limits()
+
+
+def _run_reference(a):
     hidden, experts, top_k = a.hidden, a.experts, a.top_k
     ffn = 4 * hidden
     steps, warmup = a.steps, a.warmup
