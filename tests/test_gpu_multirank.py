@@ -139,8 +139,12 @@ def test_tp_nccl_matches_simulated(world, k, cf, env, e=8):
         assert err(res["dbd"], full.bank.bias_down.grad[r * el:(r + 1) * el].float().cpu().numpy()) < 2e-2
         assert abs(res["l_aux"] - float(l_aux.detach())) < 1e-5
         assert res["ar"] == 2 and res["gs"] == 1
-    # every rank holds the identical replicated output
-    assert np.array_equal(got[0]["out"], got[1]["out"])
+    # every rank holds the identical replicated output, input gradient and synced gate
+    # gradient (the peer-memory sums run in rank order on every rank)
+    for r in range(1, world):
+        assert np.array_equal(got[0]["out"], got[r]["out"])
+        assert np.array_equal(got[0]["dx"], got[r]["dx"])
+        assert np.array_equal(got[0]["dwg"], got[r]["dwg"])
 
 
 def _dp_worker(rank, world, port, q, k, cf):
