@@ -1,5 +1,6 @@
-"""Interleaved A/B of the router kernels (DMMA fp64 tensor-core vs CUDA-core DFMA) at C2 and C3
-shapes, CUDA-event timed on the launching stream, plus a bit-identity check of their outputs."""
+"""Interleaved A/B of the router forms (CUDA-core fp64 DFMA, FP64 tensor-core DMMA, bf16
+tensor-core with the guard band and fp64 fix-up) at C2 and C3 shapes, CUDA-event timed on the
+launching stream, plus an identity check of their routing (indices, counts, weights, l_aux)."""
 import os
 import sys
 
